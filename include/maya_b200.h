@@ -1,0 +1,160 @@
+/*
+ * maya_b200.h — C ABI of the B200 batched trace-driven simulator engine.
+ *
+ * The engine replaces, for a batch of collated jobs, the reference call chain
+ *     annotate(job, RooflineEstimator())      pkg/src/dltsim/estimate.py:329-361
+ *     simulate(annotated, cluster)            pkg/src/dltsim/sim.py:476-485
+ *     _rank(trials) / SearchResult.best       pkg/src/dltsim/search.py:349-357, 337-339
+ * i.e. the body of PipelineEvaluator.__call__ after trace generation
+ * (search.py:200-209).  Plain pointers and sizes only; every function returns
+ * 0 on success or a negative MAYA_E* code, with maya_last_error() giving a
+ * thread-local message.
+ *
+ * Inputs are "raw jobs": the JobTrace/AnnotatedJob fields the simulator reads,
+ * flattened to integer arrays (see paper_2503_20191_b200/rawtrace.py for the
+ * event payload table).  String ids (op kinds, dtypes) are batch-global and
+ * resolved by the caller.
+ */
+#ifndef MAYA_B200_H
+#define MAYA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MAYA_ABI_VERSION 1
+#define MAYA_MAX_DTYPES 16
+
+/* return codes */
+#define MAYA_OK 0
+#define MAYA_EINVAL -1      /* malformed input (reference would raise ValueError/KeyError) */
+#define MAYA_ECUDA -2       /* CUDA runtime failure */
+#define MAYA_ENOMEM -3
+#define MAYA_ESTATE -4      /* call order violated */
+
+/* per-job status (maya_job_result.status) */
+#define MAYA_ST_OK 0
+#define MAYA_ST_DEADLOCK 1      /* sim.py:382-402 SimDeadlockError */
+#define MAYA_ST_INTERNAL 2      /* sim.py:334-337 / 345 RuntimeError */
+#define MAYA_ST_ESTIMATION 3    /* estimate.py EstimationError (missing dtype peak, bad collective) */
+#define MAYA_ST_OVERFLOW 4      /* a time or intermediate left the representable range */
+#define MAYA_ST_BAD_INPUT 5     /* trace shape the engine does not represent */
+
+/* event kinds (trace.py:160-174 order) */
+enum {
+  MAYA_EV_HOSTGAP = 0, MAYA_EV_KERNEL, MAYA_EV_MEMALLOC, MAYA_EV_MEMFREE, MAYA_EV_MEMCPY,
+  MAYA_EV_MEMSET, MAYA_EV_RECORD, MAYA_EV_WAIT, MAYA_EV_ESYNC, MAYA_EV_SSYNC, MAYA_EV_DSYNC,
+  MAYA_EV_COMMINIT, MAYA_EV_COLLECTIVE
+};
+
+/* DeviceClass (cluster.py:39-59) in integer form. */
+typedef struct maya_device_params {
+  int64_t peak_flops[MAYA_MAX_DTYPES]; /* by batch dtype id; 0 = no peak for this dtype */
+  int64_t hbm_bytes_per_s;
+  int64_t alpha_ns[2];                 /* [0] intra_host, [1] inter_host; mixed -> inter */
+  int64_t beta_bytes_per_s[2];
+} maya_device_params;
+
+/* RooflineEstimator (estimate.py:103-134): efficiency as exact fractions
+ * (Fraction(str(eff)), estimate.py:114-115) per batch op-kind id. */
+typedef struct maya_roofline_params {
+  int32_t n_op_kinds;
+  const int64_t *eff_num;
+  const int64_t *eff_den;
+  int64_t overhead_ns;
+} maya_roofline_params;
+
+/* One collated job (JobTrace + optional AnnotatedJob durations). */
+typedef struct maya_raw_job {
+  int32_t num_ranks;
+  int32_t devices_per_host;
+  int64_t capacity;            /* device_memory_bytes for the OOM check (sim.py:239) */
+  int32_t device;              /* index into the device table */
+  int32_t n_reps;
+  const int32_t *rank_rep;     /* [num_ranks] representative of each rank */
+  const int64_t *ev_off;       /* [n_reps + 1] */
+  const uint8_t *ev_kind;      /* [E] MAYA_EV_* */
+  const int32_t *ev_stream;    /* [E] */
+  const int64_t *ev_f;         /* [E][4] payload, rawtrace.py table */
+  int32_t n_comms;
+  const int32_t *comm_nranks;  /* [n_comms] */
+  const int8_t *comm_topo;     /* [n_comms] 0 intra, 1 inter, 2 mixed */
+  const int64_t *call_off;     /* [n_comms + 1] */
+  const int8_t *call_kind;     /* [n_calls] 0..4, -1 unused */
+  const int64_t *call_bytes;   /* [n_calls] */
+  const int64_t *rank_comm_off;/* [num_ranks + 1] */
+  const int32_t *rank_comm;    /* global comm of each CommInit of the rank's rep */
+  const int64_t *kernel_ns;    /* [E] host durations, or NULL -> roofline on device */
+  const int64_t *wire_ns;      /* [n_calls] host wire times, or NULL -> alpha-beta on device */
+} maya_raw_job;
+
+/* SimReport fields the search consumes (sim.py:59-72, search.py:209). */
+typedef struct maya_job_result {
+  int64_t total_ns;
+  int64_t peak_mem_bytes;
+  int32_t oom;
+  int32_t status;              /* MAYA_ST_* */
+  int32_t first_oom_rank;      /* -1 if none */
+  int32_t first_oom_seq;
+  int64_t dispatched_ops;
+  int64_t completed_ops;
+  int64_t rank_ops;            /* sum over ranks of rep trace length (work units) */
+  int64_t rounds;              /* scheduler rounds used (engine diagnostic) */
+} maya_job_result;
+
+/* Top-k entry of the search reduction (search.py:349-357 order). */
+typedef struct maya_topk_entry {
+  int64_t time_ns;
+  int32_t key_rank;            /* position of config.key() among the batch's keys */
+  int32_t job;                 /* job index in the batch */
+} maya_topk_entry;
+
+typedef struct maya_engine maya_engine;
+
+const char *maya_last_error(void);
+int maya_abi_version(void);
+
+/* Engine lifetime: one engine per CUDA device, not re-entrant. */
+int maya_open(int cuda_device, maya_engine **out);
+int maya_close(maya_engine *eng);
+
+/* Batch assembly (host).  maya_batch_add_job packs a raw job into the
+ * engine's pinned staging SoA; pointers need only live for the call. */
+int maya_batch_reset(maya_engine *eng);
+int maya_batch_set_devices(maya_engine *eng, int32_t n, const maya_device_params *devs);
+int maya_batch_set_roofline(maya_engine *eng, const maya_roofline_params *roof);
+int maya_batch_add_job(maya_engine *eng, const maya_raw_job *job, int32_t key_rank);
+int maya_batch_add_jobs(maya_engine *eng, int32_t n, const maya_raw_job *jobs,
+                        const int32_t *key_ranks, int32_t n_threads);
+int maya_batch_num_jobs(maya_engine *eng);
+
+/* Upload the staged batch to HBM (the H2D leg). */
+int maya_upload(maya_engine *eng);
+
+/* Run estimators + memory scan + scheduler (+ timeline if record != 0) on the
+ * resident batch; asynchronous on the engine stream. */
+int maya_run(maya_engine *eng, int32_t record_timeline);
+
+/* Download per-job results (the D2H leg); synchronises the engine stream. */
+int maya_results(maya_engine *eng, maya_job_result *out);
+
+/* Fused search reduction on device: the k best jobs by
+ * (time_ns asc, key_rank asc) over OK, non-OOM jobs with time_ns > 0 first,
+ * then time_ns == 0 jobs (their MFU is 0.0, search.py:784 / sim.py:493-494). */
+int maya_topk(maya_engine *eng, int32_t k, maya_topk_entry *out, int32_t *n_out);
+
+/* Timeline of one job after maya_run(record_timeline=1): per timed op
+ * (rank, stream, seq, start, end), ordered by rank then stream then FIFO. */
+int maya_timeline_size(maya_engine *eng, int32_t job, int64_t *n);
+int maya_timeline(maya_engine *eng, int32_t job, int32_t *rank, int32_t *stream,
+                  int32_t *seq, int64_t *start, int64_t *end);
+
+/* Device time of the last maya_run, per phase (ms): estimate, memscan, schedule. */
+int maya_last_timings(maya_engine *eng, float *ms3);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
