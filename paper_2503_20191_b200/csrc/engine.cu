@@ -1,0 +1,573 @@
+// C ABI of the engine (include/maya_b200.h): batch assembly, upload, run,
+// results, search reduction, timeline.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/maya_b200.h"
+#include "kernels.cuh"
+#include "pack.h"
+
+using namespace maya;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(MAYA_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// One array of the arena: host bytes copied at [off, off + bytes).
+struct Seg {
+  size_t off = 0, bytes = 0;
+};
+
+}  // namespace
+
+struct maya_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {};
+  // staged jobs
+  std::vector<JobPack> packs;
+  std::vector<maya_device_params> devs;
+  std::vector<int64_t> eff_num, eff_den;
+  int64_t overhead_ns = 1000;
+  // arena (inputs) and scratch (device only)
+  void *h_arena = nullptr;
+  size_t h_arena_cap = 0;
+  void *d_arena = nullptr;
+  size_t d_arena_cap = 0;
+  size_t arena_bytes = 0;
+  void *d_scratch = nullptr;
+  size_t d_scratch_cap = 0;
+  size_t scratch_bytes = 0;
+  bool uploaded = false, ran = false, recorded = false;
+  DevBatch db{};
+  DevTables tables{};
+  // segments
+  Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_slots, s_walkers, s_reps, s_ops, s_streams,
+      s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order;
+  Seg x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
+      x_results, x_err, x_topk, x_topk_out, x_topk_n;
+  uint64_t n_tl = 0;
+  std::vector<uint64_t> job_tl;      // per job timeline base
+  std::vector<uint64_t> job_ops;     // per job batch op base (for op_seq/streams)
+  float last_ms[3] = {0, 0, 0};
+};
+
+extern "C" {
+
+const char *maya_last_error(void) { return g_err.c_str(); }
+int maya_abi_version(void) { return MAYA_ABI_VERSION; }
+
+int maya_open(int cuda_device, maya_engine **out) {
+  maya_engine *e = new maya_engine();
+  e->device = cuda_device;
+  cudaError_t err = cudaSetDevice(cuda_device);
+  if (err != cudaSuccess) {
+    delete e;
+    return fail(MAYA_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(err));
+  }
+  err = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
+  if (err != cudaSuccess) {
+    delete e;
+    return fail(MAYA_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(err));
+  }
+  for (auto &ev : e->ev) cudaEventCreate(&ev);
+  *out = e;
+  return MAYA_OK;
+}
+
+int maya_close(maya_engine *e) {
+  if (!e) return MAYA_OK;
+  cudaSetDevice(e->device);
+  if (e->h_arena) cudaFreeHost(e->h_arena);
+  if (e->d_arena) cudaFree(e->d_arena);
+  if (e->d_scratch) cudaFree(e->d_scratch);
+  for (auto &ev : e->ev) if (ev) cudaEventDestroy(ev);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+  return MAYA_OK;
+}
+
+int maya_batch_reset(maya_engine *e) {
+  e->packs.clear();
+  e->uploaded = e->ran = e->recorded = false;
+  return MAYA_OK;
+}
+
+int maya_batch_set_devices(maya_engine *e, int32_t n, const maya_device_params *devs) {
+  if (n < 0 || n > 8) return fail(MAYA_EINVAL, "at most 8 device classes per batch");
+  e->devs.assign(devs, devs + n);
+  return MAYA_OK;
+}
+
+int maya_batch_set_roofline(maya_engine *e, const maya_roofline_params *roof) {
+  if (roof->n_op_kinds < 0 || roof->n_op_kinds > 64)
+    return fail(MAYA_EINVAL, "at most 64 op kinds per batch");
+  e->eff_num.assign(roof->eff_num, roof->eff_num + roof->n_op_kinds);
+  e->eff_den.assign(roof->eff_den, roof->eff_den + roof->n_op_kinds);
+  for (int i = 0; i < roof->n_op_kinds; i++)
+    if (e->eff_num[i] <= 0 || e->eff_den[i] <= 0)
+      return fail(MAYA_EINVAL, "efficiency fractions must be positive");
+  e->overhead_ns = roof->overhead_ns;
+  return MAYA_OK;
+}
+
+int maya_batch_add_job(maya_engine *e, const maya_raw_job *job, int32_t key_rank) {
+  return maya_batch_add_jobs(e, 1, job, &key_rank, 1);
+}
+
+int maya_batch_add_jobs(maya_engine *e, int32_t n, const maya_raw_job *jobs,
+                        const int32_t *key_ranks, int32_t n_threads) {
+  if (n < 0) return fail(MAYA_EINVAL, "negative job count");
+  for (int i = 0; i < n; i++)
+    if (jobs[i].device < 0 || jobs[i].device >= 8)
+      return fail(MAYA_EINVAL, "job device index out of range");
+  size_t base = e->packs.size();
+  e->packs.resize(base + n);
+  std::atomic<int> next(0);
+  auto work = [&]() {
+    for (;;) {
+      int i = next.fetch_add(1);
+      if (i >= n) break;
+      pack_job(jobs[i], key_ranks ? key_ranks[i] : i, e->packs[base + i]);
+    }
+  };
+  int nt = std::max(1, std::min<int>(n_threads, n));
+  if (nt == 1) {
+    work();
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; t++) th.emplace_back(work);
+    for (auto &t : th) t.join();
+  }
+  e->uploaded = e->ran = false;
+  return MAYA_OK;
+}
+
+int maya_batch_num_jobs(maya_engine *e) { return (int)e->packs.size(); }
+
+int maya_upload(maya_engine *e) {
+  CU(cudaSetDevice(e->device));
+  const size_t nj = e->packs.size();
+  // totals
+  size_t n_ranks = 0, n_rank_comm = 0, n_comms = 0, n_slots = 0, n_walkers = 0, n_reps = 0,
+         n_ops = 0, n_streams = 0, n_colls = 0, n_syncs = 0, n_counts = 0, n_mems = 0,
+         n_feats = 0, n_fire = 0, n_delay = 0, n_wstate = 0;
+  uint64_t n_tl = 0;
+  e->job_tl.resize(nj);
+  e->job_ops.resize(nj);
+  for (size_t j = 0; j < nj; j++) {
+    const JobPack &P = e->packs[j];
+    n_ranks += P.ranks.size();
+    n_rank_comm += P.rank_comm.size();
+    n_comms += P.comms.size();
+    n_slots += P.slots.size();
+    n_walkers += P.walkers.size();
+    n_reps += P.reps.size();
+    e->job_ops[j] = n_ops;
+    n_ops += P.ops.size();
+    n_streams += P.streams.size();
+    n_colls += P.coll_lc.size();
+    n_syncs += P.syncs.size();
+    n_counts += P.counts.size();
+    n_mems += P.mems.size();
+    n_feats += P.feats.size();
+    n_fire += P.n_fire;
+    n_delay += P.n_delay;
+    if (P.walkers.size() + P.ranks.size() > SMEM_STATES) n_wstate += P.walkers.size() + P.ranks.size();
+    e->job_tl[j] = n_tl;
+    n_tl += (uint64_t)P.hdr.dev_ops;
+  }
+  if (n_reps > 0xffffffffull) return fail(MAYA_EINVAL, "too many representatives in batch");
+  e->n_tl = n_tl;
+  // arena layout
+  size_t off = 0;
+  auto seg = [&](Seg &s, size_t bytes) {
+    s.off = off;
+    s.bytes = bytes;
+    off = align_up(off + bytes, 256);
+  };
+  seg(e->s_jobs, nj * sizeof(JobHdr));
+  seg(e->s_order, nj * sizeof(int32_t));
+  seg(e->s_ranks, n_ranks * sizeof(RankRec));
+  seg(e->s_rank_comm, n_rank_comm * sizeof(uint32_t));
+  seg(e->s_comms, n_comms * sizeof(CommRec));
+  seg(e->s_slots, n_slots * sizeof(SlotRec));
+  seg(e->s_walkers, n_walkers * sizeof(Walker));
+  seg(e->s_reps, n_reps * sizeof(RepHdr));
+  seg(e->s_ops, n_ops * sizeof(Op));
+  seg(e->s_streams, n_streams * sizeof(StreamRange));
+  seg(e->s_coll_lc, n_colls * sizeof(uint32_t));
+  seg(e->s_coll_idx, n_colls * sizeof(uint32_t));
+  seg(e->s_syncs, n_syncs * sizeof(SyncRec));
+  seg(e->s_counts, n_counts * sizeof(uint32_t));
+  seg(e->s_mems, n_mems * sizeof(MemRec));
+  seg(e->s_feats, n_feats * sizeof(Feature));
+  e->arena_bytes = off;
+  // scratch layout
+  off = 0;
+  seg(e->x_feat_ns, n_feats * 8);
+  seg(e->x_wire, n_slots * 8);
+  seg(e->x_fire, n_fire * 8);
+  seg(e->x_delay, n_delay * 8);
+  seg(e->x_wstate, n_wstate * sizeof(WState));
+  seg(e->x_cslots, n_slots * sizeof(CollSlot));
+  seg(e->x_repout, n_reps * sizeof(RepOut));
+  seg(e->x_results, nj * sizeof(maya_job_result));
+  seg(e->x_err, 16);
+  seg(e->x_topk, topk_scratch_bytes((uint32_t)nj, 64));
+  seg(e->x_topk_out, 64 * sizeof(maya_topk_entry));
+  seg(e->x_topk_n, 16);
+  seg(e->x_tl_start, 0);
+  seg(e->x_tl_end, 0);
+  e->scratch_bytes = off;
+
+  if (e->arena_bytes > e->h_arena_cap) {
+    if (e->h_arena) cudaFreeHost(e->h_arena);
+    e->h_arena = nullptr;
+    size_t cap = align_up(e->arena_bytes + e->arena_bytes / 4, 1 << 20);
+    CU(cudaMallocHost(&e->h_arena, cap));
+    e->h_arena_cap = cap;
+  }
+  if (e->arena_bytes > e->d_arena_cap) {
+    if (e->d_arena) cudaFree(e->d_arena);
+    e->d_arena = nullptr;
+    size_t cap = align_up(e->arena_bytes + e->arena_bytes / 4, 1 << 20);
+    CU(cudaMalloc(&e->d_arena, cap));
+    e->d_arena_cap = cap;
+  }
+  if (e->scratch_bytes > e->d_scratch_cap) {
+    if (e->d_scratch) cudaFree(e->d_scratch);
+    e->d_scratch = nullptr;
+    size_t cap = align_up(e->scratch_bytes + e->scratch_bytes / 4, 1 << 20);
+    CU(cudaMalloc(&e->d_scratch, cap));
+    e->d_scratch_cap = cap;
+  }
+  char *H = (char *)e->h_arena;
+  // job order: largest work first (LPT over the CTA scheduler)
+  {
+    std::vector<int32_t> order(nj);
+    for (size_t j = 0; j < nj; j++) order[j] = (int32_t)j;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      return e->packs[a].hdr.dev_ops > e->packs[b].hdr.dev_ops;
+    });
+    memcpy(H + e->s_order.off, order.data(), nj * sizeof(int32_t));
+  }
+  // per-job bases (serial prefix), then parallel copy
+  struct Base {
+    size_t ranks, rank_comm, comms, slots, walkers, reps, ops, streams, colls, syncs, counts,
+        mems, feats, fire, delay, wstate;
+  };
+  std::vector<Base> bases(nj);
+  {
+    Base b{};
+    for (size_t j = 0; j < nj; j++) {
+      const JobPack &P = e->packs[j];
+      bases[j] = b;
+      b.ranks += P.ranks.size();
+      b.rank_comm += P.rank_comm.size();
+      b.comms += P.comms.size();
+      b.slots += P.slots.size();
+      b.walkers += P.walkers.size();
+      b.reps += P.reps.size();
+      b.ops += P.ops.size();
+      b.streams += P.streams.size();
+      b.colls += P.coll_lc.size();
+      b.syncs += P.syncs.size();
+      b.counts += P.counts.size();
+      b.mems += P.mems.size();
+      b.feats += P.feats.size();
+      b.fire += P.n_fire;
+      b.delay += P.n_delay;
+      if (P.walkers.size() + P.ranks.size() > SMEM_STATES) b.wstate += P.walkers.size() + P.ranks.size();
+    }
+  }
+  auto copy_job = [&](size_t j) {
+    const JobPack &P = e->packs[j];
+    const Base &B = bases[j];
+    JobHdr h = P.hdr;
+    h.ranks = B.ranks;
+    h.rank_comm = B.rank_comm;
+    h.comms = B.comms;
+    h.slots = B.slots;
+    h.walkers = B.walkers;
+    h.feats = B.feats;
+    h.fire = B.fire;
+    h.delay = B.delay;
+    h.wstate = B.wstate;
+    h.timeline = e->job_tl[j];
+    memcpy(H + e->s_jobs.off + j * sizeof(JobHdr), &h, sizeof h);
+    RankRec *rk = (RankRec *)(H + e->s_ranks.off) + B.ranks;
+    for (size_t r = 0; r < P.ranks.size(); r++) {
+      RankRec x = P.ranks[r];
+      x.rep += (uint32_t)B.reps;
+      rk[r] = x;
+    }
+    RepHdr *rp = (RepHdr *)(H + e->s_reps.off) + B.reps;
+    for (size_t r = 0; r < P.reps.size(); r++) {
+      RepHdr x = P.reps[r];
+      x.ops += B.ops;
+      x.streams += B.streams;
+      x.colls += B.colls;
+      x.syncs += B.syncs;
+      x.counts += B.counts;
+      x.mems += B.mems;
+      x.job = (uint32_t)j;
+      rp[r] = x;
+    }
+#define CPY(SEG, VEC, BASE)                                                             \
+  if (!P.VEC.empty())                                                                   \
+    memcpy(H + e->SEG.off + (BASE) * sizeof(P.VEC[0]), P.VEC.data(),                    \
+           P.VEC.size() * sizeof(P.VEC[0]));
+    CPY(s_rank_comm, rank_comm, B.rank_comm)
+    CPY(s_comms, comms, B.comms)
+    CPY(s_slots, slots, B.slots)
+    CPY(s_walkers, walkers, B.walkers)
+    CPY(s_ops, ops, B.ops)
+    CPY(s_streams, streams, B.streams)
+    CPY(s_coll_lc, coll_lc, B.colls)
+    CPY(s_coll_idx, coll_idx, B.colls)
+    CPY(s_syncs, syncs, B.syncs)
+    CPY(s_counts, counts, B.counts)
+    CPY(s_mems, mems, B.mems)
+    CPY(s_feats, feats, B.feats)
+#undef CPY
+  };
+  {
+    int nt = (int)std::min<size_t>(8, std::max<size_t>(1, nj / 64));
+    std::atomic<size_t> next(0);
+    auto work = [&]() {
+      for (;;) {
+        size_t j = next.fetch_add(1);
+        if (j >= nj) break;
+        copy_job(j);
+      }
+    };
+    if (nt <= 1) {
+      work();
+    } else {
+      std::vector<std::thread> th;
+      for (int t = 0; t < nt; t++) th.emplace_back(work);
+      for (auto &t : th) t.join();
+    }
+  }
+  CU(cudaMemcpyAsync(e->d_arena, e->h_arena, e->arena_bytes, cudaMemcpyHostToDevice, e->stream));
+  // device view
+  char *D = (char *)e->d_arena;
+  char *X = (char *)e->d_scratch;
+  DevBatch &db = e->db;
+  db.jobs = (const JobHdr *)(D + e->s_jobs.off);
+  db.order = (const int32_t *)(D + e->s_order.off);
+  db.ranks = (const RankRec *)(D + e->s_ranks.off);
+  db.rank_comm = (const uint32_t *)(D + e->s_rank_comm.off);
+  db.comms = (const CommRec *)(D + e->s_comms.off);
+  db.slots = (const SlotRec *)(D + e->s_slots.off);
+  db.walkers = (const Walker *)(D + e->s_walkers.off);
+  db.reps = (const RepHdr *)(D + e->s_reps.off);
+  db.ops = (const Op *)(D + e->s_ops.off);
+  db.streams = (const StreamRange *)(D + e->s_streams.off);
+  db.coll_lc = (const uint32_t *)(D + e->s_coll_lc.off);
+  db.coll_idx = (const uint32_t *)(D + e->s_coll_idx.off);
+  db.syncs = (const SyncRec *)(D + e->s_syncs.off);
+  db.counts = (const uint32_t *)(D + e->s_counts.off);
+  db.mems = (const MemRec *)(D + e->s_mems.off);
+  db.feats = (const Feature *)(D + e->s_feats.off);
+  db.feat_ns = (int64_t *)(X + e->x_feat_ns.off);
+  db.wire = (int64_t *)(X + e->x_wire.off);
+  db.fire = (int64_t *)(X + e->x_fire.off);
+  db.delay = (int64_t *)(X + e->x_delay.off);
+  db.wstate = (WState *)(X + e->x_wstate.off);
+  db.cslots = (CollSlot *)(X + e->x_cslots.off);
+  db.repout = (RepOut *)(X + e->x_repout.off);
+  db.results = (maya_job_result *)(X + e->x_results.off);
+  db.err_flag = (int32_t *)(X + e->x_err.off);
+  db.tl_start = nullptr;
+  db.tl_end = nullptr;
+  db.n_jobs = (uint32_t)nj;
+  db.n_reps = (uint32_t)n_reps;
+  db.n_feats = (uint32_t)n_feats;
+  db.n_slots = (uint32_t)n_slots;
+  // estimator tables
+  DevTables &t = e->tables;
+  memset(&t, 0, sizeof t);
+  t.n_devs = (int32_t)e->devs.size();
+  for (size_t i = 0; i < e->devs.size(); i++) t.devs[i] = e->devs[i];
+  t.n_op_kinds = (int32_t)e->eff_num.size();
+  for (size_t i = 0; i < e->eff_num.size(); i++) {
+    t.eff_num[i] = e->eff_num[i];
+    t.eff_den[i] = e->eff_den[i];
+  }
+  t.overhead_ns = e->overhead_ns;
+  for (size_t j = 0; j < nj; j++) {
+    const JobPack &P = e->packs[j];
+    if (P.hdr.status == MAYA_ST_OK && (int)P.hdr.device >= t.n_devs && !P.feats.empty())
+      return fail(MAYA_EINVAL, "job references a device class that was not set");
+  }
+  e->uploaded = true;
+  e->ran = false;
+  return MAYA_OK;
+}
+
+int maya_run(maya_engine *e, int32_t record_timeline) {
+  if (!e->uploaded) return fail(MAYA_ESTATE, "maya_run before maya_upload");
+  CU(cudaSetDevice(e->device));
+  DevBatch db = e->db;
+  if (record_timeline) {
+    size_t need = e->scratch_bytes + align_up(e->n_tl * 8, 256) * 2;
+    if (need > e->d_scratch_cap) {
+      // grow scratch, keeping the layout (scratch contents are rebuilt per run)
+      void *p = nullptr;
+      CU(cudaStreamSynchronize(e->stream));
+      CU(cudaMalloc(&p, need));
+      cudaFree(e->d_scratch);
+      e->d_scratch = p;
+      e->d_scratch_cap = need;
+      char *X = (char *)p;
+      db.feat_ns = (int64_t *)(X + e->x_feat_ns.off);
+      db.wire = (int64_t *)(X + e->x_wire.off);
+      db.fire = (int64_t *)(X + e->x_fire.off);
+      db.delay = (int64_t *)(X + e->x_delay.off);
+      db.wstate = (WState *)(X + e->x_wstate.off);
+      db.cslots = (CollSlot *)(X + e->x_cslots.off);
+      db.repout = (RepOut *)(X + e->x_repout.off);
+      db.results = (maya_job_result *)(X + e->x_results.off);
+      db.err_flag = (int32_t *)(X + e->x_err.off);
+      e->db = db;
+    }
+    char *X = (char *)e->d_scratch;
+    db.tl_start = (int64_t *)(X + e->scratch_bytes);
+    db.tl_end = (int64_t *)(X + e->scratch_bytes + align_up(e->n_tl * 8, 256));
+    e->db.tl_start = db.tl_start;
+    e->db.tl_end = db.tl_end;
+  }
+  char *X = (char *)e->d_scratch;
+  CU(cudaEventRecord(e->ev[0], e->stream));
+  CU(cudaMemsetAsync(X + e->x_err.off, 0, 16, e->stream));
+  launch_estimate(db, e->tables, e->stream);
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(e->ev[1], e->stream));
+  CU(cudaMemsetAsync(X + e->x_fire.off, 0xff, e->x_fire.bytes, e->stream));
+  CU(cudaMemsetAsync(X + e->x_cslots.off, 0, e->x_cslots.bytes, e->stream));
+  launch_memscan(db, e->stream);
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(e->ev[2], e->stream));
+  launch_schedule(db, record_timeline ? 1 : 0, e->stream);
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(e->ev[3], e->stream));
+  e->ran = true;
+  e->recorded = record_timeline != 0;
+  return MAYA_OK;
+}
+
+int maya_results(maya_engine *e, maya_job_result *out) {
+  if (!e->ran) return fail(MAYA_ESTATE, "maya_results before maya_run");
+  CU(cudaSetDevice(e->device));
+  const size_t nj = e->packs.size();
+  int32_t err_flag = 0;
+  CU(cudaMemcpyAsync(out, e->db.results, nj * sizeof(maya_job_result), cudaMemcpyDeviceToHost,
+                     e->stream));
+  CU(cudaMemcpyAsync(&err_flag, e->db.err_flag, sizeof err_flag, cudaMemcpyDeviceToHost,
+                     e->stream));
+  CU(cudaStreamSynchronize(e->stream));
+  cudaEventElapsedTime(&e->last_ms[0], e->ev[0], e->ev[1]);
+  cudaEventElapsedTime(&e->last_ms[1], e->ev[1], e->ev[2]);
+  cudaEventElapsedTime(&e->last_ms[2], e->ev[2], e->ev[3]);
+  if (err_flag) {
+    // Estimation errors are raised by annotate() for ANY event, before the
+    // simulation (estimate.py:344-347): attribute failed features to jobs.
+    std::vector<int64_t> fns(e->db.n_feats), wns(e->db.n_slots);
+    CU(cudaMemcpy(fns.data(), e->db.feat_ns, fns.size() * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(wns.data(), e->db.wire, wns.size() * 8, cudaMemcpyDeviceToHost));
+    size_t fb = 0, sb = 0;
+    for (size_t j = 0; j < nj; j++) {
+      const JobPack &P = e->packs[j];
+      bool bad = false;
+      for (size_t f = 0; f < P.feats.size(); f++) bad |= fns[fb + f] < 0;
+      for (size_t s = 0; s < P.slots.size(); s++) bad |= wns[sb + s] < 0;
+      if (bad && out[j].status == MAYA_ST_OK) out[j].status = MAYA_ST_ESTIMATION;
+      if (bad && out[j].status == MAYA_ST_DEADLOCK) out[j].status = MAYA_ST_ESTIMATION;
+      fb += P.feats.size();
+      sb += P.slots.size();
+    }
+  }
+  return MAYA_OK;
+}
+
+int maya_last_timings(maya_engine *e, float *ms3) {
+  for (int i = 0; i < 3; i++) ms3[i] = e->last_ms[i];
+  return MAYA_OK;
+}
+
+int maya_topk(maya_engine *e, int32_t k, maya_topk_entry *out, int32_t *n_out) {
+  if (!e->ran) return fail(MAYA_ESTATE, "maya_topk before maya_run");
+  if (k < 1 || k > 64) return fail(MAYA_EINVAL, "k must be in [1, 64]");
+  CU(cudaSetDevice(e->device));
+  char *X = (char *)e->d_scratch;
+  maya_topk_entry *d_out = (maya_topk_entry *)(X + e->x_topk_out.off);
+  int32_t *d_n = (int32_t *)(X + e->x_topk_n.off);
+  launch_topk(e->db, k, d_out, d_n, X + e->x_topk.off, e->stream);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(n_out, d_n, sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
+  CU(cudaMemcpyAsync(out, d_out, k * sizeof(maya_topk_entry), cudaMemcpyDeviceToHost, e->stream));
+  CU(cudaStreamSynchronize(e->stream));
+  return MAYA_OK;
+}
+
+int maya_timeline_size(maya_engine *e, int32_t job, int64_t *n) {
+  if (job < 0 || (size_t)job >= e->packs.size()) return fail(MAYA_EINVAL, "job index");
+  *n = e->packs[job].hdr.dev_ops;
+  return MAYA_OK;
+}
+
+int maya_timeline(maya_engine *e, int32_t job, int32_t *rank, int32_t *stream, int32_t *seq,
+                  int64_t *start, int64_t *end) {
+  if (!e->recorded) return fail(MAYA_ESTATE, "no timeline recorded");
+  if (job < 0 || (size_t)job >= e->packs.size()) return fail(MAYA_EINVAL, "job index");
+  CU(cudaSetDevice(e->device));
+  const JobPack &P = e->packs[job];
+  const uint64_t n = (uint64_t)P.hdr.dev_ops;
+  if (n) {
+    CU(cudaMemcpyAsync(start, e->db.tl_start + e->job_tl[job], n * 8, cudaMemcpyDeviceToHost,
+                       e->stream));
+    CU(cudaMemcpyAsync(end, e->db.tl_end + e->job_tl[job], n * 8, cudaMemcpyDeviceToHost,
+                       e->stream));
+  }
+  CU(cudaStreamSynchronize(e->stream));
+  uint64_t t = 0;
+  for (size_t r = 0; r < P.ranks.size(); r++) {
+    const RepHdr &h = P.reps[P.ranks[r].rep];
+    for (uint32_t s = 0; s < h.n_streams; s++) {
+      const StreamRange &sr = P.streams[h.streams + s];
+      for (uint32_t i = 0; i < sr.len; i++, t++) {
+        rank[t] = (int32_t)r;
+        stream[t] = sr.raw;
+        const uint64_t o = h.ops + sr.begin + i;
+        // tag in high bits of seq: (seq << 2) | tag so callers can filter timed ops
+        seq[t] = (int32_t)((P.op_seq[o] << 2) | op_tag(P.ops[o].meta));
+      }
+    }
+  }
+  return MAYA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,35 @@
+// Host-side ingestion: raw job (reference schema as arrays) -> device SoA.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "../../include/maya_b200.h"
+#include "soa.h"
+
+namespace maya {
+
+// Everything one job contributes to a batch; all indices are job-local.
+struct JobPack {
+  JobHdr hdr{};
+  std::vector<RepHdr> reps;
+  std::vector<Op> ops;
+  std::vector<uint32_t> op_seq;        // event seq of each op (timeline)
+  std::vector<StreamRange> streams;
+  std::vector<uint32_t> coll_lc, coll_idx;
+  std::vector<SyncRec> syncs;
+  std::vector<uint32_t> counts;
+  std::vector<MemRec> mems;
+  std::vector<Feature> feats;
+  std::vector<CommRec> comms;
+  std::vector<SlotRec> slots;
+  std::vector<RankRec> ranks;
+  std::vector<uint32_t> rank_comm;
+  std::vector<Walker> walkers;
+  uint64_t n_fire = 0, n_delay = 0;
+  std::string message;                 // why status != OK
+};
+
+// Pack one job.  Never throws; input problems become hdr.status + message.
+void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &out);
+
+}  // namespace maya

@@ -1,0 +1,179 @@
+"""Python handle on the CUDA engine (libmaya_b200.so, C ABI in include/maya_b200.h).
+
+There is no CPU fallback: if the extension is missing or no CUDA device is
+usable, construction raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Mapping, Sequence
+
+import numpy as np
+
+from ._abi import (Batch, DeviceParamsC, JobResultC, RawJobC, RooflineC, TopkEntryC,
+                   RESULT_DTYPE, TOPK_DTYPE, DEFAULT_KERNEL_OVERHEAD_NS)
+from .rawtrace import RawJob
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmaya_b200.so")
+_lib = None
+
+EXPORTED = (
+    "maya_last_error", "maya_abi_version", "maya_open", "maya_close", "maya_batch_reset",
+    "maya_batch_set_devices", "maya_batch_set_roofline", "maya_batch_add_job",
+    "maya_batch_add_jobs", "maya_batch_num_jobs", "maya_upload", "maya_run", "maya_results",
+    "maya_topk", "maya_timeline_size", "maya_timeline", "maya_last_timings",
+)
+
+
+class EngineError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load the in-tree extension; raise loudly if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise EngineError(f"CUDA extension {LIB_PATH} is missing: run `python __graft_entry__.py` "
+                          f"(build) or `make -C paper_2503_20191_b200/csrc`")
+    L = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    vp = C.c_void_p
+    L.maya_last_error.restype = C.c_char_p
+    L.maya_open.argtypes = [C.c_int, P(vp)]
+    L.maya_close.argtypes = [vp]
+    L.maya_batch_reset.argtypes = [vp]
+    L.maya_batch_set_devices.argtypes = [vp, C.c_int32, P(DeviceParamsC)]
+    L.maya_batch_set_roofline.argtypes = [vp, P(RooflineC)]
+    L.maya_batch_add_job.argtypes = [vp, P(RawJobC), C.c_int32]
+    L.maya_batch_add_jobs.argtypes = [vp, C.c_int32, P(RawJobC), P(C.c_int32), C.c_int32]
+    L.maya_batch_num_jobs.argtypes = [vp]
+    L.maya_upload.argtypes = [vp]
+    L.maya_run.argtypes = [vp, C.c_int32]
+    L.maya_results.argtypes = [vp, P(JobResultC)]
+    L.maya_topk.argtypes = [vp, C.c_int32, P(TopkEntryC), P(C.c_int32)]
+    L.maya_timeline_size.argtypes = [vp, C.c_int32, P(C.c_int64)]
+    L.maya_timeline.argtypes = [vp, C.c_int32, P(C.c_int32), P(C.c_int32), P(C.c_int32),
+                                P(C.c_int64), P(C.c_int64)]
+    L.maya_last_timings.argtypes = [vp, P(C.c_float)]
+    _lib = L
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise EngineError(f"maya error {rc}: {lib().maya_last_error().decode()}")
+
+
+@dataclass
+class Timeline:
+    rank: np.ndarray
+    stream: np.ndarray
+    seq: np.ndarray
+    tag: np.ndarray       # 0 kernel-class, 1 collective, 2 record, 3 wait
+    start: np.ndarray
+    end: np.ndarray
+
+    def timed(self) -> "Timeline":
+        """Only the ops the reference records (kernels and collectives, sim.py:375)."""
+        m = self.tag <= 1
+        return Timeline(self.rank[m], self.stream[m], self.seq[m], self.tag[m], self.start[m],
+                        self.end[m])
+
+
+class Engine:
+    """One engine per CUDA device (C ABI: maya_open ... maya_close)."""
+
+    def __init__(self, device: int = 0):
+        L = lib()
+        self._h = C.c_void_p()
+        _check(L.maya_open(int(device), C.byref(self._h)))
+        self.device = device
+        self.batch: Batch | None = None
+        self.n_jobs = 0
+
+    def close(self) -> None:
+        if self._h:
+            lib().maya_close(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- batch ------------------------------------------------------------------
+
+    def load(self, jobs: Sequence[RawJob] | Batch, efficiency: Mapping[str, float] | None = None,
+             overhead_ns: int = DEFAULT_KERNEL_OVERHEAD_NS,
+             key_ranks: Sequence[int] | None = None, threads: int = 8) -> None:
+        """Pack jobs (host, multi-threaded) and upload them to HBM."""
+        b = jobs if isinstance(jobs, Batch) else Batch(jobs, efficiency, overhead_ns)
+        self.stage(b, key_ranks, threads)
+        self.upload()
+
+    def stage(self, b: Batch, key_ranks: Sequence[int] | None = None, threads: int = 8) -> None:
+        L = lib()
+        self.batch = b
+        n = len(b.jobs)
+        _check(L.maya_batch_reset(self._h))
+        _check(L.maya_batch_set_devices(self._h, len(b.devices), b.c_devices))
+        _check(L.maya_batch_set_roofline(self._h, C.byref(b.c_roof)))
+        kr = (np.arange(n, dtype=np.int32) if key_ranks is None
+              else np.ascontiguousarray(key_ranks, dtype=np.int32))
+        _check(L.maya_batch_add_jobs(self._h, n, b.c_jobs, kr.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     int(threads)))
+        self.n_jobs = n
+
+    def upload(self) -> None:
+        _check(lib().maya_upload(self._h))
+
+    def run(self, record_timeline: bool = False) -> None:
+        _check(lib().maya_run(self._h, 1 if record_timeline else 0))
+
+    def results(self) -> np.ndarray:
+        out = np.zeros(self.n_jobs, dtype=RESULT_DTYPE)
+        _check(lib().maya_results(self._h, out.ctypes.data_as(C.POINTER(JobResultC))))
+        return out
+
+    def simulate(self, jobs: Sequence[RawJob] | Batch, record_timeline: bool = False,
+                 **kw) -> np.ndarray:
+        self.load(jobs, **kw)
+        self.run(record_timeline)
+        return self.results()
+
+    def topk(self, k: int) -> np.ndarray:
+        out = np.zeros(k, dtype=TOPK_DTYPE)
+        n = C.c_int32()
+        _check(lib().maya_topk(self._h, int(k), out.ctypes.data_as(C.POINTER(TopkEntryC)),
+                               C.byref(n)))
+        return out[:n.value]
+
+    def timeline(self, job: int) -> Timeline:
+        L = lib()
+        n = C.c_int64()
+        _check(L.maya_timeline_size(self._h, int(job), C.byref(n)))
+        n = n.value
+        rank = np.zeros(max(n, 1), np.int32)
+        stream = np.zeros(max(n, 1), np.int32)
+        seq = np.zeros(max(n, 1), np.int32)
+        start = np.zeros(max(n, 1), np.int64)
+        end = np.zeros(max(n, 1), np.int64)
+        P = C.POINTER
+        _check(L.maya_timeline(self._h, int(job), rank.ctypes.data_as(P(C.c_int32)),
+                               stream.ctypes.data_as(P(C.c_int32)),
+                               seq.ctypes.data_as(P(C.c_int32)),
+                               start.ctypes.data_as(P(C.c_int64)),
+                               end.ctypes.data_as(P(C.c_int64))))
+        return Timeline(rank[:n], stream[:n], seq[:n] >> 2, seq[:n] & 3, start[:n], end[:n])
+
+    def last_timings_ms(self) -> tuple[float, float, float]:
+        t = (C.c_float * 3)()
+        _check(lib().maya_last_timings(self._h, t))
+        return tuple(t)
