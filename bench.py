@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 batched simulator on the BASELINE C2 workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): GPT-3 1.3B
+(24 x 2048, seq 2048, vocab 51200, bf16) on ClusterSpec(1, 8, 80 GiB, "fast"),
+the first 512 valid configs of enumerate_space(SearchSpace(global_batch=512)),
+5 us dispatch gaps, RooflineEstimator.  One STEP = evaluate the whole
+512-config batch: kernel-roofline + alpha-beta estimators, memory scan,
+max-plus scheduler, and the fused top-k search reduction.  Under torchrun
+each rank evaluates its own 512-config search (weak scaling): rank r uses
+global_batch 512 * 2**r (identical lattice validity, same op counts), and the
+per-rank top-k candidates are merged with one NCCL all_gather.
+
+value  = configs/s with traces resident in HBM (CUDA events, L2 flushed
+         between timed steps by a 256 MiB write on the engine stream).
+e2e    = configs/s through the C ABI from the config list: native trace
+         generation + SoA packing (host, C++ threads), H2D of the arena,
+         kernels, D2H of results and the top-k.
+Reference arm: the CPU oracle port (oracle/: native generator + C++
+restatement of the reference's event-driven simulator) on all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_CONFIGS = 512
+TOPK = 8
+MODEL = ("gpt3-1.3b", 24, 2048, 2048, 51200, "bf16")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--threads", type=int, default=0, help="host threads (0 = all)")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def workload(rank: int):
+    from paper_2503_20191_b200 import workload as W
+    model = W.ModelSpec(*MODEL)
+    cluster = W.ClusterSpec(1, 8, 80 * 2 ** 30, W.load_device_preset("fast"))
+    gb = 512 * (2 ** rank)
+    configs = W.enumerate_space(W.SearchSpace(global_batch=gb), model, cluster)[:N_CONFIGS]
+    return model, cluster, configs
+
+
+def key_ranks(configs):
+    order = sorted(range(len(configs)), key=lambda i: configs[i].key())
+    kr = [0] * len(configs)
+    for pos, i in enumerate(order):
+        kr[i] = pos
+    return kr
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 9:
+                rows.append(p)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows)
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def load_golden_c2():
+    path = os.path.join(REPO, "tests", "golden", "c2_results.json")
+    with open(path) as f:
+        return json.load(f)
+
+
+def parity_c2(configs, res) -> dict:
+    """Rank-0 batch against the reference's own C2 results (tests/golden)."""
+    gold = {tuple(r["key"]): r for r in load_golden_c2()}
+    bad = 0
+    for cfg, r in zip(configs, res):
+        g = gold[tuple(cfg.key())]
+        if (int(r["status"]) != 0 or int(r["total_ns"]) != g["total_ns"]
+                or int(r["peak_mem_bytes"]) != g["peak_mem_bytes"] or bool(r["oom"]) != g["oom"]):
+            bad += 1
+    ok = [g for g in gold.values() if not g["oom"]]
+    ok.sort(key=lambda g: (g["total_ns"], tuple(g["key"])))
+    return {"checked": len(configs), "mismatches": bad, "reference_best": ok[0]["key"],
+            "reference_best_ns": ok[0]["total_ns"]}
+
+
+def cpu_baseline(model, cluster, configs, seconds: float, threads: int) -> dict:
+    """Oracle port (native generator + C++ restatement of sim.py) on host cores."""
+    from oracle import oracle
+    from paper_2503_20191_b200 import workload as W
+    import numpy as np
+    jobs, t_gen = [], 0.0
+    t0 = time.perf_counter()
+    for cfg in configs:
+        jobs.append(W.generate_job(model, cfg, cluster, dispatch_overhead_ns=5000))
+        if time.perf_counter() - t0 > seconds / 3:
+            break
+    t_gen = time.perf_counter() - t0
+    from paper_2503_20191_b200._abi import Batch
+    b = Batch(jobs)
+    t1 = time.perf_counter()
+    reps = 0
+    while True:
+        oracle.simulate_many(jobs, threads=threads, batch=b)
+        reps += 1
+        if time.perf_counter() - t1 > seconds * 2 / 3:
+            break
+    t_sim = (time.perf_counter() - t1) / reps
+    n = len(jobs)
+    rank_ops = sum(j.rank_ops() for j in jobs)
+    per_cfg = t_gen / n + t_sim / n
+    return {"value": round(1.0 / per_cfg, 2), "unit": "configs/s", "cores": threads,
+            "kind": "port",
+            "sample": f"first {n} of the {len(configs)} C2 configs: native generation "
+                      f"(1 thread, {t_gen:.2f}s) + oracle annotate+simulate "
+                      f"({threads} threads, {t_sim:.3f}s per pass, {reps} passes)",
+            "sim_only_configs_per_s": round(n / t_sim, 2),
+            "sim_only_rank_ops_per_s": round(rank_ops / t_sim, 1)}
+
+
+def bench_reference(args):
+    """--impl reference: the CPU port of the reference path, rank 0 only."""
+    import torch  # noqa: F401  (torchrun parity with our arm)
+    rank = int(os.environ.get("RANK", "0"))
+    n = args.gpus
+    if rank != 0:
+        return
+    from oracle import oracle
+    from paper_2503_20191_b200 import workload as W
+    from paper_2503_20191_b200._abi import Batch
+    threads = args.threads or host_threads()
+    model, cluster, configs = workload(0)
+
+    def step():
+        t0 = time.perf_counter()
+        jobs = [W.generate_job(model, c, cluster, dispatch_overhead_ns=5000) for c in configs]
+        res = oracle.simulate_many(jobs, threads=threads, batch=Batch(jobs))
+        return time.perf_counter() - t0, res, jobs
+
+    for _ in range(max(0, args.warmup)):
+        step()
+    times = []
+    rank_ops = 0
+    for _ in range(args.steps):
+        dt, res, jobs = step()
+        times.append(dt)
+        rank_ops = int(res["rank_ops"].sum())
+    ms = 1000 * sum(times) / len(times)
+    val = N_CONFIGS / (ms / 1000)
+    line = {
+        "impl": "reference", "metric": "simulated configs/sec", "value": round(val, 3),
+        "unit": "configs/s", "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": "C2: GPT-3 1.3B, 512 configs x 8 ranks (rank 0's batch)"},
+        "trace_ops_per_s": round(rank_ops / (ms / 1000), 1),
+        "cpu_baseline": {"value": round(val, 3), "unit": "configs/s", "cores": threads,
+                         "kind": "port",
+                         "sample": "full 512-config C2 batch per step: native generator "
+                                   "(1 thread) + oracle/sim_oracle.cpp annotate+simulate "
+                                   f"({threads} threads)"},
+        "e2e": {"value": round(val, 3), "unit": "configs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the scheduler from the committed ncu summary."""
+    path = os.path.join(REPO, "profiles", "schedule_kernel_ncu.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def bench_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2503_20191_b200.engine import Engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    threads = args.threads or max(1, host_threads() // max(1, world))
+
+    model, cluster, configs = workload(rank)
+    kr = key_ranks(configs)
+    eng = Engine(local)
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
+    st = eng.stage_generated(model, configs, cluster, dispatch_overhead_ns=5000, key_ranks=kr,
+                             threads=threads)
+    assert (st == 0).all(), "invalid configs in the C2 lattice"
+    stats = eng.batch_stats()
+    eng.upload()
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        eng.run()
+        return eng.topk(TOPK)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    res = eng.results()
+    parity = parity_c2(configs, res) if rank == 0 else None
+
+    # --- device-resident throughput -------------------------------------------------
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    sched_ms = []
+    top = None
+    for i in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xff)          # L2 flush, outside the timed window
+            ev[i][0].record(stream)
+        top = step()
+        ev[i][1].record(stream)
+        sched_ms.append(eng.last_timings_ms()[2])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    clocks = sampler.stop()
+    ms = sum(step_ms) / len(step_ms)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # search reduction across GPUs: all_gather of k x 16 B candidates (NCCL)
+    cand = np.zeros((TOPK, 2), dtype=np.int64)
+    for q, e in enumerate(top):
+        cand[q] = (int(e["time_ns"]), (rank << 32) | int(e["key_rank"]))
+    for q in range(len(top), TOPK):
+        cand[q] = (np.iinfo(np.int64).max, -1)
+    ct = torch.from_numpy(cand).to(dev)
+    if world > 1:
+        gathered = [torch.empty_like(ct) for _ in range(world)]
+        dist.all_gather(gathered, ct)
+        allc = torch.cat(gathered).cpu().numpy()
+    else:
+        allc = cand
+    order = np.lexsort((allc[:, 1], allc[:, 0]))
+    best = allc[order[0]]
+    best_rank, best_kr = int(best[1]) >> 32, int(best[1]) & 0xffffffff
+
+    # --- end to end through the C ABI with host buffers -------------------------------
+    e2e_steps = args.e2e_steps or args.steps
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for i in range(e2e_steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.stage_generated(model, configs, cluster, dispatch_overhead_ns=5000, key_ranks=kr,
+                            threads=threads)
+        eng.upload()
+        eng.run()
+        r = eng.results()
+        eng.topk(TOPK)
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    torch.cuda.synchronize()
+    e = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    e2e_ms_max = float(e.item())
+
+    if rank == 0:
+        n_total = N_CONFIGS * world
+        value = n_total / (ms_max / 1000)
+        rank_ops = stats["rank_ops"]
+        # algorithmic bytes of one scheduler launch
+        alg_bytes = (16 * stats["rep_events"] + 4 * stats["rank_comms"]
+                     + 16 * (stats["features"] + stats["slots"]) + 24 * stats["jobs"])
+        sched = statistics.median(sched_ms)
+        peak, peak_kind = measured_peak_hbm()
+        achieved = alg_bytes / (sched / 1000) / 1e9
+        line = {
+            "metric": "simulated configs/sec", "value": round(value, 2), "unit": "configs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic: native restatement of the reference trace generator "
+                    "(event-for-event identical, tests/test_gen.py)",
+            "config": {"workload": "C2: GPT-3 1.3B (24x2048, seq 2048, vocab 51200) on 1x8 "
+                                   "'fast' 80 GiB; enumerate_space(SearchSpace(global_batch="
+                                   "512*2**rank))[:512]; 5 us gaps; RooflineEstimator",
+                       "configs_per_gpu": N_CONFIGS, "ranks_per_config": 8,
+                       "rank_ops_per_gpu": rank_ops, "topk": TOPK,
+                       "l2": "flushed between timed steps (256 MiB write on the engine stream)",
+                       "parallelism": f"config-sharded x{world}"},
+            "trace_ops_per_s": round(rank_ops * world / (ms_max / 1000), 1),
+            "e2e": {"value": round(n_total / (e2e_ms_max / 1000), 2), "unit": "configs/s",
+                    "ms_per_step": round(e2e_ms_max, 3),
+                    "h2d_bytes_per_step": int(stats["arena_bytes"]),
+                    "d2h_bytes_per_step": int(N_CONFIGS * 64 + TOPK * 16),
+                    "path": "config list -> native gen+pack (C++ threads) -> H2D -> kernels "
+                            "-> D2H results + top-k"},
+            "roofline": {"bound": "hbm", "kernel": "schedule_kernel",
+                         "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 5), "traffic": ncu_traffic(),
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel_ms": round(sched, 4), "peak_source": peak_kind,
+                         "note": "C2 is latency-bound (dedup makes compulsory bytes << work)"},
+            "clocks": clocks,
+            "gpu_launches": 6 * args.steps,
+            "best": {"rank": best_rank, "key_rank": best_kr, "time_ns": int(best[0])},
+            "parity": parity,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(model, cluster, configs, args.cpu_seconds,
+                                                host_threads())
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -151,8 +151,75 @@ int maya_timeline_size(maya_engine *eng, int32_t job, int64_t *n);
 int maya_timeline(maya_engine *eng, int32_t job, int32_t *rank, int32_t *stream,
                   int32_t *seq, int64_t *start, int64_t *end);
 
+/* The engine's CUDA stream (cudaStream_t) so callers can time on it. */
+int maya_get_stream(maya_engine *eng, void **stream);
+
+/* Bytes of the staged SoA arena (what maya_upload copies host -> device). */
+int64_t maya_arena_bytes(maya_engine *eng);
+
+/* Batch totals of the staged batch: [0] jobs, [1] sum of rep trace events,
+ * [2] sum over ranks of rep CommInits, [3] kernel features, [4] group-call
+ * slots, [5] device ops (stream-major records), [6] rank-ops, [7] arena bytes,
+ * [8] ranks, [9] reps. */
+int maya_batch_stats(maya_engine *eng, int64_t *out10);
+
 /* Device time of the last maya_run, per phase (ms): estimate, memscan, schedule. */
 int maya_last_timings(maya_engine *eng, float *ms3);
+
+/* ---- native trace generation (workload.py frontend + collate.py) -------- */
+
+/* ModelSpec (workload.py:96-128); dtype 0 bf16, 1 fp16, 2 fp32. */
+typedef struct maya_model {
+  int64_t num_layers, hidden_size, seq_len, vocab_size;
+  int32_t dtype;
+  int32_t pad;
+} maya_model;
+
+/* ConfigPoint (workload.py:131-165). */
+typedef struct maya_config {
+  int32_t tp, pp, micro_mult, virtual_stages;
+  int32_t act_recompute, seq_parallel, dist_optimizer;
+  int32_t pad;
+  int64_t global_batch;
+} maya_config;
+
+/* ClusterSpec (cluster.py:62-92) without the device class. */
+typedef struct maya_cluster {
+  int32_t num_hosts, devices_per_host;
+  int64_t device_memory_bytes;
+} maya_cluster;
+
+/* schedule: -1 default_schedule (workload.py:218-221), 0 gpipe, 1 1f1b, 2 interleaved */
+typedef struct maya_gen maya_gen;
+
+typedef struct maya_gen_view {
+  maya_raw_job job;        /* device = 0; kernel_ns = wire_ns = NULL */
+  int32_t num_hosts;
+  int32_t n_comm_names;
+  const int64_t *rep_ranks;
+  const char *comm_names;  /* n_comm_names names joined by '\n' (sorted, = JobTrace.groups) */
+  int64_t n_events;
+  int64_t n_calls;
+  int64_t n_rank_comm;
+} maya_gen_view;
+
+/* Op-kind / dtype id tables used by generated jobs' ev_f. */
+const char *maya_gen_op_kind_name(int32_t id);
+const char *maya_gen_dtype_name(int32_t id);
+
+int maya_gen_job(const maya_model *model, const maya_config *cfg, const maya_cluster *cluster,
+                 int32_t schedule, int64_t dispatch_overhead_ns, maya_gen **out);
+int maya_gen_view_of(const maya_gen *g, maya_gen_view *view);
+int maya_gen_free(maya_gen *g);
+
+/* Generate + pack n configs straight into the engine batch (no host round
+ * trip through arrays).  status_out[i] receives 0 or MAYA_EINVAL for an
+ * invalid configuration (ConfigError, workload.py:168-208); such jobs are
+ * staged with status MAYA_ST_BAD_INPUT. */
+int maya_batch_add_generated(maya_engine *eng, const maya_model *model, int32_t n,
+                             const maya_config *cfgs, const maya_cluster *cluster,
+                             int32_t device, int32_t schedule, int64_t dispatch_overhead_ns,
+                             const int32_t *key_ranks, int32_t n_threads, int32_t *status_out);
 
 #ifdef __cplusplus
 }

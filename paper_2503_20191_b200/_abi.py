@@ -102,6 +102,10 @@ class Batch:
         self._dt_id: dict[str, int] = {}
         self._keep: list = []
         self.devices: list = []
+        # generated jobs use fixed id tables (csrc/gen.cpp): intern them first
+        from .workload import GEN_DTYPES, GEN_OP_KINDS
+        self._intern(GEN_OP_KINDS, self.op_kinds, self._op_id)
+        self._intern(GEN_DTYPES, self.dtypes, self._dt_id)
         self._dev_id: dict = {}
         self.c_jobs = (RawJobC * len(self.jobs))()
         for i, job in enumerate(self.jobs):

@@ -12,6 +12,7 @@
 
 #include "../../include/maya_b200.h"
 #include "kernels.cuh"
+#include "gen.h"
 #include "pack.h"
 
 using namespace maya;
@@ -513,6 +514,30 @@ int maya_results(maya_engine *e, maya_job_result *out) {
   return MAYA_OK;
 }
 
+int maya_get_stream(maya_engine *e, void **stream) {
+  *stream = (void *)e->stream;
+  return MAYA_OK;
+}
+
+int64_t maya_arena_bytes(maya_engine *e) { return (int64_t)e->arena_bytes; }
+
+int maya_batch_stats(maya_engine *e, int64_t *o) {
+  for (int i = 0; i < 10; i++) o[i] = 0;
+  o[0] = (int64_t)e->packs.size();
+  for (const JobPack &P : e->packs) {
+    for (const RepHdr &h : P.reps) o[1] += h.n_events;
+    o[2] += (int64_t)P.rank_comm.size();
+    o[3] += (int64_t)P.feats.size();
+    o[4] += (int64_t)P.slots.size();
+    o[5] += (int64_t)P.ops.size();
+    o[6] += P.hdr.rank_ops;
+    o[8] += (int64_t)P.ranks.size();
+    o[9] += (int64_t)P.reps.size();
+  }
+  o[7] = (int64_t)e->arena_bytes;
+  return MAYA_OK;
+}
+
 int maya_last_timings(maya_engine *e, float *ms3) {
   for (int i = 0; i < 3; i++) ms3[i] = e->last_ms[i];
   return MAYA_OK;
@@ -567,6 +592,89 @@ int maya_timeline(maya_engine *e, int32_t job, int32_t *rank, int32_t *stream, i
       }
     }
   }
+  return MAYA_OK;
+}
+
+// ---- native generation ----------------------------------------------------
+
+struct maya_gen {
+  GenJob job;
+};
+
+const char *maya_gen_op_kind_name(int32_t id) {
+  return (id >= 0 && id < 12) ? GEN_OP_KINDS[id] : nullptr;
+}
+const char *maya_gen_dtype_name(int32_t id) { return (id >= 0 && id < 3) ? GEN_DTYPES[id] : nullptr; }
+
+int maya_gen_job(const maya_model *model, const maya_config *cfg, const maya_cluster *cluster,
+                 int32_t schedule, int64_t dispatch_overhead_ns, maya_gen **out) {
+  maya_gen *g = new maya_gen();
+  std::string err;
+  int rc = generate_job(*model, *cfg, *cluster, schedule, dispatch_overhead_ns, g->job, &err);
+  if (rc != MAYA_OK) {
+    delete g;
+    return fail(rc, err);
+  }
+  *out = g;
+  return MAYA_OK;
+}
+
+int maya_gen_view_of(const maya_gen *g, maya_gen_view *v) {
+  memset(v, 0, sizeof *v);
+  v->job = g->job.raw(0);
+  v->num_hosts = g->job.num_hosts;
+  v->n_comm_names = (int32_t)g->job.comm_names.size();
+  v->rep_ranks = g->job.rep_ranks.data();
+  v->comm_names = g->job.comm_blob.c_str();
+  v->n_events = (int64_t)g->job.ev_kind.size();
+  v->n_calls = (int64_t)g->job.call_kind.size();
+  v->n_rank_comm = (int64_t)g->job.rank_comm.size();
+  return MAYA_OK;
+}
+
+int maya_gen_free(maya_gen *g) {
+  delete g;
+  return MAYA_OK;
+}
+
+int maya_batch_add_generated(maya_engine *e, const maya_model *model, int32_t n,
+                             const maya_config *cfgs, const maya_cluster *cluster, int32_t device,
+                             int32_t schedule, int64_t dispatch_overhead_ns,
+                             const int32_t *key_ranks, int32_t n_threads, int32_t *status_out) {
+  if (n < 0) return fail(MAYA_EINVAL, "negative job count");
+  if (device < 0 || device >= 8) return fail(MAYA_EINVAL, "device index out of range");
+  size_t base = e->packs.size();
+  e->packs.resize(base + n);
+  std::atomic<int> next(0);
+  auto work = [&]() {
+    GenJob g;
+    for (;;) {
+      int i = next.fetch_add(1);
+      if (i >= n) break;
+      std::string err;
+      int rc = generate_job(*model, cfgs[i], *cluster, schedule, dispatch_overhead_ns, g, &err);
+      if (status_out) status_out[i] = rc;
+      JobPack &P = e->packs[base + i];
+      if (rc != MAYA_OK) {
+        P = JobPack();
+        P.hdr.status = MAYA_ST_BAD_INPUT;
+        P.hdr.key_rank = key_ranks ? key_ranks[i] : i;
+        P.message = err;
+        continue;
+      }
+      maya_raw_job raw = g.raw(device);
+      pack_job(raw, key_ranks ? key_ranks[i] : i, P);
+    }
+  };
+  int nt = std::max(1, std::min<int>(n_threads, n));
+  if (nt == 1) {
+    work();
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; t++) th.emplace_back(work);
+    for (auto &t : th) t.join();
+  }
+  e->uploaded = e->ran = false;
   return MAYA_OK;
 }
 

@@ -1,0 +1,673 @@
+// Native restatement of the reference's synthetic frontend and collator:
+//   validate_config            pkg/src/dltsim/workload.py:168-208
+//   rank coords / comm ids     workload.py:226-278
+//   unique_workers             workload.py:281-298
+//   kernel inventory           workload.py:316-378 (_gemm, _elem, _layer_fwd_kernels,
+//                              _embed/_head_fwd_kernels, _bwd_of)
+//   memory model               workload.py:381-445
+//   pipeline_order             workload.py:450-505
+//   _TraceBuilder / generate_trace  workload.py:510-780
+//   collate (groups, calls, comm_map)  pkg/src/dltsim/collate.py:256-372
+//   topology_of                pkg/src/dltsim/cluster.py:79-92
+// Output is a raw job identical, event for event, to
+// rawtrace.from_reference(collate(*generate_representatives(...))) — checked
+// by tests/test_gen.py against the reference's own traces.
+#include "gen.h"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <unordered_map>
+
+namespace maya {
+
+const char *const GEN_OP_KINDS[12] = {"gemm", "layernorm", "softmax", "gelu", "add", "embed",
+                                      "cross_entropy", "optimizer_step", "memcpy_h2d",
+                                      "memcpy_d2h", "memcpy_d2d", "memset"};
+const char *const GEN_DTYPES[3] = {"bf16", "fp16", "fp32"};
+
+enum { OK_GEMM = 0, OK_LAYERNORM, OK_SOFTMAX, OK_GELU, OK_ADD, OK_EMBED, OK_CROSS_ENTROPY,
+       OK_OPTIMIZER, OK_MEMCPY_H2D, OK_MEMCPY_D2H, OK_MEMCPY_D2D, OK_MEMSET };
+enum { DT_FP32 = 2 };
+enum { K_ALLREDUCE = 0, K_ALLGATHER, K_REDUCESCATTER, K_BROADCAST, K_SENDRECV };
+enum { STREAM_COMPUTE = 0, STREAM_GRAD_COMM = 1, FIRST_P2P_STREAM = 2 };
+
+namespace {
+
+struct GenFail {
+  std::string msg;
+};
+
+typedef __int128 i128;
+
+inline int64_t chk(i128 v) {
+  if (v > (i128)INT64_MAX || v < -(i128)INT64_MAX) throw GenFail{"generated size overflows int64"};
+  return (int64_t)v;
+}
+
+// Python floor division for the (always non-negative) sizes used here.
+inline int64_t fdiv(i128 a, i128 b) {
+  i128 q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) q -= 1;
+  return chk(q);
+}
+
+struct KSpec {
+  int op;
+  int64_t flops, bytes;
+};
+
+KSpec gemm(i128 m, i128 n, i128 k, i128 esz) {  // workload.py:316-318
+  return KSpec{OK_GEMM, chk(2 * m * n * k), chk(esz * (m * k + k * n + m * n))};
+}
+KSpec elem(int op, i128 elems, i128 flops_per, i128 esz, i128 rw = 2) {  // :321-324
+  return KSpec{op, chk(flops_per * elems), chk(rw * elems * esz)};
+}
+
+struct Shape {
+  i128 s, h, v, esz, L;
+};
+
+std::vector<KSpec> layer_fwd(const Shape &M, i128 b, i128 tp, bool sp) {  // :327-348
+  const i128 s = M.s, h = M.h, esz = M.esz;
+  const i128 u = sp ? tp : 1;
+  std::vector<KSpec> ks;
+  ks.push_back(elem(OK_LAYERNORM, fdiv(b * s * h, u), 8, esz));
+  ks.push_back(gemm(b * s, fdiv(3 * h, tp), h, esz));
+  ks.push_back(KSpec{OK_GEMM, fdiv(2 * b * s * s * h, tp),
+                     chk(esz * (fdiv(2 * b * s * h, tp) + fdiv(b * s * s, tp)))});
+  ks.push_back(elem(OK_SOFTMAX, fdiv(b * s * s, tp), 5, esz));
+  ks.push_back(KSpec{OK_GEMM, fdiv(2 * b * s * s * h, tp),
+                     chk(esz * (fdiv(b * s * s, tp) + fdiv(2 * b * s * h, tp)))});
+  ks.push_back(gemm(b * s, h, fdiv(h, tp), esz));
+  ks.push_back(elem(OK_ADD, fdiv(b * s * h, u), 1, esz, 3));
+  ks.push_back(elem(OK_LAYERNORM, fdiv(b * s * h, u), 8, esz));
+  ks.push_back(gemm(b * s, fdiv(4 * h, tp), h, esz));
+  ks.push_back(elem(OK_GELU, fdiv(4 * b * s * h, tp), 8, esz));
+  ks.push_back(gemm(b * s, h, fdiv(4 * h, tp), esz));
+  ks.push_back(elem(OK_ADD, fdiv(b * s * h, u), 1, esz, 3));
+  return ks;
+}
+
+KSpec embed_fwd(const Shape &M, i128 b, i128 tp, bool sp) {  // :351-354
+  const i128 u = sp ? tp : 1;
+  return KSpec{OK_EMBED, 0, chk((i128)fdiv(b * M.s * M.h * M.esz, u) + b * M.s * 8)};
+}
+
+std::vector<KSpec> head_fwd(const Shape &M, i128 b, i128 tp, bool sp) {  // :357-364
+  const i128 u = sp ? tp : 1;
+  std::vector<KSpec> ks;
+  ks.push_back(elem(OK_LAYERNORM, fdiv(b * M.s * M.h, u), 8, M.esz));
+  ks.push_back(gemm(b * M.s, fdiv(M.v, tp), M.h, M.esz));
+  ks.push_back(elem(OK_CROSS_ENTROPY, fdiv(b * M.s * M.v, tp), 5, M.esz));
+  return ks;
+}
+
+std::vector<KSpec> bwd_of(const std::vector<KSpec> &fwd, size_t a, size_t e) {  // :367-378
+  std::vector<KSpec> out;
+  for (size_t q = e; q-- > a;) {
+    const KSpec &k = fwd[q];
+    if (k.op == OK_GEMM) {
+      out.push_back(k);
+      out.push_back(k);
+    } else {
+      out.push_back(KSpec{k.op, chk((i128)2 * k.flops), chk((i128)k.bytes + k.bytes / 2)});
+    }
+  }
+  return out;
+}
+
+i128 layer_stash_elems(const Shape &M, i128 b, i128 tp, bool sp, bool rc) {  // :381-387
+  const i128 s = M.s, h = M.h, u = sp ? tp : 1;
+  if (rc) return fdiv(b * s * h, u);
+  return (i128)fdiv(12 * b * s * h, tp) + fdiv(2 * b * s * s, tp) + fdiv(5 * b * s * h, u);
+}
+
+struct Chunk {
+  int64_t vs, layers;
+  bool has_embed, has_head;
+};
+
+std::vector<Chunk> device_chunks(const Shape &M, int p, int v, int stage) {  // :400-408
+  const int64_t total_vs = (int64_t)p * v;
+  const int64_t lpc = fdiv(M.L, total_vs);
+  std::vector<Chunk> out;
+  for (int c = 0; c < v; c++) {
+    int64_t vs = stage + (int64_t)c * p;
+    out.push_back(Chunk{vs, lpc, vs == 0, vs == total_vs - 1});
+  }
+  return out;
+}
+
+int64_t chunk_stash_bytes(const Shape &M, const maya_config &c, i128 b, const Chunk &ch) {
+  const i128 tp = c.tp, u = c.seq_parallel ? tp : 1;  // :411-420
+  i128 elems = (i128)ch.layers * layer_stash_elems(M, b, tp, c.seq_parallel, c.act_recompute);
+  if (ch.has_head && !c.act_recompute)
+    elems += (i128)fdiv(M.s * b * M.v, tp) + fdiv(b * M.s * M.h, u);
+  return chk(elems * M.esz);
+}
+
+int64_t device_param_elems(const Shape &M, const maya_config &c, int stage) {  // :423-434
+  const i128 h = M.h, v = M.v;
+  const i128 per_layer = fdiv(12 * h * h, c.tp);
+  i128 total = 0;
+  for (const Chunk &ch : device_chunks(M, c.pp, c.virtual_stages, stage)) {
+    total += (i128)ch.layers * per_layer;
+    if (ch.has_embed) total += fdiv(v * h, c.tp);
+    if (ch.has_head) total += fdiv(v * h, c.tp);
+  }
+  return chk(total);
+}
+
+enum Phase { FWD = 0, BWD = 1 };
+struct Step {
+  int phase;
+  int64_t mb;
+  int chunk;
+};
+
+// workload.py:450-505
+std::vector<Step> pipeline_order(int schedule, int64_t p, int64_t m, int64_t v, int64_t stage) {
+  std::vector<Step> order;
+  if (schedule == 0) {
+    if (v != 1) throw GenFail{"gpipe schedule runs with virtual_stages == 1"};
+    for (int64_t j = 0; j < m; j++) order.push_back({FWD, j, 0});
+    for (int64_t j = 0; j < m; j++) order.push_back({BWD, j, 0});
+    return order;
+  }
+  if (schedule == 1) {
+    if (v != 1) throw GenFail{"1f1b schedule runs with virtual_stages == 1"};
+    if (m < p) throw GenFail{"1f1b with too few microbatches has no steady state"};
+    int64_t warmup = std::min(p - 1 - stage, m);
+    for (int64_t j = 0; j < warmup; j++) order.push_back({FWD, j, 0});
+    for (int64_t i = 0; i < m - warmup; i++) {
+      order.push_back({FWD, warmup + i, 0});
+      order.push_back({BWD, i, 0});
+    }
+    for (int64_t j = m - warmup; j < m; j++) order.push_back({BWD, j, 0});
+    return order;
+  }
+  if (schedule == 2) {
+    if (v < 2) throw GenFail{"interleaved schedule requires virtual_stages > 1"};
+    if (m % p != 0) throw GenFail{"interleaved schedule needs microbatches % pp == 0"};
+    const int64_t total = m * v, group = p * v;
+    auto fwd_step = [&](int64_t st) {
+      return Step{FWD, st % p + (st / group) * p, (int)((st % group) / p)};
+    };
+    auto bwd_step = [&](int64_t st) {
+      return Step{BWD, st % p + (st / group) * p, (int)(v - 1 - (st % group) / p)};
+    };
+    int64_t warmup = std::min(total, (p - stage - 1) * 2 + (v - 1) * p);
+    for (int64_t i = 0; i < warmup; i++) order.push_back(fwd_step(i));
+    for (int64_t i = 0; i < total - warmup; i++) {
+      order.push_back(fwd_step(warmup + i));
+      order.push_back(bwd_step(i));
+    }
+    for (int64_t i = total - warmup; i < total; i++) order.push_back(bwd_step(i));
+    return order;
+  }
+  throw GenFail{"unknown schedule"};
+}
+
+// -- rank coordinates and communicators (workload.py:226-278)
+
+struct Coords {
+  int64_t t, d, p;
+};
+
+inline int64_t rank_of(const Coords &C, int64_t i, int64_t j, int64_t k) {
+  return k * C.t * C.d + j * C.t + i;
+}
+
+enum CommType { C_TP = 0, C_DP, C_PF, C_PB };
+struct CommRole {
+  int type;
+  int64_t a, b, c;  // TP: stage, dp; DP: tp, stage; PF/PB: boundary, tp, dp
+  int32_t nranks, my_rank;
+};
+
+std::string comm_name(const CommRole &r) {
+  char buf[96];
+  switch (r.type) {
+    case C_TP: snprintf(buf, sizeof buf, "tp.p%lld.d%lld", (long long)r.a, (long long)r.b); break;
+    case C_DP: snprintf(buf, sizeof buf, "dp.t%lld.p%lld", (long long)r.a, (long long)r.b); break;
+    case C_PF:
+      snprintf(buf, sizeof buf, "pf%lld.t%lld.d%lld", (long long)r.a, (long long)r.b,
+               (long long)r.c);
+      break;
+    default:
+      snprintf(buf, sizeof buf, "pb%lld.t%lld.d%lld", (long long)r.a, (long long)r.b,
+               (long long)r.c);
+  }
+  return buf;
+}
+
+std::vector<CommRole> worker_comms(const Coords &C, int64_t v, int64_t rank) {
+  const int64_t i = rank % C.t, j = (rank / C.t) % C.d, k = rank / (C.t * C.d);
+  std::vector<CommRole> out;
+  if (C.t > 1) out.push_back({C_TP, k, j, 0, (int32_t)C.t, (int32_t)i});
+  if (C.d > 1) out.push_back({C_DP, i, k, 0, (int32_t)C.d, (int32_t)j});
+  const int64_t total_vs = C.p * v;
+  for (int64_t c = 0; c < v; c++) {
+    int64_t vs = k + c * C.p;
+    if (vs > 0) {
+      out.push_back({C_PF, vs - 1, i, j, 2, 1});
+      out.push_back({C_PB, vs - 1, i, j, 2, 0});
+    }
+    if (vs < total_vs - 1) {
+      out.push_back({C_PF, vs, i, j, 2, 0});
+      out.push_back({C_PB, vs, i, j, 2, 1});
+    }
+  }
+  return out;
+}
+
+// members of a communicator by position (resolved by collate from CommInits)
+std::vector<int64_t> comm_members(const Coords &C, const CommRole &r) {
+  std::vector<int64_t> m;
+  switch (r.type) {
+    case C_TP:
+      for (int64_t i = 0; i < C.t; i++) m.push_back(rank_of(C, i, r.b, r.a));
+      break;
+    case C_DP:
+      for (int64_t j = 0; j < C.d; j++) m.push_back(rank_of(C, r.a, j, r.b));
+      break;
+    case C_PF:  // position 0 sends (holds vs == boundary), 1 receives
+      m.push_back(rank_of(C, r.b, r.c, r.a % C.p));
+      m.push_back(rank_of(C, r.b, r.c, (r.a + 1) % C.p));
+      break;
+    default:    // PB: position 0 holds vs == boundary + 1 (sends gradients)
+      m.push_back(rank_of(C, r.b, r.c, (r.a + 1) % C.p));
+      m.push_back(rank_of(C, r.b, r.c, r.a % C.p));
+  }
+  return m;
+}
+
+// -- _TraceBuilder (workload.py:510-568)
+
+struct Builder {
+  std::vector<uint8_t> &kind;
+  std::vector<int32_t> &stream;
+  std::vector<int64_t> &f;
+  int64_t overhead;
+  int32_t dtype;
+  std::vector<int32_t> comm_nranks;          // per local comm
+  std::vector<int64_t> call_idx;             // per local comm
+  std::vector<std::vector<std::pair<int8_t, int64_t>>> calls;  // per local comm
+  std::unordered_map<int64_t, int64_t> next_version, last_version;
+  int64_t next_alloc = 0;
+
+  void ev(uint8_t k, int32_t s, int64_t a, int64_t b = 0, int64_t c = 0, int64_t d = 0) {
+    kind.push_back(k);
+    stream.push_back(s);
+    f.push_back(a);
+    f.push_back(b);
+    f.push_back(c);
+    f.push_back(d);
+  }
+  void gap() {
+    if (overhead > 0) ev(MAYA_EV_HOSTGAP, 0, overhead);
+  }
+  void kernel(int32_t s, const KSpec &k) {
+    gap();
+    ev(MAYA_EV_KERNEL, s, k.op, dtype, k.flops, k.bytes);
+  }
+  void memcpy_h2d(int32_t s, int64_t n) {
+    gap();
+    ev(MAYA_EV_MEMCPY, s, OK_MEMCPY_H2D, DT_FP32, 0, n);
+  }
+  void memset_(int32_t s, int64_t n) {
+    gap();
+    ev(MAYA_EV_MEMSET, s, OK_MEMSET, DT_FP32, 0, n);
+  }
+  void collective(int32_t s, int lc, int kind_, int64_t n) {
+    int64_t idx = call_idx[lc]++;
+    ev(MAYA_EV_COLLECTIVE, s, lc, idx, kind_, n);
+    calls[lc].emplace_back((int8_t)kind_, n);
+  }
+  void record(int32_t s, int64_t e) {
+    int64_t ver = next_version[e];
+    next_version[e] = ver + 1;
+    last_version[e] = ver;
+    ev(MAYA_EV_RECORD, s, e, ver);
+  }
+  void wait_last(int32_t s, int64_t e) { ev(MAYA_EV_WAIT, s, e, last_version[e]); }
+  int64_t alloc(int64_t n) {
+    int64_t aid = next_alloc++;
+    ev(MAYA_EV_MEMALLOC, 0, aid, n);
+    return aid;
+  }
+  void free_(int64_t aid) { ev(MAYA_EV_MEMFREE, 0, aid); }
+};
+
+struct RepCalls {
+  std::vector<std::vector<std::pair<int8_t, int64_t>>> calls;  // per local comm
+};
+
+// workload.py:571-780 for one representative rank; appends events.
+void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int schedule,
+                    int64_t rank, int64_t overhead, int32_t dtype, GenJob &G, RepCalls &rc) {
+  const int64_t t = C.t, d = C.d;
+  const int64_t i = rank % t, j = (rank / t) % d, stage = rank / (t * d);
+  const int64_t p = cfg.pp, v = cfg.virtual_stages, total_vs = p * v;
+  const int64_t m = (int64_t)cfg.micro_mult * cfg.pp;
+  const i128 b = fdiv(cfg.global_batch, (i128)d * m);
+  const i128 s = M.s, h = M.h, esz = M.esz;
+  const bool sp = cfg.seq_parallel != 0;
+  const i128 u = sp ? t : 1;
+
+  Builder B{G.ev_kind, G.ev_stream, G.ev_f, overhead, dtype, {}, {}, {}, {}, {}, 0};
+  std::vector<CommRole> roles = worker_comms(C, v, rank);
+  // local comm index of each role (first CommInit of a comm id)
+  std::map<std::string, int> local;
+  for (const CommRole &r : roles) {
+    std::string nm = comm_name(r);
+    int lc = (int)B.comm_nranks.size();
+    if (!local.emplace(nm, lc).second) throw GenFail{"duplicate communicator"};
+    B.comm_nranks.push_back(r.nranks);
+    B.call_idx.push_back(0);
+    B.calls.emplace_back();
+    B.ev(MAYA_EV_COMMINIT, 0, lc, r.nranks, r.my_rank);
+  }
+  auto lc_of = [&](int type, int64_t a, int64_t b2, int64_t c2) {
+    CommRole r{type, a, b2, c2, 0, 0};
+    auto it = local.find(comm_name(r));
+    if (it == local.end()) throw GenFail{"communicator missing from worker_comms"};
+    return it->second;
+  };
+
+  std::vector<Chunk> chunks = device_chunks(M, (int)p, (int)v, (int)stage);
+  std::map<std::pair<int64_t, int>, int32_t> p2p_stream;  // (boundary, role) -> stream
+  std::map<std::pair<int, int64_t>, int64_t> eid;         // (key kind, boundary) -> id
+  enum { R_FIN = 0, R_BOUT, R_FOUT, R_BIN };
+  enum { E_FIN = 0, E_BOUT, E_FOUT, E_BIN, E_GRADS, E_DP_DONE, E_OPT_DONE, E_AG_DONE };
+  int32_t next_stream = FIRST_P2P_STREAM;
+  int64_t next_eid = 0;
+  for (const Chunk &ch : chunks) {
+    if (ch.vs > 0) {
+      p2p_stream[{ch.vs - 1, R_FIN}] = next_stream++;
+      p2p_stream[{ch.vs - 1, R_BOUT}] = next_stream++;
+      eid[{E_FIN, ch.vs - 1}] = next_eid++;
+      eid[{E_BOUT, ch.vs - 1}] = next_eid++;
+    }
+    if (ch.vs < total_vs - 1) {
+      p2p_stream[{ch.vs, R_FOUT}] = next_stream++;
+      p2p_stream[{ch.vs, R_BIN}] = next_stream++;
+      eid[{E_FOUT, ch.vs}] = next_eid++;
+      eid[{E_BIN, ch.vs}] = next_eid++;
+    }
+  }
+  for (int key : {E_GRADS, E_DP_DONE, E_OPT_DONE, E_AG_DONE}) eid[{key, -1}] = next_eid++;
+
+  // static allocations (device_memory_bytes, :437-445)
+  const int64_t params = device_param_elems(M, cfg, (int)stage);
+  int64_t opt = chk((i128)12 * params);
+  if (cfg.dist_optimizer) opt = -fdiv(-(i128)opt, d);
+  B.alloc(chk((i128)params * esz));
+  const int64_t grads_bytes = chk((i128)params * 4);
+  B.alloc(grads_bytes);
+  B.alloc(opt);
+  B.memset_(STREAM_COMPUTE, grads_bytes);
+
+  const int64_t p2p_payload = fdiv(b * s * h * esz, u);
+  const int64_t tp_coll_bytes = chk(b * s * h * esz);
+  const int64_t loss_reduce_bytes = chk(b * s * 8);
+  const int tp_lc = t > 1 ? lc_of(C_TP, stage, j, 0) : -1;
+  std::map<std::pair<int, int64_t>, int64_t> act_ids;
+
+  const std::vector<KSpec> lks = layer_fwd(M, b, t, sp);
+  const std::vector<KSpec> hks = head_fwd(M, b, t, sp);
+  const KSpec eks = embed_fwd(M, b, t, sp);
+  const std::vector<KSpec> mlp_bwd = bwd_of(lks, 7, 12);
+  const std::vector<KSpec> attn_bwd = bwd_of(lks, 0, 7);
+  const std::vector<KSpec> head_bwd = bwd_of(hks, 0, 3);
+
+  auto tp_pair_fwd = [&]() {
+    if (t > 1) B.collective(STREAM_COMPUTE, tp_lc, sp ? K_REDUCESCATTER : K_ALLREDUCE, tp_coll_bytes);
+  };
+  auto tp_gather_fwd = [&]() {
+    if (t > 1 && sp) B.collective(STREAM_COMPUTE, tp_lc, K_ALLGATHER, tp_coll_bytes);
+  };
+  auto emit_layer_fwd = [&]() {
+    B.kernel(STREAM_COMPUTE, lks[0]);
+    tp_gather_fwd();
+    for (int q = 1; q < 6; q++) B.kernel(STREAM_COMPUTE, lks[q]);
+    tp_pair_fwd();
+    B.kernel(STREAM_COMPUTE, lks[6]);
+    B.kernel(STREAM_COMPUTE, lks[7]);
+    tp_gather_fwd();
+    for (int q = 8; q < 11; q++) B.kernel(STREAM_COMPUTE, lks[q]);
+    tp_pair_fwd();
+    B.kernel(STREAM_COMPUTE, lks[11]);
+  };
+  auto emit_layer_fwd_compute_only = [&]() {
+    for (const KSpec &k : lks) B.kernel(STREAM_COMPUTE, k);
+  };
+  auto emit_head_fwd = [&](bool compute_only) {
+    B.kernel(STREAM_COMPUTE, hks[0]);
+    if (!compute_only) tp_gather_fwd();
+    B.kernel(STREAM_COMPUTE, hks[1]);
+    B.kernel(STREAM_COMPUTE, hks[2]);
+    if (!compute_only && t > 1) B.collective(STREAM_COMPUTE, tp_lc, K_ALLREDUCE, loss_reduce_bytes);
+  };
+  auto emit_layer_bwd = [&]() {
+    if (t > 1) B.collective(STREAM_COMPUTE, tp_lc, sp ? K_ALLGATHER : K_ALLREDUCE, tp_coll_bytes);
+    for (const KSpec &k : mlp_bwd) B.kernel(STREAM_COMPUTE, k);
+    if (t > 1 && sp) B.collective(STREAM_COMPUTE, tp_lc, K_REDUCESCATTER, tp_coll_bytes);
+    if (t > 1) B.collective(STREAM_COMPUTE, tp_lc, sp ? K_ALLGATHER : K_ALLREDUCE, tp_coll_bytes);
+    for (const KSpec &k : attn_bwd) B.kernel(STREAM_COMPUTE, k);
+    if (t > 1 && sp) B.collective(STREAM_COMPUTE, tp_lc, K_REDUCESCATTER, tp_coll_bytes);
+  };
+  auto emit_forward = [&](int64_t mb, int chunk_id) {
+    const Chunk &ch = chunks[chunk_id];
+    const int64_t vs = ch.vs;
+    act_ids[{chunk_id, mb}] = B.alloc(chunk_stash_bytes(M, cfg, b, ch));
+    if (vs > 0) {
+      int32_t fin = p2p_stream[{vs - 1, R_FIN}];
+      B.collective(fin, lc_of(C_PF, vs - 1, i, j), K_SENDRECV, p2p_payload);
+      B.record(fin, eid[{E_FIN, vs - 1}]);
+      B.wait_last(STREAM_COMPUTE, eid[{E_FIN, vs - 1}]);
+    } else {
+      B.memcpy_h2d(STREAM_COMPUTE, chk(b * s * 8));
+      B.kernel(STREAM_COMPUTE, eks);
+    }
+    for (int64_t l = 0; l < ch.layers; l++) emit_layer_fwd();
+    if (ch.has_head) emit_head_fwd(false);
+    if (vs < total_vs - 1) {
+      int32_t fout = p2p_stream[{vs, R_FOUT}];
+      B.record(STREAM_COMPUTE, eid[{E_FOUT, vs}]);
+      B.wait_last(fout, eid[{E_FOUT, vs}]);
+      B.collective(fout, lc_of(C_PF, vs, i, j), K_SENDRECV, p2p_payload);
+    }
+  };
+  auto emit_backward = [&](int64_t mb, int chunk_id) {
+    const Chunk &ch = chunks[chunk_id];
+    const int64_t vs = ch.vs;
+    if (vs < total_vs - 1) {
+      int32_t bin = p2p_stream[{vs, R_BIN}];
+      B.collective(bin, lc_of(C_PB, vs, i, j), K_SENDRECV, p2p_payload);
+      B.record(bin, eid[{E_BIN, vs}]);
+      B.wait_last(STREAM_COMPUTE, eid[{E_BIN, vs}]);
+    }
+    if (cfg.act_recompute) {
+      if (ch.has_embed) B.kernel(STREAM_COMPUTE, eks);
+      for (int64_t l = 0; l < ch.layers; l++) emit_layer_fwd_compute_only();
+      if (ch.has_head) emit_head_fwd(true);
+    }
+    if (ch.has_head)
+      for (const KSpec &k : head_bwd) B.kernel(STREAM_COMPUTE, k);
+    for (int64_t l = 0; l < ch.layers; l++) emit_layer_bwd();
+    if (ch.has_embed) B.kernel(STREAM_COMPUTE, eks);
+    if (vs > 0) {
+      int32_t bout = p2p_stream[{vs - 1, R_BOUT}];
+      B.record(STREAM_COMPUTE, eid[{E_BOUT, vs - 1}]);
+      B.wait_last(bout, eid[{E_BOUT, vs - 1}]);
+      B.collective(bout, lc_of(C_PB, vs - 1, i, j), K_SENDRECV, p2p_payload);
+    }
+    auto it = act_ids.find({chunk_id, mb});
+    B.free_(it->second);
+    act_ids.erase(it);
+  };
+
+  for (const Step &st : pipeline_order(schedule, p, m, v, stage)) {
+    if (st.phase == FWD) emit_forward(st.mb, st.chunk);
+    else emit_backward(st.mb, st.chunk);
+  }
+
+  // gradient reduction and optimizer step (:757-777)
+  const int64_t grad_comm_bytes = chk((i128)params * esz);
+  if (d > 1) {
+    const int dp_lc = lc_of(C_DP, i, stage, 0);
+    B.record(STREAM_COMPUTE, eid[{E_GRADS, -1}]);
+    B.wait_last(STREAM_GRAD_COMM, eid[{E_GRADS, -1}]);
+    B.collective(STREAM_GRAD_COMM, dp_lc, cfg.dist_optimizer ? K_REDUCESCATTER : K_ALLREDUCE,
+                 grad_comm_bytes);
+    B.record(STREAM_GRAD_COMM, eid[{E_DP_DONE, -1}]);
+    B.wait_last(STREAM_COMPUTE, eid[{E_DP_DONE, -1}]);
+  }
+  B.kernel(STREAM_COMPUTE, KSpec{OK_OPTIMIZER, chk((i128)6 * params), chk((i128)16 * params)});
+  if (d > 1 && cfg.dist_optimizer) {
+    const int dp_lc = lc_of(C_DP, i, stage, 0);
+    B.record(STREAM_COMPUTE, eid[{E_OPT_DONE, -1}]);
+    B.wait_last(STREAM_GRAD_COMM, eid[{E_OPT_DONE, -1}]);
+    B.collective(STREAM_GRAD_COMM, dp_lc, K_ALLGATHER, grad_comm_bytes);
+    B.record(STREAM_GRAD_COMM, eid[{E_AG_DONE, -1}]);
+    B.wait_last(STREAM_COMPUTE, eid[{E_AG_DONE, -1}]);
+  }
+  B.ev(MAYA_EV_DSYNC, 0, 0);
+  rc.calls = std::move(B.calls);
+}
+
+// workload.py:168-208 (cluster divisibility + model + schedule rules)
+void validate(const maya_model &model, const maya_config &c, int64_t n, int schedule) {
+  if (std::min({(int64_t)c.tp, (int64_t)c.pp, (int64_t)c.micro_mult, (int64_t)c.virtual_stages,
+                c.global_batch}) < 1)
+    throw GenFail{"tp/pp/micro_mult/virtual_stages/global_batch must be >= 1"};
+  if (n % ((int64_t)c.tp * c.pp) != 0) throw GenFail{"tp*pp does not divide device count"};
+  const int64_t d = n / ((int64_t)c.tp * c.pp), m = (int64_t)c.micro_mult * c.pp;
+  std::string errs;
+  if (c.global_batch % (d * m) != 0) errs += "global_batch not divisible by dp*microbatches; ";
+  if (model.hidden_size % c.tp) errs += "hidden_size not divisible by tp; ";
+  if (model.seq_len % c.tp) errs += "seq_len not divisible by tp; ";
+  if (model.vocab_size % c.tp) errs += "vocab_size not divisible by tp; ";
+  if (model.num_layers % ((int64_t)c.pp * c.virtual_stages))
+    errs += "num_layers not divisible by pp*virtual_stages; ";
+  if (c.virtual_stages > 1 && c.pp == 1) errs += "virtual_stages > 1 requires pp > 1; ";
+  if (schedule == 2 && c.virtual_stages == 1) errs += "interleaved schedule requires virtual_stages > 1; ";
+  if (schedule != 2 && c.virtual_stages > 1) errs += "schedule requires virtual_stages == 1; ";
+  if (schedule == 1 && m < c.pp) errs += "1f1b needs microbatches >= pp for warmup; ";
+  if (!errs.empty()) throw GenFail{errs};
+}
+
+}  // namespace
+
+maya_raw_job GenJob::raw(int32_t device) const {
+  maya_raw_job r{};
+  r.num_ranks = num_ranks;
+  r.devices_per_host = devices_per_host;
+  r.capacity = capacity;
+  r.device = device;
+  r.n_reps = (int32_t)rep_ranks.size();
+  r.rank_rep = rank_rep.data();
+  r.ev_off = ev_off.data();
+  r.ev_kind = ev_kind.data();
+  r.ev_stream = ev_stream.data();
+  r.ev_f = ev_f.data();
+  r.n_comms = (int32_t)comm_nranks.size();
+  r.comm_nranks = comm_nranks.data();
+  r.comm_topo = comm_topo.data();
+  r.call_off = call_off.data();
+  r.call_kind = call_kind.data();
+  r.call_bytes = call_bytes.data();
+  r.rank_comm_off = rank_comm_off.data();
+  r.rank_comm = rank_comm.data();
+  r.kernel_ns = nullptr;
+  r.wire_ns = nullptr;
+  return r;
+}
+
+int generate_job(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
+                 int32_t schedule, int64_t overhead, GenJob &G, std::string *err) {
+  G = GenJob();
+  try {
+    if (cl.num_hosts < 1 || cl.devices_per_host < 1) throw GenFail{"empty cluster"};
+    if (model.dtype < 0 || model.dtype > 2) throw GenFail{"unknown dtype"};
+    const int64_t n = (int64_t)cl.num_hosts * cl.devices_per_host;
+    if (schedule < 0) schedule = cfg.virtual_stages > 1 ? 2 : 1;  // default_schedule
+    validate(model, cfg, n, schedule);
+    Shape M{model.seq_len, model.hidden_size, model.vocab_size,
+            model.dtype == 2 ? 4 : 2, model.num_layers};
+    Coords C{cfg.tp, n / ((int64_t)cfg.tp * cfg.pp), cfg.pp};
+    G.num_ranks = (int32_t)n;
+    G.num_hosts = cl.num_hosts;
+    G.devices_per_host = cl.devices_per_host;
+    G.capacity = cl.device_memory_bytes;
+    // representatives: one per stage (unique_workers, :281-298)
+    std::vector<RepCalls> rcalls(cfg.pp);
+    G.ev_off.push_back(0);
+    for (int k = 0; k < cfg.pp; k++) {
+      int64_t rep = rank_of(C, 0, 0, k);
+      G.rep_ranks.push_back(rep);
+      generate_trace(M, cfg, C, schedule, rep, overhead, model.dtype, G, rcalls[k]);
+      G.ev_off.push_back((int64_t)G.ev_kind.size());
+    }
+    G.rank_rep.resize(n);
+    for (int64_t r = 0; r < n; r++) G.rank_rep[r] = (int32_t)(r / (C.t * C.d));
+    // communicators: every role of every rank (collate.py:297-322)
+    struct CInfo {
+      CommRole role;
+      int32_t stage_of_first;  // stage of position-0 rank
+      int32_t lc_of_first;     // local comm index of the role in that rank's rep
+    };
+    std::unordered_map<std::string, CInfo> comms;
+    std::vector<std::vector<std::string>> names_by_rank(n);
+    for (int64_t r = 0; r < n; r++) {
+      std::vector<CommRole> roles = worker_comms(C, cfg.virtual_stages, r);
+      for (size_t q = 0; q < roles.size(); q++) {
+        std::string nm = comm_name(roles[q]);
+        names_by_rank[r].push_back(nm);
+        if (roles[q].my_rank == 0 && !comms.count(nm))
+          comms.emplace(nm, CInfo{roles[q], (int32_t)(r / (C.t * C.d)), (int32_t)q});
+      }
+    }
+    std::vector<std::string> names;
+    names.reserve(comms.size());
+    for (auto &kv : comms) names.push_back(kv.first);
+    std::sort(names.begin(), names.end());
+    std::unordered_map<std::string, int32_t> gid;
+    G.call_off.push_back(0);
+    for (size_t g = 0; g < names.size(); g++) {
+      gid[names[g]] = (int32_t)g;
+      const CInfo &ci = comms[names[g]];
+      std::vector<int64_t> mem = comm_members(C, ci.role);
+      std::vector<int64_t> hosts;
+      for (int64_t r : mem) hosts.push_back(r / cl.devices_per_host);
+      std::vector<int64_t> uh = hosts;
+      std::sort(uh.begin(), uh.end());
+      uh.erase(std::unique(uh.begin(), uh.end()), uh.end());
+      int8_t topo = uh.size() == 1 ? 0 : (uh.size() == hosts.size() ? 1 : 2);
+      G.comm_names.push_back(names[g]);
+      G.comm_nranks.push_back(ci.role.nranks);
+      G.comm_topo.push_back(topo);
+      const auto &cl2 = rcalls[ci.stage_of_first].calls[ci.lc_of_first];
+      for (auto &kb : cl2) {
+        G.call_kind.push_back(kb.first);
+        G.call_bytes.push_back(kb.second);
+      }
+      G.call_off.push_back((int64_t)G.call_kind.size());
+      G.comm_blob += names[g];
+      G.comm_blob += '\n';
+    }
+    G.rank_comm_off.push_back(0);
+    for (int64_t r = 0; r < n; r++) {
+      for (const std::string &nm : names_by_rank[r]) G.rank_comm.push_back(gid.at(nm));
+      G.rank_comm_off.push_back((int64_t)G.rank_comm.size());
+    }
+  } catch (const GenFail &f) {
+    if (err) *err = f.msg;
+    return MAYA_EINVAL;
+  }
+  return MAYA_OK;
+}
+
+}  // namespace maya

@@ -1,0 +1,42 @@
+// Native trace generation (row f1 of SURVEY §8f): the synthetic Megatron-style
+// frontend of pkg/src/dltsim/workload.py plus the group resolution of
+// collate.py, producing a raw job (include/maya_b200.h) directly.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "../../include/maya_b200.h"
+
+namespace maya {
+
+// Fixed string tables of generated jobs (ids used in ev_f).
+extern const char *const GEN_OP_KINDS[12];
+extern const char *const GEN_DTYPES[3];
+
+struct GenJob {
+  int32_t num_ranks = 0, num_hosts = 0, devices_per_host = 0;
+  int64_t capacity = 0;
+  std::vector<int64_t> rep_ranks;
+  std::vector<int32_t> rank_rep;
+  std::vector<int64_t> ev_off;
+  std::vector<uint8_t> ev_kind;
+  std::vector<int32_t> ev_stream;
+  std::vector<int64_t> ev_f;
+  std::vector<std::string> comm_names;
+  std::vector<int32_t> comm_nranks;
+  std::vector<int8_t> comm_topo;
+  std::vector<int64_t> call_off;
+  std::vector<int8_t> call_kind;
+  std::vector<int64_t> call_bytes;
+  std::vector<int64_t> rank_comm_off;
+  std::vector<int32_t> rank_comm;
+  std::string comm_blob;  // comm names joined by '\n'
+
+  maya_raw_job raw(int32_t device) const;
+};
+
+// Returns 0 or a negative code with *err set (invalid configuration).
+int generate_job(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
+                 int32_t schedule, int64_t dispatch_overhead_ns, GenJob &out, std::string *err);
+
+}  // namespace maya

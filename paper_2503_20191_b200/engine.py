@@ -16,6 +16,7 @@ import numpy as np
 from ._abi import (Batch, DeviceParamsC, JobResultC, RawJobC, RooflineC, TopkEntryC,
                    RESULT_DTYPE, TOPK_DTYPE, DEFAULT_KERNEL_OVERHEAD_NS)
 from .rawtrace import RawJob
+from .workload import ConfigC
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmaya_b200.so")
@@ -26,6 +27,9 @@ EXPORTED = (
     "maya_batch_set_devices", "maya_batch_set_roofline", "maya_batch_add_job",
     "maya_batch_add_jobs", "maya_batch_num_jobs", "maya_upload", "maya_run", "maya_results",
     "maya_topk", "maya_timeline_size", "maya_timeline", "maya_last_timings",
+    "maya_get_stream", "maya_arena_bytes", "maya_gen_job", "maya_gen_view_of", "maya_gen_free",
+    "maya_gen_op_kind_name", "maya_gen_dtype_name", "maya_batch_add_generated",
+    "maya_batch_stats",
 )
 
 
@@ -61,6 +65,10 @@ def lib():
     L.maya_timeline.argtypes = [vp, C.c_int32, P(C.c_int32), P(C.c_int32), P(C.c_int32),
                                 P(C.c_int64), P(C.c_int64)]
     L.maya_last_timings.argtypes = [vp, P(C.c_float)]
+    L.maya_get_stream.argtypes = [vp, P(vp)]
+    L.maya_arena_bytes.argtypes = [vp]
+    L.maya_arena_bytes.restype = C.c_int64
+    L.maya_batch_stats.argtypes = [vp, P(C.c_int64)]
     _lib = L
     return L
 
@@ -172,6 +180,51 @@ class Engine:
                                start.ctypes.data_as(P(C.c_int64)),
                                end.ctypes.data_as(P(C.c_int64))))
         return Timeline(rank[:n], stream[:n], seq[:n] >> 2, seq[:n] & 3, start[:n], end[:n])
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        _check(lib().maya_get_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def batch_stats(self) -> dict:
+        o = (C.c_int64 * 10)()
+        _check(lib().maya_batch_stats(self._h, o))
+        keys = ("jobs", "rep_events", "rank_comms", "features", "slots", "device_ops",
+                "rank_ops", "arena_bytes", "ranks", "reps")
+        return {k: int(v) for k, v in zip(keys, o)}
+
+    def arena_bytes(self) -> int:
+        return int(lib().maya_arena_bytes(self._h))
+
+    def stage_generated(self, model, configs, cluster, schedule=None,
+                        dispatch_overhead_ns: int = 5000, efficiency=None,
+                        overhead_ns: int = DEFAULT_KERNEL_OVERHEAD_NS,
+                        key_ranks=None, threads: int = 8) -> np.ndarray:
+        """Generate + pack configs natively into the batch (no RawJob round trip).
+        Returns per-config generation status (0 ok, <0 invalid config)."""
+        from .rawtrace import DeviceParams
+        from .workload import _gen_lib, cluster_c, config_c, model_c, schedule_code
+        L = _gen_lib()
+        b = Batch([], efficiency, overhead_ns)
+        b.devices.append(DeviceParams.from_reference(cluster.device))
+        b.c_devices = (DeviceParamsC * 1)()
+        b._fill_device(b.c_devices[0], b.devices[0])
+        self.batch = b
+        n = len(configs)
+        _check(L.maya_batch_reset(self._h))
+        _check(L.maya_batch_set_devices(self._h, 1, b.c_devices))
+        _check(L.maya_batch_set_roofline(self._h, C.byref(b.c_roof)))
+        cfgs = (ConfigC * max(n, 1))(*[config_c(c) for c in configs])
+        kr = (np.arange(n, dtype=np.int32) if key_ranks is None
+              else np.ascontiguousarray(key_ranks, dtype=np.int32))
+        st = np.zeros(max(n, 1), dtype=np.int32)
+        P = C.POINTER
+        _check(L.maya_batch_add_generated(
+            self._h, C.byref(model_c(model)), n, cfgs, C.byref(cluster_c(cluster)), 0,
+            schedule_code(schedule), int(dispatch_overhead_ns),
+            kr.ctypes.data_as(P(C.c_int32)), int(threads), st.ctypes.data_as(P(C.c_int32))))
+        self.n_jobs = n
+        return st[:n]
 
     def last_timings_ms(self) -> tuple[float, float, float]:
         t = (C.c_float * 3)()

@@ -369,3 +369,27 @@ def from_annotated(annotated, cluster=None, name: str = "") -> RawJob:
         cap = cluster.device_memory_bytes
     return from_reference(job, kernel_ns=annotated.kernel_ns, wire_ns=annotated.wire_ns,
                           capacity=cap, name=name)
+
+
+def raw_digest(job: RawJob) -> str:
+    """Content hash of a RawJob independent of string-table ordering."""
+    import hashlib
+    h = hashlib.sha256()
+    f = job.ev_f.copy()
+    kc = np.isin(job.ev_kind, (EV_KERNEL, EV_MEMCPY, EV_MEMSET))
+    used_ops: list = []
+    used_dts: list = []
+    if kc.any():
+        used_ops = sorted(set(job.op_kind_names[i] for i in np.unique(job.ev_f[kc, 0])))
+        used_dts = sorted(set(job.dtype_names[i] for i in np.unique(job.ev_f[kc, 1])))
+        om = np.array([used_ops.index(n) if n in used_ops else -1 for n in job.op_kind_names])
+        dm = np.array([used_dts.index(n) if n in used_dts else -1 for n in job.dtype_names])
+        f[kc, 0] = om[f[kc, 0]]
+        f[kc, 1] = dm[f[kc, 1]]
+    h.update(repr((used_ops, used_dts, job.num_hosts, job.devices_per_host, job.capacity,
+                   list(job.comm_names))).encode())
+    for a in (job.rep_ranks, job.rank_rep, job.ev_off, job.ev_kind, job.ev_stream, f,
+              job.comm_nranks, job.comm_topo, job.call_off, job.call_kind, job.call_bytes,
+              job.rank_comm_off, job.rank_comm):
+        h.update(np.ascontiguousarray(a, dtype=np.int64).tobytes())
+    return h.hexdigest()

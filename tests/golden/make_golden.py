@@ -486,11 +486,13 @@ def c2_results():
         job = collate(tr, ex, c)
         rep = simulate(annotate(job, RooflineEstimator()))
         digest = hashlib.sha256("".join(dumps_trace(t) for t in tr).encode()).hexdigest()
+        from paper_2503_20191_b200.rawtrace import from_reference, raw_digest
+        raw_sha = raw_digest(from_reference(job))
         rows.append({"key": list(cfg.key()), "total_ns": rep.total_ns,
                      "peak_mem_bytes": rep.peak_mem_bytes, "oom": rep.oom,
                      "n_events": sum(len(t.events) for t in tr),
                      "rank_ops": sum(len(job.trace_of(r).events) for r in job.all_ranks()),
-                     "trace_sha256": digest})
+                     "trace_sha256": digest, "raw_sha256": raw_sha})
     print(f"C2: {len(rows)} configs in {time.time() - t0:.1f}s")
     return rows
 
@@ -515,8 +517,9 @@ def main():
         with open(os.path.join(HERE, "estimators.json"), "w") as f:
             json.dump(estimator_cases(), f)
     if args.c2:
+        rows = c2_results()
         with open(os.path.join(HERE, "c2_results.json"), "w") as f:
-            json.dump(c2_results(), f)
+            json.dump(rows, f)
 
 
 if __name__ == "__main__":
