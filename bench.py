@@ -266,8 +266,8 @@ def bench_ours(args):
     st = eng.stage_generated(model, configs, cluster, dispatch_overhead_ns=5000, key_ranks=kr,
                              threads=threads)
     assert (st == 0).all(), "invalid configs in the C2 lattice"
-    stats = eng.batch_stats()
     eng.upload()
+    stats = eng.batch_stats()
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
 
     def step():
@@ -278,6 +278,8 @@ def bench_ours(args):
         step()
     res = eng.results()
     parity = parity_c2(configs, res) if rank == 0 else None
+    st2 = eng.batch_stats()
+    launches_per_step = st2["run_launches"] + st2["topk_launches"]
 
     # --- device-resident throughput -------------------------------------------------
     sampler = ClockSampler(local)
@@ -387,7 +389,8 @@ def bench_ours(args):
                          "kernel_ms": round(sched, 4), "peak_source": peak_kind,
                          "note": "C2 is latency-bound (dedup makes compulsory bytes << work)"},
             "clocks": clocks,
-            "gpu_launches": 6 * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
+            "rounds": {"max": int(res["rounds"].max()), "median": float(np.median(res["rounds"]))},
             "best": {"rank": best_rank, "key_rank": best_kr, "time_ns": int(best[0])},
             "parity": parity,
         }

@@ -130,6 +130,12 @@ int maya_batch_add_jobs(maya_engine *eng, int32_t n, const maya_raw_job *jobs,
                         const int32_t *key_ranks, int32_t n_threads);
 int maya_batch_num_jobs(maya_engine *eng);
 
+/* Engine options (apply to jobs staged afterwards). */
+#define MAYA_OPT_COLLAPSE 1   /* exact rank-class collapse (default on) */
+int maya_set_options(maya_engine *eng, int32_t options);
+/* Per staged job: 1 if it is simulated as rank classes. */
+int maya_batch_collapsed(maya_engine *eng, uint8_t *out);
+
 /* Upload the staged batch to HBM (the H2D leg). */
 int maya_upload(maya_engine *eng);
 
@@ -160,8 +166,13 @@ int64_t maya_arena_bytes(maya_engine *eng);
 /* Batch totals of the staged batch: [0] jobs, [1] sum of rep trace events,
  * [2] sum over ranks of rep CommInits, [3] kernel features, [4] group-call
  * slots, [5] device ops (stream-major records), [6] rank-ops, [7] arena bytes,
- * [8] ranks, [9] reps. */
-int maya_batch_stats(maya_engine *eng, int64_t *out10);
+ * [8] ranks, [9] reps, [10] kernels launched by the last maya_run,
+ * [11] kernels launched by the last maya_topk. */
+int maya_batch_stats(maya_engine *eng, int64_t *out12);
+
+/* Scheduler phase counters of instrumented builds (-DMAYA_PROFILE); returns
+ * 0 (and leaves out8 untouched) in product builds. */
+int maya_prof_read(unsigned long long *out8, int reset);
 
 /* Device time of the last maya_run, per phase (ms): estimate, memscan, schedule. */
 int maya_last_timings(maya_engine *eng, float *ms3);

@@ -46,6 +46,10 @@ struct maya_engine {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {};
+  cudaStream_t vstream[4] = {};     // one stream per scheduler variant
+  cudaEvent_t vev[5] = {};          // fork / join
+  uint32_t var_n[4] = {0, 0, 0, 0}; // jobs per variant (order segments)
+  uint32_t var_smem[4] = {0, 0, 0, 0};  // dynamic smem per variant launch
   // staged jobs
   std::vector<JobPack> packs;
   std::vector<maya_device_params> devs;
@@ -65,13 +69,15 @@ struct maya_engine {
   DevTables tables{};
   // segments
   Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_slots, s_walkers, s_reps, s_ops, s_streams,
-      s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order;
-  Seg x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
+      s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids;
+  Seg x_exec, x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
       x_results, x_err, x_topk, x_topk_out, x_topk_n;
   uint64_t n_tl = 0;
   std::vector<uint64_t> job_tl;      // per job timeline base
   std::vector<uint64_t> job_ops;     // per job batch op base (for op_seq/streams)
   float last_ms[3] = {0, 0, 0};
+  int64_t run_launches = 0, topk_launches = 0;
+  int32_t options = MAYA_OPT_COLLAPSE;
 };
 
 extern "C" {
@@ -93,6 +99,8 @@ int maya_open(int cuda_device, maya_engine **out) {
     return fail(MAYA_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(err));
   }
   for (auto &ev : e->ev) cudaEventCreate(&ev);
+  for (auto &s : e->vstream) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  for (auto &ev : e->vev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   *out = e;
   return MAYA_OK;
 }
@@ -104,6 +112,8 @@ int maya_close(maya_engine *e) {
   if (e->d_arena) cudaFree(e->d_arena);
   if (e->d_scratch) cudaFree(e->d_scratch);
   for (auto &ev : e->ev) if (ev) cudaEventDestroy(ev);
+  for (auto &ev : e->vev) if (ev) cudaEventDestroy(ev);
+  for (auto &s : e->vstream) if (s) cudaStreamDestroy(s);
   if (e->stream) cudaStreamDestroy(e->stream);
   delete e;
   return MAYA_OK;
@@ -150,7 +160,8 @@ int maya_batch_add_jobs(maya_engine *e, int32_t n, const maya_raw_job *jobs,
     for (;;) {
       int i = next.fetch_add(1);
       if (i >= n) break;
-      pack_job(jobs[i], key_ranks ? key_ranks[i] : i, e->packs[base + i]);
+      pack_job(jobs[i], key_ranks ? key_ranks[i] : i, e->packs[base + i],
+               (e->options & MAYA_OPT_COLLAPSE) != 0);
     }
   };
   int nt = std::max(1, std::min<int>(n_threads, n));
@@ -167,13 +178,23 @@ int maya_batch_add_jobs(maya_engine *e, int32_t n, const maya_raw_job *jobs,
 
 int maya_batch_num_jobs(maya_engine *e) { return (int)e->packs.size(); }
 
+int maya_set_options(maya_engine *e, int32_t options) {
+  e->options = options;
+  return MAYA_OK;
+}
+
+int maya_batch_collapsed(maya_engine *e, uint8_t *out) {
+  for (size_t j = 0; j < e->packs.size(); j++) out[j] = e->packs[j].collapsed ? 1 : 0;
+  return MAYA_OK;
+}
+
 int maya_upload(maya_engine *e) {
   CU(cudaSetDevice(e->device));
   const size_t nj = e->packs.size();
   // totals
   size_t n_ranks = 0, n_rank_comm = 0, n_comms = 0, n_slots = 0, n_walkers = 0, n_reps = 0,
          n_ops = 0, n_streams = 0, n_colls = 0, n_syncs = 0, n_counts = 0, n_mems = 0,
-         n_feats = 0, n_fire = 0, n_delay = 0, n_wstate = 0;
+         n_feats = 0, n_fire = 0, n_delay = 0, n_wstate = 0, n_rcolls = 0;
   uint64_t n_tl = 0;
   e->job_tl.resize(nj);
   e->job_ops.resize(nj);
@@ -195,11 +216,17 @@ int maya_upload(maya_engine *e) {
     n_feats += P.feats.size();
     n_fire += P.n_fire;
     n_delay += P.n_delay;
-    if (P.walkers.size() + P.ranks.size() > SMEM_STATES) n_wstate += P.walkers.size() + P.ranks.size();
+    n_rcolls += P.rcolls.size();
+    {
+      const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
+                                         (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0);
+      if (L.bytes > sched_smem_cap()) n_wstate += spill_bytes(P.walkers.size(), P.ranks.size());
+    }
     e->job_tl[j] = n_tl;
-    n_tl += (uint64_t)P.hdr.dev_ops;
+    for (const RankRec &rr : P.ranks) n_tl += P.reps[rr.rep].n_ops;
   }
   if (n_reps > 0xffffffffull) return fail(MAYA_EINVAL, "too many representatives in batch");
+  if (n_feats >= 0xffffffffull) return fail(MAYA_EINVAL, "too many kernel features in batch");
   e->n_tl = n_tl;
   // arena layout
   size_t off = 0;
@@ -215,6 +242,7 @@ int maya_upload(maya_engine *e) {
   seg(e->s_comms, n_comms * sizeof(CommRec));
   seg(e->s_slots, n_slots * sizeof(SlotRec));
   seg(e->s_walkers, n_walkers * sizeof(Walker));
+  seg(e->s_wids, n_walkers * sizeof(uint32_t));
   seg(e->s_reps, n_reps * sizeof(RepHdr));
   seg(e->s_ops, n_ops * sizeof(Op));
   seg(e->s_streams, n_streams * sizeof(StreamRange));
@@ -224,14 +252,16 @@ int maya_upload(maya_engine *e) {
   seg(e->s_counts, n_counts * sizeof(uint32_t));
   seg(e->s_mems, n_mems * sizeof(MemRec));
   seg(e->s_feats, n_feats * sizeof(Feature));
+  seg(e->s_rcolls, n_rcolls * sizeof(RankColl));
   e->arena_bytes = off;
   // scratch layout
   off = 0;
+  seg(e->x_exec, n_ops * sizeof(ExecOp));
   seg(e->x_feat_ns, n_feats * 8);
   seg(e->x_wire, n_slots * 8);
   seg(e->x_fire, n_fire * 8);
   seg(e->x_delay, n_delay * 8);
-  seg(e->x_wstate, n_wstate * sizeof(WState));
+  seg(e->x_wstate, n_wstate);
   seg(e->x_cslots, n_slots * sizeof(CollSlot));
   seg(e->x_repout, n_reps * sizeof(RepOut));
   seg(e->x_results, nj * sizeof(maya_job_result));
@@ -265,19 +295,35 @@ int maya_upload(maya_engine *e) {
     e->d_scratch_cap = cap;
   }
   char *H = (char *)e->h_arena;
-  // job order: largest work first (LPT over the CTA scheduler)
+  // job order: grouped by scheduler variant, largest work first in each group
+  // (LPT over the CTA scheduler)
   {
     std::vector<int32_t> order(nj);
-    for (size_t j = 0; j < nj; j++) order[j] = (int32_t)j;
+    std::vector<int> var(nj);
+    for (size_t j = 0; j < nj; j++) {
+      order[j] = (int32_t)j;
+      var[j] = sched_variant((uint32_t)e->packs[j].walkers.size(),
+                             (uint32_t)e->packs[j].ranks.size());
+    }
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      if (var[a] != var[b]) return var[a] < var[b];
       return e->packs[a].hdr.dev_ops > e->packs[b].hdr.dev_ops;
     });
+    for (int v = 0; v < 4; v++) e->var_n[v] = e->var_smem[v] = 0;
+    for (size_t j = 0; j < nj; j++) {
+      e->var_n[var[j]]++;
+      const JobPack &P = e->packs[j];
+      const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
+                                         (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0);
+      if (L.bytes <= sched_smem_cap() && L.bytes > e->var_smem[var[j]])
+        e->var_smem[var[j]] = L.bytes;
+    }
     memcpy(H + e->s_order.off, order.data(), nj * sizeof(int32_t));
   }
   // per-job bases (serial prefix), then parallel copy
   struct Base {
     size_t ranks, rank_comm, comms, slots, walkers, reps, ops, streams, colls, syncs, counts,
-        mems, feats, fire, delay, wstate;
+        mems, feats, fire, delay, wstate, rcolls;
   };
   std::vector<Base> bases(nj);
   {
@@ -300,7 +346,10 @@ int maya_upload(maya_engine *e) {
       b.feats += P.feats.size();
       b.fire += P.n_fire;
       b.delay += P.n_delay;
-      if (P.walkers.size() + P.ranks.size() > SMEM_STATES) b.wstate += P.walkers.size() + P.ranks.size();
+      b.rcolls += P.rcolls.size();
+      const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
+                                         (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0);
+      if (L.bytes > sched_smem_cap()) b.wstate += spill_bytes(P.walkers.size(), P.ranks.size());
     }
   }
   auto copy_job = [&](size_t j) {
@@ -317,6 +366,7 @@ int maya_upload(maya_engine *e) {
     h.delay = B.delay;
     h.wstate = B.wstate;
     h.timeline = e->job_tl[j];
+    h.rcolls = B.rcolls;
     memcpy(H + e->s_jobs.off + j * sizeof(JobHdr), &h, sizeof h);
     RankRec *rk = (RankRec *)(H + e->s_ranks.off) + B.ranks;
     for (size_t r = 0; r < P.ranks.size(); r++) {
@@ -344,7 +394,16 @@ int maya_upload(maya_engine *e) {
     CPY(s_comms, comms, B.comms)
     CPY(s_slots, slots, B.slots)
     CPY(s_walkers, walkers, B.walkers)
-    CPY(s_ops, ops, B.ops)
+    CPY(s_wids, wids, B.walkers)
+    {  // ops: KERN args become batch-global feature ids
+      Op *dst = (Op *)(H + e->s_ops.off) + B.ops;
+      for (size_t q = 0; q < P.ops.size(); q++) {
+        Op o = P.ops[q];
+        if (op_tag(o.meta) == TAG_KERN) o.arg += (uint32_t)B.feats;
+        dst[q] = o;
+      }
+    }
+    CPY(s_rcolls, rcolls, B.rcolls)
     CPY(s_streams, streams, B.streams)
     CPY(s_coll_lc, coll_lc, B.colls)
     CPY(s_coll_idx, coll_idx, B.colls)
@@ -384,6 +443,7 @@ int maya_upload(maya_engine *e) {
   db.comms = (const CommRec *)(D + e->s_comms.off);
   db.slots = (const SlotRec *)(D + e->s_slots.off);
   db.walkers = (const Walker *)(D + e->s_walkers.off);
+  db.wids = (const uint32_t *)(D + e->s_wids.off);
   db.reps = (const RepHdr *)(D + e->s_reps.off);
   db.ops = (const Op *)(D + e->s_ops.off);
   db.streams = (const StreamRange *)(D + e->s_streams.off);
@@ -393,11 +453,14 @@ int maya_upload(maya_engine *e) {
   db.counts = (const uint32_t *)(D + e->s_counts.off);
   db.mems = (const MemRec *)(D + e->s_mems.off);
   db.feats = (const Feature *)(D + e->s_feats.off);
+  db.rcolls = (const RankColl *)(D + e->s_rcolls.off);
+  db.exec = (ExecOp *)(X + e->x_exec.off);
+  db.n_ops = n_ops;
   db.feat_ns = (int64_t *)(X + e->x_feat_ns.off);
   db.wire = (int64_t *)(X + e->x_wire.off);
   db.fire = (int64_t *)(X + e->x_fire.off);
   db.delay = (int64_t *)(X + e->x_delay.off);
-  db.wstate = (WState *)(X + e->x_wstate.off);
+  db.spill = (uint8_t *)(X + e->x_wstate.off);
   db.cslots = (CollSlot *)(X + e->x_cslots.off);
   db.repout = (RepOut *)(X + e->x_repout.off);
   db.results = (maya_job_result *)(X + e->x_results.off);
@@ -444,11 +507,12 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
       e->d_scratch = p;
       e->d_scratch_cap = need;
       char *X = (char *)p;
+      db.exec = (ExecOp *)(X + e->x_exec.off);
       db.feat_ns = (int64_t *)(X + e->x_feat_ns.off);
       db.wire = (int64_t *)(X + e->x_wire.off);
       db.fire = (int64_t *)(X + e->x_fire.off);
       db.delay = (int64_t *)(X + e->x_delay.off);
-      db.wstate = (WState *)(X + e->x_wstate.off);
+      db.spill = (uint8_t *)(X + e->x_wstate.off);
       db.cslots = (CollSlot *)(X + e->x_cslots.off);
       db.repout = (RepOut *)(X + e->x_repout.off);
       db.results = (maya_job_result *)(X + e->x_results.off);
@@ -471,10 +535,31 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   CU(cudaMemsetAsync(X + e->x_cslots.off, 0, e->x_cslots.bytes, e->stream));
   launch_memscan(db, e->stream);
   CU(cudaGetLastError());
-  CU(cudaEventRecord(e->ev[2], e->stream));
-  launch_schedule(db, record_timeline ? 1 : 0, e->stream);
+  launch_resolve(db, e->stream);
   CU(cudaGetLastError());
+  CU(cudaEventRecord(e->ev[2], e->stream));
+  {
+    // variants run concurrently on their own streams (fork/join)
+    CU(cudaEventRecord(e->vev[4], e->stream));
+    uint32_t off = 0;
+    for (int v = 0; v < 4; v++) {
+      if (!e->var_n[v]) continue;
+      CU(cudaStreamWaitEvent(e->vstream[v], e->vev[4], 0));
+      launch_schedule_variant(db, v, db.order + off, e->var_n[v], record_timeline ? 1 : 0,
+                              e->var_smem[v], e->vstream[v]);
+      CU(cudaGetLastError());
+      CU(cudaEventRecord(e->vev[v], e->vstream[v]));
+      CU(cudaStreamWaitEvent(e->stream, e->vev[v], 0));
+      off += e->var_n[v];
+    }
+  }
   CU(cudaEventRecord(e->ev[3], e->stream));
+  {
+    int64_t n = (db.n_feats ? 1 : 0) + (db.n_slots ? 1 : 0) + (db.n_reps ? 1 : 0) +
+                (db.n_ops ? 1 : 0);
+    for (int v = 0; v < 4; v++) n += e->var_n[v] ? 1 : 0;
+    e->run_launches = n;
+  }
   e->ran = true;
   e->recorded = record_timeline != 0;
   return MAYA_OK;
@@ -490,6 +575,11 @@ int maya_results(maya_engine *e, maya_job_result *out) {
   CU(cudaMemcpyAsync(&err_flag, e->db.err_flag, sizeof err_flag, cudaMemcpyDeviceToHost,
                      e->stream));
   CU(cudaStreamSynchronize(e->stream));
+  for (size_t j = 0; j < nj; j++) {
+    const JobPack &P = e->packs[j];
+    if (out[j].first_oom_rank >= 0 && (size_t)out[j].first_oom_rank < P.rank_orig.size())
+      out[j].first_oom_rank = P.rank_orig[out[j].first_oom_rank];
+  }
   cudaEventElapsedTime(&e->last_ms[0], e->ev[0], e->ev[1]);
   cudaEventElapsedTime(&e->last_ms[1], e->ev[1], e->ev[2]);
   cudaEventElapsedTime(&e->last_ms[2], e->ev[2], e->ev[3]);
@@ -514,6 +604,9 @@ int maya_results(maya_engine *e, maya_job_result *out) {
   return MAYA_OK;
 }
 
+// Engine-internal profiling counters (builds with -DMAYA_PROFILE; else returns 0).
+int maya_prof_read(unsigned long long *out8, int reset) { return prof_read(out8, reset); }
+
 int maya_get_stream(maya_engine *e, void **stream) {
   *stream = (void *)e->stream;
   return MAYA_OK;
@@ -522,7 +615,9 @@ int maya_get_stream(maya_engine *e, void **stream) {
 int64_t maya_arena_bytes(maya_engine *e) { return (int64_t)e->arena_bytes; }
 
 int maya_batch_stats(maya_engine *e, int64_t *o) {
-  for (int i = 0; i < 10; i++) o[i] = 0;
+  for (int i = 0; i < 12; i++) o[i] = 0;
+  o[10] = e->run_launches;
+  o[11] = e->topk_launches;
   o[0] = (int64_t)e->packs.size();
   for (const JobPack &P : e->packs) {
     for (const RepHdr &h : P.reps) o[1] += h.n_events;
@@ -551,6 +646,7 @@ int maya_topk(maya_engine *e, int32_t k, maya_topk_entry *out, int32_t *n_out) {
   maya_topk_entry *d_out = (maya_topk_entry *)(X + e->x_topk_out.off);
   int32_t *d_n = (int32_t *)(X + e->x_topk_n.off);
   launch_topk(e->db, k, d_out, d_n, X + e->x_topk.off, e->stream);
+  e->topk_launches = e->db.n_jobs ? 2 : 0;
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(n_out, d_n, sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
   CU(cudaMemcpyAsync(out, d_out, k * sizeof(maya_topk_entry), cudaMemcpyDeviceToHost, e->stream));
@@ -560,7 +656,7 @@ int maya_topk(maya_engine *e, int32_t k, maya_topk_entry *out, int32_t *n_out) {
 
 int maya_timeline_size(maya_engine *e, int32_t job, int64_t *n) {
   if (job < 0 || (size_t)job >= e->packs.size()) return fail(MAYA_EINVAL, "job index");
-  *n = e->packs[job].hdr.dev_ops;
+  *n = e->packs[job].hdr.dev_ops;   // all ranks (classes are expanded)
   return MAYA_OK;
 }
 
@@ -570,25 +666,31 @@ int maya_timeline(maya_engine *e, int32_t job, int32_t *rank, int32_t *stream, i
   if (job < 0 || (size_t)job >= e->packs.size()) return fail(MAYA_EINVAL, "job index");
   CU(cudaSetDevice(e->device));
   const JobPack &P = e->packs[job];
-  const uint64_t n = (uint64_t)P.hdr.dev_ops;
-  if (n) {
-    CU(cudaMemcpyAsync(start, e->db.tl_start + e->job_tl[job], n * 8, cudaMemcpyDeviceToHost,
-                       e->stream));
-    CU(cudaMemcpyAsync(end, e->db.tl_end + e->job_tl[job], n * 8, cudaMemcpyDeviceToHost,
-                       e->stream));
+  uint64_t n_sim = 0;
+  for (const RankRec &rr : P.ranks) n_sim += P.reps[rr.rep].n_ops;
+  std::vector<int64_t> s(n_sim), en(n_sim);
+  if (n_sim) {
+    CU(cudaMemcpyAsync(s.data(), e->db.tl_start + e->job_tl[job], n_sim * 8,
+                       cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaMemcpyAsync(en.data(), e->db.tl_end + e->job_tl[job], n_sim * 8,
+                       cudaMemcpyDeviceToHost, e->stream));
   }
   CU(cudaStreamSynchronize(e->stream));
   uint64_t t = 0;
-  for (size_t r = 0; r < P.ranks.size(); r++) {
-    const RepHdr &h = P.reps[P.ranks[r].rep];
-    for (uint32_t s = 0; s < h.n_streams; s++) {
-      const StreamRange &sr = P.streams[h.streams + s];
+  for (size_t r = 0; r < P.rank_sim.size(); r++) {
+    const RankRec &rr = P.ranks[P.rank_sim[r]];
+    const RepHdr &h = P.reps[rr.rep];
+    for (uint32_t sidx = 0; sidx < h.n_streams; sidx++) {
+      const StreamRange &sr = P.streams[h.streams + sidx];
       for (uint32_t i = 0; i < sr.len; i++, t++) {
+        const uint64_t src = rr.tl + sr.begin + i;
         rank[t] = (int32_t)r;
         stream[t] = sr.raw;
         const uint64_t o = h.ops + sr.begin + i;
-        // tag in high bits of seq: (seq << 2) | tag so callers can filter timed ops
+        // tag in the low bits of seq: (seq << 2) | tag so callers can filter timed ops
         seq[t] = (int32_t)((P.op_seq[o] << 2) | op_tag(P.ops[o].meta));
+        start[t] = s[src];
+        end[t] = en[src];
       }
     }
   }
@@ -663,7 +765,7 @@ int maya_batch_add_generated(maya_engine *e, const maya_model *model, int32_t n,
         continue;
       }
       maya_raw_job raw = g.raw(device);
-      pack_job(raw, key_ranks ? key_ranks[i] : i, P);
+      pack_job(raw, key_ranks ? key_ranks[i] : i, P, (e->options & MAYA_OPT_COLLAPSE) != 0);
     }
   };
   int nt = std::max(1, std::min<int>(n_threads, n));

@@ -158,8 +158,23 @@ void launch_memscan(const DevBatch &b, cudaStream_t s) {
 
 // ---------------------------------------------------------------------------
 // scheduler
+//
+// resolve: Op + estimator output -> ExecOp (duration inlined), one thread per op.
 
-static constexpr int SCHED_THREADS = 256;
+__global__ void resolve_kernel(DevBatch b) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b.n_ops) return;
+  const Op op = b.ops[i];
+  const uint32_t tag = op_tag(op.meta);
+  uint64_t pay;
+  if (tag == TAG_KERN) {
+    const int64_t d = b.feat_ns[op.arg];   // batch-global feature id
+    pay = (d < 0 || d >= (int64_t)(EXEC_BAD >> 2)) ? (EXEC_BAD >> 2) : (uint64_t)d;
+  } else {
+    pay = (op.arg == NO_REC) ? (EXEC_NONE >> 2) : (uint64_t)op.arg;
+  }
+  b.exec[i] = ExecOp{op.disp, (pay << 2) | tag};
+}
 
 template <typename T>
 __device__ __forceinline__ T vload(const T *p) {
@@ -170,105 +185,290 @@ __device__ __forceinline__ void vstore(T *p, T v) {
   *(volatile T *)p = v;
 }
 
-struct SchedCtx {
+static constexpr unsigned FULL = 0xffffffffu;
+
+#ifdef MAYA_PROFILE
+// per-batch cycle counters: [0] walk windows, [1] slow ops, [2] idle sleep,
+// [3] sweeps (skip checks + ctx), [4] windows, [5] slow-op calls, [6] wakes, [7] passes
+__device__ unsigned long long g_prof[8];
+#define PROF_T(v) long long v = clock64()
+#define PROF_ADD(i, v) atomicAdd(&g_prof[i], (unsigned long long)(v))
+#else
+#define PROF_T(v)
+#define PROF_ADD(i, v)
+#endif
+static constexpr int64_t NEG = INT64_MIN / 4;          // -inf of the max-plus scan
+static constexpr int64_t LIM_T = (int64_t)1 << 60;     // times beyond: exact serial path
+static constexpr uint64_t LIM_D = (uint64_t)1 << 56;   // durations beyond: exact serial path
+
+// Per-walker state (one (rank, stream) FIFO), kept in shared memory (or the
+// global spill) between rounds; uniform across the lanes of the warp.
+struct WSt {
+  int64_t x;              // completion time of the last op processed
+  int64_t cdel;           // host delay of the current sync segment
+  uint32_t i, flags, seg, bound;
+  const void *wa;         // wake condition of a blocked walker: counter / record entry
+  uint32_t wt;            // target count
+  uint32_t wk;            // WAKE_*
+};
+enum { WAKE_NONE = 0, WAKE_COUNT = 1, WAKE_FIRE = 2, WAKE_ROUND = 3 };
+static_assert(sizeof(WSt) == WSTATE_BYTES, "WSt layout");
+
+// Walker context: loop-invariant pointers of one (rank, stream) FIFO
+// (cached in shared memory for on-chip jobs).
+struct WCtx {
+  const ExecOp *ops;      // stream's first op
+  int64_t *fire;          // rank's record table
+  const int64_t *delay;   // rank's host-delay table (n_syncs + 1)
+  const RankColl *rc;     // rank's collective table
+  const uint32_t *cnt;    // counts[0][stream] of the rep (stride ns)
+  uint64_t tl;            // timeline row of the stream's first op
+  uint32_t len, rank, ns, nsync;
+};
+static_assert(sizeof(WCtx) == WCTX_BYTES, "WCtx layout");
+
+struct JobSh {            // per-CTA view of the job
   const JobHdr *J;
-  WState *ws;        // [n_walkers] walkers, then [n_ranks] host states (i = resolved syncs)
-  int64_t *fire;     // job base
-  int64_t *delay;    // job base
+  CollSlot *ring;         // smem rings (2 per comm) or null -> global slots
+  const uint32_t *cb;     // call_base per comm (smem u32, or CommRec stride in global)
+  uint32_t cb_stride;
+  uint32_t *hostk;        // resolved host syncs per rank
+  WSt *st;                // walker states
+  const uint32_t *wid;    // rank-major (rank, stream) position -> walker index
+  WCtx *ctx;              // cached contexts (smem) or null
+  unsigned *epoch;        // CTA progress epoch
   int record;
 };
 
-// Advance one (rank, stream) walker as far as its dependencies allow.
-// Returns true if it made progress; sets *err on estimation/overflow/internal.
-__device__ bool advance_walker(const DevBatch &b, const SchedCtx &c, uint32_t w, int64_t &tmax,
-                               int &err) {
-  const JobHdr &J = *c.J;
+__device__ __forceinline__ void load_ctx(const DevBatch &b, const JobHdr &J, uint32_t w,
+                                         int record, WCtx &c) {
   const Walker wk = b.walkers[J.walkers + w];
   const RankRec rr = b.ranks[J.ranks + wk.rank];
   const RepHdr &h = b.reps[rr.rep];
   const StreamRange sr = b.streams[h.streams + wk.stream];
-  WState st = c.ws[w];
-  if (st.i >= sr.len) return false;
-  const uint32_t hk = vload(&c.ws[J.n_walkers + wk.rank].i);
-  const Op *ops = b.ops + h.ops + sr.begin;
-  int64_t *fire = c.fire + rr.fire;
-  const int64_t *delay = c.delay + rr.delay;
-  int64_t x = st.x;
-  uint32_t i = st.i, flags = st.flags;
-  uint32_t cseg = 0;
-  int64_t cdel = 0;
+  c.ops = b.exec + h.ops + sr.begin;
+  c.fire = b.fire + J.fire + rr.fire;
+  c.delay = b.delay + J.delay + rr.delay;
+  c.rc = b.rcolls + J.rcolls + rr.rslot;
+  c.cnt = b.counts + h.counts + wk.stream;
+  c.len = sr.len;
+  c.rank = wk.rank;
+  c.ns = h.n_streams;
+  c.nsync = h.n_syncs;
+  c.tl = J.timeline + rr.tl + sr.begin;
+  (void)record;
+}
+
+enum { STEP_OK = 0, STEP_BLOCK = 1, STEP_ERR = 2 };
+
+struct SlowRes {
+  int64_t nx;       // completion time
+  uint32_t code;    // status | flags << 2 | adv << 3 | err << 4 | wake kind << 8
+  uint32_t wt;      // wake target (WAKE_COUNT)
+  const void *wa;   // wake address
+};
+
+// One op outside the scanned kernel runs: record, wait, collective
+// rendezvous (sim.py:287-347), or a kernel whose values need the exact
+// overflow-checked path.  Executed by lane 0 of the walker's warp.
+__device__ __noinline__ SlowRes slow_op(CollSlot *cslots, const int64_t *wire, CollSlot *ring,
+                                        const uint32_t *cbt, uint32_t cb_stride, unsigned *epoch,
+                                        int64_t *fire, const RankColl *rc, uint64_t w,
+                                        int64_t ready, uint32_t flags) {
+  const uint32_t tag = (uint32_t)(w & 3);
+  const uint64_t pay = w >> 2;
+  if (tag == TAG_KERN) {
+    if (w == EXEC_BAD)
+      return SlowRes{0, STEP_ERR | (flags << 2) | (MAYA_ST_ESTIMATION << 4), 0, nullptr};
+    if ((int64_t)pay > INT64_MAX - ready)
+      return SlowRes{0, STEP_ERR | (flags << 2) | (MAYA_ST_OVERFLOW << 4), 0, nullptr};
+    return SlowRes{ready + (int64_t)pay, STEP_OK | (flags << 2), 0, nullptr};
+  }
+  if (tag == TAG_REC) {
+    vstore(&fire[pay], ready);
+    __threadfence_block();
+    atomicAdd(epoch, 1u);   // wake warps waiting on this event
+    return SlowRes{ready, STEP_OK | (flags << 2), 0, nullptr};
+  }
+  if (tag == TAG_WAIT) {
+    if (pay == (EXEC_NONE >> 2))
+      return SlowRes{0, STEP_BLOCK | (flags << 2) | (WAKE_ROUND << 8), 0, nullptr};
+    const int64_t f = vload(&fire[pay]);
+    if (f < 0) return SlowRes{0, STEP_BLOCK | (flags << 2) | (WAKE_FIRE << 8), 0, &fire[pay]};
+    return SlowRes{ready > f ? ready : f, STEP_OK | (flags << 2), 0, nullptr};
+  }
+  // TAG_COLL: rendezvous of all members (sim.py:326-343)
+  const RankColl ent = rc[pay];
+  const uint32_t nr = (uint32_t)(ent >> 48);
+  const uint32_t g = (uint32_t)(ent >> 32) & 0xffffu;
+  const uint32_t idx = (uint32_t)ent;
+  const uint32_t cb = cbt[g * cb_stride];
+  CollSlot *cs;
+  uint32_t target;
+  if (ring) {
+    cs = ring + 2 * g + (idx & 1u);
+    target = ((idx >> 1) + 1u) * nr;
+  } else {
+    cs = cslots + cb + idx;
+    target = nr;
+  }
+  uint32_t adv = 0;
+  if (!(flags & 1u)) {
+    atomicMax(&cs->maxarr, (unsigned long long)ready);
+    __threadfence_block();
+    const uint32_t old = atomicAdd(&cs->count, 1u);
+    flags |= 1u;
+    adv = 1;
+    if (old + 1 == target) atomicAdd(epoch, 1u);   // wake the other members
+    if (old + 1 > target)
+      return SlowRes{0, STEP_ERR | (flags << 2) | (adv << 3) | (MAYA_ST_INTERNAL << 4)};
+    if (old + 1 < target) return SlowRes{0, STEP_BLOCK | (flags << 2) | (adv << 3)};
+  } else if (vload(&cs->count) < target) {
+    return SlowRes{0, STEP_BLOCK | (flags << 2)};
+  }
+  __threadfence_block();
+  const int64_t m = (int64_t)vload(&cs->maxarr);
+  const int64_t wt = wire[cb + idx];
+  if (wt > INT64_MAX - m)
+    return SlowRes{0, STEP_ERR | (flags << 2) | (adv << 3) | (MAYA_ST_OVERFLOW << 4)};
+  return SlowRes{m + wt, STEP_OK | (adv << 3)};   // flags cleared
+}
+
+__device__ __forceinline__ ExecOp load_exec(const ExecOp *p) {
+  const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(p));
+  return ExecOp{v.x, (uint64_t)v.y};
+}
+
+// Warp-cooperative walker: advance one (rank, stream) FIFO 32 records at a
+// time.  A kernel op is the max-plus affine map  x -> max(x + d, disp + d)
+// (ready = max(dispatch, prev done); done = ready + d), so a run of kernel ops
+// is one segmented inclusive scan of (a, b) pairs across the lanes; ballots
+// locate the records, waits and collectives, which lane 0 applies in order.
+__device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt &s,
+                          int64_t &tmax, int &err, uint32_t lane) {
+  if (s.i >= c.len) return false;
+  const JobHdr &J = *sh.J;
+  const uint32_t hk = sh.hostk[c.rank];
+  const uint32_t limit = hk < c.nsync ? c.cnt[hk * c.ns] : c.len;
   bool adv = false;
-  while (i < sr.len) {
-    const Op op = ops[i];
-    const uint32_t seg = op_seg(op.meta);
-    if (seg > hk) break;  // not dispatched yet: host blocked at an earlier sync
-    if (seg != cseg) { cseg = seg; cdel = delay[seg]; }
-    int64_t ready = op.disp + cdel;
-    if (ready < x) ready = x;
-    int64_t nx;
-    const uint32_t tag = op_tag(op.meta);
-    if (tag == TAG_KERN) {
-      const int64_t d = b.feat_ns[J.feats + op.arg];
-      if (d < 0) { err = MAYA_ST_ESTIMATION; break; }
-      if (d > INT64_MAX - ready) { err = MAYA_ST_OVERFLOW; break; }
-      nx = ready + d;
-    } else if (tag == TAG_REC) {
-      vstore(&fire[op.arg], ready);
-      nx = ready;
-    } else if (tag == TAG_WAIT) {
-      if (op.arg == NO_REC) break;
-      const int64_t f = vload(&fire[op.arg]);
-      if (f < 0) break;
-      nx = ready > f ? ready : f;
-    } else {  // TAG_COLL: rendezvous of all members (sim.py:326-343)
-      const uint32_t lc = b.coll_lc[h.colls + op.arg];
-      const uint32_t ci = b.coll_idx[h.colls + op.arg];
-      const uint32_t g = b.rank_comm[J.rank_comm + rr.comm + lc];
-      const CommRec cm = b.comms[J.comms + g];
-      const uint64_t slot = J.slots + cm.call_base + ci;
-      CollSlot *cs = b.cslots + slot;
-      if (!(flags & 1u)) {
-        atomicMax(&cs->maxarr, (unsigned long long)ready);
-        __threadfence_block();
-        const uint32_t old = atomicAdd(&cs->count, 1u);
-        flags |= 1u;
-        adv = true;
-        if (old + 1 > (uint32_t)cm.nranks) { err = MAYA_ST_INTERNAL; break; }
-        if (old + 1 < (uint32_t)cm.nranks) break;
-      } else if (vload(&cs->count) < (uint32_t)cm.nranks) {
+  s.wk = WAKE_ROUND;   // until something else is known: wait for the next round
+  while (s.i < limit) {
+    while (s.i >= s.bound && s.seg < c.nsync) {  // next host-sync segment
+      s.seg++;
+      s.cdel = c.delay[s.seg];
+      s.bound = s.seg < c.nsync ? c.cnt[s.seg * c.ns] : c.len;
+    }
+    PROF_T(t_win);
+    const uint32_t end = s.bound < limit ? s.bound : limit;
+    const uint32_t n = min(32u, end - s.i);
+    const bool valid = lane < n;
+    ExecOp e{0, 0};
+    if (valid) e = load_exec(c.ops + s.i + lane);
+    if (lane < 4 && s.i + 32 + lane * 8 < c.len)   // next window's lines into L1
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(c.ops + s.i + 32 + lane * 8));
+    const uint32_t tag = (uint32_t)(e.w & 3);
+    const uint64_t dur = e.w >> 2;
+    const int64_t rdisp = e.disp + s.cdel;
+    const bool special = valid && (tag != TAG_KERN || dur >= LIM_D || rdisp >= LIM_T ||
+                                   s.x >= LIM_T);
+    const uint32_t smask = __ballot_sync(FULL, special);
+    // segmented inclusive max-plus scan; segments restart after special ops
+    int64_t A = 0, B = NEG;
+    if (valid && !special) {
+      A = (int64_t)dur;
+      B = rdisp + (int64_t)dur;
+    }
+    bool flag = (lane == 0) || ((smask >> (lane - 1)) & 1u);
+#pragma unroll
+    for (uint32_t off = 1; off < 32; off <<= 1) {
+      const int64_t A2 = __shfl_up_sync(FULL, A, off);
+      const int64_t B2 = __shfl_up_sync(FULL, B, off);
+      const bool f2 = __shfl_up_sync(FULL, flag, off);
+      if (lane >= off && !flag) {
+        const int64_t nb = B2 + A;
+        B = nb > B ? nb : B;
+        A = A2 + A;
+        flag = f2;
+      }
+    }
+    // apply special ops in order
+    int64_t xin = s.x, d = 0;
+    uint32_t p = 0, commit = n, spec = smask;
+    bool blocked = false;
+    while (spec) {
+      const uint32_t q = __ffs(spec) - 1;
+      spec &= spec - 1;
+      if (lane >= p && lane < q) {
+        const int64_t v = xin + A;
+        d = v > B ? v : B;
+      }
+      const int64_t xq = q > p ? __shfl_sync(FULL, d, q - 1) : xin;
+      const int64_t qd = __shfl_sync(FULL, rdisp, q);
+      const uint64_t qw = __shfl_sync(FULL, e.w, q);
+      const int64_t ready = qd > xq ? qd : xq;
+      SlowRes r{0, 0, 0, nullptr};
+      PROF_T(t_slow);
+      if (lane == 0)
+        r = slow_op(b.cslots + J.slots, b.wire + J.slots, sh.ring, sh.cb, sh.cb_stride,
+                    sh.epoch, c.fire, c.rc, qw, ready, s.flags);
+      r.nx = __shfl_sync(FULL, r.nx, 0);
+      r.code = __shfl_sync(FULL, r.code, 0);
+#ifdef MAYA_PROFILE
+      if (lane == 0) { PROF_ADD(1, clock64() - t_slow); PROF_ADD(5, 1); }
+#endif
+      s.flags = (r.code >> 2) & 1u;
+      if (r.code & 8u) adv = true;
+      const uint32_t stc = r.code & 3u;
+      if (stc != STEP_OK) {
+        if (stc == STEP_ERR) err = (int)((r.code >> 4) & 15u);
+        s.wk = (r.code >> 8) & 3u;
+        s.wt = __shfl_sync(FULL, r.wt, 0);
+        s.wa = (const void *)__shfl_sync(FULL, (unsigned long long)r.wa, 0);
+        blocked = true;
+        commit = q;
         break;
       }
-      __threadfence_block();
-      const int64_t m = (int64_t)vload(&cs->maxarr);
-      const int64_t wt = b.wire[slot];
-      if (wt > INT64_MAX - m) { err = MAYA_ST_OVERFLOW; break; }
-      nx = m + wt;
-      flags = 0;
+      if (lane == q) d = r.nx;
+      xin = r.nx;
+      p = q + 1;
     }
-    if (c.record) {
-      const uint64_t t = J.timeline + rr.tl + sr.begin + i;
-      b.tl_start[t] = ready;
-      b.tl_end[t] = nx;
+    if (!blocked && lane >= p && lane < n) {
+      const int64_t v = xin + A;
+      d = v > B ? v : B;
     }
-    x = nx;
-    i++;
-    adv = true;
+    if (commit > 0) {
+      if (sh.record) {
+        int64_t prev = __shfl_up_sync(FULL, d, 1);
+        if (lane == 0) prev = s.x;
+        if (lane < commit) {
+          b.tl_start[c.tl + s.i + lane] = rdisp > prev ? rdisp : prev;
+          b.tl_end[c.tl + s.i + lane] = d;
+        }
+      }
+      s.x = __shfl_sync(FULL, d, commit - 1);
+      s.i += commit;
+      adv = true;
+    }
+#ifdef MAYA_PROFILE
+    if (lane == 0) { PROF_ADD(0, clock64() - t_win); PROF_ADD(4, 1); }
+#endif
+    if (blocked) break;
+    s.wk = WAKE_ROUND;
   }
-  c.ws[w] = WState{x, i, flags};
-  if (x > tmax) tmax = x;
+  if (s.x > tmax) tmax = s.x;
   return adv;
 }
 
 // Resolve as many host syncs of rank r as the stream states allow
-// (sim.py:243-263, 272-283): H' = max(H, X) with H = gap prefix + delay.
-__device__ bool advance_host(const DevBatch &b, const SchedCtx &c, uint32_t r) {
-  const JobHdr &J = *c.J;
+// (sim.py:243-263, 272-283): H' = max(H, X), H = gap prefix + delay.
+__device__ bool host_step(const DevBatch &b, const JobSh &sh, uint32_t r, int64_t *delay_job) {
+  const JobHdr &J = *sh.J;
   const RankRec rr = b.ranks[J.ranks + r];
   const RepHdr &h = b.reps[rr.rep];
-  if (h.n_syncs == 0) return false;
-  uint32_t k = c.ws[J.n_walkers + r].i;
+  uint32_t k = sh.hostk[r];
   if (k >= h.n_syncs) return false;
-  int64_t d = c.delay[rr.delay + k];
+  int64_t *delay = delay_job + rr.delay;
+  int64_t d = delay[k];
   bool adv = false;
   while (k < h.n_syncs) {
     const SyncRec s = b.syncs[h.syncs + k];
@@ -278,7 +478,7 @@ __device__ bool advance_host(const DevBatch &b, const SchedCtx &c, uint32_t r) {
       if (s.arg == NO_REC) {
         ok = false;
       } else {
-        X = vload(&c.fire[rr.fire + s.arg]);
+        X = vload(&b.fire[J.fire + rr.fire + s.arg]);
         ok = X >= 0;
       }
     } else {
@@ -289,34 +489,36 @@ __device__ bool advance_host(const DevBatch &b, const SchedCtx &c, uint32_t r) {
       for (uint32_t ls = s0; ls < s1; ls++) {
         const uint32_t cnt = b.counts[h.counts + s.cnt + ls];
         if (cnt == 0) continue;
-        const WState w = c.ws[rr.walker + ls];
-        if (w.i < cnt) { ok = false; break; }
-        if (w.x > X) X = w.x;
+        const WSt &ws = sh.st[sh.wid[rr.walker + ls]];
+        if (ws.i < cnt) { ok = false; break; }
+        if (ws.x > X) X = ws.x;
       }
     }
     if (!ok) break;
     if (X > s.gpre + d) d = X - s.gpre;
     k++;
-    c.delay[rr.delay + k] = d;
+    delay[k] = d;
     adv = true;
   }
-  c.ws[J.n_walkers + r].i = k;
+  sh.hostk[r] = k;
   return adv;
 }
 
-__global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(DevBatch b, int record) {
-  __shared__ WState s_states[SMEM_STATES];
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, const int32_t *order,
+                                                             int record, uint32_t smem_cap) {
+  extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ unsigned long long s_tmax;
-  __shared__ int s_err, s_incomplete;
-  __shared__ long long s_oom_t;
-  __shared__ int s_oom_rank;
-  __shared__ long long s_peak;
+  __shared__ int s_err, s_incomplete, s_oom_rank, s_active;
+  __shared__ unsigned s_epoch;
+  __shared__ long long s_oom_t, s_peak;
 
-  const uint32_t j = b.order ? (uint32_t)b.order[blockIdx.x] : blockIdx.x;
+  const uint32_t j = (uint32_t)order[blockIdx.x];
   const JobHdr &J = b.jobs[j];
   maya_job_result *res = b.results + j;
+  const uint32_t tid = threadIdx.x, nt = NW * 32, lane = tid & 31, wp = tid >> 5;
   if (J.status != MAYA_ST_OK) {
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       maya_job_result r = {};
       r.status = J.status;
       r.first_oom_rank = -1;
@@ -326,14 +528,30 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(DevBatch b, int
     }
     return;
   }
-  const uint32_t W = J.n_walkers, R = J.n_ranks, S = W + R;
-  SchedCtx c;
-  c.J = &J;
-  c.ws = (S <= (uint32_t)SMEM_STATES) ? s_states : b.wstate + J.wstate;
-  c.fire = b.fire + J.fire;
-  c.delay = b.delay + J.delay;
-  c.record = record;
-  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  const uint32_t W = J.n_walkers, R = J.n_ranks;
+  const SchedLayout L = sched_layout(W, R, J.n_comms, (J.flags & JOB_RING) != 0);
+  const bool on_chip = L.bytes <= smem_cap;
+  uint8_t *base = on_chip ? dsm : b.spill + J.wstate;
+  JobSh sh;
+  sh.J = &J;
+  sh.ring = (on_chip && L.ring_on) ? (CollSlot *)(dsm + L.ring) : nullptr;
+  if (on_chip) {
+    uint32_t *cb = (uint32_t *)(dsm + L.cb);
+    for (uint32_t g = tid; g < J.n_comms; g += nt) cb[g] = b.comms[J.comms + g].call_base;
+    sh.cb = cb;
+    sh.cb_stride = 1;
+  } else {
+    sh.cb = &b.comms[J.comms].call_base;
+    sh.cb_stride = sizeof(CommRec) / 4;
+  }
+  if (sh.ring)
+    for (uint32_t q = tid; q < 2 * J.n_comms; q += nt) sh.ring[q] = CollSlot{0, 0, 0};
+  sh.hostk = (uint32_t *)(base + (on_chip ? L.hostk : 0));
+  sh.st = (WSt *)(base + (on_chip ? L.state : ((4 * R + 15) & ~15u)));
+  sh.wid = b.wids + J.walkers;
+  sh.ctx = on_chip ? (WCtx *)(dsm + L.ctx) : nullptr;
+  sh.epoch = &s_epoch;
+  sh.record = record;
   if (tid == 0) {
     s_tmax = 0;
     s_err = 0;
@@ -341,9 +559,19 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(DevBatch b, int
     s_oom_t = INT64_MAX;
     s_oom_rank = INT32_MAX;
     s_peak = 0;
+    s_epoch = 0;
   }
-  for (uint32_t w = tid; w < S; w += nt) c.ws[w] = WState{0, 0, 0};
-  for (uint32_t r = tid; r < R; r += nt) c.delay[b.ranks[J.ranks + r].delay] = 0;
+  int64_t *delay_job = b.delay + J.delay;
+  for (uint32_t r = tid; r < R; r += nt) {
+    delay_job[b.ranks[J.ranks + r].delay] = 0;
+    sh.hostk[r] = 0;
+  }
+  for (uint32_t w = tid; w < W; w += nt) {
+    WCtx c;
+    load_ctx(b, J, w, 0, c);
+    sh.st[w] = WSt{0, 0, 0, 0, 0, c.nsync ? c.cnt[0] : c.len, nullptr, 0, WAKE_NONE};
+    if (sh.ctx) sh.ctx[w] = c;
+  }
   __syncthreads();
 
   int64_t tmax = 0;
@@ -351,33 +579,101 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(DevBatch b, int
   int64_t rounds = 0;
   for (;;) {
     int progress = 0;
-    for (uint32_t r = tid; r < R; r += nt) progress |= advance_host(b, c, r);
+    for (uint32_t r = tid; r < R; r += nt) progress |= host_step(b, sh, r, delay_job);
+    if (tid == 0) s_active = (int)min(R, (uint32_t)NW);
     __syncthreads();
-    for (uint32_t w = tid; w < W; w += nt) progress |= advance_walker(b, c, w, tmax, err);
+    if (wp < R) {
+      // a warp sweeps its FIFOs while anything in the CTA makes progress; an
+      // idle warp sleeps on the progress epoch; when every warp is idle the
+      // round ends (host syncs, termination and deadlock are decided there)
+      bool fresh = true;   // first sweep of the round re-examines every walker
+      for (;;) {
+        const uint32_t e0 = vload(&s_epoch);
+        bool pass = false;
+        PROF_T(t_sweep);
+        for (uint32_t r = wp; r < R; r += NW) {
+          const RankRec rr = b.ranks[J.ranks + r];
+          const uint32_t ns = b.reps[rr.rep].n_streams;
+          for (uint32_t w = rr.walker; w < rr.walker + ns; w++) {
+            WSt s = sh.st[w];
+            if (s.wk == WAKE_ROUND && !fresh) continue;
+            if (s.wk == WAKE_COUNT && vload((const uint32_t *)s.wa) < s.wt) continue;
+            if (s.wk == WAKE_FIRE && vload((const int64_t *)s.wa) < 0) continue;
+            WCtx c;
+            if (sh.ctx) {
+              if (s.i >= sh.ctx[w].len) continue;
+              c = sh.ctx[w];
+            } else {
+              load_ctx(b, J, w, record, c);
+            }
+            pass |= warp_walk(b, sh, c, s, tmax, err, lane);
+            __syncwarp();
+            if (lane == 0) sh.st[w] = s;
+          }
+        }
+        if (err) {
+          if (lane == 0) {
+            atomicAdd(&s_epoch, 1u);
+            atomicSub(&s_active, 1);
+          }
+          break;
+        }
+#ifdef MAYA_PROFILE
+        if (lane == 0) { PROF_ADD(3, clock64() - t_sweep); PROF_ADD(7, 1); }
+#endif
+        fresh = false;
+        if (pass) {
+          progress = 1;
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence_block();
+            atomicAdd(&s_epoch, 1u);
+          }
+          continue;
+        }
+        int wake = 0;
+        PROF_T(t_idle);
+        if (lane == 0) {
+          atomicSub(&s_active, 1);
+          unsigned ns = 32;
+          for (;;) {
+            if (vload(&s_epoch) != e0) { wake = 1; break; }
+            if (vload(&s_active) <= 0) break;
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+          }
+          if (wake) atomicAdd(&s_active, 1);
+        }
+        wake = __shfl_sync(FULL, wake, 0);
+#ifdef MAYA_PROFILE
+        if (lane == 0) { PROF_ADD(2, clock64() - t_idle); PROF_ADD(6, wake); }
+#endif
+        if (!wake) break;
+      }
+    }
     rounds++;
     if (err) { atomicMax(&s_err, err); progress = 0; }
     if (!__syncthreads_or(progress)) break;
   }
-  // completion + host end time (the trailing gaps extend the makespan, sim.py:365-366)
   for (uint32_t w = tid; w < W; w += nt) {
     const Walker wk = b.walkers[J.walkers + w];
     const RankRec rr = b.ranks[J.ranks + wk.rank];
     const StreamRange sr = b.streams[b.reps[rr.rep].streams + wk.stream];
-    if (c.ws[w].i < sr.len) s_incomplete = 1;
+    if (sh.st[w].i < sr.len) s_incomplete = 1;
   }
+  // epilogue: host end time, peak memory, first OOM (sim.py:235-242, 365-366)
   for (uint32_t r = tid; r < R; r += nt) {
     const RankRec rr = b.ranks[J.ranks + r];
     const RepHdr &h = b.reps[rr.rep];
-    const uint32_t k = c.ws[W + r].i;
+    const uint32_t k = sh.hostk[r];
     if (k < h.n_syncs) { s_incomplete = 1; continue; }
-    const int64_t hend = h.gend + c.delay[rr.delay + h.n_syncs];
+    const int64_t hend = h.gend + delay_job[rr.delay + h.n_syncs];
     if (hend > tmax) tmax = hend;
     const RepOut ro = b.repout[rr.rep];
     atomicMax(&s_peak, (long long)ro.peak);
     if (ro.first_exceed >= 0) {
       const MemRec m = b.mems[h.mems + ro.first_exceed];
-      const int64_t t = m.gpre + c.delay[rr.delay + m.seg];
-      atomicMin(&s_oom_t, (long long)t);
+      atomicMin(&s_oom_t, (long long)(m.gpre + delay_job[rr.delay + m.seg]));
     }
   }
   atomicMax(&s_tmax, (unsigned long long)tmax);
@@ -388,7 +684,7 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(DevBatch b, int
     if (ro.first_exceed >= 0 && !s_incomplete) {
       const RepHdr &h = b.reps[rr.rep];
       const MemRec m = b.mems[h.mems + ro.first_exceed];
-      if (m.gpre + c.delay[rr.delay + m.seg] == s_oom_t) atomicMin(&s_oom_rank, (int)r);
+      if (m.gpre + delay_job[rr.delay + m.seg] == s_oom_t) atomicMin(&s_oom_rank, (int)r);
     }
   }
   __syncthreads();
@@ -414,8 +710,57 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(DevBatch b, int
   }
 }
 
-void launch_schedule(const DevBatch &b, int record, cudaStream_t s) {
-  if (b.n_jobs) schedule_kernel<<<b.n_jobs, SCHED_THREADS, 0, s>>>(b, record);
+static const uint32_t SCHED_SMEM_CAP = 96 * 1024;
+
+int sched_variant(uint32_t W, uint32_t R) {
+  (void)W;
+  const uint32_t nw = sched_warps(R);
+  return nw == 4 ? 0 : nw == 8 ? 1 : 2;
+}
+
+void launch_resolve(const DevBatch &b, cudaStream_t s) {
+  if (b.n_ops) resolve_kernel<<<(unsigned)((b.n_ops + 255) / 256), 256, 0, s>>>(b);
+}
+
+template <int NW>
+static void launch_nw(const DevBatch &b, const int32_t *order, uint32_t n, int record,
+                      uint32_t smem, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sched_warp_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SCHED_SMEM_CAP);
+    attr = true;
+  }
+  sched_warp_kernel<NW><<<n, NW * 32, smem, s>>>(b, order, record, smem);
+}
+
+void launch_schedule_variant(const DevBatch &b, int variant, const int32_t *order, uint32_t n,
+                             int record, uint32_t smem, cudaStream_t s) {
+  if (!n) return;
+  if (smem > SCHED_SMEM_CAP) smem = SCHED_SMEM_CAP;
+  switch (variant) {
+    case 0: launch_nw<4>(b, order, n, record, smem, s); break;
+    case 1: launch_nw<8>(b, order, n, record, smem, s); break;
+    default: launch_nw<16>(b, order, n, record, smem, s); break;
+  }
+}
+
+uint32_t sched_smem_cap() { return SCHED_SMEM_CAP; }
+
+int prof_read(unsigned long long *out8, int reset) {
+#ifdef MAYA_PROFILE
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, g_prof, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_prof, z, sizeof z);
+  }
+  return 1;
+#else
+  (void)out8;
+  (void)reset;
+  return 0;
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -8,6 +8,10 @@
 
 namespace maya {
 
+// ExecOp.w sentinels
+static const uint64_t EXEC_BAD = ~0ull << 2;             // KERN whose estimator failed
+static const uint64_t EXEC_NONE = ((~0ull) >> 2) << 2;   // WAIT on a never-recorded event
+
 // Device view of one uploaded batch (all pointers into the device arena).
 struct DevBatch {
   const JobHdr *jobs;
@@ -15,7 +19,8 @@ struct DevBatch {
   const uint32_t *rank_comm;
   const CommRec *comms;
   const SlotRec *slots;
-  const Walker *walkers;
+  const Walker *walkers;      // heaviest stream first
+  const uint32_t *wids;       // rank-major (rank, stream) -> walker index
   const RepHdr *reps;
   const Op *ops;
   const StreamRange *streams;
@@ -25,12 +30,14 @@ struct DevBatch {
   const uint32_t *counts;
   const MemRec *mems;
   const Feature *feats;
+  const RankColl *rcolls;
+  ExecOp *exec;
   // scratch / outputs
   int64_t *feat_ns;
   int64_t *wire;
   int64_t *fire;
   int64_t *delay;
-  WState *wstate;
+  uint8_t *spill;             // per-job global spill (JobHdr.wstate = byte offset)
   CollSlot *cslots;
   RepOut *repout;
   int64_t *tl_start;
@@ -39,6 +46,7 @@ struct DevBatch {
   const int32_t *order;       // CTA -> job (largest first)
   int32_t *err_flag;          // any estimator failure
   uint32_t n_jobs, n_reps, n_feats, n_slots;
+  uint64_t n_ops;
 };
 
 struct DevTables {
@@ -51,7 +59,12 @@ struct DevTables {
 
 void launch_estimate(const DevBatch &b, const DevTables &t, cudaStream_t s);
 void launch_memscan(const DevBatch &b, cudaStream_t s);
-void launch_schedule(const DevBatch &b, int record, cudaStream_t s);
+int sched_variant(uint32_t n_walkers, uint32_t n_ranks);   // 0..3
+void launch_resolve(const DevBatch &b, cudaStream_t s);
+void launch_schedule_variant(const DevBatch &b, int variant, const int32_t *order, uint32_t n,
+                             int record, uint32_t smem, cudaStream_t s);
+uint32_t sched_smem_cap();
+int prof_read(unsigned long long *out8, int reset);   // MAYA_PROFILE builds only
 void launch_topk(const DevBatch &b, int k, maya_topk_entry *out, int32_t *n_out, void *scratch,
                  cudaStream_t s);
 size_t topk_scratch_bytes(uint32_t n_jobs, int k);

@@ -14,6 +14,7 @@
 // once per unique (op_kind, dtype, flops, bytes) (estimate.py:329-352).
 #include "pack.h"
 
+#include <algorithm>
 #include <cstring>
 #include <unordered_map>
 
@@ -100,6 +101,10 @@ void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
   std::vector<std::vector<uint32_t>> snap;  // per sync: ops dispatched per local stream
   std::unordered_map<int64_t, int64_t> alloc;
   std::unordered_map<uint64_t, uint32_t> coll_seen;
+  // ring eligibility: per local comm, one issuing stream and call_idx 0,1,2,...
+  std::vector<int32_t> comm_stream(n_local_comms, INT32_MIN);
+  std::vector<int64_t> comm_next(n_local_comms, 0);
+  bool ring_ok = true;
   const uint64_t coll0 = P.coll_lc.size();
   int64_t gpre = 0;
   uint32_t seg = 0;
@@ -189,6 +194,9 @@ void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
         uint64_t ck = ((uint64_t)f[0] << 32) | (uint64_t)f[1];
         if (!coll_seen.emplace(ck, 0).second)
           throw Fail{MAYA_ST_BAD_INPUT, "collective (comm, call_idx) issued twice by one rank"};
+        if (comm_stream[f[0]] == INT32_MIN) comm_stream[f[0]] = job.ev_stream[i];
+        if (comm_stream[f[0]] != job.ev_stream[i] || comm_next[f[0]] != f[1]) ring_ok = false;
+        comm_next[f[0]] = f[1] + 1;
         uint32_t ci = (uint32_t)(P.coll_lc.size() - coll0);
         P.coll_lc.push_back((uint32_t)f[0]);
         P.coll_idx.push_back((uint32_t)f[1]);
@@ -225,11 +233,196 @@ void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
   h.n_mems = (uint32_t)(P.mems.size() - mem0);
   h.gend = gpre;
   P.reps.push_back(h);
+  P.rep_ring_ok.push_back(ring_ok ? 1 : 0);
 }
 
 }  // namespace
 
-void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P) {
+// --- exact rank-class collapse -------------------------------
+//
+// Equitable refinement: colour = representative trace; refine by, for each
+// CommInit of the rank's representative in order, (topology, multiset of member
+// colours).  Ranks of one class see identical inputs at every step of the
+// max-plus iteration, so their op times are identical (Kleene iteration from a
+// class-constant start stays class-constant).  The reduced job simulates one
+// rank per class; communicators reached from class members at the same local
+// index are identified (union-find) and must resolve consistently, otherwise
+// the job is simulated full-rank.  A collective of a reduced communicator
+// waits for one arrival per member class; its wire time keeps the real nranks
+// and topology.
+struct SimView {
+  std::vector<int32_t> rank_orig;              // sim rank -> original rank
+  std::vector<int32_t> rank_sim;               // original rank -> sim rank
+  std::vector<std::vector<int32_t>> rank_comm; // sim rank -> sim comm per local index
+  std::vector<int32_t> comm_real;              // sim comm -> a real comm (calls, topo, nranks)
+  std::vector<int32_t> comm_rdv;               // sim comm -> arrivals per call
+};
+
+namespace {
+
+struct DSU {
+  std::vector<int32_t> p;
+  explicit DSU(int n) : p(n) { for (int i = 0; i < n; i++) p[i] = i; }
+  int find(int x) { while (p[x] != x) { p[x] = p[p[x]]; x = p[x]; } return x; }
+  void unite(int a, int b) { a = find(a); b = find(b); if (a != b) p[std::max(a, b)] = std::min(a, b); }
+};
+
+uint64_t mix64(uint64_t h, uint64_t v) {
+  h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  return h * 0xff51afd7ed558ccdull;
+}
+
+bool build_collapsed(const maya_raw_job &job, const std::vector<uint32_t> &rep_comms,
+                     SimView &V) {
+  const int R = job.num_ranks, G = job.n_comms;
+  if (R <= 1) return false;
+  std::vector<std::vector<int32_t>> members(G);
+  for (int r = 0; r < R; r++)
+    for (int64_t q = job.rank_comm_off[r]; q < job.rank_comm_off[r + 1]; q++)
+      members[job.rank_comm[q]].push_back(r);
+  std::vector<int32_t> color(R);
+  int ncol = 0;
+  {
+    std::unordered_map<int32_t, int32_t> m;
+    for (int r = 0; r < R; r++) {
+      auto it = m.emplace(job.rank_rep[r], (int32_t)m.size()).first;
+      color[r] = it->second;
+    }
+    ncol = (int)m.size();
+  }
+  for (int iter = 0; iter < 64; iter++) {
+    std::vector<uint64_t> csig(G);
+    std::vector<int32_t> buf;
+    for (int g = 0; g < G; g++) {
+      buf.clear();
+      for (int32_t m : members[g]) buf.push_back(color[m]);
+      std::sort(buf.begin(), buf.end());
+      uint64_t h = mix64(0x51ed, (uint64_t)job.comm_topo[g]);
+      for (int32_t x : buf) h = mix64(h, (uint64_t)x);
+      csig[g] = h;
+    }
+    // exact signature: (colour, [(comm signature) per local index]); hashed
+    // signatures are confirmed by full comparison
+    std::unordered_map<uint64_t, std::vector<int32_t>> buckets;
+    std::vector<int32_t> ncolor(R, -1);
+    int n2 = 0;
+    auto sig_of = [&](int r) {
+      std::vector<uint64_t> s;
+      s.push_back((uint64_t)color[r]);
+      for (int64_t q = job.rank_comm_off[r]; q < job.rank_comm_off[r + 1]; q++)
+        s.push_back(csig[job.rank_comm[q]]);
+      return s;
+    };
+    std::vector<std::vector<uint64_t>> sigs(R);
+    for (int r = 0; r < R; r++) {
+      sigs[r] = sig_of(r);
+      uint64_t h = 0x9e37;
+      for (uint64_t v : sigs[r]) h = mix64(h, v);
+      auto &bk = buckets[h];
+      int found = -1;
+      for (int32_t o : bk)
+        if (sigs[o] == sigs[r]) { found = ncolor[o]; break; }
+      if (found < 0) { found = n2++; bk.push_back(r); }
+      ncolor[r] = found;
+    }
+    bool stable = n2 == ncol;
+    color.swap(ncolor);
+    ncol = n2;
+    if (stable) break;
+    if (iter == 63) return false;
+  }
+  if (ncol == R) return false;  // nothing to collapse
+  // class representatives: lowest rank
+  std::vector<int32_t> rho(ncol, -1);
+  for (int r = 0; r < R; r++)
+    if (rho[color[r]] < 0) rho[color[r]] = r;
+  // identify communicators reached at the same local index by class members
+  DSU dsu(G);
+  for (int r = 0; r < R; r++) {
+    const int p = rho[color[r]];
+    const int64_t nr = job.rank_comm_off[r + 1] - job.rank_comm_off[r];
+    if (nr != job.rank_comm_off[p + 1] - job.rank_comm_off[p]) return false;
+    for (int64_t k = 0; k < nr; k++)
+      dsu.unite(job.rank_comm[job.rank_comm_off[r] + k], job.rank_comm[job.rank_comm_off[p] + k]);
+  }
+  // every reduced comm: one local index per member class, equal call tables
+  std::unordered_map<int32_t, int32_t> sim_of;   // dsu root -> sim comm
+  V = SimView();
+  V.rank_sim.assign(color.begin(), color.end());
+  for (int c = 0; c < ncol; c++) {
+    const int p = rho[c];
+    V.rank_orig.push_back(p);
+    std::vector<int32_t> lc;
+    std::vector<int32_t> roots;
+    for (int64_t q = job.rank_comm_off[p]; q < job.rank_comm_off[p + 1]; q++) {
+      const int32_t g = job.rank_comm[q];
+      const int32_t root = dsu.find(g);
+      for (int32_t x : roots)
+        if (x == root) return false;  // two local comms of one class fold together
+      roots.push_back(root);
+      auto it = sim_of.find(root);
+      if (it == sim_of.end()) {
+        it = sim_of.emplace(root, (int32_t)V.comm_real.size()).first;
+        V.comm_real.push_back(g);
+        V.comm_rdv.push_back(0);
+      }
+      lc.push_back(it->second);
+    }
+    V.rank_comm.push_back(std::move(lc));
+  }
+  // arrivals per call = number of member classes; check group consistency
+  std::vector<std::vector<int32_t>> cls_of(V.comm_real.size());
+  for (int g = 0; g < G; g++) {
+    auto it = sim_of.find(dsu.find(g));
+    if (it == sim_of.end()) continue;
+    const int32_t sg = it->second, g0 = V.comm_real[sg];
+    if (job.comm_topo[g] != job.comm_topo[g0] || job.comm_nranks[g] != job.comm_nranks[g0])
+      return false;
+    const int64_t n0 = job.call_off[g0 + 1] - job.call_off[g0];
+    if (job.call_off[g + 1] - job.call_off[g] != n0) return false;
+    for (int64_t i = 0; i < n0; i++) {
+      const int64_t a = job.call_off[g] + i, b = job.call_off[g0] + i;
+      if (job.call_kind[a] != job.call_kind[b] || job.call_bytes[a] != job.call_bytes[b])
+        return false;
+      if (job.wire_ns && job.wire_ns[a] != job.wire_ns[b]) return false;
+    }
+    for (int32_t m : members[g]) cls_of[sg].push_back(color[m]);
+  }
+  for (size_t sg = 0; sg < cls_of.size(); sg++) {
+    auto &v = cls_of[sg];
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    V.comm_rdv[sg] = (int32_t)v.size();
+    // each member class's representative must reach this comm exactly once
+    for (int32_t cl : v) {
+      int hits = 0;
+      for (int32_t x : V.rank_comm[cl]) hits += (x == (int32_t)sg);
+      if (hits != 1) return false;
+    }
+  }
+  (void)rep_comms;
+  return true;
+}
+
+void full_view(const maya_raw_job &job, SimView &V) {
+  V = SimView();
+  for (int r = 0; r < job.num_ranks; r++) {
+    V.rank_orig.push_back(r);
+    V.rank_sim.push_back(r);
+    std::vector<int32_t> lc;
+    for (int64_t q = job.rank_comm_off[r]; q < job.rank_comm_off[r + 1]; q++)
+      lc.push_back(job.rank_comm[q]);
+    V.rank_comm.push_back(std::move(lc));
+  }
+  for (int g = 0; g < job.n_comms; g++) {
+    V.comm_real.push_back(g);
+    V.comm_rdv.push_back(job.comm_nranks[g]);
+  }
+}
+
+}  // namespace
+
+void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P, bool collapse) {
   P = JobPack();
   JobHdr &H = P.hdr;
   H.key_rank = key_rank;
@@ -246,14 +439,33 @@ void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P) {
       pack_rep(job, rep, P, feat_map, fixed_map, rep_comms[rep]);
       P.reps.back().job = 0;
     }
-    // communicators and their call slots (JobTrace.groups / .calls)
+    // validate rank tables
+    for (int r = 0; r < job.num_ranks; r++) {
+      int rep = job.rank_rep[r];
+      if (rep < 0 || rep >= job.n_reps) throw Fail{MAYA_ST_BAD_INPUT, "rank_rep out of range"};
+      int64_t cb = job.rank_comm_off[r], ce = job.rank_comm_off[r + 1];
+      if ((uint64_t)(ce - cb) < rep_comms[rep])
+        throw Fail{MAYA_ST_BAD_INPUT, "rank lacks comm translation"};
+      for (int64_t q = cb; q < ce; q++)
+        if (job.rank_comm[q] < 0 || job.rank_comm[q] >= job.n_comms)
+          throw Fail{MAYA_ST_BAD_INPUT, "rank_comm out of range"};
+    }
     const int64_t n_calls = job.call_off[job.n_comms];
     if (n_calls > 0x7fffffff) throw Fail{MAYA_ST_BAD_INPUT, "too many group calls"};
-    for (int g = 0; g < job.n_comms; g++) {
-      CommRec c{job.comm_nranks[g], job.comm_topo[g], (uint32_t)job.call_off[g],
-                (uint32_t)(job.call_off[g + 1] - job.call_off[g])};
-      if (c.topo < 0 || c.topo > 2) throw Fail{MAYA_ST_BAD_INPUT, "topology class"};
-      P.comms.push_back(c);
+    // the ranks / communicators the scheduler simulates (collapsed or full)
+    SimView V;
+    P.collapsed = collapse && build_collapsed(job, rep_comms, V);
+    if (!P.collapsed) full_view(job, V);
+    P.rank_orig = V.rank_orig;
+    P.rank_sim = V.rank_sim;
+    // communicators and their call slots (JobTrace.groups / .calls)
+    for (size_t sg = 0; sg < V.comm_real.size(); sg++) {
+      const int g = V.comm_real[sg];
+      CommRec cr{job.comm_nranks[g], job.comm_topo[g], (uint32_t)P.slots.size(),
+                 (uint32_t)(job.call_off[g + 1] - job.call_off[g])};
+      if (cr.topo < 0 || cr.topo > 2) throw Fail{MAYA_ST_BAD_INPUT, "topology class"};
+      P.comms.push_back(cr);
+      P.comm_rdv.push_back(V.comm_rdv[sg]);
       for (int64_t s = job.call_off[g]; s < job.call_off[g + 1]; s++) {
         int64_t fixed = -1;
         if (job.wire_ns && job.call_kind[s] >= 0) {
@@ -261,49 +473,62 @@ void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P) {
           if (fixed < 0) throw Fail{MAYA_ST_BAD_INPUT, "negative host wire time"};
         }
         if (job.call_kind[s] > 4) throw Fail{MAYA_ST_BAD_INPUT, "collective kind"};
-        P.slots.push_back(SlotRec{job.call_bytes[s], fixed, job.call_kind[s], c.nranks, c.topo,
+        P.slots.push_back(SlotRec{job.call_bytes[s], fixed, job.call_kind[s], cr.nranks, cr.topo,
                                   job.device});
       }
     }
-    // ranks
-    uint64_t fire = 0, delay = 0, walk = 0, tl = 0;
+    // work accounting over ALL ranks (sim.py:183-184)
     int64_t rank_ops = 0, dev_ops = 0;
     for (int r = 0; r < job.num_ranks; r++) {
-      int rep = job.rank_rep[r];
-      if (rep < 0 || rep >= job.n_reps) throw Fail{MAYA_ST_BAD_INPUT, "rank_rep out of range"};
+      const RepHdr &h = P.reps[job.rank_rep[r]];
+      rank_ops += h.n_events;
+      dev_ops += h.n_ops;
+    }
+    // simulated ranks
+    uint64_t fire = 0, delay = 0, walk = 0, tl = 0;
+    for (size_t sr = 0; sr < V.rank_orig.size(); sr++) {
+      const int rep = job.rank_rep[V.rank_orig[sr]];
       const RepHdr &h = P.reps[rep];
-      int64_t cb = job.rank_comm_off[r], ce = job.rank_comm_off[r + 1];
-      if ((uint64_t)(ce - cb) < rep_comms[rep])
-        throw Fail{MAYA_ST_BAD_INPUT, "rank lacks comm translation"};
       RankRec rr{(uint32_t)rep, (uint32_t)P.rank_comm.size(), (uint32_t)fire, (uint32_t)delay,
-                 (uint32_t)walk, (uint32_t)tl};
-      for (int64_t q = cb; q < ce; q++) {
-        int32_t g = job.rank_comm[q];
-        if (g < 0 || g >= job.n_comms) throw Fail{MAYA_ST_BAD_INPUT, "rank_comm out of range"};
-        P.rank_comm.push_back((uint32_t)g);
-      }
-      for (uint32_t s = 0; s < h.n_streams; s++) P.walkers.push_back(Walker{(uint32_t)r, s});
+                 (uint32_t)walk, (uint32_t)tl, 0, 0};
+      for (int32_t g : V.rank_comm[sr]) P.rank_comm.push_back((uint32_t)g);
+      for (uint32_t s = 0; s < h.n_streams; s++) P.walkers.push_back(Walker{(uint32_t)sr, s});
       P.ranks.push_back(rr);
       fire += h.n_recs;
       delay += h.n_syncs + 1;
       walk += h.n_streams;
       tl += h.n_ops;
-      rank_ops += h.n_events;
-      dev_ops += h.n_ops;
       if (fire > 0xffffffffull || delay > 0xffffffffull || tl > 0xffffffffull)
         throw Fail{MAYA_ST_BAD_INPUT, "job too large for 32-bit per-job tables"};
     }
-    // each collective of a rep must address a real call slot for every rank
-    for (int r = 0; r < job.num_ranks; r++) {
-      const RepHdr &h = P.reps[job.rank_rep[r]];
-      const RankRec &rr = P.ranks[r];
-      for (uint32_t c = 0; c < h.n_colls; c++) {
-        uint32_t g = P.rank_comm[rr.comm + P.coll_lc[h.colls + c]];
-        if (P.coll_idx[h.colls + c] >= P.comms[g].n_calls ||
-            P.slots[P.comms[g].call_base + P.coll_idx[h.colls + c]].kind < 0)
+    // each collective of a rep must address a real call slot for every rank;
+    // per-rank collective tables (arrivals | comm | call_idx)
+    bool ring = P.comms.size() <= 0xffff;
+    for (uint8_t ok : P.rep_ring_ok) ring = ring && ok;
+    for (size_t sr = 0; sr < P.ranks.size(); sr++) {
+      RankRec &rr = P.ranks[sr];
+      const RepHdr &h = P.reps[rr.rep];
+      rr.rslot = (uint32_t)P.rcolls.size();
+      for (uint32_t c2 = 0; c2 < h.n_colls; c2++) {
+        uint32_t g = P.rank_comm[rr.comm + P.coll_lc[h.colls + c2]];
+        uint32_t idx = P.coll_idx[h.colls + c2];
+        if (idx >= P.comms[g].n_calls || P.slots[P.comms[g].call_base + idx].kind < 0)
           throw Fail{MAYA_ST_BAD_INPUT, "collective call missing from the job's call table"};
+        int64_t nr = P.comm_rdv[g];
+        if (nr < 1 || nr > 0xffff || g > 0xffff)
+          throw Fail{MAYA_ST_BAD_INPUT, "communicator too large for the engine"};
+        if (ring && (uint64_t)(P.comms[g].n_calls / 2 + 1) * (uint64_t)nr > 0xffffffffull)
+          ring = false;
+        P.rcolls.push_back(((uint64_t)nr << 48) | ((uint64_t)g << 32) | idx);
       }
+      if (P.rcolls.size() > 0xffffffffull) throw Fail{MAYA_ST_BAD_INPUT, "too many collectives"};
     }
+    // walkers rank-major: a scheduler warp owns whole ranks
+    P.wids.resize(P.walkers.size());
+    for (size_t w = 0; w < P.walkers.size(); w++) P.wids[w] = (uint32_t)w;
+    H.flags = ring ? JOB_RING : 0;
+    H.n_rcolls = (uint32_t)P.rcolls.size();
+    H.n_ranks = (uint32_t)P.ranks.size();
     H.n_comms = (uint32_t)P.comms.size();
     H.n_slots = (uint32_t)P.slots.size();
     H.n_walkers = (uint32_t)P.walkers.size();

@@ -24,12 +24,19 @@ struct JobPack {
   std::vector<SlotRec> slots;
   std::vector<RankRec> ranks;
   std::vector<uint32_t> rank_comm;
-  std::vector<Walker> walkers;
+  std::vector<Walker> walkers;         // rank-major (rank, local stream)
+  std::vector<uint32_t> wids;          // rank-major (rank, stream) -> index into walkers
+  std::vector<RankColl> rcolls;        // per rank, per rep collective
+  std::vector<uint8_t> rep_ring_ok;    // per rep: every comm used from one stream, idx 0,1,..
+  std::vector<int32_t> comm_rdv;        // arrivals per call of each simulated comm
+  std::vector<int32_t> rank_orig;       // simulated rank -> original rank
+  std::vector<int32_t> rank_sim;        // original rank -> simulated rank
+  bool collapsed = false;               // ranks are classes
   uint64_t n_fire = 0, n_delay = 0;
   std::string message;                 // why status != OK
 };
 
 // Pack one job.  Never throws; input problems become hdr.status + message.
-void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &out);
+void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &out, bool collapse);
 
 }  // namespace maya

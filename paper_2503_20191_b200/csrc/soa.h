@@ -31,8 +31,49 @@ enum OpTag : uint32_t { TAG_KERN = 0, TAG_COLL = 1, TAG_REC = 2, TAG_WAIT = 3 };
 enum SyncType : uint32_t { SYNC_ESYNC = 0, SYNC_SSYNC = 1, SYNC_DSYNC = 2 };
 
 static const uint32_t NO_REC = 0xFFFFFFFFu;
-// jobs whose walker + rank states fit are scheduled out of shared memory
-static const uint32_t SMEM_STATES = 2560;
+// On-chip layout of one job inside a scheduler CTA (shared by the engine,
+// which sizes dynamic shared memory, and the kernel).  When the whole layout
+// does not fit the CTA's dynamic shared memory, host-sync counters and walker
+// states go to a per-job global spill area of spill_bytes() and collectives
+// rendezvous through global slots.
+struct SchedLayout {
+  uint32_t ring, cb, hostk, state, ctx, bytes;   // byte offsets / total
+  bool ring_on;                             // smem rings for collectives
+};
+static const uint32_t RING_MAX_COMMS = 4096;
+static const uint32_t WSTATE_BYTES = 48;
+static const uint32_t WCTX_BYTES = 64;
+__host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+__host__ __device__ inline SchedLayout sched_layout(uint32_t W, uint32_t R, uint32_t n_comms,
+                                                    bool ring_flag) {
+  SchedLayout L;
+  L.ring_on = ring_flag && n_comms <= RING_MAX_COMMS;
+  uint32_t off = 0;
+  L.ring = off;
+  if (L.ring_on) off += 32u * n_comms;
+  L.cb = off;
+  off = align16(off + 4u * n_comms);
+  L.hostk = off;
+  off = align16(off + 4u * R);
+  L.state = off;
+  off += WSTATE_BYTES * W;
+  L.ctx = off;
+  off += WCTX_BYTES * W;
+  L.bytes = off;
+  return L;
+}
+// global spill (hostk + states) for jobs whose layout exceeds the CTA budget
+inline uint64_t spill_bytes(uint64_t W, uint64_t R) {
+  return ((4 * R + 15) & ~15ull) + WSTATE_BYTES * W + 16;
+}
+// warps per scheduler CTA for a job with R ranks (4..16, power of two): a
+// warp owns all stream FIFOs of its ranks (they are coupled by event
+// record/wait; ranks couple only through collectives)
+__host__ __device__ inline uint32_t sched_warps(uint32_t R) {
+  uint32_t nw = 4;
+  while (nw < R && nw < 16) nw <<= 1;
+  return nw;
+}
 
 // 16-byte device op record.
 struct alignas(16) Op {
@@ -114,7 +155,22 @@ struct RankRec {
   uint32_t delay;      // job-local delay-table base (n_syncs + 1 entries)
   uint32_t walker;     // job-local index of this rank's first walker
   uint32_t tl;         // job-local timeline base (sum of device ops of lower ranks)
+  uint32_t rslot;      // job-local base of this rank's collective table (one per rep coll)
+  uint32_t pad;
 };
+
+// Scheduler op record, produced on device by the resolve pass from Op and the
+// estimator output: everything a walker needs, no dependent gathers.
+struct alignas(16) ExecOp {
+  int64_t disp;        // gap prefix (host dispatch offset)
+  uint64_t w;          // tag (2 bits) | payload << 2: KERN duration, REC/WAIT ordinal,
+                       // COLL rep-local collective index
+};
+
+// Per-(rank, rep collective) entry: nranks << 48 | job-local comm << 32 | call_idx
+typedef uint64_t RankColl;
+
+enum JobFlags : uint32_t { JOB_RING = 1 };  // collectives rendezvous in shared-memory rings
 
 struct JobHdr {
   uint64_t ranks;      // batch RankRec index
@@ -125,14 +181,17 @@ struct JobHdr {
   uint64_t feats;      // batch feature index
   uint64_t fire;       // batch fire-table base (int64 entries)
   uint64_t delay;      // batch delay-table base (int64 entries)
-  uint64_t wstate;     // batch walker-state base
+  uint64_t wstate;     // byte offset of the job's spill area (scheduler state overflow)
   uint64_t timeline;   // batch timeline base (per rank-op slots), if recorded
+  uint64_t rcolls;     // batch RankColl base
   int64_t capacity;
   int64_t rank_ops;
   int64_t dev_ops;     // sum over ranks of device ops (dispatched == completed when OK)
   uint32_t n_ranks, n_comms, n_slots, n_walkers, n_feats, device;
   int32_t key_rank;
   int32_t status;      // pre-set by the packer (BAD_INPUT, INTERNAL) else 0
+  uint32_t flags;      // JobFlags
+  uint32_t n_rcolls;
 };
 
 struct Walker {
@@ -140,11 +199,6 @@ struct Walker {
   uint32_t stream;     // local stream index of rank's rep
 };
 
-struct WState {        // per-walker scheduler state
-  int64_t x;           // completion time of the last op processed
-  uint32_t i;          // next op (stream-relative)
-  uint32_t flags;      // bit0: arrival posted for the collective at i
-};
 
 struct CollSlot {      // collective rendezvous (sim.py:326-343)
   unsigned long long maxarr;

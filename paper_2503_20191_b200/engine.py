@@ -29,7 +29,7 @@ EXPORTED = (
     "maya_topk", "maya_timeline_size", "maya_timeline", "maya_last_timings",
     "maya_get_stream", "maya_arena_bytes", "maya_gen_job", "maya_gen_view_of", "maya_gen_free",
     "maya_gen_op_kind_name", "maya_gen_dtype_name", "maya_batch_add_generated",
-    "maya_batch_stats",
+    "maya_batch_stats", "maya_set_options", "maya_batch_collapsed", "maya_prof_read",
 )
 
 
@@ -69,6 +69,8 @@ def lib():
     L.maya_arena_bytes.argtypes = [vp]
     L.maya_arena_bytes.restype = C.c_int64
     L.maya_batch_stats.argtypes = [vp, P(C.c_int64)]
+    L.maya_set_options.argtypes = [vp, C.c_int32]
+    L.maya_batch_collapsed.argtypes = [vp, P(C.c_uint8)]
     _lib = L
     return L
 
@@ -97,13 +99,23 @@ class Timeline:
 class Engine:
     """One engine per CUDA device (C ABI: maya_open ... maya_close)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, collapse: bool = True):
         L = lib()
         self._h = C.c_void_p()
         _check(L.maya_open(int(device), C.byref(self._h)))
+        self.set_collapse(collapse)
         self.device = device
         self.batch: Batch | None = None
         self.n_jobs = 0
+
+    def set_collapse(self, on: bool) -> None:
+        """Exact rank-class collapse of deduplicated jobs."""
+        _check(lib().maya_set_options(self._h, 1 if on else 0))
+
+    def collapsed(self) -> np.ndarray:
+        out = np.zeros(max(self.n_jobs, 1), dtype=np.uint8)
+        _check(lib().maya_batch_collapsed(self._h, out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out[:self.n_jobs].astype(bool)
 
     def close(self) -> None:
         if self._h:
@@ -187,10 +199,10 @@ class Engine:
         return s.value or 0
 
     def batch_stats(self) -> dict:
-        o = (C.c_int64 * 10)()
+        o = (C.c_int64 * 12)()
         _check(lib().maya_batch_stats(self._h, o))
         keys = ("jobs", "rep_events", "rank_comms", "features", "slots", "device_ops",
-                "rank_ops", "arena_bytes", "ranks", "reps")
+                "rank_ops", "arena_bytes", "ranks", "reps", "run_launches", "topk_launches")
         return {k: int(v) for k, v in zip(keys, o)}
 
     def arena_bytes(self) -> int:
