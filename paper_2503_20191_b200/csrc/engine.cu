@@ -69,8 +69,8 @@ struct maya_engine {
   DevTables tables{};
   // segments
   Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_slots, s_walkers, s_reps, s_ops, s_streams,
-      s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids;
-  Seg x_exec, x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
+      s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot;
+  Seg x_exec, x_rcw, x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
       x_results, x_err, x_topk, x_topk_out, x_topk_n;
   uint64_t n_tl = 0;
   std::vector<uint64_t> job_tl;      // per job timeline base
@@ -227,6 +227,7 @@ int maya_upload(maya_engine *e) {
   }
   if (n_reps > 0xffffffffull) return fail(MAYA_EINVAL, "too many representatives in batch");
   if (n_feats >= 0xffffffffull) return fail(MAYA_EINVAL, "too many kernel features in batch");
+  if (n_slots >= 0xffffffffull) return fail(MAYA_EINVAL, "too many collective calls in batch");
   e->n_tl = n_tl;
   // arena layout
   size_t off = 0;
@@ -253,10 +254,12 @@ int maya_upload(maya_engine *e) {
   seg(e->s_mems, n_mems * sizeof(MemRec));
   seg(e->s_feats, n_feats * sizeof(Feature));
   seg(e->s_rcolls, n_rcolls * sizeof(RankColl));
+  seg(e->s_rcslot, n_rcolls * sizeof(uint32_t));
   e->arena_bytes = off;
   // scratch layout
   off = 0;
   seg(e->x_exec, n_ops * sizeof(ExecOp));
+  seg(e->x_rcw, n_rcolls * sizeof(int64_t));
   seg(e->x_feat_ns, n_feats * 8);
   seg(e->x_wire, n_slots * 8);
   seg(e->x_fire, n_fire * 8);
@@ -404,6 +407,14 @@ int maya_upload(maya_engine *e) {
       }
     }
     CPY(s_rcolls, rcolls, B.rcolls)
+    {  // batch-global call slot of every rank-collective entry
+      uint32_t *dst = (uint32_t *)(H + e->s_rcslot.off) + B.rcolls;
+      for (size_t q = 0; q < P.rcolls.size(); q++) {
+        const RankColl ent = P.rcolls[q];
+        const uint32_t g = (uint32_t)(ent >> 32) & 0xffffu, idx = (uint32_t)ent;
+        dst[q] = (uint32_t)(B.slots + P.comms[g].call_base + idx);
+      }
+    }
     CPY(s_streams, streams, B.streams)
     CPY(s_coll_lc, coll_lc, B.colls)
     CPY(s_coll_idx, coll_idx, B.colls)
@@ -454,6 +465,9 @@ int maya_upload(maya_engine *e) {
   db.mems = (const MemRec *)(D + e->s_mems.off);
   db.feats = (const Feature *)(D + e->s_feats.off);
   db.rcolls = (const RankColl *)(D + e->s_rcolls.off);
+  db.rcslot = (const uint32_t *)(D + e->s_rcslot.off);
+  db.rcw = (int64_t *)(X + e->x_rcw.off);
+  db.n_rcolls = n_rcolls;
   db.exec = (ExecOp *)(X + e->x_exec.off);
   db.n_ops = n_ops;
   db.feat_ns = (int64_t *)(X + e->x_feat_ns.off);
@@ -508,6 +522,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
       e->d_scratch_cap = need;
       char *X = (char *)p;
       db.exec = (ExecOp *)(X + e->x_exec.off);
+      db.rcw = (int64_t *)(X + e->x_rcw.off);
       db.feat_ns = (int64_t *)(X + e->x_feat_ns.off);
       db.wire = (int64_t *)(X + e->x_wire.off);
       db.fire = (int64_t *)(X + e->x_fire.off);
@@ -556,7 +571,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   CU(cudaEventRecord(e->ev[3], e->stream));
   {
     int64_t n = (db.n_feats ? 1 : 0) + (db.n_slots ? 1 : 0) + (db.n_reps ? 1 : 0) +
-                (db.n_ops ? 1 : 0);
+                (db.n_ops ? 1 : 0) + (db.n_rcolls ? 1 : 0);
     for (int v = 0; v < 4; v++) n += e->var_n[v] ? 1 : 0;
     e->run_launches = n;
   }

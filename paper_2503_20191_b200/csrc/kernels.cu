@@ -176,6 +176,13 @@ __global__ void resolve_kernel(DevBatch b) {
   b.exec[i] = ExecOp{op.disp, (pay << 2) | tag};
 }
 
+// wire time of every (rank, rep collective) entry, gathered once per run
+__global__ void resolve_colls_kernel(DevBatch b) {
+  uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= b.n_rcolls) return;
+  b.rcw[e] = b.wire[b.rcslot[e]];
+}
+
 template <typename T>
 __device__ __forceinline__ T vload(const T *p) {
   return *(const volatile T *)p;
@@ -220,7 +227,7 @@ struct WCtx {
   const ExecOp *ops;      // stream's first op
   int64_t *fire;          // rank's record table
   const int64_t *delay;   // rank's host-delay table (n_syncs + 1)
-  const RankColl *rc;     // rank's collective table
+  uint64_t rc;            // batch index of the rank's collective table (rcolls / rcw)
   const uint32_t *cnt;    // counts[0][stream] of the rep (stride ns)
   uint64_t tl;            // timeline row of the stream's first op
   uint32_t len, rank, ns, nsync;
@@ -249,7 +256,7 @@ __device__ __forceinline__ void load_ctx(const DevBatch &b, const JobHdr &J, uin
   c.ops = b.exec + h.ops + sr.begin;
   c.fire = b.fire + J.fire + rr.fire;
   c.delay = b.delay + J.delay + rr.delay;
-  c.rc = b.rcolls + J.rcolls + rr.rslot;
+  c.rc = J.rcolls + rr.rslot;
   c.cnt = b.counts + h.counts + wk.stream;
   c.len = sr.len;
   c.rank = wk.rank;
@@ -267,72 +274,6 @@ struct SlowRes {
   uint32_t wt;      // wake target (WAKE_COUNT)
   const void *wa;   // wake address
 };
-
-// One op outside the scanned kernel runs: record, wait, collective
-// rendezvous (sim.py:287-347), or a kernel whose values need the exact
-// overflow-checked path.  Executed by lane 0 of the walker's warp.
-__device__ __noinline__ SlowRes slow_op(CollSlot *cslots, const int64_t *wire, CollSlot *ring,
-                                        const uint32_t *cbt, uint32_t cb_stride, unsigned *epoch,
-                                        int64_t *fire, const RankColl *rc, uint64_t w,
-                                        int64_t ready, uint32_t flags) {
-  const uint32_t tag = (uint32_t)(w & 3);
-  const uint64_t pay = w >> 2;
-  if (tag == TAG_KERN) {
-    if (w == EXEC_BAD)
-      return SlowRes{0, STEP_ERR | (flags << 2) | (MAYA_ST_ESTIMATION << 4), 0, nullptr};
-    if ((int64_t)pay > INT64_MAX - ready)
-      return SlowRes{0, STEP_ERR | (flags << 2) | (MAYA_ST_OVERFLOW << 4), 0, nullptr};
-    return SlowRes{ready + (int64_t)pay, STEP_OK | (flags << 2), 0, nullptr};
-  }
-  if (tag == TAG_REC) {
-    vstore(&fire[pay], ready);
-    __threadfence_block();
-    atomicAdd(epoch, 1u);   // wake warps waiting on this event
-    return SlowRes{ready, STEP_OK | (flags << 2), 0, nullptr};
-  }
-  if (tag == TAG_WAIT) {
-    if (pay == (EXEC_NONE >> 2))
-      return SlowRes{0, STEP_BLOCK | (flags << 2) | (WAKE_ROUND << 8), 0, nullptr};
-    const int64_t f = vload(&fire[pay]);
-    if (f < 0) return SlowRes{0, STEP_BLOCK | (flags << 2) | (WAKE_FIRE << 8), 0, &fire[pay]};
-    return SlowRes{ready > f ? ready : f, STEP_OK | (flags << 2), 0, nullptr};
-  }
-  // TAG_COLL: rendezvous of all members (sim.py:326-343)
-  const RankColl ent = rc[pay];
-  const uint32_t nr = (uint32_t)(ent >> 48);
-  const uint32_t g = (uint32_t)(ent >> 32) & 0xffffu;
-  const uint32_t idx = (uint32_t)ent;
-  const uint32_t cb = cbt[g * cb_stride];
-  CollSlot *cs;
-  uint32_t target;
-  if (ring) {
-    cs = ring + 2 * g + (idx & 1u);
-    target = ((idx >> 1) + 1u) * nr;
-  } else {
-    cs = cslots + cb + idx;
-    target = nr;
-  }
-  uint32_t adv = 0;
-  if (!(flags & 1u)) {
-    atomicMax(&cs->maxarr, (unsigned long long)ready);
-    __threadfence_block();
-    const uint32_t old = atomicAdd(&cs->count, 1u);
-    flags |= 1u;
-    adv = 1;
-    if (old + 1 == target) atomicAdd(epoch, 1u);   // wake the other members
-    if (old + 1 > target)
-      return SlowRes{0, STEP_ERR | (flags << 2) | (adv << 3) | (MAYA_ST_INTERNAL << 4)};
-    if (old + 1 < target) return SlowRes{0, STEP_BLOCK | (flags << 2) | (adv << 3)};
-  } else if (vload(&cs->count) < target) {
-    return SlowRes{0, STEP_BLOCK | (flags << 2)};
-  }
-  __threadfence_block();
-  const int64_t m = (int64_t)vload(&cs->maxarr);
-  const int64_t wt = wire[cb + idx];
-  if (wt > INT64_MAX - m)
-    return SlowRes{0, STEP_ERR | (flags << 2) | (adv << 3) | (MAYA_ST_OVERFLOW << 4)};
-  return SlowRes{m + wt, STEP_OK | (adv << 3)};   // flags cleared
-}
 
 __device__ __forceinline__ ExecOp load_exec(const ExecOp *p) {
   const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(p));
@@ -369,6 +310,16 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
     const uint32_t tag = (uint32_t)(e.w & 3);
     const uint64_t dur = e.w >> 2;
     const int64_t rdisp = e.disp + s.cdel;
+    // collective metadata of every COLL lane, loaded in parallel (overlaps the scan)
+    uint32_t c_nr = 0, c_gi = 0, c_cb = 0;
+    int64_t c_wt = 0;
+    if (valid && tag == TAG_COLL) {
+      const RankColl ent = __ldg(&b.rcolls[c.rc + dur]);
+      c_wt = __ldg(&b.rcw[c.rc + dur]);      // independent of ent: wire inlined by resolve
+      c_nr = (uint32_t)(ent >> 48);
+      c_gi = (uint32_t)(ent >> 32) & 0xffffu;
+      c_cb = (uint32_t)ent;                  // call_idx
+    }
     const bool special = valid && (tag != TAG_KERN || dur >= LIM_D || rdisp >= LIM_T ||
                                    s.x >= LIM_T);
     const uint32_t smask = __ballot_sync(FULL, special);
@@ -406,28 +357,104 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
       const int64_t qd = __shfl_sync(FULL, rdisp, q);
       const uint64_t qw = __shfl_sync(FULL, e.w, q);
       const int64_t ready = qd > xq ? qd : xq;
-      SlowRes r{0, 0, 0, nullptr};
+      const uint32_t qtag = (uint32_t)(qw & 3);
+      const uint64_t qpay = qw >> 2;
       PROF_T(t_slow);
-      if (lane == 0)
-        r = slow_op(b.cslots + J.slots, b.wire + J.slots, sh.ring, sh.cb, sh.cb_stride,
-                    sh.epoch, c.fire, c.rc, qw, ready, s.flags);
-      r.nx = __shfl_sync(FULL, r.nx, 0);
-      r.code = __shfl_sync(FULL, r.code, 0);
+      int64_t nx = 0;
+      uint32_t stc = STEP_OK, wk = WAKE_NONE, wt = 0, eno = 0;
+      const void *wa = nullptr;
+      if (qtag == TAG_KERN) {            // exact, overflow-checked path
+        if (qw == EXEC_BAD) { stc = STEP_ERR; eno = MAYA_ST_ESTIMATION; }
+        else if ((int64_t)qpay > INT64_MAX - ready) { stc = STEP_ERR; eno = MAYA_ST_OVERFLOW; }
+        else nx = ready + (int64_t)qpay;
+      } else if (qtag == TAG_REC) {      // fire the event (sim.py:287-300)
+        if (lane == 0) vstore(&c.fire[qpay], ready);
+        nx = ready;
+      } else if (qtag == TAG_WAIT) {     // StreamWaitEvent (sim.py:311-319)
+        if (qpay == (EXEC_NONE >> 2)) {
+          stc = STEP_BLOCK;
+          wk = WAKE_ROUND;
+        } else {
+          const int64_t f = vload(&c.fire[qpay]);
+          if (f < 0) {
+            stc = STEP_BLOCK;
+            wk = WAKE_FIRE;
+            wa = &c.fire[qpay];
+          } else {
+            nx = ready > f ? ready : f;
+          }
+        }
+      } else {                           // collective rendezvous (sim.py:326-343)
+        const uint32_t nr = __shfl_sync(FULL, c_nr, q);
+        const int64_t w8 = __shfl_sync(FULL, c_wt, q);
+        if (nr == 1) {                   // one member (class): no wait
+          if (w8 > INT64_MAX - ready) { stc = STEP_ERR; eno = MAYA_ST_OVERFLOW; }
+          else nx = ready + w8;
+        } else {
+          const uint32_t g = __shfl_sync(FULL, c_gi, q);
+          const uint32_t idx = __shfl_sync(FULL, c_cb, q);
+          const uint32_t slot = sh.cb[g * sh.cb_stride] + idx;
+          CollSlot *cs;
+          uint32_t target;
+          if (sh.ring) {
+            cs = sh.ring + 2 * g + (idx & 1u);
+            target = ((idx >> 1) + 1u) * nr;
+          } else {
+            cs = b.cslots + J.slots + slot;
+            target = nr;
+          }
+          uint32_t code = 0;
+          if (lane == 0) {
+            bool done = true;
+            if (!(s.flags & 1u)) {
+              atomicMax(&cs->maxarr, (unsigned long long)ready);
+              __threadfence_block();
+              const uint32_t old = atomicAdd(&cs->count, 1u);
+              code |= 2u;                               // arrival posted
+              if (old + 1 > target) code |= 4u;         // internal error
+              else if (old + 1 < target) done = false;
+            } else if (vload(&cs->count) < target) {
+              done = false;
+            }
+            if (done && !(code & 4u)) {
+              __threadfence_block();
+              nx = (int64_t)vload(&cs->maxarr);
+              code |= 1u;
+            }
+          }
+          code = __shfl_sync(FULL, code, 0);
+          nx = __shfl_sync(FULL, nx, 0);
+          if (code & 2u) { s.flags |= 1u; adv = true; }
+          if (code & 4u) {
+            stc = STEP_ERR;
+            eno = MAYA_ST_INTERNAL;
+          } else if (!(code & 1u)) {
+            stc = STEP_BLOCK;
+            wk = WAKE_COUNT;
+            wt = target;
+            wa = &cs->count;
+          } else if (w8 > INT64_MAX - nx) {
+            stc = STEP_ERR;
+            eno = MAYA_ST_OVERFLOW;
+          } else {
+            nx += w8;
+            s.flags = 0;
+          }
+        }
+      }
 #ifdef MAYA_PROFILE
       if (lane == 0) { PROF_ADD(1, clock64() - t_slow); PROF_ADD(5, 1); }
 #endif
-      s.flags = (r.code >> 2) & 1u;
-      if (r.code & 8u) adv = true;
-      const uint32_t stc = r.code & 3u;
       if (stc != STEP_OK) {
-        if (stc == STEP_ERR) err = (int)((r.code >> 4) & 15u);
-        s.wk = (r.code >> 8) & 3u;
-        s.wt = __shfl_sync(FULL, r.wt, 0);
-        s.wa = (const void *)__shfl_sync(FULL, (unsigned long long)r.wa, 0);
+        if (stc == STEP_ERR) err = (int)eno;
+        s.wk = wk;
+        s.wt = wt;
+        s.wa = wa;
         blocked = true;
         commit = q;
         break;
       }
+      SlowRes r{nx, 0, 0, nullptr};
       if (lane == q) d = r.nx;
       xin = r.nx;
       p = q + 1;
@@ -577,6 +604,12 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
   int64_t tmax = 0;
   int err = 0;
   int64_t rounds = 0;
+  uint32_t my_wb = 0, my_we = 0;   // walkers of this warp's first rank
+  if (wp < R) {
+    const RankRec rr = b.ranks[J.ranks + wp];
+    my_wb = rr.walker;
+    my_we = rr.walker + b.reps[rr.rep].n_streams;
+  }
   for (;;) {
     int progress = 0;
     for (uint32_t r = tid; r < R; r += nt) progress |= host_step(b, sh, r, delay_job);
@@ -588,13 +621,16 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
       // round ends (host syncs, termination and deadlock are decided there)
       bool fresh = true;   // first sweep of the round re-examines every walker
       for (;;) {
-        const uint32_t e0 = vload(&s_epoch);
         bool pass = false;
         PROF_T(t_sweep);
         for (uint32_t r = wp; r < R; r += NW) {
-          const RankRec rr = b.ranks[J.ranks + r];
-          const uint32_t ns = b.reps[rr.rep].n_streams;
-          for (uint32_t w = rr.walker; w < rr.walker + ns; w++) {
+          uint32_t wb = my_wb, we = my_we;
+          if (r != wp) {
+            const RankRec rr = b.ranks[J.ranks + r];
+            wb = rr.walker;
+            we = rr.walker + b.reps[rr.rep].n_streams;
+          }
+          for (uint32_t w = wb; w < we; w++) {
             WSt s = sh.st[w];
             if (s.wk == WAKE_ROUND && !fresh) continue;
             if (s.wk == WAKE_COUNT && vload((const uint32_t *)s.wa) < s.wt) continue;
@@ -612,10 +648,7 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
           }
         }
         if (err) {
-          if (lane == 0) {
-            atomicAdd(&s_epoch, 1u);
-            atomicSub(&s_active, 1);
-          }
+          if (lane == 0) atomicSub(&s_active, 1);
           break;
         }
 #ifdef MAYA_PROFILE
@@ -624,26 +657,43 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
         fresh = false;
         if (pass) {
           progress = 1;
-          __syncwarp();
-          if (lane == 0) {
-            __threadfence_block();
-            atomicAdd(&s_epoch, 1u);
-          }
           continue;
         }
         int wake = 0;
         PROF_T(t_idle);
-        if (lane == 0) {
-          atomicSub(&s_active, 1);
-          unsigned ns = 32;
-          for (;;) {
-            if (vload(&s_epoch) != e0) { wake = 1; break; }
-            if (vload(&s_active) <= 0) break;
+        // idle: poll the wake conditions of this warp's blocked walkers (lane
+        // parallel) until one holds, or until no warp of the CTA is walking
+        if (lane == 0) atomicSub(&s_active, 1);
+        __syncwarp();
+        unsigned ns = 32;
+        for (int poll = 0;; poll++) {
+          bool any = false;
+          for (uint32_t r = wp; r < R && !any; r += NW) {
+            uint32_t wb = my_wb, we = my_we;
+            if (r != wp) {
+              const RankRec rr = b.ranks[J.ranks + r];
+              wb = rr.walker;
+              we = rr.walker + b.reps[rr.rep].n_streams;
+            }
+            for (uint32_t w = wb + lane; w < we; w += 32) {
+              const uint32_t wk = sh.st[w].wk;
+              if (wk == WAKE_COUNT)
+                any |= vload((const uint32_t *)sh.st[w].wa) >= sh.st[w].wt;
+              else if (wk == WAKE_FIRE)
+                any |= vload((const int64_t *)sh.st[w].wa) >= 0;
+            }
+          }
+          if (__any_sync(FULL, any)) {
+            wake = 1;
+            break;
+          }
+          if (vload(&s_active) <= 0) break;
+          if (poll >= 32) {
             __nanosleep(ns);
             if (ns < 256) ns <<= 1;
           }
-          if (wake) atomicAdd(&s_active, 1);
         }
+        if (wake && lane == 0) atomicAdd(&s_active, 1);
         wake = __shfl_sync(FULL, wake, 0);
 #ifdef MAYA_PROFILE
         if (lane == 0) { PROF_ADD(2, clock64() - t_idle); PROF_ADD(6, wake); }
@@ -720,6 +770,8 @@ int sched_variant(uint32_t W, uint32_t R) {
 
 void launch_resolve(const DevBatch &b, cudaStream_t s) {
   if (b.n_ops) resolve_kernel<<<(unsigned)((b.n_ops + 255) / 256), 256, 0, s>>>(b);
+  if (b.n_rcolls)
+    resolve_colls_kernel<<<(unsigned)((b.n_rcolls + 255) / 256), 256, 0, s>>>(b);
 }
 
 template <int NW>

@@ -31,6 +31,8 @@ struct DevBatch {
   const MemRec *mems;
   const Feature *feats;
   const RankColl *rcolls;
+  const uint32_t *rcslot;     // batch-global call slot of each rank-collective entry
+  int64_t *rcw;               // wire time of each rank-collective entry (resolve)
   ExecOp *exec;
   // scratch / outputs
   int64_t *feat_ns;
@@ -46,7 +48,7 @@ struct DevBatch {
   const int32_t *order;       // CTA -> job (largest first)
   int32_t *err_flag;          // any estimator failure
   uint32_t n_jobs, n_reps, n_feats, n_slots;
-  uint64_t n_ops;
+  uint64_t n_ops, n_rcolls;
 };
 
 struct DevTables {
