@@ -1,0 +1,524 @@
+"""Drop-in, reference-shaped API over the CUDA engine.
+
+Mirrors the reference's hot-path entry points so that a dltsim user can swap
+them in:
+
+* ``simulate(annotated, cluster=None, record_timeline=False) -> SimReport``
+  — pkg/src/dltsim/sim.py:476-485 (SimReport fields :59-105, errors :46-47);
+* ``compute_mfu(report, model_flops, cluster, dtype)`` — sim.py:488-497;
+* ``GpuPipelineEvaluator`` — the ``PipelineEvaluator`` of search.py:187-209
+  (same fields, ``__call__(config) -> EvalResult``) plus ``evaluate_many`` /
+  ``prefetch`` that run a whole population as one GPU batch;
+* ``evaluate_space`` — every valid config of a SearchSpace in one batch plus
+  the fused device top-k, ranked exactly like ``_rank`` (search.py:349-357).
+
+Reference classes (SimReport, RankStats, EvalResult, SimDeadlockError) are
+used when dltsim is importable, else the same-named mirrors below.
+"""
+
+from __future__ import annotations
+
+import functools
+from dataclasses import dataclass, field
+from typing import Mapping, Sequence
+
+import numpy as np
+
+from ._abi import (ST_DEADLOCK, ST_ESTIMATION, ST_INTERNAL, ST_OK, ST_OVERFLOW, STATUS_NAMES,
+                   DEFAULT_EFFICIENCY, DEFAULT_KERNEL_OVERHEAD_NS, Batch)
+from .rawtrace import RawJob, from_annotated, from_reference
+from . import workload as W
+
+
+# --- reference-compatible result types ------------------------------------------
+
+class SimDeadlockError(Exception):
+    """Queue drained with blocked work left (sim.py:46-47)."""
+
+
+class EstimationError(Exception):
+    """estimate.py:59-60."""
+
+
+@dataclass
+class RankStats:
+    compute_busy_ns: int = 0
+    comm_busy_ns: int = 0
+    exposed_comm_ns: int = 0
+    idle_ns: int = 0
+    peak_mem_bytes: int = 0
+
+
+@dataclass
+class SimReport:
+    total_ns: int
+    per_rank: dict
+    oom: bool
+    first_oom: tuple | None
+    dispatched_ops: int
+    completed_ops: int
+    mfu: float | None = None
+    timeline: list = field(default_factory=list)
+
+    @property
+    def peak_mem_bytes(self) -> int:
+        return max((s.peak_mem_bytes for s in self.per_rank.values()), default=0)
+
+    @property
+    def exposed_comm_ns(self) -> int:
+        return max((s.exposed_comm_ns for s in self.per_rank.values()), default=0)
+
+
+@dataclass(frozen=True)
+class EvalResult:
+    time_ns: int
+    mfu: float | None
+    peak_mem_bytes: int
+    oom: bool
+
+
+def _ref_types():
+    """Use dltsim's own classes when the reference is importable."""
+    try:
+        from dltsim import sim as rs
+        from dltsim import search as rsearch
+        from dltsim import estimate as rest
+        return dict(SimReport=rs.SimReport, RankStats=rs.RankStats,
+                    SimDeadlockError=rs.SimDeadlockError, EvalResult=rsearch.EvalResult,
+                    EstimationError=rest.EstimationError)
+    except Exception:
+        return dict(SimReport=SimReport, RankStats=RankStats,
+                    SimDeadlockError=SimDeadlockError, EvalResult=EvalResult,
+                    EstimationError=EstimationError)
+
+
+# --- engine singletons (one per CUDA device per process) -------------------------
+
+@functools.lru_cache(maxsize=None)
+def _engine(device: int = 0):
+    from .engine import Engine
+    return Engine(device)
+
+
+def _raise_for(status: int, what: str = "") -> None:
+    T = _ref_types()
+    if status == ST_OK:
+        return
+    if status == ST_DEADLOCK:
+        raise T["SimDeadlockError"](f"simulation deadlocked with blocked work{what}")
+    if status == ST_ESTIMATION:
+        raise T["EstimationError"](f"estimator failed{what}")
+    if status == ST_INTERNAL:
+        raise RuntimeError(f"internal error{what}")
+    raise ValueError(f"engine status {STATUS_NAMES[status]}{what}")
+
+
+def _is_default_roofline(est) -> bool:
+    return (type(est).__name__ == "RooflineEstimator" and hasattr(est, "efficiency")
+            and hasattr(est, "overhead_ns"))
+
+
+# --- simulate() ----------------------------------------------------------------------
+
+def _rank_stats(tl, total: int, n_ranks: int, peaks) -> dict:
+    """Per-rank busy/exposed/idle from the GPU timeline (sim.py:406-473)."""
+    T = _ref_types()
+    out = {}
+    timed = tl.timed()
+    for r in range(n_ranks):
+        m = timed.rank == r
+        a, b, tag = timed.start[m], timed.end[m], timed.tag[m]
+        comp = _merge(a[tag == 0], b[tag == 0])
+        comm = _merge(a[tag == 1], b[tag == 1])
+        busy = _merge(a, b)
+        out[r] = T["RankStats"](
+            compute_busy_ns=int(sum(y - x for x, y in comp)),
+            comm_busy_ns=int(sum(y - x for x, y in comm)),
+            exposed_comm_ns=_subtract_len(comm, comp),
+            idle_ns=int(total - sum(y - x for x, y in busy)),
+            peak_mem_bytes=int(peaks[r]))
+    return out
+
+
+def _merge(a, b):
+    out = []
+    for x, y in sorted(zip(a.tolist(), b.tolist())):
+        if y <= x:
+            continue
+        if out and x <= out[-1][1]:
+            if y > out[-1][1]:
+                out[-1] = (out[-1][0], y)
+        else:
+            out.append((x, y))
+    return out
+
+
+def _subtract_len(base, cut) -> int:
+    total, ci = 0, 0
+    for a, b in base:
+        pos = a
+        while ci < len(cut) and cut[ci][1] <= pos:
+            ci += 1
+        k = ci
+        while pos < b:
+            if k >= len(cut) or cut[k][0] >= b:
+                total += b - pos
+                break
+            ca, cb = cut[k]
+            if ca > pos:
+                total += ca - pos
+            pos = max(pos, cb)
+            k += 1
+    return total
+
+
+def simulate_raw(jobs: Sequence[RawJob], device: int = 0, record_timeline: bool = False,
+                 efficiency: Mapping[str, float] | None = None,
+                 overhead_ns: int = DEFAULT_KERNEL_OVERHEAD_NS):
+    """Batch entry on raw jobs: returns (results array, engine)."""
+    eng = _engine(device)
+    res = eng.simulate(list(jobs), record_timeline=record_timeline, efficiency=efficiency,
+                       overhead_ns=overhead_ns)
+    return res, eng
+
+
+def simulate(annotated, cluster=None, record_timeline: bool = False, device: int = 0):
+    """Drop-in for dltsim.simulate (sim.py:476-485) on the GPU engine."""
+    raw = from_annotated(annotated, cluster)
+    res, eng = simulate_raw([raw], device, record_timeline=True)
+    r = res[0]
+    _raise_for(int(r["status"]))
+    tl = eng.timeline(0)
+    rep_peak = _rep_peaks(raw)
+    peaks = [rep_peak[raw.rank_rep[q]] for q in range(raw.num_ranks)]
+    per_rank = _rank_stats(tl, int(r["total_ns"]), raw.num_ranks, peaks)
+    timeline = []
+    if record_timeline:
+        names = _timeline_names(raw, eng)
+        timed = tl.timed()
+        order = np.lexsort((timed.start, timed.end, timed.rank))
+        timeline = [(int(timed.rank[i]), int(timed.stream[i]), names(timed, i),
+                     int(timed.start[i]), int(timed.end[i])) for i in order]
+    T = _ref_types()
+    return T["SimReport"](
+        total_ns=int(r["total_ns"]), per_rank=per_rank, oom=bool(r["oom"]),
+        first_oom=((int(r["first_oom_rank"]), int(r["first_oom_seq"])) if r["oom"] else None),
+        dispatched_ops=int(r["dispatched_ops"]), completed_ops=int(r["completed_ops"]),
+        timeline=timeline)
+
+
+def _rep_peaks(raw: RawJob) -> list:
+    from .rawtrace import EV_MEMALLOC, EV_MEMFREE
+    out = []
+    for rep in range(raw.n_reps):
+        sl = raw.rep_events(rep)
+        kinds, f = raw.ev_kind[sl], raw.ev_f[sl]
+        alloc = {}
+        mem = peak = 0
+        for k, row in zip(kinds.tolist(), f.tolist()):
+            if k == EV_MEMALLOC:
+                alloc[row[0]] = row[1]
+                mem += row[1]
+            elif k == EV_MEMFREE:
+                mem -= alloc[row[0]]
+            else:
+                continue
+            peak = max(peak, mem)
+        out.append(peak)
+    return out
+
+
+def _timeline_names(raw: RawJob, eng):
+    from .rawtrace import COLLECTIVE_KINDS, EV_COLLECTIVE
+    ops = raw.op_kind_names
+
+    def name(tl, i):
+        rep = raw.rank_rep[int(tl.rank[i])]
+        ev = int(raw.ev_off[rep]) + int(tl.seq[i])
+        if raw.ev_kind[ev] == EV_COLLECTIVE:
+            return COLLECTIVE_KINDS[int(raw.ev_f[ev, 2])]
+        return ops[int(raw.ev_f[ev, 0])]
+    return name
+
+
+def compute_mfu(report, model_flops: int, cluster, dtype: str) -> float | None:
+    """sim.py:488-497, verbatim arithmetic (int/int true division)."""
+    if report.oom:
+        return None
+    if report.total_ns <= 0:
+        return 0.0
+    peak = cluster.device.peak_flops[dtype]
+    achieved_per_s = model_flops * 1_000_000_000 / report.total_ns
+    return achieved_per_s / (cluster.num_devices * peak)
+
+
+def _mfu(total_ns: int, oom: bool, model_flops: int, cluster, dtype: str):
+    if oom:
+        return None
+    if total_ns <= 0:
+        return 0.0
+    return (model_flops * 1_000_000_000 / total_ns) / (cluster.num_devices
+                                                       * cluster.device.peak_flops[dtype])
+
+
+# --- model flops (workload.py:117-128) -------------------------------------------------
+
+def iteration_flops(model, global_batch: int) -> int:
+    if hasattr(model, "iteration_flops"):
+        return model.iteration_flops(global_batch)
+    s, h, v, b = model.seq_len, model.hidden_size, model.vocab_size, global_batch
+    layer = (8 * b * s * h + 2 * b * s * 3 * h * h + 2 * b * s * s * h + 5 * b * s * s
+             + 2 * b * s * s * h + 2 * b * s * h * h + b * s * h + 8 * b * s * h
+             + 2 * b * s * 4 * h * h + 8 * 4 * b * s * h + 2 * b * s * h * 4 * h + b * s * h)
+    head = 8 * b * s * h + 2 * b * s * v * h + 5 * b * s * v
+    return 3 * (model.num_layers * layer + head)
+
+
+# --- PipelineEvaluator drop-in -----------------------------------------------------------
+
+class GpuPipelineEvaluator:
+    """search.py:187-209 on the GPU: generate -> collate -> annotate -> simulate.
+
+    ``__call__`` evaluates one config (cached if prefetched); ``evaluate_many``
+    runs a population as one batch.  Not picklable into worker processes (it
+    owns a CUDA engine): use ``run_search(..., jobs=1)``.
+    """
+
+    def __init__(self, model, cluster, estimator=None, dispatch_overhead_ns: int = 0,
+                 schedule=None, device: int = 0, threads: int = 8):
+        self.model = model
+        self.cluster = cluster
+        self.estimator = estimator
+        self.dispatch_overhead_ns = dispatch_overhead_ns
+        self.schedule = schedule
+        self.device = device
+        self.threads = threads
+        self._cache: dict = {}
+
+    def _efficiency(self):
+        est = self.estimator
+        if est is None:
+            return dict(DEFAULT_EFFICIENCY), DEFAULT_KERNEL_OVERHEAD_NS
+        if _is_default_roofline(est):
+            return dict(est.efficiency), int(est.overhead_ns)
+        return None, None
+
+    def evaluate_many(self, configs: Sequence) -> list:
+        """EvalResult per config, or the exception its evaluation raised."""
+        T = _ref_types()
+        configs = list(configs)
+        out: list = [None] * len(configs)
+        todo = []
+        for i, c in enumerate(configs):
+            sched = self.schedule or W.default_schedule(c)
+            errors = W.validate_config(self.model, c, self.cluster, sched)
+            if errors:
+                out[i] = W.ConfigError("; ".join(errors))
+            else:
+                todo.append(i)
+        if not todo:
+            return out
+        eff, overhead = self._efficiency()
+        eng = _engine(self.device)
+        sub = [configs[i] for i in todo]
+        if eff is not None:
+            st = eng.stage_generated(self.model, sub, self.cluster, schedule=self.schedule,
+                                     dispatch_overhead_ns=self.dispatch_overhead_ns,
+                                     efficiency=eff, overhead_ns=overhead, threads=self.threads)
+            eng.upload()
+        else:  # user estimator: host annotations per unique feature (estimate.py:329-361)
+            raws = [self._annotated_raw(c) for c in sub]
+            eng.load(raws, threads=self.threads)
+        eng.run()
+        res = eng.results()
+        flops = {}
+        for k, i in enumerate(todo):
+            r = res[k]
+            st_ = int(r["status"])
+            if st_ != ST_OK:
+                try:
+                    _raise_for(st_, f" (config {configs[i].label()})")
+                except Exception as exc:  # noqa: BLE001 - surfaced to the caller
+                    out[i] = exc
+                continue
+            gb = configs[i].global_batch
+            if gb not in flops:
+                flops[gb] = iteration_flops(self.model, gb)
+            mfu = _mfu(int(r["total_ns"]), bool(r["oom"]), flops[gb], self.cluster,
+                       self.model.dtype)
+            out[i] = T["EvalResult"](int(r["total_ns"]), mfu, int(r["peak_mem_bytes"]),
+                                     bool(r["oom"]))
+        return out
+
+    def _annotated_raw(self, config) -> RawJob:
+        raw = W.generate_job(self.model, config, self.cluster, self.schedule,
+                             self.dispatch_overhead_ns)
+        return annotate_raw(raw, self.estimator, self.cluster.device)
+
+    def prefetch(self, configs: Sequence) -> None:
+        for c, r in zip(configs, self.evaluate_many(configs)):
+            self._cache[c.key()] = r
+
+    def __call__(self, config):
+        r = self._cache.get(config.key())
+        if r is None:
+            r = self.evaluate_many([config])[0]
+        if isinstance(r, Exception):
+            raise r
+        return r
+
+
+def annotate_raw(raw: RawJob, estimator, device) -> RawJob:
+    """Host-computed durations for an arbitrary EstimatorInterface, one call per
+    unique feature (the reference calls it once per event, estimate.py:339-352)."""
+    from .rawtrace import EV_KERNEL, EV_MEMCPY, EV_MEMSET, COLLECTIVE_KINDS, TOPOLOGIES
+    import dataclasses
+    kc = np.isin(raw.ev_kind, (EV_KERNEL, EV_MEMCPY, EV_MEMSET))
+    kn = np.full(raw.n_events, -1, dtype=np.int64)
+    cache: dict = {}
+    KernelAttrs = _kernel_attrs_type()
+    for i in np.nonzero(kc)[0].tolist():
+        op, dt, fl, by = (int(x) for x in raw.ev_f[i])
+        key = (op, dt, fl, by)
+        if key not in cache:
+            attrs = KernelAttrs.make({}, raw.dtype_names[dt], fl, by)
+            cache[key] = int(estimator.estimate_kernel(raw.op_kind_names[op], attrs, device))
+        kn[i] = cache[key]
+    wire = np.zeros(len(raw.call_kind), dtype=np.int64)
+    for g in range(len(raw.comm_nranks)):
+        for c in range(int(raw.call_off[g]), int(raw.call_off[g + 1])):
+            if raw.call_kind[c] < 0:
+                continue
+            wire[c] = int(estimator.estimate_collective(
+                COLLECTIVE_KINDS[raw.call_kind[c]], int(raw.call_bytes[c]),
+                int(raw.comm_nranks[g]), TOPOLOGIES[raw.comm_topo[g]], device))
+    return dataclasses.replace(raw, kernel_ns=kn, wire_ns=wire)
+
+
+def _kernel_attrs_type():
+    try:
+        from dltsim.trace import KernelAttrs
+        return KernelAttrs
+    except Exception:
+        @dataclass(frozen=True)
+        class KernelAttrs:
+            dims: tuple
+            dtype: str
+            flops: int
+            bytes_moved: int
+
+            @staticmethod
+            def make(dims, dtype, flops, bytes_moved):
+                return KernelAttrs(tuple(sorted(dict(dims).items())), dtype, flops, bytes_moved)
+        return KernelAttrs
+
+
+# --- whole-space search with the fused device reduction --------------------------------
+
+@dataclass
+class SpaceResult:
+    configs: list
+    results: list            # EvalResult or exception per config (enumeration order)
+    best: list               # top-k configs in _rank order (search.py:349-357)
+    best_time_ns: list
+
+
+def key_ranks(configs) -> np.ndarray:
+    order = sorted(range(len(configs)), key=lambda i: configs[i].key())
+    kr = np.zeros(len(configs), dtype=np.int32)
+    kr[order] = np.arange(len(configs), dtype=np.int32)
+    return kr
+
+
+def evaluate_space(space, model, cluster, k: int = 8, dispatch_overhead_ns: int = 0,
+                   schedule=None, device: int = 0, threads: int = 8,
+                   efficiency: Mapping[str, float] | None = None,
+                   overhead_ns: int = DEFAULT_KERNEL_OVERHEAD_NS) -> SpaceResult:
+    """Every valid config of ``space`` as one GPU batch; the k best by the
+    reference ranking come from the fused device top-k."""
+    T = _ref_types()
+    configs = W.enumerate_space(space, model, cluster)
+    eng = _engine(device)
+    kr = key_ranks(configs)
+    eng.stage_generated(model, configs, cluster, schedule=schedule,
+                        dispatch_overhead_ns=dispatch_overhead_ns, efficiency=efficiency,
+                        overhead_ns=overhead_ns, key_ranks=kr, threads=threads)
+    eng.upload()
+    eng.run()
+    res = eng.results()
+    top = eng.topk(k)
+    fl = iteration_flops(model, configs[0].global_batch) if configs else 0
+    results = []
+    for c, r in zip(configs, res):
+        if int(r["status"]) != ST_OK:
+            results.append(RuntimeError(STATUS_NAMES[int(r["status"])]))
+        else:
+            results.append(T["EvalResult"](int(r["total_ns"]), _mfu(
+                int(r["total_ns"]), bool(r["oom"]), fl, cluster, model.dtype),
+                int(r["peak_mem_bytes"]), bool(r["oom"])))
+    return SpaceResult(configs, results, [configs[int(t["job"])] for t in top],
+                       [int(t["time_ns"]) for t in top])
+
+
+def merge_topk(candidates: np.ndarray, k: int) -> np.ndarray:
+    """Merge per-GPU top-k candidate rows (time_ns, global key rank, config id)
+    with the device comparator; time_ns == 0 sorts after every positive time."""
+    c = np.asarray(candidates, dtype=np.int64).reshape(-1, 3)
+    c = c[c[:, 0] >= 0]
+    t = np.where(c[:, 0] == 0, np.iinfo(np.int64).max, c[:, 0])
+    order = np.lexsort((c[:, 2], c[:, 1], t))
+    return c[order[:k]]
+
+
+def shard_lpt(costs: Sequence[int], n: int) -> list:
+    """Greedy LPT assignment of configs (by estimated cost) to n GPUs."""
+    import heapq
+    heap = [(0, g) for g in range(n)]
+    heapq.heapify(heap)
+    out = [[] for _ in range(n)]
+    for i in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        load, g = heapq.heappop(heap)
+        out[g].append(i)
+        heapq.heappush(heap, (load + costs[i], g))
+    return [sorted(x) for x in out]
+
+
+def evaluate_space_distributed(space, model, cluster, k: int = 8, dispatch_overhead_ns: int = 0,
+                               schedule=None, threads: int = 8):
+    """One process per GPU (torch.distributed): configs sharded by LPT on a
+    cost proxy, local fused top-k, one all_gather of k x 24 B per GPU, merge."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    configs = W.enumerate_space(space, model, cluster)
+    kr = key_ranks(configs)
+    costs = [c.micro_mult * c.pp * c.virtual_stages for c in configs]
+    mine = shard_lpt(costs, world)[rank]
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else 0
+    eng = _engine(dev)
+    sub = [configs[i] for i in mine]
+    eng.stage_generated(model, sub, cluster, schedule=schedule,
+                        dispatch_overhead_ns=dispatch_overhead_ns, key_ranks=kr[mine],
+                        threads=threads)
+    eng.upload()
+    eng.run()
+    eng.results()
+    top = eng.topk(k)
+    cand = np.full((k, 3), -1, dtype=np.int64)
+    for q, t in enumerate(top):
+        cand[q] = (int(t["time_ns"]), int(t["key_rank"]), mine[int(t["job"])])
+    return gather_merge(cand, k), configs
+
+
+def gather_merge(cand: np.ndarray, k: int) -> np.ndarray:
+    """all_gather of the (k, 3) candidate block then the global merge; NCCL on
+    GPUs, gloo on CPU (tests)."""
+    import torch
+    import torch.distributed as dist
+    backend = dist.get_backend()
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else "cpu"
+    t = torch.from_numpy(np.ascontiguousarray(cand)).to(dev)
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t)
+    allc = torch.cat(parts).cpu().numpy()
+    return merge_topk(allc, k)
