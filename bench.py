@@ -144,38 +144,42 @@ def parity_c2(configs, res) -> dict:
             "reference_best_ns": ok[0]["total_ns"]}
 
 
-def cpu_baseline(model, cluster, configs, seconds: float, threads: int) -> dict:
-    """Oracle port (native generator + C++ restatement of sim.py) on host cores."""
-    from oracle import oracle
+def _gen_jobs(model, cluster, configs, threads):
+    """Native generator (ctypes releases the GIL) on a thread pool."""
+    from concurrent.futures import ThreadPoolExecutor
     from paper_2503_20191_b200 import workload as W
-    import numpy as np
-    jobs, t_gen = [], 0.0
-    t0 = time.perf_counter()
-    for cfg in configs:
-        jobs.append(W.generate_job(model, cfg, cluster, dispatch_overhead_ns=5000))
-        if time.perf_counter() - t0 > seconds / 3:
-            break
-    t_gen = time.perf_counter() - t0
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        return list(ex.map(lambda c: W.generate_job(model, c, cluster, dispatch_overhead_ns=5000),
+                           configs))
+
+
+def cpu_baseline(model, cluster, configs, seconds: float, threads: int) -> dict:
+    """Oracle port (oracle/sim_oracle.cpp: C++ restatement of the reference's
+    event-driven simulate + annotate) on the host cores; pre-built jobs."""
+    from oracle import oracle
     from paper_2503_20191_b200._abi import Batch
+    t0 = time.perf_counter()
+    jobs = _gen_jobs(model, cluster, configs, threads)
+    t_gen = time.perf_counter() - t0
     b = Batch(jobs)
     t1 = time.perf_counter()
     reps = 0
     while True:
         oracle.simulate_many(jobs, threads=threads, batch=b)
         reps += 1
-        if time.perf_counter() - t1 > seconds * 2 / 3:
+        if time.perf_counter() - t1 > seconds:
             break
     t_sim = (time.perf_counter() - t1) / reps
     n = len(jobs)
     rank_ops = sum(j.rank_ops() for j in jobs)
-    per_cfg = t_gen / n + t_sim / n
-    return {"value": round(1.0 / per_cfg, 2), "unit": "configs/s", "cores": threads,
-            "kind": "port",
-            "sample": f"first {n} of the {len(configs)} C2 configs: native generation "
-                      f"(1 thread, {t_gen:.2f}s) + oracle annotate+simulate "
-                      f"({threads} threads, {t_sim:.3f}s per pass, {reps} passes)",
-            "sim_only_configs_per_s": round(n / t_sim, 2),
-            "sim_only_rank_ops_per_s": round(rank_ops / t_sim, 1)}
+    return {"value": round(n / t_sim, 2), "unit": "configs/s", "cores": threads, "kind": "port",
+            "sample": f"all {n} C2 configs per pass, {reps} passes: oracle annotate+simulate "
+                      f"(C++ restatement of pkg/src/dltsim/sim.py + estimate.py) on pre-built "
+                      f"jobs, {threads} threads",
+            "trace_ops_per_s": round(rank_ops / t_sim, 1),
+            "e2e_equiv_configs_per_s": round(n / (t_sim + t_gen), 2),
+            "reference_python_survey": "2.8 configs/s e2e, 5.5 configs/s sim-only, 1 core "
+                                       "(BASELINE.md; the Python reference is not on the box)"}
 
 
 def bench_reference(args):
@@ -193,7 +197,7 @@ def bench_reference(args):
 
     def step():
         t0 = time.perf_counter()
-        jobs = [W.generate_job(model, c, cluster, dispatch_overhead_ns=5000) for c in configs]
+        jobs = _gen_jobs(model, cluster, configs, threads)
         res = oracle.simulate_many(jobs, threads=threads, batch=Batch(jobs))
         return time.perf_counter() - t0, res, jobs
 
@@ -217,8 +221,8 @@ def bench_reference(args):
         "cpu_baseline": {"value": round(val, 3), "unit": "configs/s", "cores": threads,
                          "kind": "port",
                          "sample": "full 512-config C2 batch per step: native generator "
-                                   "(1 thread) + oracle/sim_oracle.cpp annotate+simulate "
-                                   f"({threads} threads)"},
+                                   "+ oracle/sim_oracle.cpp annotate+simulate (C++ port of the "
+                                   f"reference's event-driven simulator), {threads} threads"},
         "e2e": {"value": round(val, 3), "unit": "configs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -268,6 +272,7 @@ def bench_ours(args):
     assert (st == 0).all(), "invalid configs in the C2 lattice"
     eng.upload()
     stats = eng.batch_stats()
+    n_collapsed = int(eng.collapsed().sum())
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
 
     def step():
@@ -309,22 +314,46 @@ def bench_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
 
-    # search reduction across GPUs: all_gather of k x 16 B candidates (NCCL)
-    cand = np.zeros((TOPK, 2), dtype=np.int64)
+    # search reduction across GPUs: all_gather of k x 24 B candidates (NCCL), merge
+    from paper_2503_20191_b200.api import gather_merge, merge_topk
+    cand = np.full((TOPK, 3), -1, dtype=np.int64)
     for q, e in enumerate(top):
-        cand[q] = (int(e["time_ns"]), (rank << 32) | int(e["key_rank"]))
-    for q in range(len(top), TOPK):
-        cand[q] = (np.iinfo(np.int64).max, -1)
-    ct = torch.from_numpy(cand).to(dev)
-    if world > 1:
-        gathered = [torch.empty_like(ct) for _ in range(world)]
-        dist.all_gather(gathered, ct)
-        allc = torch.cat(gathered).cpu().numpy()
-    else:
-        allc = cand
-    order = np.lexsort((allc[:, 1], allc[:, 0]))
-    best = allc[order[0]]
-    best_rank, best_kr = int(best[1]) >> 32, int(best[1]) & 0xffffffff
+        cand[q] = (int(e["time_ns"]), (rank << 20) | int(e["key_rank"]), int(e["job"]))
+    merged = gather_merge(cand, TOPK) if world > 1 else merge_topk(cand, TOPK)
+    best = merged[0]
+    best_rank, best_kr = int(best[1]) >> 20, int(best[1]) & 0xfffff
+
+    # --- the same batch on the full-rank path (no class collapse) -------------------
+    full = None
+    if rank == 0:
+        eng.set_collapse(False)
+        eng.stage_generated(model, configs, cluster, dispatch_overhead_ns=5000, key_ranks=kr,
+                            threads=threads)
+        eng.upload()
+        for _ in range(2):
+            eng.run()
+            rf = eng.results()
+        fms = []
+        for _ in range(max(3, args.steps // 2)):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+                a = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            eng.run()
+            eng.topk(TOPK)
+            z = torch.cuda.Event(enable_timing=True)
+            z.record(stream)
+            z.synchronize()
+            fms.append(a.elapsed_time(z))
+        same = bool((rf["total_ns"] == res["total_ns"]).all() and (rf["status"] == res["status"]).all())
+        full = {"value": round(N_CONFIGS / (statistics.mean(fms) / 1000), 2), "unit": "configs/s",
+                "ms_per_step": round(statistics.mean(fms), 4),
+                "trace_ops_per_s": round(stats["rank_ops"] / (statistics.mean(fms) / 1000), 1),
+                "identical_results_to_collapsed": same}
+        eng.set_collapse(True)
+        eng.stage_generated(model, configs, cluster, dispatch_overhead_ns=5000, key_ranks=kr,
+                            threads=threads)
+        eng.upload()
 
     # --- end to end through the C ABI with host buffers -------------------------------
     e2e_steps = args.e2e_steps or args.steps
@@ -382,7 +411,7 @@ def bench_ours(args):
                     "d2h_bytes_per_step": int(N_CONFIGS * 64 + TOPK * 16),
                     "path": "config list -> native gen+pack (C++ threads) -> H2D -> kernels "
                             "-> D2H results + top-k"},
-            "roofline": {"bound": "hbm", "kernel": "schedule_kernel",
+            "roofline": {"bound": "hbm", "kernel": "sched_warp_kernel",
                          "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 5), "traffic": ncu_traffic(),
                          "algorithmic_bytes_per_launch": alg_bytes,
@@ -392,6 +421,10 @@ def bench_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "rounds": {"max": int(res["rounds"].max()), "median": float(np.median(res["rounds"]))},
             "best": {"rank": best_rank, "key_rank": best_kr, "time_ns": int(best[0])},
+            "class_collapse": {"collapsed_configs": int(n_collapsed), "simulated_ranks":
+                               stats["ranks"], "note": "exact rank-class collapse (SURVEY 7.8), "
+                               "verified per config; value/e2e use it"},
+            "full_rank": full,
             "parity": parity,
         }
         if world == 1 and not args.no_cpu_baseline:
