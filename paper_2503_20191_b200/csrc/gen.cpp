@@ -294,16 +294,19 @@ struct Builder {
   std::vector<int32_t> comm_nranks;          // per local comm
   std::vector<int64_t> call_idx;             // per local comm
   std::vector<std::vector<std::pair<int8_t, int64_t>>> calls;  // per local comm
-  std::unordered_map<int64_t, int64_t> next_version, last_version;
+  std::vector<int64_t> next_version, last_version;   // by event id (small)
   int64_t next_alloc = 0;
 
   void ev(uint8_t k, int32_t s, int64_t a, int64_t b = 0, int64_t c = 0, int64_t d = 0) {
     kind.push_back(k);
     stream.push_back(s);
-    f.push_back(a);
-    f.push_back(b);
-    f.push_back(c);
-    f.push_back(d);
+    const size_t n = f.size();
+    f.resize(n + 4);
+    int64_t *p = f.data() + n;
+    p[0] = a;
+    p[1] = b;
+    p[2] = c;
+    p[3] = d;
   }
   void gap() {
     if (overhead > 0) ev(MAYA_EV_HOSTGAP, 0, overhead);
@@ -326,6 +329,10 @@ struct Builder {
     calls[lc].emplace_back((int8_t)kind_, n);
   }
   void record(int32_t s, int64_t e) {
+    if ((size_t)e >= next_version.size()) {
+      next_version.resize(e + 1, 0);
+      last_version.resize(e + 1, 0);
+    }
     int64_t ver = next_version[e];
     next_version[e] = ver + 1;
     last_version[e] = ver;
@@ -357,6 +364,13 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   const i128 u = sp ? t : 1;
 
   Builder B{G.ev_kind, G.ev_stream, G.ev_f, overhead, dtype, {}, {}, {}, {}, {}, 0};
+  {  // reserve for this trace: ~ (2 x kernels per layer-microbatch) + specials
+    const size_t est = (size_t)(cfg.micro_mult) * (size_t)cfg.pp * (size_t)(M.L / cfg.pp + 2) *
+                           (cfg.act_recompute ? 110 : 80) + 4096;
+    G.ev_kind.reserve(G.ev_kind.size() + est);
+    G.ev_stream.reserve(G.ev_stream.size() + est);
+    G.ev_f.reserve(G.ev_f.size() + 4 * est);
+  }
   std::vector<CommRole> roles = worker_comms(C, v, rank);
   // local comm index of each role (first CommInit of a comm id)
   std::map<std::string, int> local;

@@ -49,6 +49,7 @@ struct RepBuild {
   std::vector<std::vector<Op>> sops;           // per local stream
   std::vector<std::vector<uint32_t>> sseq;
   int last_raw = INT32_MIN, last_local = -1;
+  size_t reserve_hint = 0;
 
   int local_stream(int32_t raw, bool create) {
     if (raw == last_raw) return last_local;
@@ -58,10 +59,19 @@ struct RepBuild {
     raw_of.push_back(raw);
     sops.emplace_back();
     sseq.emplace_back();
+    if (sops.size() == 1) {   // the first stream is usually the compute stream
+      sops.back().reserve(reserve_hint);
+      sseq.back().reserve(reserve_hint);
+    }
     last_raw = raw;
     last_local = (int)raw_of.size() - 1;
     return last_local;
   }
+};
+
+struct FeatCacheEnt {
+  int64_t k[4];
+  uint32_t fid;
 };
 
 void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
@@ -98,8 +108,12 @@ void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
   };
 
   RepBuild RB;
+  RB.reserve_hint = (size_t)(e - b) / 2 + 16;
+  FeatCacheEnt fcache[64];
+  for (auto &ce : fcache) ce.fid = UINT32_MAX;
   std::vector<std::vector<uint32_t>> snap;  // per sync: ops dispatched per local stream
-  std::unordered_map<int64_t, int64_t> alloc;
+  std::unordered_map<int64_t, int64_t> alloc_big;   // alloc_id -> bytes (large ids)
+  std::vector<int64_t> alloc_small;                  // alloc_id -> bytes + 1 (0: none)
   std::unordered_map<uint64_t, uint32_t> coll_seen;
   // ring eligibility: per local comm, one issuing stream and call_idx 0,1,2,...
   std::vector<int32_t> comm_stream(n_local_comms, INT32_MIN);
@@ -152,29 +166,50 @@ void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
             fid = it->second;
           }
         } else {
-          FeatKey key{f[0], f[1], f[2], f[3]};
-          auto it = feat_map.find(key);
-          if (it == feat_map.end()) {
-            fid = (uint32_t)P.feats.size();
-            feat_map.emplace(key, fid);
-            P.feats.push_back(Feature{f[2], f[3], -1, (int32_t)f[0], (int16_t)f[1],
-                                      (int16_t)job.device});
+          // direct-mapped cache in front of the hash map: kernel templates repeat
+          const uint64_t hk = ((uint64_t)f[2] * 0x9e3779b97f4a7c15ull) ^ (uint64_t)f[3] ^
+                              ((uint64_t)f[0] << 48) ^ ((uint64_t)f[1] << 56);
+          FeatCacheEnt &ce = fcache[(hk >> 58) & 63];
+          if (ce.fid != UINT32_MAX && ce.k[0] == f[0] && ce.k[1] == f[1] && ce.k[2] == f[2] &&
+              ce.k[3] == f[3]) {
+            fid = ce.fid;
           } else {
-            fid = it->second;
+            FeatKey key{f[0], f[1], f[2], f[3]};
+            auto it = feat_map.find(key);
+            if (it == feat_map.end()) {
+              fid = (uint32_t)P.feats.size();
+              feat_map.emplace(key, fid);
+              P.feats.push_back(Feature{f[2], f[3], -1, (int32_t)f[0], (int16_t)f[1],
+                                        (int16_t)job.device});
+            } else {
+              fid = it->second;
+            }
+            ce = FeatCacheEnt{{f[0], f[1], f[2], f[3]}, fid};
           }
         }
         emit(TAG_KERN, fid);
         break;
       }
       case MAYA_EV_MEMALLOC:
-        alloc[f[0]] = f[1];
+        if (f[0] >= 0 && f[0] < (1 << 20)) {
+          if ((size_t)f[0] >= alloc_small.size()) alloc_small.resize(f[0] + 64, INT64_MIN);
+          alloc_small[f[0]] = f[1];
+        } else {
+          alloc_big[f[0]] = f[1];
+        }
         P.mems.push_back(MemRec{f[1], gpre, seg, seq});
         break;
       case MAYA_EV_MEMFREE: {
-        auto it = alloc.find(f[0]);
-        if (it == alloc.end())
+        int64_t sz = INT64_MIN;
+        if (f[0] >= 0 && (size_t)f[0] < alloc_small.size()) {
+          sz = alloc_small[f[0]];
+        } else {
+          auto it = alloc_big.find(f[0]);
+          if (it != alloc_big.end()) sz = it->second;
+        }
+        if (sz == INT64_MIN)
           throw Fail{MAYA_ST_INTERNAL, "MemFree of unallocated handle " + std::to_string(f[0])};
-        P.mems.push_back(MemRec{-it->second, gpre, seg, seq});
+        P.mems.push_back(MemRec{-sz, gpre, seg, seq});
         break;
       }
       case MAYA_EV_RECORD: emit(TAG_REC, ord(f)); break;
