@@ -219,8 +219,9 @@ int maya_upload(maya_engine *e) {
     n_rcolls += P.rcolls.size();
     {
       const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
-                                         (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0);
-      if (L.bytes > sched_smem_cap()) n_wstate += spill_bytes(P.walkers.size(), P.ranks.size());
+                                         (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0,
+                                         P.hdr.n_fire, P.hdr.n_rcolls, sched_smem_cap());
+      if (!L.on_chip) n_wstate += spill_bytes(P.walkers.size(), P.ranks.size());
     }
     e->job_tl[j] = n_tl;
     for (const RankRec &rr : P.ranks) n_tl += P.reps[rr.rep].n_ops;
@@ -259,7 +260,7 @@ int maya_upload(maya_engine *e) {
   // scratch layout
   off = 0;
   seg(e->x_exec, n_ops * sizeof(ExecOp));
-  seg(e->x_rcw, n_rcolls * sizeof(int64_t));
+  seg(e->x_rcw, n_rcolls * sizeof(RCX));
   seg(e->x_feat_ns, n_feats * 8);
   seg(e->x_wire, n_slots * 8);
   seg(e->x_fire, n_fire * 8);
@@ -317,9 +318,9 @@ int maya_upload(maya_engine *e) {
       e->var_n[var[j]]++;
       const JobPack &P = e->packs[j];
       const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
-                                         (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0);
-      if (L.bytes <= sched_smem_cap() && L.bytes > e->var_smem[var[j]])
-        e->var_smem[var[j]] = L.bytes;
+                                         (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0,
+                                         P.hdr.n_fire, P.hdr.n_rcolls, sched_smem_cap());
+      if (L.bytes > e->var_smem[var[j]]) e->var_smem[var[j]] = L.bytes;
     }
     memcpy(H + e->s_order.off, order.data(), nj * sizeof(int32_t));
   }
@@ -351,8 +352,9 @@ int maya_upload(maya_engine *e) {
       b.delay += P.n_delay;
       b.rcolls += P.rcolls.size();
       const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
-                                         (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0);
-      if (L.bytes > sched_smem_cap()) b.wstate += spill_bytes(P.walkers.size(), P.ranks.size());
+                                         (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0,
+                                         P.hdr.n_fire, P.hdr.n_rcolls, sched_smem_cap());
+      if (!L.on_chip) b.wstate += spill_bytes(P.walkers.size(), P.ranks.size());
     }
   }
   auto copy_job = [&](size_t j) {
@@ -466,7 +468,7 @@ int maya_upload(maya_engine *e) {
   db.feats = (const Feature *)(D + e->s_feats.off);
   db.rcolls = (const RankColl *)(D + e->s_rcolls.off);
   db.rcslot = (const uint32_t *)(D + e->s_rcslot.off);
-  db.rcw = (int64_t *)(X + e->x_rcw.off);
+  db.rcx = (RCX *)(X + e->x_rcw.off);
   db.n_rcolls = n_rcolls;
   db.exec = (ExecOp *)(X + e->x_exec.off);
   db.n_ops = n_ops;
@@ -522,7 +524,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
       e->d_scratch_cap = need;
       char *X = (char *)p;
       db.exec = (ExecOp *)(X + e->x_exec.off);
-      db.rcw = (int64_t *)(X + e->x_rcw.off);
+      db.rcx = (RCX *)(X + e->x_rcw.off);
       db.feat_ns = (int64_t *)(X + e->x_feat_ns.off);
       db.wire = (int64_t *)(X + e->x_wire.off);
       db.fire = (int64_t *)(X + e->x_fire.off);

@@ -180,7 +180,7 @@ __global__ void resolve_kernel(DevBatch b) {
 __global__ void resolve_colls_kernel(DevBatch b) {
   uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= b.n_rcolls) return;
-  b.rcw[e] = b.wire[b.rcslot[e]];
+  b.rcx[e] = RCX{b.rcolls[e], b.wire[b.rcslot[e]]};
 }
 
 template <typename T>
@@ -197,9 +197,10 @@ static constexpr unsigned FULL = 0xffffffffu;
 #ifdef MAYA_PROFILE
 // per-batch cycle counters: [0] walk windows, [1] slow ops, [2] idle sleep,
 // [3] sweeps (skip checks + ctx), [4] windows, [5] slow-op calls, [6] wakes, [7] passes
+// accumulated per thread (lane 0 of each warp) and flushed once at kernel exit
 __device__ unsigned long long g_prof[8];
 #define PROF_T(v) long long v = clock64()
-#define PROF_ADD(i, v) atomicAdd(&g_prof[i], (unsigned long long)(v))
+#define PROF_ADD(i, v) (prof_acc[i] += (unsigned long long)(v))
 #else
 #define PROF_T(v)
 #define PROF_ADD(i, v)
@@ -227,7 +228,7 @@ struct WCtx {
   const ExecOp *ops;      // stream's first op
   int64_t *fire;          // rank's record table
   const int64_t *delay;   // rank's host-delay table (n_syncs + 1)
-  uint64_t rc;            // batch index of the rank's collective table (rcolls / rcw)
+  const RCX *rc;          // rank's collective entries + wire times (smem or global)
   const uint32_t *cnt;    // counts[0][stream] of the rep (stride ns)
   uint64_t tl;            // timeline row of the stream's first op
   uint32_t len, rank, ns, nsync;
@@ -243,20 +244,23 @@ struct JobSh {            // per-CTA view of the job
   WSt *st;                // walker states
   const uint32_t *wid;    // rank-major (rank, stream) position -> walker index
   WCtx *ctx;              // cached contexts (smem) or null
+  int64_t *fire;          // job's record-time table (smem or global)
+  const RCX *rcx;         // job's rank-collective table (smem or global)
   unsigned *epoch;        // CTA progress epoch
   int record;
 };
 
 __device__ __forceinline__ void load_ctx(const DevBatch &b, const JobHdr &J, uint32_t w,
-                                         int record, WCtx &c) {
+                                         int record, WCtx &c, int64_t *fire_job,
+                                         const RCX *rcx_job) {
   const Walker wk = b.walkers[J.walkers + w];
   const RankRec rr = b.ranks[J.ranks + wk.rank];
   const RepHdr &h = b.reps[rr.rep];
   const StreamRange sr = b.streams[h.streams + wk.stream];
   c.ops = b.exec + h.ops + sr.begin;
-  c.fire = b.fire + J.fire + rr.fire;
+  c.fire = fire_job + rr.fire;
   c.delay = b.delay + J.delay + rr.delay;
-  c.rc = J.rcolls + rr.rslot;
+  c.rc = rcx_job + rr.rslot;
   c.cnt = b.counts + h.counts + wk.stream;
   c.len = sr.len;
   c.rank = wk.rank;
@@ -281,12 +285,24 @@ __device__ __forceinline__ ExecOp load_exec(const ExecOp *p) {
 }
 
 // Warp-cooperative walker: advance one (rank, stream) FIFO 32 records at a
-// time.  A kernel op is the max-plus affine map  x -> max(x + d, disp + d)
-// (ready = max(dispatch, prev done); done = ready + d), so a run of kernel ops
-// is one segmented inclusive scan of (a, b) pairs across the lanes; ballots
-// locate the records, waits and collectives, which lane 0 applies in order.
+// time.  Every op whose inputs are already known is a max-plus affine map of
+// the stream clock x (ready = max(x, disp)):
+//   kernel                       x -> max(x + d, disp + d)
+//   record                       x -> max(x, disp)            (fire = result)
+//   wait on a fired event f      x -> max(x, max(disp, f))
+//   collective, one member class x -> max(x + w, disp + w)
+//   collective, all others in    x -> max(x + w, max(disp, M) + w)
+// so a window is one segmented inclusive scan of (a, b) pairs across the
+// lanes (5 shuffle steps).  Their inputs (fired times, slot counters, wire
+// times) are loaded lane-parallel first; only true blockers -- waits on
+// unfired events, arrivals that are not the last, overflow-checked kernels --
+// are applied in order by lane 0, and segments restart after them.
 __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt &s,
-                          int64_t &tmax, int &err, uint32_t lane) {
+                          int64_t &tmax, int &err, uint32_t lane
+#ifdef MAYA_PROFILE
+                          , unsigned long long *prof_acc
+#endif
+                          ) {
   if (s.i >= c.len) return false;
   const JobHdr &J = *sh.J;
   const uint32_t hk = sh.hostk[c.rank];
@@ -294,12 +310,12 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
   bool adv = false;
   s.wk = WAKE_ROUND;   // until something else is known: wait for the next round
   while (s.i < limit) {
+    PROF_T(t_win);
     while (s.i >= s.bound && s.seg < c.nsync) {  // next host-sync segment
       s.seg++;
       s.cdel = c.delay[s.seg];
       s.bound = s.seg < c.nsync ? c.cnt[s.seg * c.ns] : c.len;
     }
-    PROF_T(t_win);
     const uint32_t end = s.bound < limit ? s.bound : limit;
     const uint32_t n = min(32u, end - s.i);
     const bool valid = lane < n;
@@ -308,28 +324,61 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
     if (lane < 4 && s.i + 32 + lane * 8 < c.len)   // next window's lines into L1
       asm volatile("prefetch.global.L1 [%0];" ::"l"(c.ops + s.i + 32 + lane * 8));
     const uint32_t tag = (uint32_t)(e.w & 3);
-    const uint64_t dur = e.w >> 2;
+    const uint64_t pay = e.w >> 2;
     const int64_t rdisp = e.disp + s.cdel;
-    // collective metadata of every COLL lane, loaded in parallel (overlaps the scan)
-    uint32_t c_nr = 0, c_gi = 0, c_cb = 0;
-    int64_t c_wt = 0;
-    if (valid && tag == TAG_COLL) {
-      const RankColl ent = __ldg(&b.rcolls[c.rc + dur]);
-      c_wt = __ldg(&b.rcw[c.rc + dur]);      // independent of ent: wire inlined by resolve
-      c_nr = (uint32_t)(ent >> 48);
-      c_gi = (uint32_t)(ent >> 32) & 0xffffu;
-      c_cb = (uint32_t)ent;                  // call_idx
+    // lane-parallel classification: affine map (A, B), side effect, or blocker
+    int64_t A = 0, B = NEG, w8 = 0;
+    uint32_t fx = 0;            // side effect at commit: 1 record fire, 2 post last arrival
+    uint32_t target = 0;
+    CollSlot *cs = nullptr;
+    bool blocker = false;
+    if (valid) {
+      if (s.x >= LIM_T || rdisp >= LIM_T) {
+        blocker = true;
+      } else if (tag == TAG_KERN) {
+        if (pay >= LIM_D) blocker = true;      // also EXEC_BAD
+        else { A = (int64_t)pay; B = rdisp + A; }
+      } else if (tag == TAG_REC) {
+        A = 0; B = rdisp; fx = 1;
+      } else if (tag == TAG_WAIT) {
+        const int64_t f = pay == (EXEC_NONE >> 2) ? -1 : vload(&c.fire[pay]);
+        if (f < 0) blocker = true;
+        else { A = 0; B = rdisp > f ? rdisp : f; }
+      } else {
+        const RCX rx = c.rc[pay];
+        const RankColl ent = rx.ent;
+        w8 = rx.wire;
+        const uint32_t nr = (uint32_t)(ent >> 48);
+        const uint32_t g = (uint32_t)(ent >> 32) & 0xffffu;
+        const uint32_t idx = (uint32_t)ent;
+        if (w8 >= (int64_t)LIM_D) {
+          blocker = true;
+        } else if (nr == 1) {                  // one member (class): no wait
+          A = w8; B = rdisp + w8;
+        } else {
+          if (sh.ring) {
+            cs = sh.ring + 2 * g + (idx & 1u);
+            target = ((idx >> 1) + 1u) * nr;
+          } else {
+            cs = b.cslots + J.slots + sh.cb[g * sh.cb_stride] + idx;
+            target = nr;
+          }
+          const uint32_t cnt = vload(&cs->count);
+          if (lane == 0 && (s.flags & 1u)) {   // our arrival already posted
+            if (cnt >= target) { A = NEG; B = (int64_t)vload(&cs->maxarr) + w8; }
+            else blocker = true;
+          } else if (cnt + 1 == target) {      // every other member is in: we complete it
+            const int64_t m = (int64_t)vload(&cs->maxarr);
+            A = w8; B = (rdisp > m ? rdisp : m) + w8; fx = 2;
+          } else {
+            blocker = true;
+          }
+        }
+      }
     }
-    const bool special = valid && (tag != TAG_KERN || dur >= LIM_D || rdisp >= LIM_T ||
-                                   s.x >= LIM_T);
-    const uint32_t smask = __ballot_sync(FULL, special);
-    // segmented inclusive max-plus scan; segments restart after special ops
-    int64_t A = 0, B = NEG;
-    if (valid && !special) {
-      A = (int64_t)dur;
-      B = rdisp + (int64_t)dur;
-    }
-    bool flag = (lane == 0) || ((smask >> (lane - 1)) & 1u);
+    const uint32_t bmask = __ballot_sync(FULL, blocker);
+    if (blocker) { A = 0; B = NEG; }
+    bool flag = (lane == 0) || ((bmask >> (lane - 1)) & 1u);
 #pragma unroll
     for (uint32_t off = 1; off < 32; off <<= 1) {
       const int64_t A2 = __shfl_up_sync(FULL, A, off);
@@ -342,20 +391,50 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
         flag = f2;
       }
     }
-    // apply special ops in order
+    // finalize segments; apply blockers in order
     int64_t xin = s.x, d = 0;
-    uint32_t p = 0, commit = n, spec = smask;
+    uint32_t p = 0, commit = n, spec = bmask;
     bool blocked = false;
-    while (spec) {
-      const uint32_t q = __ffs(spec) - 1;
-      spec &= spec - 1;
-      if (lane >= p && lane < q) {
+    for (;;) {
+      const uint32_t q = spec ? (uint32_t)(__ffs(spec) - 1) : n;
+      const bool in_seg = lane >= p && lane < q;
+      if (in_seg) {
         const int64_t v = xin + A;
         d = v > B ? v : B;
       }
+      int64_t prev = __shfl_up_sync(FULL, d, 1);
+      if (lane == p) prev = xin;
+      if (in_seg && fx) {
+        if (fx == 1) {
+          vstore(&c.fire[pay], d);
+        } else {
+          const int64_t ready = rdisp > prev ? rdisp : prev;
+          atomicMax(&cs->maxarr, (unsigned long long)ready);
+          __threadfence_block();
+          if (atomicAdd(&cs->count, 1u) + 1 != target) err = MAYA_ST_INTERNAL;
+        }
+      }
+      if (sh.record && in_seg) {
+        b.tl_start[c.tl + s.i + lane] = rdisp > prev ? rdisp : prev;
+        b.tl_end[c.tl + s.i + lane] = d;
+      }
+      if (__any_sync(FULL, in_seg && fx)) {
+        adv = true;
+        __threadfence_block();
+      }
+      if (__any_sync(FULL, err != 0)) {
+        err = __reduce_max_sync(FULL, (unsigned)err);
+        blocked = true;
+        commit = q;
+        break;
+      }
+      if (q >= n) break;
+      spec &= spec - 1;
+      // blocker q: applied by lane 0 (sim.py:311-343 semantics)
       const int64_t xq = q > p ? __shfl_sync(FULL, d, q - 1) : xin;
       const int64_t qd = __shfl_sync(FULL, rdisp, q);
       const uint64_t qw = __shfl_sync(FULL, e.w, q);
+      const int64_t qw8 = __shfl_sync(FULL, w8, q);
       const int64_t ready = qd > xq ? qd : xq;
       const uint32_t qtag = (uint32_t)(qw & 3);
       const uint64_t qpay = qw >> 2;
@@ -363,82 +442,80 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
       int64_t nx = 0;
       uint32_t stc = STEP_OK, wk = WAKE_NONE, wt = 0, eno = 0;
       const void *wa = nullptr;
-      if (qtag == TAG_KERN) {            // exact, overflow-checked path
-        if (qw == EXEC_BAD) { stc = STEP_ERR; eno = MAYA_ST_ESTIMATION; }
-        else if ((int64_t)qpay > INT64_MAX - ready) { stc = STEP_ERR; eno = MAYA_ST_OVERFLOW; }
-        else nx = ready + (int64_t)qpay;
-      } else if (qtag == TAG_REC) {      // fire the event (sim.py:287-300)
-        if (lane == 0) vstore(&c.fire[qpay], ready);
-        nx = ready;
-      } else if (qtag == TAG_WAIT) {     // StreamWaitEvent (sim.py:311-319)
-        if (qpay == (EXEC_NONE >> 2)) {
-          stc = STEP_BLOCK;
-          wk = WAKE_ROUND;
-        } else {
-          const int64_t f = vload(&c.fire[qpay]);
+      if (ready >= LIM_T || (qtag == TAG_KERN)) {    // exact, overflow-checked
+        int64_t dd = 0;
+        if (qtag == TAG_KERN) {
+          if (qw == EXEC_BAD) { stc = STEP_ERR; eno = MAYA_ST_ESTIMATION; }
+          dd = (int64_t)qpay;
+        }
+        if (stc == STEP_OK && qtag == TAG_KERN) {
+          if (dd > INT64_MAX - ready) { stc = STEP_ERR; eno = MAYA_ST_OVERFLOW; }
+          else nx = ready + dd;
+        }
+      }
+      if (stc == STEP_OK && qtag != TAG_KERN) {
+        if (qtag == TAG_REC) {
+          if (lane == 0) vstore(&c.fire[qpay], ready);
+          nx = ready;
+        } else if (qtag == TAG_WAIT) {
+          const int64_t f = qpay == (EXEC_NONE >> 2) ? -1 : vload(&c.fire[qpay]);
           if (f < 0) {
             stc = STEP_BLOCK;
-            wk = WAKE_FIRE;
-            wa = &c.fire[qpay];
+            s.flags = 0;
+            wk = qpay == (EXEC_NONE >> 2) ? WAKE_ROUND : WAKE_FIRE;
+            wa = qpay == (EXEC_NONE >> 2) ? nullptr : &c.fire[qpay];
           } else {
             nx = ready > f ? ready : f;
           }
-        }
-      } else {                           // collective rendezvous (sim.py:326-343)
-        const uint32_t nr = __shfl_sync(FULL, c_nr, q);
-        const int64_t w8 = __shfl_sync(FULL, c_wt, q);
-        if (nr == 1) {                   // one member (class): no wait
-          if (w8 > INT64_MAX - ready) { stc = STEP_ERR; eno = MAYA_ST_OVERFLOW; }
-          else nx = ready + w8;
-        } else {
-          const uint32_t g = __shfl_sync(FULL, c_gi, q);
-          const uint32_t idx = __shfl_sync(FULL, c_cb, q);
-          const uint32_t slot = sh.cb[g * sh.cb_stride] + idx;
-          CollSlot *cs;
-          uint32_t target;
-          if (sh.ring) {
-            cs = sh.ring + 2 * g + (idx & 1u);
-            target = ((idx >> 1) + 1u) * nr;
+        } else {                                   // collective rendezvous
+          const RankColl ent = c.rc[qpay].ent;
+          const uint32_t nr = (uint32_t)(ent >> 48);
+          const uint32_t g = (uint32_t)(ent >> 32) & 0xffffu;
+          const uint32_t idx = (uint32_t)ent;
+          if (nr == 1) {
+            if (qw8 > INT64_MAX - ready) { stc = STEP_ERR; eno = MAYA_ST_OVERFLOW; }
+            else nx = ready + qw8;
           } else {
-            cs = b.cslots + J.slots + slot;
-            target = nr;
-          }
-          uint32_t code = 0;
-          if (lane == 0) {
-            bool done = true;
-            if (!(s.flags & 1u)) {
-              atomicMax(&cs->maxarr, (unsigned long long)ready);
-              __threadfence_block();
-              const uint32_t old = atomicAdd(&cs->count, 1u);
-              code |= 2u;                               // arrival posted
-              if (old + 1 > target) code |= 4u;         // internal error
-              else if (old + 1 < target) done = false;
-            } else if (vload(&cs->count) < target) {
-              done = false;
+            CollSlot *qs;
+            uint32_t tgt;
+            if (sh.ring) {
+              qs = sh.ring + 2 * g + (idx & 1u);
+              tgt = ((idx >> 1) + 1u) * nr;
+            } else {
+              qs = b.cslots + J.slots + sh.cb[g * sh.cb_stride] + idx;
+              tgt = nr;
             }
-            if (done && !(code & 4u)) {
-              __threadfence_block();
-              nx = (int64_t)vload(&cs->maxarr);
-              code |= 1u;
+            uint32_t code = 0;
+            int64_t m = 0;
+            const bool posted = q == 0 && (s.flags & 1u);   // flag belongs to the op at s.i
+            if (lane == 0) {
+              bool done = true;
+              if (!posted) {
+                atomicMax(&qs->maxarr, (unsigned long long)ready);
+                __threadfence_block();
+                const uint32_t old = atomicAdd(&qs->count, 1u);
+                code |= 2u;
+                if (old + 1 > tgt) code |= 4u;
+                else if (old + 1 < tgt) done = false;
+              } else if (vload(&qs->count) < tgt) {
+                done = false;
+              }
+              if (done && !(code & 4u)) {
+                __threadfence_block();
+                m = (int64_t)vload(&qs->maxarr);
+                code |= 1u;
+              }
             }
-          }
-          code = __shfl_sync(FULL, code, 0);
-          nx = __shfl_sync(FULL, nx, 0);
-          if (code & 2u) { s.flags |= 1u; adv = true; }
-          if (code & 4u) {
-            stc = STEP_ERR;
-            eno = MAYA_ST_INTERNAL;
-          } else if (!(code & 1u)) {
-            stc = STEP_BLOCK;
-            wk = WAKE_COUNT;
-            wt = target;
-            wa = &cs->count;
-          } else if (w8 > INT64_MAX - nx) {
-            stc = STEP_ERR;
-            eno = MAYA_ST_OVERFLOW;
-          } else {
-            nx += w8;
-            s.flags = 0;
+            code = __shfl_sync(FULL, code, 0);
+            m = __shfl_sync(FULL, m, 0);
+            if (code & 2u) adv = true;
+            if (code & 4u) { stc = STEP_ERR; eno = MAYA_ST_INTERNAL; }
+            else if (!(code & 1u)) {
+              stc = STEP_BLOCK; wk = WAKE_COUNT; wt = tgt; wa = &qs->count;
+              s.flags = (posted || (code & 2u)) ? 1u : 0u;   // for the new s.i (= this op)
+            }
+            else if (qw8 > INT64_MAX - m) { stc = STEP_ERR; eno = MAYA_ST_OVERFLOW; }
+            else { nx = m + qw8; }
           }
         }
       }
@@ -447,6 +524,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
 #endif
       if (stc != STEP_OK) {
         if (stc == STEP_ERR) err = (int)eno;
+        if (stc == STEP_ERR && q > 0) s.flags = 0;
         s.wk = wk;
         s.wt = wt;
         s.wa = wa;
@@ -454,27 +532,23 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
         commit = q;
         break;
       }
-      SlowRes r{nx, 0, 0, nullptr};
-      if (lane == q) d = r.nx;
-      xin = r.nx;
-      p = q + 1;
-    }
-    if (!blocked && lane >= p && lane < n) {
-      const int64_t v = xin + A;
-      d = v > B ? v : B;
-    }
-    if (commit > 0) {
-      if (sh.record) {
-        int64_t prev = __shfl_up_sync(FULL, d, 1);
-        if (lane == 0) prev = s.x;
-        if (lane < commit) {
-          b.tl_start[c.tl + s.i + lane] = rdisp > prev ? rdisp : prev;
-          b.tl_end[c.tl + s.i + lane] = d;
+      if (lane == q) {
+        d = nx;
+        if (sh.record) {
+          b.tl_start[c.tl + s.i + lane] = ready;
+          b.tl_end[c.tl + s.i + lane] = nx;
         }
       }
+      xin = nx;
+      p = q + 1;
+    }
+    if (commit > 0) {
       s.x = __shfl_sync(FULL, d, commit - 1);
       s.i += commit;
       adv = true;
+      // the arrival flag belongs to the op at s.i: a committed op 0 completed it;
+      // a blocker at q > 0 set it for the new s.i
+      if (!blocked) s.flags = 0;
     }
 #ifdef MAYA_PROFILE
     if (lane == 0) { PROF_ADD(0, clock64() - t_win); PROF_ADD(4, 1); }
@@ -505,7 +579,7 @@ __device__ bool host_step(const DevBatch &b, const JobSh &sh, uint32_t r, int64_
       if (s.arg == NO_REC) {
         ok = false;
       } else {
-        X = vload(&b.fire[J.fire + rr.fire + s.arg]);
+        X = vload(&sh.fire[rr.fire + s.arg]);
         ok = X >= 0;
       }
     } else {
@@ -556,8 +630,9 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
     return;
   }
   const uint32_t W = J.n_walkers, R = J.n_ranks;
-  const SchedLayout L = sched_layout(W, R, J.n_comms, (J.flags & JOB_RING) != 0);
-  const bool on_chip = L.bytes <= smem_cap;
+  const SchedLayout L = sched_layout(W, R, J.n_comms, (J.flags & JOB_RING) != 0, J.n_fire,
+                                     J.n_rcolls, smem_cap);
+  const bool on_chip = L.on_chip;
   uint8_t *base = on_chip ? dsm : b.spill + J.wstate;
   JobSh sh;
   sh.J = &J;
@@ -577,6 +652,15 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
   sh.st = (WSt *)(base + (on_chip ? L.state : ((4 * R + 15) & ~15u)));
   sh.wid = b.wids + J.walkers;
   sh.ctx = on_chip ? (WCtx *)(dsm + L.ctx) : nullptr;
+  sh.fire = L.fire_on ? (int64_t *)(dsm + L.fire) : b.fire + J.fire;
+  sh.rcx = L.rcx_on ? (const RCX *)(dsm + L.rcx) : b.rcx + J.rcolls;
+  if (L.fire_on)
+    for (uint32_t q = tid; q < J.n_fire; q += nt) ((int64_t *)(dsm + L.fire))[q] = -1;
+  if (L.rcx_on) {   // stage the job's collective table (contiguous, 16 B records)
+    const RCX *src = b.rcx + J.rcolls;
+    RCX *dst = (RCX *)(dsm + L.rcx);
+    for (uint32_t q = tid; q < J.n_rcolls; q += nt) dst[q] = src[q];
+  }
   sh.epoch = &s_epoch;
   sh.record = record;
   if (tid == 0) {
@@ -595,7 +679,7 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
   }
   for (uint32_t w = tid; w < W; w += nt) {
     WCtx c;
-    load_ctx(b, J, w, 0, c);
+    load_ctx(b, J, w, 0, c, sh.fire, sh.rcx);
     sh.st[w] = WSt{0, 0, 0, 0, 0, c.nsync ? c.cnt[0] : c.len, nullptr, 0, WAKE_NONE};
     if (sh.ctx) sh.ctx[w] = c;
   }
@@ -604,6 +688,9 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
   int64_t tmax = 0;
   int err = 0;
   int64_t rounds = 0;
+#ifdef MAYA_PROFILE
+  unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   uint32_t my_wb = 0, my_we = 0;   // walkers of this warp's first rank
   if (wp < R) {
     const RankRec rr = b.ranks[J.ranks + wp];
@@ -640,9 +727,13 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
               if (s.i >= sh.ctx[w].len) continue;
               c = sh.ctx[w];
             } else {
-              load_ctx(b, J, w, record, c);
+              load_ctx(b, J, w, record, c, sh.fire, sh.rcx);
             }
-            pass |= warp_walk(b, sh, c, s, tmax, err, lane);
+            pass |= warp_walk(b, sh, c, s, tmax, err, lane
+#ifdef MAYA_PROFILE
+                              , prof_acc
+#endif
+                              );
             __syncwarp();
             if (lane == 0) sh.st[w] = s;
           }
@@ -705,6 +796,10 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
     if (err) { atomicMax(&s_err, err); progress = 0; }
     if (!__syncthreads_or(progress)) break;
   }
+#ifdef MAYA_PROFILE
+  if (lane == 0)
+    for (int q = 0; q < 8; q++) atomicAdd(&g_prof[q], prof_acc[q]);
+#endif
   for (uint32_t w = tid; w < W; w += nt) {
     const Walker wk = b.walkers[J.walkers + w];
     const RankRec rr = b.ranks[J.ranks + wk.rank];
@@ -760,7 +855,7 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
   }
 }
 
-static const uint32_t SCHED_SMEM_CAP = 96 * 1024;
+static const uint32_t SCHED_SMEM_CAP = 112 * 1024;
 
 int sched_variant(uint32_t W, uint32_t R) {
   (void)W;

@@ -32,7 +32,7 @@ struct DevBatch {
   const Feature *feats;
   const RankColl *rcolls;
   const uint32_t *rcslot;     // batch-global call slot of each rank-collective entry
-  int64_t *rcw;               // wire time of each rank-collective entry (resolve)
+  RCX *rcx;                   // entry + wire time of each rank-collective entry (resolve)
   ExecOp *exec;
   // scratch / outputs
   int64_t *feat_ns;

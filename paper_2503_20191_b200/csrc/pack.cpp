@@ -563,6 +563,7 @@ void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P, bool collap
     for (size_t w = 0; w < P.walkers.size(); w++) P.wids[w] = (uint32_t)w;
     H.flags = ring ? JOB_RING : 0;
     H.n_rcolls = (uint32_t)P.rcolls.size();
+    H.n_fire = (uint32_t)fire;
     H.n_ranks = (uint32_t)P.ranks.size();
     H.n_comms = (uint32_t)P.comms.size();
     H.n_slots = (uint32_t)P.slots.size();

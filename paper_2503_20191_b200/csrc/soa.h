@@ -37,29 +37,50 @@ static const uint32_t NO_REC = 0xFFFFFFFFu;
 // states go to a per-job global spill area of spill_bytes() and collectives
 // rendezvous through global slots.
 struct SchedLayout {
-  uint32_t ring, cb, hostk, state, ctx, bytes;   // byte offsets / total
-  bool ring_on;                             // smem rings for collectives
+  uint32_t ring, cb, hostk, state, ctx, fire, rcx, bytes;   // byte offsets / total
+  bool on_chip;     // walker state/contexts, host-sync counters in smem
+  bool ring_on;     // collectives rendezvous in smem rings
+  bool fire_on;     // event-record times in smem
+  bool rcx_on;      // per-rank collective entries + wire times in smem
 };
 static const uint32_t RING_MAX_COMMS = 4096;
 static const uint32_t WSTATE_BYTES = 48;
 static const uint32_t WCTX_BYTES = 64;
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+// Greedy: the walker core must fit; then record times; then collective tables.
 __host__ __device__ inline SchedLayout sched_layout(uint32_t W, uint32_t R, uint32_t n_comms,
-                                                    bool ring_flag) {
-  SchedLayout L;
+                                                    bool ring_flag, uint32_t n_fire,
+                                                    uint32_t n_rcolls, uint32_t cap) {
+  SchedLayout L{};
   L.ring_on = ring_flag && n_comms <= RING_MAX_COMMS;
-  uint32_t off = 0;
-  L.ring = off;
-  if (L.ring_on) off += 32u * n_comms;
-  L.cb = off;
-  off = align16(off + 4u * n_comms);
-  L.hostk = off;
-  off = align16(off + 4u * R);
-  L.state = off;
-  off += WSTATE_BYTES * W;
-  L.ctx = off;
-  off += WCTX_BYTES * W;
-  L.bytes = off;
+  uint64_t off = 0;
+  L.ring = (uint32_t)off;
+  if (L.ring_on) off += 32ull * n_comms;
+  L.cb = (uint32_t)off;
+  off = align16((uint32_t)(off + 4ull * n_comms));
+  L.hostk = (uint32_t)off;
+  off = align16((uint32_t)(off + 4ull * R));
+  L.state = (uint32_t)off;
+  off += (uint64_t)WSTATE_BYTES * W;
+  L.ctx = (uint32_t)off;
+  off += (uint64_t)WCTX_BYTES * W;
+  L.on_chip = off <= cap;
+  if (!L.on_chip) {
+    L.ring_on = false;
+    L.bytes = 0;
+    return L;
+  }
+  L.fire = (uint32_t)off;
+  if (off + 8ull * n_fire <= cap) {
+    L.fire_on = true;
+    off += 8ull * n_fire;
+  }
+  L.rcx = (uint32_t)off;
+  if (off + 16ull * n_rcolls <= cap) {
+    L.rcx_on = true;
+    off += 16ull * n_rcolls;
+  }
+  L.bytes = (uint32_t)off;
   return L;
 }
 // global spill (hostk + states) for jobs whose layout exceeds the CTA budget
@@ -192,6 +213,14 @@ struct JobHdr {
   int32_t status;      // pre-set by the packer (BAD_INPUT, INTERNAL) else 0
   uint32_t flags;      // JobFlags
   uint32_t n_rcolls;
+  uint32_t n_fire;     // record-time entries of the simulated ranks
+  uint32_t pad2;
+};
+
+// per-(rank, rep collective) entry with its wire time (resolve_colls_kernel)
+struct RCX {
+  uint64_t ent;        // RankColl
+  int64_t wire;
 };
 
 struct Walker {

@@ -400,6 +400,41 @@ def workload_cases():
     return cases
 
 
+def synth_cases():
+    """C5 synthetic per-rank-distinct jobs, validated and simulated by the reference."""
+    sys.path.insert(0, HERE)
+    sys.path.insert(0, os.path.dirname(HERE))
+    from dltsim import trace as T
+    from dltsim.cluster import ClusterSpec, load_device_preset
+    from dltsim.collate import collate
+    from dltsim.estimate import RooflineEstimator
+    from paper_2503_20191_b200.synth import c5_job
+    from refmirror import to_reference_like
+
+    def conv(ev):
+        n = type(ev).__name__
+        if n == "KernelLaunch":
+            return T.KernelLaunch(ev.stream, ev.op_kind, T.KernelAttrs.make(
+                {}, ev.attrs.dtype, ev.attrs.flops, ev.attrs.bytes_moved))
+        return getattr(T, n)(**ev.__dict__)
+
+    cases = []
+    for cfg, (R, n) in enumerate([(8, 640), (16, 1280), (24, 320), (3, 2000), (64, 640)]):
+        raw = c5_job(R, n, cfg=cfg)
+        ann = to_reference_like(raw)
+        traces = []
+        for r, wt in sorted(ann.job.reps.items()):
+            tr = T.WorkerTrace(r, *divmod(r, raw.devices_per_host),
+                               tuple(conv(e) for e in wt.events))
+            assert not T.validate_trace(tr)
+            traces.append(tr)
+        cl = ClusterSpec(raw.num_hosts, raw.devices_per_host, raw.capacity,
+                         load_device_preset("fast"))
+        cases.append(run_case(raw.name, collate(traces, {}, cl), RooflineEstimator(),
+                              timeline_limit=0))
+    return cases
+
+
 def estimator_cases():
     from fractions import Fraction
     from dltsim.cluster import DeviceClass, LinkClass, load_device_preset
@@ -506,7 +541,7 @@ def main():
     setup(args.ref)
     only = set(args.only.split(",")) if args.only else None
     todo = [("unit", unit_cases), ("syncfree", syncfree_cases), ("multirank", multirank_cases),
-            ("workload", workload_cases)]
+            ("workload", workload_cases), ("synth", synth_cases)]
     for name, fn in todo:
         if only and name not in only:
             continue

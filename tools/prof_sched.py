@@ -12,7 +12,7 @@ L = E.lib()
 L.maya_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 eng = E.Engine(0)
 names = ["walk_cyc", "slow_cyc", "idle_cyc", "sweep_cyc", "windows", "slow_calls", "wakes", "passes"]
-for label in sys.argv[1:] or ["tp2.pp2.mm8.vs4.rsz", "tp8.pp1.mm8.vs1.rsz", "tp1.pp8.mm8.vs1.rsz"]:
+for label in (sys.argv[1:] if len(sys.argv) > 1 else ([] if os.environ.get("C5") else ["tp2.pp2.mm8.vs4.rsz", "tp1.pp8.mm8.vs1.rsz"])):
     sub = [c for c in cfgs if c.label() == label]
     eng.stage_generated(model, sub, cluster, dispatch_overhead_ns=5000)
     eng.upload()
@@ -22,3 +22,18 @@ for label in sys.argv[1:] or ["tp2.pp2.mm8.vs4.rsz", "tp8.pp1.mm8.vs1.rsz", "tp1
     eng.run(); r = eng.results()
     L.maya_prof_read(buf, 1)
     print(label, "sched ms", round(eng.last_timings_ms()[2], 3), dict(zip(names, list(buf))))
+
+if os.environ.get("C5"):
+    from paper_2503_20191_b200.synth import c5_job
+    for spec in os.environ["C5"].split(","):
+        R, n, B = (int(x) for x in spec.split("x"))
+        jobs = [c5_job(R, n, cfg=c) for c in range(B)]
+        eng.load(jobs, threads=16)
+        eng.run(); eng.results()
+        buf = (C.c_ulonglong * 8)()
+        L.maya_prof_read(buf, 1)
+        eng.run(); r = eng.results()
+        L.maya_prof_read(buf, 1)
+        st = eng.batch_stats()
+        print(f"C5 {spec} sched ms", round(eng.last_timings_ms()[2], 3), "dev_ops", st["device_ops"],
+              dict(zip(names, list(buf))))
