@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <memory>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -40,6 +41,22 @@ struct Seg {
   size_t off = 0, bytes = 0;
 };
 
+// JobPacks are pooled across batches: their vectors keep capacity, so
+// re-staging a batch does not fault in fresh pages (which serialises host
+// threads in the kernel's page-fault path).
+struct PackPool {
+  std::vector<std::unique_ptr<JobPack>> pool;
+  size_t n = 0;
+  size_t size() const { return n; }
+  void clear() { n = 0; }
+  void resize(size_t m) {
+    while (pool.size() < m) pool.push_back(std::make_unique<JobPack>());
+    n = m;
+  }
+  JobPack &operator[](size_t i) { return *pool[i]; }
+  const JobPack &operator[](size_t i) const { return *pool[i]; }
+};
+
 }  // namespace
 
 struct maya_engine {
@@ -51,7 +68,7 @@ struct maya_engine {
   uint32_t var_n[4] = {0, 0, 0, 0}; // jobs per variant (order segments)
   uint32_t var_smem[4] = {0, 0, 0, 0};  // dynamic smem per variant launch
   // staged jobs
-  std::vector<JobPack> packs;
+  PackPool packs;
   std::vector<maya_device_params> devs;
   std::vector<int64_t> eff_num, eff_den;
   int64_t overhead_ns = 1000;
@@ -636,7 +653,8 @@ int maya_batch_stats(maya_engine *e, int64_t *o) {
   o[10] = e->run_launches;
   o[11] = e->topk_launches;
   o[0] = (int64_t)e->packs.size();
-  for (const JobPack &P : e->packs) {
+  for (size_t j = 0; j < e->packs.size(); j++) {
+    const JobPack &P = e->packs[j];
     for (const RepHdr &h : P.reps) o[1] += h.n_events;
     o[2] += (int64_t)P.rank_comm.size();
     o[3] += (int64_t)P.feats.size();
@@ -775,7 +793,7 @@ int maya_batch_add_generated(maya_engine *e, const maya_model *model, int32_t n,
       if (status_out) status_out[i] = rc;
       JobPack &P = e->packs[base + i];
       if (rc != MAYA_OK) {
-        P = JobPack();
+        P.clear();
         P.hdr.status = MAYA_ST_BAD_INPUT;
         P.hdr.key_rank = key_ranks ? key_ranks[i] : i;
         P.message = err;

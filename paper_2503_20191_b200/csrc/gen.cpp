@@ -602,7 +602,7 @@ maya_raw_job GenJob::raw(int32_t device) const {
 
 int generate_job(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
                  int32_t schedule, int64_t overhead, GenJob &G, std::string *err) {
-  G = GenJob();
+  G.clear();   // keep capacity: a worker thread reuses one GenJob across configs
   try {
     if (cl.num_hosts < 1 || cl.devices_per_host < 1) throw GenFail{"empty cluster"};
     if (model.dtype < 0 || model.dtype > 2) throw GenFail{"unknown dtype"};

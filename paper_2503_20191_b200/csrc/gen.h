@@ -33,6 +33,14 @@ struct GenJob {
   std::string comm_blob;  // comm names joined by '\n'
 
   maya_raw_job raw(int32_t device) const;
+  void clear() {
+    num_ranks = num_hosts = devices_per_host = 0;
+    capacity = 0;
+    rep_ranks.clear(); rank_rep.clear(); ev_off.clear(); ev_kind.clear(); ev_stream.clear();
+    ev_f.clear(); comm_names.clear(); comm_nranks.clear(); comm_topo.clear(); call_off.clear();
+    call_kind.clear(); call_bytes.clear(); rank_comm_off.clear(); rank_comm.clear();
+    comm_blob.clear();
+  }
 };
 
 // Returns 0 or a negative code with *err set (invalid configuration).

@@ -458,7 +458,7 @@ void full_view(const maya_raw_job &job, SimView &V) {
 }  // namespace
 
 void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P, bool collapse) {
-  P = JobPack();
+  P.clear();
   JobHdr &H = P.hdr;
   H.key_rank = key_rank;
   H.capacity = job.capacity;

@@ -34,6 +34,17 @@ struct JobPack {
   bool collapsed = false;               // ranks are classes
   uint64_t n_fire = 0, n_delay = 0;
   std::string message;                 // why status != OK
+
+  void clear() {   // keeps capacity (see engine.cu PackPool)
+    hdr = JobHdr{};
+    reps.clear(); ops.clear(); op_seq.clear(); streams.clear(); coll_lc.clear();
+    coll_idx.clear(); syncs.clear(); counts.clear(); mems.clear(); feats.clear(); comms.clear();
+    slots.clear(); ranks.clear(); rank_comm.clear(); walkers.clear(); wids.clear();
+    rcolls.clear(); rep_ring_ok.clear(); comm_rdv.clear(); rank_orig.clear(); rank_sim.clear();
+    collapsed = false;
+    n_fire = n_delay = 0;
+    message.clear();
+  }
 };
 
 // Pack one job.  Never throws; input problems become hdr.status + message.
