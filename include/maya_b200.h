@@ -132,6 +132,10 @@ int maya_batch_num_jobs(maya_engine *eng);
 
 /* Engine options (apply to jobs staged afterwards). */
 #define MAYA_OPT_COLLAPSE 1   /* exact rank-class collapse (default on) */
+#define MAYA_OPT_WARP_SCHED 2 /* schedule every job with the warp-window kernel instead of
+                                 the lane-parallel kernel (A/B and parity testing) */
+#define MAYA_OPT_LANE_SCHED 4 /* schedule every job that fits with the lane-parallel kernel
+                                 (default: per job, by the shape of its FIFOs) */
 int maya_set_options(maya_engine *eng, int32_t options);
 /* Per staged job: 1 if it is simulated as rank classes. */
 int maya_batch_collapsed(maya_engine *eng, uint8_t *out);
@@ -172,7 +176,7 @@ int maya_batch_stats(maya_engine *eng, int64_t *out12);
 
 /* Scheduler phase counters of instrumented builds (-DMAYA_PROFILE); returns
  * 0 (and leaves out8 untouched) in product builds. */
-int maya_prof_read(unsigned long long *out8, int reset);
+int maya_prof_read(unsigned long long *out16, int reset);  /* 8 warp-window + 8 lane counters */
 
 /* Device time of the last maya_run, per phase (ms): estimate, memscan, schedule. */
 int maya_last_timings(maya_engine *eng, float *ms3);

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <functional>
 #include <atomic>
 #include <memory>
 #include <cstdio>
@@ -63,10 +65,14 @@ struct maya_engine {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {};
-  cudaStream_t vstream[4] = {};     // one stream per scheduler variant
-  cudaEvent_t vev[5] = {};          // fork / join
-  uint32_t var_n[4] = {0, 0, 0, 0}; // jobs per variant (order segments)
-  uint32_t var_smem[4] = {0, 0, 0, 0};  // dynamic smem per variant launch
+  // scheduler launch groups: 0-2 warp-window kernel (4/8/16 warps), 3-10 lane
+  // kernel warp jobs (by shared-memory region class), 11-14 lane kernel CTA
+  // jobs (2/4/8/16 warps); each group runs on its own stream (fork/join)
+  static const int NVAR = 15;
+  cudaStream_t vstream[NVAR] = {};
+  cudaEvent_t vev[NVAR + 1] = {};
+  uint32_t var_n[NVAR] = {};        // jobs per group (order segments)
+  uint32_t var_smem[NVAR] = {};     // dynamic smem per group launch
   // staged jobs
   PackPool packs;
   std::vector<maya_device_params> devs;
@@ -86,7 +92,8 @@ struct maya_engine {
   DevTables tables{};
   // segments
   Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_slots, s_walkers, s_reps, s_ops, s_streams,
-      s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot;
+      s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
+      s_lane_jobs, s_lane_wslot, s_lane_perm;
   Seg x_exec, x_rcw, x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
       x_results, x_err, x_topk, x_topk_out, x_topk_n;
   uint64_t n_tl = 0;
@@ -96,6 +103,137 @@ struct maya_engine {
   int64_t run_launches = 0, topk_launches = 0;
   int32_t options = MAYA_OPT_COLLAPSE;
 };
+
+namespace {
+
+// Lane-scheduler plan of one job: launch shape, ring depth and which tables
+// live in shared memory, greedily from the fastest layout down to what fits
+// the per-job budget (sized so that a large batch keeps many jobs resident
+// per SM; a small batch gets the whole CTA budget per job).
+//   variants 3..10: warp jobs, region classes LANE_REGION[v-3]
+//   variants 11..14: CTA jobs of 2/4/8/16 warps
+//   -1: the job runs on the warp-window kernel (variants 0..2)
+static const uint32_t LANE_REGION[8] = {14u << 10, 20u << 10, 28u << 10, 40u << 10,
+                                        56u << 10, 80u << 10, 112u << 10, LANE_SMEM_CAP};
+static const uint32_t LANE_WARP_JOB_MAX_FIFOS = 128;   // 4 FIFOs per lane
+
+struct LanePlan {
+  int variant = -1;
+  uint32_t flags = 0, n_slots = 0, smem = 0, lgd_max = 0, threads = 32, per_lane = 1, fc_log2 = 0;
+};
+
+uint32_t lane_slots_of(uint32_t len, uint32_t lgd_max) {
+  if (len == 0 || lgd_max == 0xff) return 0;
+  const uint32_t chunks = (len + LANE_SLOT_OPS - 1) / LANE_SLOT_OPS;
+  uint32_t lg = 0;
+  while ((1u << lg) < chunks && lg < lgd_max) lg++;
+  return 1u << lg;
+}
+
+uint32_t lane_fifo_len(const JobPack &P, uint32_t w) {
+  const Walker wk = P.walkers[w];
+  const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
+  return P.streams[h.streams + wk.stream].len;
+}
+
+LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
+  LanePlan pl;
+  if (P.hdr.status != MAYA_ST_OK) { pl.variant = 3; return pl; }
+  const uint32_t W = (uint32_t)P.walkers.size(), R = (uint32_t)P.ranks.size();
+  if (!force) {
+    // Lockstep lanes pay off when many FIFOs carry work; a few long FIFOs
+    // (compute streams) are serial chains the warp-window kernel scans 32 ops
+    // per step.
+    // Criterion: the 16th longest FIFO is at least a quarter of the longest.
+    if (W < 16) return pl;
+    std::vector<uint32_t> l(W);
+    for (uint32_t w = 0; w < W; w++) l[w] = lane_fifo_len(P, w);
+    std::nth_element(l.begin(), l.begin() + 15, l.end(), std::greater<uint32_t>());
+    const uint32_t mx = *std::max_element(l.begin(), l.begin() + 16);
+    if (l[15] < 64 || 4ull * l[15] < mx) return pl;
+  }
+  const uint32_t nc = (uint32_t)P.comms.size();
+  const uint32_t ring = (P.hdr.flags & JOB_RING) && nc <= RING_MAX_COMMS ? LANE_COLL_RING : 0;
+  if (W > 16 * LANE_MAX_THREADS) return pl;
+  const bool warp_job = W <= LANE_WARP_JOB_MAX_FIFOS;
+  if (!warp_job) budget = LANE_SMEM_CAP;
+  std::vector<uint32_t> lens(W);
+  for (uint32_t w = 0; w < W; w++) lens[w] = lane_fifo_len(P, w);
+  // record-time cache when the table stays global: 8 live records per rank
+  uint32_t fc = 0;
+  while ((1u << fc) < 8 * R && fc < 12) fc++;
+  struct Try { uint32_t lgd, flags; };
+  const Try tries[] = {{3, LANE_FIRE_SMEM | LANE_RCX_SMEM}, {2, LANE_FIRE_SMEM | LANE_RCX_SMEM},
+                       {1, LANE_FIRE_SMEM | LANE_RCX_SMEM},
+                       {1, LANE_FIRE_SMEM}, {1, 0}, {0xff, LANE_FIRE_SMEM}, {0xff, 0}};
+  for (int pass = 0; pass < 2; pass++) {
+    const uint32_t cap = pass == 0 ? budget : LANE_SMEM_CAP;
+    for (const Try &t : tries) {
+      uint64_t slots = 0;
+      for (uint32_t w = 0; w < W; w++) slots += lane_slots_of(lens[w], t.lgd);
+      if (slots >= (1u << 28)) continue;
+      const uint32_t fl = ring | t.flags;
+      const LaneLayout L =
+          lane_layout(W, R, nc, fl, (uint32_t)slots, P.hdr.n_fire, P.hdr.n_rcolls, fc);
+      if (L.bytes > cap) continue;
+      pl.flags = fl;
+      pl.n_slots = (uint32_t)slots;
+      pl.smem = L.bytes;
+      pl.lgd_max = t.lgd;
+      pl.fc_log2 = (fl & LANE_FIRE_SMEM) ? 0 : fc;
+      if (warp_job) {
+        int v = 0;
+        while (v < 7 && LANE_REGION[v] < L.bytes) v++;
+        pl.variant = 3 + v;
+        pl.threads = 32;
+      } else {
+        uint32_t nw = 2;
+        while (nw * 32 < W && nw * 32 < LANE_MAX_THREADS) nw <<= 1;
+        pl.variant = nw == 2 ? 11 : nw == 4 ? 12 : nw == 8 ? 13 : 14;
+        pl.threads = nw * 32;
+      }
+      pl.per_lane = (W + pl.threads - 1) / pl.threads;
+      if (pl.per_lane == 0) pl.per_lane = 1;
+      return pl;
+    }
+  }
+  return pl;
+}
+
+// lane -> FIFO table (per_lane x threads).  Warp jobs: LPT on FIFO length, so
+// the heavy FIFOs (compute streams) land on distinct lanes.  CTA jobs: one
+// FIFO per thread in rank-major order (the streams of a rank and the ranks of
+// a communicator share a warp), or contiguous blocks when FIFOs outnumber
+// threads.
+void lane_perm_fill(const JobPack &P, const LanePlan &pl, uint32_t *out) {
+  const uint32_t W = (uint32_t)P.walkers.size(), T = pl.threads, K = pl.per_lane;
+  for (uint32_t q = 0; q < K * T; q++) out[q] = 0xffffffffu;
+  if (W <= T) {
+    for (uint32_t w = 0; w < W; w++) out[w] = w;
+    return;
+  }
+  if (T > 32) {
+    for (uint32_t w = 0; w < W; w++) out[(w % K) * T + w / K] = w;
+    return;
+  }
+  std::vector<uint32_t> idx(W);
+  for (uint32_t w = 0; w < W; w++) idx[w] = w;
+  std::vector<uint32_t> lens(W);
+  for (uint32_t w = 0; w < W; w++) lens[w] = lane_fifo_len(P, w);
+  std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return lens[a] > lens[b]; });
+  std::vector<uint64_t> load(T, 0);
+  std::vector<uint32_t> fill(T, 0);
+  for (uint32_t w : idx) {
+    uint32_t best = 0xffffffffu;
+    for (uint32_t t = 0; t < T; t++)
+      if (fill[t] < K && (best == 0xffffffffu || load[t] < load[best])) best = t;
+    out[fill[best] * T + best] = w;
+    fill[best]++;
+    load[best] += lens[w] + 1;
+  }
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -243,6 +381,23 @@ int maya_upload(maya_engine *e) {
     e->job_tl[j] = n_tl;
     for (const RankRec &rr : P.ranks) n_tl += P.reps[rr.rep].n_ops;
   }
+  // scheduler plans (lane kernel unless disabled or the job does not fit it)
+  std::vector<LanePlan> plans(nj);
+  size_t n_perm = 0;
+  {
+    // per-job shared-memory budget: the whole CTA budget for small batches,
+    // else enough to keep the batch resident (148 SMs x 228 KB)
+    const uint64_t sm_bytes = 148ull * 228 * 1024;
+    uint64_t budget = nj <= 296 ? LANE_SMEM_CAP : sm_bytes / nj;
+    if (const char *ev = getenv("MAYA_LANE_BUDGET")) budget = strtoull(ev, nullptr, 10);
+    if (budget < LANE_REGION[0]) budget = LANE_REGION[0];
+    if (budget > LANE_SMEM_CAP) budget = LANE_SMEM_CAP;
+    for (size_t j = 0; j < nj; j++) {
+      if (!(e->options & MAYA_OPT_WARP_SCHED))
+        plans[j] = plan_lane(e->packs[j], (uint32_t)budget, (e->options & MAYA_OPT_LANE_SCHED) != 0);
+      if (plans[j].variant >= 0) n_perm += (size_t)plans[j].per_lane * plans[j].threads;
+    }
+  }
   if (n_reps > 0xffffffffull) return fail(MAYA_EINVAL, "too many representatives in batch");
   if (n_feats >= 0xffffffffull) return fail(MAYA_EINVAL, "too many kernel features in batch");
   if (n_slots >= 0xffffffffull) return fail(MAYA_EINVAL, "too many collective calls in batch");
@@ -273,6 +428,9 @@ int maya_upload(maya_engine *e) {
   seg(e->s_feats, n_feats * sizeof(Feature));
   seg(e->s_rcolls, n_rcolls * sizeof(RankColl));
   seg(e->s_rcslot, n_rcolls * sizeof(uint32_t));
+  seg(e->s_lane_jobs, nj * sizeof(LaneJob));
+  seg(e->s_lane_wslot, n_walkers * sizeof(uint32_t));
+  seg(e->s_lane_perm, n_perm * sizeof(uint32_t));
   e->arena_bytes = off;
   // scratch layout
   off = 0;
@@ -323,16 +481,22 @@ int maya_upload(maya_engine *e) {
     std::vector<int> var(nj);
     for (size_t j = 0; j < nj; j++) {
       order[j] = (int32_t)j;
-      var[j] = sched_variant((uint32_t)e->packs[j].walkers.size(),
-                             (uint32_t)e->packs[j].ranks.size());
+      var[j] = plans[j].variant >= 0 ? plans[j].variant
+                                     : sched_variant((uint32_t)e->packs[j].walkers.size(),
+                                                     (uint32_t)e->packs[j].ranks.size());
     }
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
       if (var[a] != var[b]) return var[a] < var[b];
       return e->packs[a].hdr.dev_ops > e->packs[b].hdr.dev_ops;
     });
-    for (int v = 0; v < 4; v++) e->var_n[v] = e->var_smem[v] = 0;
+    for (int v = 0; v < maya_engine::NVAR; v++) e->var_n[v] = e->var_smem[v] = 0;
     for (size_t j = 0; j < nj; j++) {
       e->var_n[var[j]]++;
+      if (var[j] >= 3) {
+        const uint32_t need = (plans[j].smem + 127u) & ~127u;
+        if (need > e->var_smem[var[j]]) e->var_smem[var[j]] = need;
+        continue;
+      }
       const JobPack &P = e->packs[j];
       const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
                                          (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0,
@@ -344,7 +508,7 @@ int maya_upload(maya_engine *e) {
   // per-job bases (serial prefix), then parallel copy
   struct Base {
     size_t ranks, rank_comm, comms, slots, walkers, reps, ops, streams, colls, syncs, counts,
-        mems, feats, fire, delay, wstate, rcolls;
+        mems, feats, fire, delay, wstate, rcolls, perm;
   };
   std::vector<Base> bases(nj);
   {
@@ -368,6 +532,7 @@ int maya_upload(maya_engine *e) {
       b.fire += P.n_fire;
       b.delay += P.n_delay;
       b.rcolls += P.rcolls.size();
+      if (plans[j].variant >= 0) b.perm += (size_t)plans[j].per_lane * plans[j].threads;
       const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
                                          (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0,
                                          P.hdr.n_fire, P.hdr.n_rcolls, sched_smem_cap());
@@ -426,6 +591,26 @@ int maya_upload(maya_engine *e) {
       }
     }
     CPY(s_rcolls, rcolls, B.rcolls)
+    {  // lane-scheduler plan and per-walker ring words
+      const LanePlan &pl = plans[j];
+      LaneJob lj{pl.flags, pl.n_slots, B.walkers, B.perm, pl.per_lane, pl.fc_log2};
+      memcpy(H + e->s_lane_jobs.off + j * sizeof(LaneJob), &lj, sizeof lj);
+      if (pl.variant >= 0 && P.hdr.status == MAYA_ST_OK)
+        lane_perm_fill(P, pl, (uint32_t *)(H + e->s_lane_perm.off) + B.perm);
+      uint32_t *ws = (uint32_t *)(H + e->s_lane_wslot.off) + B.walkers;
+      uint32_t slot = 0;
+      for (size_t w = 0; w < P.walkers.size(); w++) {
+        const Walker wk = P.walkers[w];
+        const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
+        const uint32_t n = pl.variant >= 3 ? lane_slots_of(P.streams[h.streams + wk.stream].len,
+                                                           pl.lgd_max)
+                                           : 0;
+        uint32_t lg = 0;
+        while ((1u << lg) < n) lg++;
+        ws[w] = n ? (slot | (lg << 28)) : (0xfu << 28);
+        slot += n;
+      }
+    }
     {  // batch-global call slot of every rank-collective entry
       uint32_t *dst = (uint32_t *)(H + e->s_rcslot.off) + B.rcolls;
       for (size_t q = 0; q < P.rcolls.size(); q++) {
@@ -468,6 +653,9 @@ int maya_upload(maya_engine *e) {
   DevBatch &db = e->db;
   db.jobs = (const JobHdr *)(D + e->s_jobs.off);
   db.order = (const int32_t *)(D + e->s_order.off);
+  db.lane_jobs = (const LaneJob *)(D + e->s_lane_jobs.off);
+  db.lane_wslot = (const uint32_t *)(D + e->s_lane_wslot.off);
+  db.lane_perm = (const uint32_t *)(D + e->s_lane_perm.off);
   db.ranks = (const RankRec *)(D + e->s_ranks.off);
   db.rank_comm = (const uint32_t *)(D + e->s_rank_comm.off);
   db.comms = (const CommRec *)(D + e->s_comms.off);
@@ -574,13 +762,24 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   CU(cudaEventRecord(e->ev[2], e->stream));
   {
     // variants run concurrently on their own streams (fork/join)
-    CU(cudaEventRecord(e->vev[4], e->stream));
+    CU(cudaEventRecord(e->vev[maya_engine::NVAR], e->stream));
     uint32_t off = 0;
-    for (int v = 0; v < 4; v++) {
+    for (int v = 0; v < maya_engine::NVAR; v++) {
       if (!e->var_n[v]) continue;
-      CU(cudaStreamWaitEvent(e->vstream[v], e->vev[4], 0));
-      launch_schedule_variant(db, v, db.order + off, e->var_n[v], record_timeline ? 1 : 0,
-                              e->var_smem[v], e->vstream[v]);
+      CU(cudaStreamWaitEvent(e->vstream[v], e->vev[maya_engine::NVAR], 0));
+      if (v < 3) {
+        launch_schedule_variant(db, v, db.order + off, e->var_n[v], record_timeline ? 1 : 0,
+                                e->var_smem[v], e->vstream[v]);
+      } else if (v <= 10) {
+        const uint32_t region = e->var_smem[v];
+        uint32_t wpc = region ? LANE_SMEM_CAP / region : 8;
+        wpc = wpc < 1 ? 1 : wpc > 8 ? 8 : wpc;
+        launch_schedule_lane_warp(db, db.order + off, e->var_n[v], wpc, region,
+                                  record_timeline ? 1 : 0, e->vstream[v]);
+      } else {
+        launch_schedule_lane(db, db.order + off, e->var_n[v], 64u << (v - 11),
+                             record_timeline ? 1 : 0, e->var_smem[v], e->vstream[v]);
+      }
       CU(cudaGetLastError());
       CU(cudaEventRecord(e->vev[v], e->vstream[v]));
       CU(cudaStreamWaitEvent(e->stream, e->vev[v], 0));
@@ -591,7 +790,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   {
     int64_t n = (db.n_feats ? 1 : 0) + (db.n_slots ? 1 : 0) + (db.n_reps ? 1 : 0) +
                 (db.n_ops ? 1 : 0) + (db.n_rcolls ? 1 : 0);
-    for (int v = 0; v < 4; v++) n += e->var_n[v] ? 1 : 0;
+    for (int v = 0; v < maya_engine::NVAR; v++) n += e->var_n[v] ? 1 : 0;
     e->run_launches = n;
   }
   e->ran = true;
@@ -639,7 +838,12 @@ int maya_results(maya_engine *e, maya_job_result *out) {
 }
 
 // Engine-internal profiling counters (builds with -DMAYA_PROFILE; else returns 0).
-int maya_prof_read(unsigned long long *out8, int reset) { return prof_read(out8, reset); }
+// out: 16 counters (8 warp-window kernel, 8 lane kernel).
+int maya_prof_read(unsigned long long *out16, int reset) {
+  const int a = prof_read(out16, reset);
+  lane_prof_read(out16 + 8, reset);
+  return a;
+}
 
 int maya_get_stream(maya_engine *e, void **stream) {
   *stream = (void *)e->stream;

@@ -46,6 +46,9 @@ struct DevBatch {
   int64_t *tl_end;
   maya_job_result *results;
   const int32_t *order;       // CTA -> job (largest first)
+  const LaneJob *lane_jobs;   // per job: lane-scheduler layout choice
+  const uint32_t *lane_wslot; // per walker: ring slot word (soa.h)
+  const uint32_t *lane_perm;  // per job: lane -> FIFO tables
   int32_t *err_flag;          // any estimator failure
   uint32_t n_jobs, n_reps, n_feats, n_slots;
   uint64_t n_ops, n_rcolls;
@@ -66,7 +69,13 @@ void launch_resolve(const DevBatch &b, cudaStream_t s);
 void launch_schedule_variant(const DevBatch &b, int variant, const int32_t *order, uint32_t n,
                              int record, uint32_t smem, cudaStream_t s);
 uint32_t sched_smem_cap();
+void launch_schedule_lane_warp(const DevBatch &b, const int32_t *order, uint32_t n,
+                               uint32_t warps_per_cta, uint32_t region, int record,
+                               cudaStream_t s);
+void launch_schedule_lane(const DevBatch &b, const int32_t *order, uint32_t n, uint32_t threads,
+                          int record, uint32_t smem, cudaStream_t s);
 int prof_read(unsigned long long *out8, int reset);   // MAYA_PROFILE builds only
+int lane_prof_read(unsigned long long *out8, int reset);
 void launch_topk(const DevBatch &b, int k, maya_topk_entry *out, int32_t *n_out, void *scratch,
                  cudaStream_t s);
 size_t topk_scratch_bytes(uint32_t n_jobs, int k);

@@ -242,6 +242,23 @@ void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
         throw Fail{MAYA_ST_BAD_INPUT, "unknown event kind " + std::to_string(k)};
     }
   }
+  // collectives renumbered stream-major: the collectives of one FIFO are
+  // consecutive in the per-rank collective tables, so a walker reads (and
+  // prefetches) its entries sequentially
+  {
+    const uint32_t nc = (uint32_t)(P.coll_lc.size() - coll0);
+    std::vector<uint32_t> lc(nc), ix(nc);
+    uint32_t next = 0;
+    for (auto &ops : RB.sops)
+      for (Op &o : ops)
+        if (op_tag(o.meta) == TAG_COLL) {
+          lc[next] = P.coll_lc[coll0 + o.arg];
+          ix[next] = P.coll_idx[coll0 + o.arg];
+          o.arg = next++;
+        }
+    std::copy(lc.begin(), lc.end(), P.coll_lc.begin() + coll0);
+    std::copy(ix.begin(), ix.end(), P.coll_idx.begin() + coll0);
+  }
   // stream-major op layout
   h.ops = P.ops.size();
   h.streams = P.streams.size();

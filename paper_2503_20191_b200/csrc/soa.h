@@ -96,6 +96,60 @@ __host__ __device__ inline uint32_t sched_warps(uint32_t R) {
   return nw;
 }
 
+// ---- lane-parallel scheduler (sched_lane.cu) ---------------------------------
+// One CTA per job, one lane per (rank, stream) FIFO; a FIFO stages its ops in
+// a ring of 8-op (128 B) shared-memory slots filled by bulk copies.
+static const uint32_t LANE_MAX_THREADS = 512;
+static const uint32_t LANE_SMEM_CAP = 220 * 1024;
+static const uint32_t LANE_SLOT_OPS = 8;
+enum LaneFlags : uint32_t {
+  LANE_COLL_RING = 1,   // collectives rendezvous in shared-memory rings
+  LANE_FIRE_SMEM = 2,   // record times in shared memory
+  LANE_RCX_SMEM = 4,    // per-rank collective table in shared memory
+};
+struct LaneJob {
+  uint32_t flags;       // LaneFlags
+  uint32_t n_slots;     // ring slots of the job (sum over FIFOs)
+  uint64_t wslot;       // batch index of the job's first per-walker ring word
+  uint64_t perm;        // batch index of the job's lane -> FIFO table
+  uint32_t per_lane;    // FIFOs per lane (table is per_lane x group threads, 0xFFFFFFFF pad)
+  uint32_t fc_log2;     // record-time cache entries (log2; 0: none) when LANE_FIRE_SMEM is off
+};
+// per-walker ring word: first slot (job-local, 28 bits) | log2(slots) << 28
+// (0xF << 28: the FIFO reads global memory directly)
+struct LaneLayout {
+  uint32_t ring, cb, hostk, state, ctx, bars, rdata, fire, fcache, rcx, bytes;
+};
+__host__ __device__ inline LaneLayout lane_layout(uint32_t W, uint32_t R, uint32_t n_comms,
+                                                  uint32_t flags, uint32_t n_slots,
+                                                  uint32_t n_fire, uint32_t n_rcolls,
+                                                  uint32_t fc_log2) {
+  LaneLayout L{};
+  uint64_t off = 0;
+  L.ring = (uint32_t)off;
+  if (flags & LANE_COLL_RING) off += 32ull * n_comms;
+  L.cb = (uint32_t)off;
+  off = (off + 4ull * n_comms + 15) & ~15ull;
+  L.hostk = (uint32_t)off;
+  off = (off + 4ull * R + 15) & ~15ull;
+  L.state = (uint32_t)off;
+  off += 48ull * W;
+  L.ctx = (uint32_t)off;
+  off += 64ull * W;
+  L.bars = (uint32_t)off;
+  off = (off + 8ull * n_slots + 127) & ~127ull;
+  L.rdata = (uint32_t)off;
+  off += 16ull * LANE_SLOT_OPS * n_slots;
+  L.fire = (uint32_t)off;
+  if (flags & LANE_FIRE_SMEM) off += (8ull * n_fire + 15) & ~15ull;
+  L.fcache = (uint32_t)off;
+  if (!(flags & LANE_FIRE_SMEM) && fc_log2) off += 16ull << fc_log2;
+  L.rcx = (uint32_t)off;
+  if (flags & LANE_RCX_SMEM) off += 16ull * n_rcolls;
+  L.bytes = off > 0xffffffffull ? 0xffffffffu : (uint32_t)off;
+  return L;
+}
+
 // 16-byte device op record.
 struct alignas(16) Op {
   int64_t disp;    // sum of host gaps before this op in host order (ns)

@@ -99,18 +99,36 @@ class Timeline:
 class Engine:
     """One engine per CUDA device (C ABI: maya_open ... maya_close)."""
 
-    def __init__(self, device: int = 0, collapse: bool = True):
+    def __init__(self, device: int = 0, collapse: bool = True, sched: str = "auto"):
         L = lib()
         self._h = C.c_void_p()
         _check(L.maya_open(int(device), C.byref(self._h)))
-        self.set_collapse(collapse)
+        if sched not in ("auto", "lane", "warp"):
+            raise ValueError(f"sched must be 'auto', 'lane' or 'warp', not {sched!r}")
+        self._collapse = bool(collapse)
+        self._sched = sched
+        self._apply_options()
         self.device = device
         self.batch: Batch | None = None
         self.n_jobs = 0
 
     def set_collapse(self, on: bool) -> None:
         """Exact rank-class collapse of deduplicated jobs."""
-        _check(lib().maya_set_options(self._h, 1 if on else 0))
+        self._collapse = bool(on)
+        self._apply_options()
+
+    def set_sched(self, sched: str) -> None:
+        """Scheduler kernel: 'auto' (per job, default), 'lane' (lane-parallel
+        wherever it fits) or 'warp' (warp-window for every job)."""
+        if sched not in ("auto", "lane", "warp"):
+            raise ValueError(f"sched must be 'auto', 'lane' or 'warp', not {sched!r}")
+        self._sched = sched
+        self._apply_options()
+
+    def _apply_options(self) -> None:
+        opts = ((1 if self._collapse else 0) | (2 if self._sched == "warp" else 0)
+                | (4 if self._sched == "lane" else 0))
+        _check(lib().maya_set_options(self._h, opts))
 
     def collapsed(self) -> np.ndarray:
         out = np.zeros(max(self.n_jobs, 1), dtype=np.uint8)
