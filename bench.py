@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c5", default="8x10000x4096",
+                    help="C5 synthetic sweep point RANKSxOPSxCONFIGS for the HBM-roofline line "
+                         "('' to skip)")
     return ap.parse_args()
 
 
@@ -248,6 +251,54 @@ def ncu_traffic():
         return None
 
 
+def c5_sweep(spec: str, steps: int, dev_index: int) -> dict:
+    """C5: per-rank-distinct synthetic traces, the workload the
+    HBM-roofline claim is made on.  Scheduler-kernel time only (CUDA events on
+    the engine's streams), inputs resident in HBM, L2 flushed between runs."""
+    import numpy as np
+    import torch
+    from paper_2503_20191_b200.engine import Engine
+    from paper_2503_20191_b200.synth import c5_job
+    R, n, B = (int(x) for x in spec.split("x"))
+    distinct = min(B, 64)
+    jobs = [c5_job(R, n, cfg=c) for c in range(distinct)]
+    eng = Engine(dev_index)
+    eng.load([jobs[c % distinct] for c in range(B)], threads=host_threads())
+    st = eng.batch_stats()
+    dev = torch.device("cuda", dev_index)
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
+    for _ in range(2):
+        eng.run()
+        r = eng.results()
+    ok = int((r["status"] == 0).sum())
+    sched = []
+    for i in range(max(3, steps)):
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xff)
+        eng.run()
+        eng.results()
+        sched.append(eng.last_timings_ms()[2])
+    ms = statistics.median(sched)
+    alg = (16 * st["rep_events"] + 4 * st["rank_comms"] + 16 * (st["features"] + st["slots"])
+           + 24 * st["jobs"])
+    peak, peak_kind = measured_peak_hbm()
+    achieved = alg / (ms / 1000) / 1e9
+    eng.close()
+    del flush
+    return {"workload": f"C5 synthetic: {R} ranks x {n} events/rank, {B} configs per batch "
+                        f"({distinct} distinct seeds tiled; every config has its own arena copy)",
+            "configs_per_s": round(B / (ms / 1000), 1),
+            "rank_ops_per_s": round(st["rank_ops"] / (ms / 1000), 1),
+            "ok": ok, "configs": B, "sched_ms": round(ms, 4),
+            "roofline": {"bound": "hbm", "kernel": "sched_lane_warp_kernel",
+                         "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "peak_source": peak_kind,
+                         "algorithmic_bytes_per_launch": alg,
+                         "note": "16 B x rep events + tables (DESIGN.md roofline); "
+                                 "scheduler kernels only"}}
+
+
 def bench_ours(args):
     import numpy as np
     import torch
@@ -427,6 +478,8 @@ def bench_ours(args):
             "full_rank": full,
             "parity": parity,
         }
+        if world == 1 and args.c5:
+            line["c5"] = c5_sweep(args.c5, args.steps, local)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(model, cluster, configs, args.cpu_seconds,
                                                 host_threads())
