@@ -144,13 +144,17 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
     // Lockstep lanes pay off when many FIFOs carry work; a few long FIFOs
     // (compute streams) are serial chains the warp-window kernel scans 32 ops
     // per step.
-    // Criterion: the 16th longest FIFO is at least a quarter of the longest.
+    // Criterion: the 16th longest FIFO is at least a quarter of the longest,
+    // and no FIFO is longer than 8k ops.
     if (W < 16) return pl;
     std::vector<uint32_t> l(W);
     for (uint32_t w = 0; w < W; w++) l[w] = lane_fifo_len(P, w);
     std::nth_element(l.begin(), l.begin() + 15, l.end(), std::greater<uint32_t>());
     const uint32_t mx = *std::max_element(l.begin(), l.begin() + 16);
     if (l[15] < 64 || 4ull * l[15] < mx) return pl;
+    // very long FIFOs: the warp-window scan's 32 ops per step win even when
+    // many of them are busy (C5 at 100k ops/rank, C4's 16-stage pipelines)
+    if (mx > 8192) return pl;
   }
   const uint32_t nc = (uint32_t)P.comms.size();
   const uint32_t ring = (P.hdr.flags & JOB_RING) && nc <= RING_MAX_COMMS ? LANE_COLL_RING : 0;

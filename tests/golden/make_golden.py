@@ -532,11 +532,59 @@ def c2_results():
     return rows
 
 
+# C3 / C4 lattices, shared with tools/scale_bench.py and tests/test_scale.py
+C3_MODEL = ("gpt3-18.4b", 40, 6144, 2048, 51200, "bf16")
+C4_MODEL = ("llama3-70b-shaped", 80, 8192, 8192, 128256, "bf16")
+C4_KNOBS = dict(tp=(1, 2, 4, 8), pp=(2, 4, 8, 16), micro_mult=tuple(range(1, 17)),
+                virtual_stages=(2, 4, 5, 10), act_recompute=(True, False), seq_parallel=(True,),
+                dist_optimizer=(True, False))
+
+
+def scale_results():
+    """Reference results for C3/C4-shaped configs at 64-256 ranks (the reference
+    runs 1-10 s per config here), with the digest of each collated job."""
+    from dltsim.cluster import ClusterSpec, load_device_preset
+    from dltsim.collate import collate
+    from dltsim.estimate import RooflineEstimator, annotate
+    from dltsim.search import SearchSpace, enumerate_space
+    from dltsim.sim import simulate
+    from dltsim.workload import ModelSpec, default_schedule, generate_representatives
+    from paper_2503_20191_b200.rawtrace import from_reference, raw_digest
+    fast = load_device_preset("fast")
+    rows = []
+    picks = []
+    m3 = ModelSpec(*C3_MODEL)
+    for n, every in ((64, 17), (128, 41)):
+        c = ClusterSpec(n // 8, 8, 80 * 2 ** 30, fast)
+        cfgs = enumerate_space(SearchSpace(act_recompute=(True,), global_batch=1024), m3, c)
+        picks += [("C3", m3, c, cfg) for cfg in cfgs[::every]]
+    m4 = ModelSpec(*C4_MODEL)
+    c = ClusterSpec(32, 8, 80 * 2 ** 30, fast)
+    cfgs = enumerate_space(SearchSpace(**C4_KNOBS, global_batch=1024), m4, c)
+    small = [cfg for cfg in cfgs if cfg.micro_mult == 1 and cfg.pp <= 8]
+    picks += [("C4", m4, c, cfg) for cfg in small[::7][:4]]
+    t0 = time.time()
+    for tag, m, c, cfg in picks:
+        tr, ex = generate_representatives(m, cfg, c, default_schedule(cfg), dispatch_overhead_ns=5000)
+        job = collate(tr, ex, c)
+        rep = simulate(annotate(job, RooflineEstimator()))
+        rows.append({"set": tag, "model": list((m.name, m.num_layers, m.hidden_size, m.seq_len,
+                                                m.vocab_size, m.dtype)),
+                     "ranks": c.num_devices, "key": list(cfg.key()), "total_ns": rep.total_ns,
+                     "peak_mem_bytes": rep.peak_mem_bytes, "oom": rep.oom,
+                     "rank_ops": sum(len(job.trace_of(r).events) for r in job.all_ranks()),
+                     "raw_sha256": raw_digest(from_reference(job))})
+        print(f"  {tag} {c.num_devices} {cfg.label()}: {rep.total_ns} ns ({time.time() - t0:.1f}s)",
+              flush=True)
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default=os.environ.get("MAYA_REF", "/root/reference/pkg"))
     ap.add_argument("--c2", action="store_true", help="also compute c2_results.json (~3 min)")
     ap.add_argument("--only", default="")
+    ap.add_argument("--scale", action="store_true", help="also compute scale_results.json (C3/C4)")
     args = ap.parse_args()
     setup(args.ref)
     only = set(args.only.split(",")) if args.only else None
@@ -551,6 +599,9 @@ def main():
     if not only or "estimators" in only:
         with open(os.path.join(HERE, "estimators.json"), "w") as f:
             json.dump(estimator_cases(), f)
+    if args.scale:
+        with open(os.path.join(HERE, "scale_results.json"), "w") as f:
+            json.dump(scale_results(), f)
     if args.c2:
         rows = c2_results()
         with open(os.path.join(HERE, "c2_results.json"), "w") as f:
