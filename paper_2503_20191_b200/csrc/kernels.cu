@@ -208,6 +208,7 @@ __device__ unsigned long long g_prof[8];
 static constexpr int64_t NEG = INT64_MIN / 4;          // -inf of the max-plus scan
 static constexpr int64_t LIM_T = (int64_t)1 << 60;     // times beyond: exact serial path
 static constexpr uint64_t LIM_D = (uint64_t)1 << 56;   // durations beyond: exact serial path
+static constexpr uint64_t LIM_W = (uint64_t)1 << 52;   // wide-window duration guard
 
 // Per-walker state (one (rank, stream) FIFO), kept in shared memory (or the
 // global spill) between rounds; uniform across the lanes of the warp.
@@ -317,6 +318,100 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
       s.bound = s.seg < c.nsync ? c.cnt[s.seg * c.ns] : c.len;
     }
     const uint32_t end = s.bound < limit ? s.bound : limit;
+    // ---- wide window: 128 ops (4 per lane) when none of them blocks --------
+    // Every op is an affine max-plus map x -> max(x + A, B); a lane composes
+    // its 4 maps, the warp scans the 32 compositions (5 shuffle steps) and each
+    // lane expands its own 4.  Records fire in the expansion; a wait on an
+    // unfired event, a multi-member collective or a guard miss anywhere in the
+    // block sends the block back to the 32-op window below.
+    // the next 2 KB of this FIFO into L1 while this window computes (one line per lane)
+    if (lane < 16 && s.i + 128u + lane * 8u < c.len)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(c.ops + s.i + 128u + lane * 8u));
+    if (end - s.i >= 128u && s.x < LIM_T) {
+      int64_t A4[4], B4[4], rd4[4];
+      uint32_t rec4 = 0;
+      bool blk = false;
+      const ExecOp *base = c.ops + s.i + lane * 4u;
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const ExecOp ek = load_exec(base + k);
+        const uint32_t tg = (uint32_t)(ek.w & 3);
+        const uint64_t py = ek.w >> 2;
+        const int64_t rd = ek.disp + s.cdel;
+        rd4[k] = rd;
+        A4[k] = 0;
+        B4[k] = rd;
+        if (rd >= LIM_T) blk = true;
+        if (tg == TAG_KERN) {
+          if (py >= LIM_W) blk = true;   // 128 x 2^52 + 2^60 stays far below 2^63
+          A4[k] = (int64_t)py;
+          B4[k] = rd + (int64_t)py;
+        } else if (tg == TAG_REC) {
+          rec4 |= 1u << k;
+        } else if (tg == TAG_WAIT) {
+          const int64_t f = py == (EXEC_NONE >> 2) ? -1 : vload(&c.fire[py]);
+          if (f < 0) blk = true;
+          else if (f > rd) B4[k] = f;
+        } else {
+          const RCX rx = c.rc[py];
+          if ((uint32_t)(rx.ent >> 48) != 1u || rx.wire >= (int64_t)LIM_W) blk = true;
+          A4[k] = rx.wire;
+          B4[k] = rd + rx.wire;
+        }
+      }
+      if (!__any_sync(FULL, blk)) {
+        // compose the lane's 4 maps, then an inclusive warp scan
+        int64_t A = A4[0], B = B4[0];
+#pragma unroll
+        for (int k = 1; k < 4; k++) {
+          const int64_t nb = B + A4[k];
+          B = nb > B4[k] ? nb : B4[k];
+          A += A4[k];
+        }
+#pragma unroll
+        for (uint32_t off = 1; off < 32; off <<= 1) {
+          const int64_t A2 = __shfl_up_sync(FULL, A, off);
+          const int64_t B2 = __shfl_up_sync(FULL, B, off);
+          if (lane >= off) {
+            const int64_t nb = B2 + A;
+            B = nb > B ? nb : B;
+            A = A2 + A;
+          }
+        }
+        // exclusive prefix applied to the walker's clock
+        int64_t Ae = __shfl_up_sync(FULL, A, 1), Be = __shfl_up_sync(FULL, B, 1);
+        int64_t x = s.x;
+        if (lane > 0) {
+          const int64_t v = x + Ae;
+          x = v > Be ? v : Be;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int64_t ready = x > rd4[k] ? x : rd4[k];
+          const int64_t v = x + A4[k];
+          const int64_t d = v > B4[k] ? v : B4[k];
+          if (rec4 & (1u << k)) {
+            const uint64_t py = (load_exec(base + k).w) >> 2;
+            vstore(&c.fire[py], d);
+          }
+          if (sh.record) {
+            b.tl_start[c.tl + s.i + lane * 4u + k] = ready;
+            b.tl_end[c.tl + s.i + lane * 4u + k] = d;
+          }
+          x = d;
+        }
+        s.x = __shfl_sync(FULL, x, 31);
+#ifdef MAYA_PROFILE
+        if (lane == 0) { PROF_ADD(6, 1); PROF_ADD(7, 128); PROF_ADD(0, clock64() - t_win); PROF_ADD(4, 1); }
+#endif
+        s.i += 128u;
+        s.flags = 0;
+        adv = true;
+        if (__any_sync(FULL, rec4 != 0)) __threadfence_block();
+        s.wk = WAKE_ROUND;
+        continue;
+      }
+    }
     const uint32_t n = min(32u, end - s.i);
     const bool valid = lane < n;
     ExecOp e{0, 0};
@@ -542,6 +637,9 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
       xin = nx;
       p = q + 1;
     }
+#ifdef MAYA_PROFILE
+    if (lane == 0) PROF_ADD(7, commit);
+#endif
     if (commit > 0) {
       s.x = __shfl_sync(FULL, d, commit - 1);
       s.i += commit;
@@ -717,14 +815,26 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
             wb = rr.walker;
             we = rr.walker + b.reps[rr.rep].n_streams;
           }
-          for (uint32_t w = wb; w < we; w++) {
+          // lane-parallel wake check of up to 32 FIFOs, then walk the ready ones
+          for (uint32_t w0 = wb; w0 < we; w0 += 32) {
+            bool can = false;
+            if (w0 + lane < we) {
+              const uint32_t w = w0 + lane;
+              const uint32_t wk = sh.st[w].wk;
+              can = !(wk == WAKE_ROUND && !fresh);
+              if (can && wk == WAKE_COUNT)
+                can = vload((const uint32_t *)sh.st[w].wa) >= sh.st[w].wt;
+              else if (can && wk == WAKE_FIRE)
+                can = vload((const int64_t *)sh.st[w].wa) >= 0;
+              if (can && sh.ctx) can = sh.st[w].i < sh.ctx[w].len;
+            }
+            unsigned ready = __ballot_sync(FULL, can);
+            while (ready) {
+            const uint32_t w = w0 + (uint32_t)(__ffs(ready) - 1);
+            ready &= ready - 1;
             WSt s = sh.st[w];
-            if (s.wk == WAKE_ROUND && !fresh) continue;
-            if (s.wk == WAKE_COUNT && vload((const uint32_t *)s.wa) < s.wt) continue;
-            if (s.wk == WAKE_FIRE && vload((const int64_t *)s.wa) < 0) continue;
             WCtx c;
             if (sh.ctx) {
-              if (s.i >= sh.ctx[w].len) continue;
               c = sh.ctx[w];
             } else {
               load_ctx(b, J, w, record, c, sh.fire, sh.rcx);
@@ -736,6 +846,8 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
                               );
             __syncwarp();
             if (lane == 0) sh.st[w] = s;
+            __syncwarp();
+            }
           }
         }
         if (err) {
@@ -743,7 +855,7 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
           break;
         }
 #ifdef MAYA_PROFILE
-        if (lane == 0) { PROF_ADD(3, clock64() - t_sweep); PROF_ADD(7, 1); }
+        if (lane == 0) { PROF_ADD(3, clock64() - t_sweep); }
 #endif
         fresh = false;
         if (pass) {
@@ -787,7 +899,7 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
         if (wake && lane == 0) atomicAdd(&s_active, 1);
         wake = __shfl_sync(FULL, wake, 0);
 #ifdef MAYA_PROFILE
-        if (lane == 0) { PROF_ADD(2, clock64() - t_idle); PROF_ADD(6, wake); }
+        if (lane == 0) { PROF_ADD(2, clock64() - t_idle); }
 #endif
         if (!wake) break;
       }

@@ -11,13 +11,13 @@ cfgs = W.enumerate_space(W.SearchSpace(global_batch=512), model, cluster)[:512]
 L = E.lib()
 L.maya_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 eng = E.Engine(0)
-names = ["walk_cyc", "slow_cyc", "idle_cyc", "sweep_cyc", "windows", "slow_calls", "wakes", "passes"]
+names = ["walk_cyc", "slow_cyc", "idle_cyc", "sweep_cyc", "windows", "slow_calls", "wide_windows", "ops_committed"]
 for label in (sys.argv[1:] if len(sys.argv) > 1 else ([] if os.environ.get("C5") else ["tp2.pp2.mm8.vs4.rsz", "tp1.pp8.mm8.vs1.rsz"])):
     sub = [c for c in cfgs if c.label() == label]
     eng.stage_generated(model, sub, cluster, dispatch_overhead_ns=5000)
     eng.upload()
     eng.run(); eng.results()
-    buf = (C.c_ulonglong * 8)()
+    buf = (C.c_ulonglong * 16)()
     L.maya_prof_read(buf, 1)
     eng.run(); r = eng.results()
     L.maya_prof_read(buf, 1)
@@ -30,7 +30,7 @@ if os.environ.get("C5"):
         jobs = [c5_job(R, n, cfg=c) for c in range(B)]
         eng.load(jobs, threads=16)
         eng.run(); eng.results()
-        buf = (C.c_ulonglong * 8)()
+        buf = (C.c_ulonglong * 16)()
         L.maya_prof_read(buf, 1)
         eng.run(); r = eng.results()
         L.maya_prof_read(buf, 1)
