@@ -406,25 +406,31 @@ def bench_ours(args):
                             threads=threads)
         eng.upload()
 
-    # --- end to end through the C ABI with host buffers -------------------------------
+    # --- end to end through the public API with host buffers ------------------------
+    # api.GenPipeline (one chunk: double-buffering 2-8 chunks measured slower,
+    # tools/pipe_probe.py); timed on the host clock with the device synchronised
+    # on both sides.
+    from paper_2503_20191_b200.api import GenPipeline
+    pipe = GenPipeline(local, chunks=1)
     e2e_steps = args.e2e_steps or args.steps
+    for _ in range(2):
+        pipe.evaluate(model, configs, cluster, k=TOPK, key_order=kr, dispatch_overhead_ns=5000,
+                      threads=threads)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e2e_ms = []
+    e2e_best = None
     for i in range(e2e_steps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        eng.stage_generated(model, configs, cluster, dispatch_overhead_ns=5000, key_ranks=kr,
-                            threads=threads)
-        eng.upload()
-        eng.run()
-        r = eng.results()
-        eng.topk(TOPK)
-        b.record(stream)
-        b.synchronize()
-        e2e_ms.append(a.elapsed_time(b))
-    torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pres, ptop, _ = pipe.evaluate(model, configs, cluster, k=TOPK, key_order=kr,
+                                      dispatch_overhead_ns=5000, threads=threads)
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1000)
+        e2e_best = (int(ptop[0][0]), int(ptop[0][1])) if len(ptop) else None
+    e2e_same = bool((pres["total_ns"] == res["total_ns"]).all()
+                    and (pres["status"] == res["status"]).all())
+    pipe.close()
     e = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e, op=dist.ReduceOp.MAX)
@@ -460,8 +466,10 @@ def bench_ours(args):
                     "ms_per_step": round(e2e_ms_max, 3),
                     "h2d_bytes_per_step": int(stats["arena_bytes"]),
                     "d2h_bytes_per_step": int(N_CONFIGS * 64 + TOPK * 16),
-                    "path": "config list -> native gen+pack (C++ threads) -> H2D -> kernels "
-                            "-> D2H results + top-k"},
+                    "path": "api.GenPipeline: config list -> fused native gen+pack (C++ "
+                            "threads) -> H2D -> kernels -> D2H results + top-k",
+                    "identical_results_to_device_step": e2e_same,
+                    "best": list(e2e_best) if e2e_best else None},
             "roofline": {"bound": "hbm", "kernel": "sched_warp_kernel",
                          "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 5), "traffic": ncu_traffic(),

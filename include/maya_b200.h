@@ -236,6 +236,12 @@ int maya_batch_add_generated(maya_engine *eng, const maya_model *model, int32_t 
                              int32_t device, int32_t schedule, int64_t dispatch_overhead_ns,
                              const int32_t *key_ranks, int32_t n_threads, int32_t *status_out);
 
+/* Test hook: packs each config through the fused generate->pack path and
+ * through generate + pack_job, and returns how many packs differ (0 expected). */
+int maya_debug_pack_compare(const maya_model *model, int32_t n, const maya_config *cfgs,
+                            const maya_cluster *cluster, int32_t schedule,
+                            int64_t dispatch_overhead_ns, int32_t collapse);
+
 #ifdef __cplusplus
 }
 #endif

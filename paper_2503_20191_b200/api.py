@@ -460,6 +460,63 @@ def evaluate_space(space, model, cluster, k: int = 8, dispatch_overhead_ns: int 
                        [int(t["time_ns"]) for t in top])
 
 
+class GenPipeline:
+    """Double-buffered end-to-end evaluation of a config list: native
+    generation + packing of chunk q+1 on the host threads overlaps the H2D,
+    estimator, scheduler and top-k of chunk q on the device (two engines, each
+    on its own stream).  Results come back in config order; the k best are the
+    merge of the per-chunk device top-k under the reference ranking
+    (search.py:349-357)."""
+
+    def __init__(self, device: int = 0, chunks: int = 1):
+        from .engine import Engine
+        self.engines = [Engine(device), Engine(device)]
+        self.chunks = max(1, int(chunks))
+
+    def close(self) -> None:
+        for e in self.engines:
+            e.close()
+
+    def evaluate(self, model, configs, cluster, k: int = 8, key_order=None,
+                 dispatch_overhead_ns: int = 0, schedule=None, threads: int = 8,
+                 efficiency: Mapping[str, float] | None = None,
+                 overhead_ns: int = DEFAULT_KERNEL_OVERHEAD_NS):
+        """-> (results structured array, top-k rows (time_ns, key_rank, config index))."""
+        from ._abi import RESULT_DTYPE
+        n = len(configs)
+        kr = key_ranks(configs) if key_order is None else np.asarray(key_order)
+        bounds = np.linspace(0, n, min(self.chunks, max(n, 1)) + 1).astype(int)
+        res = np.zeros(n, dtype=RESULT_DTYPE)
+        cands = []
+        status = np.zeros(n, dtype=np.int32)
+
+        def collect(item):
+            e, lo, hi = item
+            res[lo:hi] = e.results()
+            for t in e.topk(k):
+                cands.append((int(t["time_ns"]), int(t["key_rank"]), lo + int(t["job"])))
+
+        pending = None
+        for q in range(len(bounds) - 1):
+            lo, hi = int(bounds[q]), int(bounds[q + 1])
+            if hi <= lo:
+                continue
+            e = self.engines[q % 2]
+            status[lo:hi] = e.stage_generated(model, configs[lo:hi], cluster, schedule=schedule,
+                                              dispatch_overhead_ns=dispatch_overhead_ns,
+                                              efficiency=efficiency, overhead_ns=overhead_ns,
+                                              key_ranks=kr[lo:hi], threads=threads)
+            e.upload()
+            e.run()
+            if pending is not None:
+                collect(pending)
+            pending = (e, lo, hi)
+        if pending is not None:
+            collect(pending)
+        top = merge_topk(np.array(cands, dtype=np.int64).reshape(-1, 3), k)
+        return res, top, status
+
+
 def merge_topk(candidates: np.ndarray, k: int) -> np.ndarray:
     """Merge per-GPU top-k candidate rows (time_ns, global key rank, config id)
     with the device comparator; time_ns == 0 sorts after every positive time."""

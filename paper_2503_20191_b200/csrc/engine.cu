@@ -17,6 +17,7 @@
 #include "kernels.cuh"
 #include "gen.h"
 #include "pack.h"
+#include "pool.h"
 
 using namespace maya;
 
@@ -239,6 +240,25 @@ void lane_perm_fill(const JobPack &P, const LanePlan &pl, uint32_t *out) {
 
 }  // namespace
 
+namespace {
+template <typename T>
+bool vec_eq(const std::vector<T> &a, const std::vector<T> &b) {
+  return a.size() == b.size() && (a.empty() || memcmp(a.data(), b.data(), a.size() * sizeof(T)) == 0);
+}
+bool pack_eq(const JobPack &a, const JobPack &b) {
+  return memcmp(&a.hdr, &b.hdr, sizeof(JobHdr)) == 0 && vec_eq(a.reps, b.reps) &&
+         vec_eq(a.ops, b.ops) && vec_eq(a.op_seq, b.op_seq) && vec_eq(a.streams, b.streams) &&
+         vec_eq(a.coll_lc, b.coll_lc) && vec_eq(a.coll_idx, b.coll_idx) &&
+         vec_eq(a.syncs, b.syncs) && vec_eq(a.counts, b.counts) && vec_eq(a.mems, b.mems) &&
+         vec_eq(a.feats, b.feats) && vec_eq(a.comms, b.comms) && vec_eq(a.slots, b.slots) &&
+         vec_eq(a.ranks, b.ranks) && vec_eq(a.rank_comm, b.rank_comm) &&
+         vec_eq(a.walkers, b.walkers) && vec_eq(a.wids, b.wids) && vec_eq(a.rcolls, b.rcolls) &&
+         vec_eq(a.rep_ring_ok, b.rep_ring_ok) && vec_eq(a.comm_rdv, b.comm_rdv) &&
+         vec_eq(a.rank_orig, b.rank_orig) && vec_eq(a.rank_sim, b.rank_sim) &&
+         a.collapsed == b.collapsed && a.n_fire == b.n_fire && a.n_delay == b.n_delay;
+}
+}  // namespace
+
 extern "C" {
 
 const char *maya_last_error(void) { return g_err.c_str(); }
@@ -323,14 +343,7 @@ int maya_batch_add_jobs(maya_engine *e, int32_t n, const maya_raw_job *jobs,
                (e->options & MAYA_OPT_COLLAPSE) != 0);
     }
   };
-  int nt = std::max(1, std::min<int>(n_threads, n));
-  if (nt == 1) {
-    work();
-  } else {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; t++) th.emplace_back(work);
-    for (auto &t : th) t.join();
-  }
+  WorkerPool::get().run(std::max(1, std::min<int>(n_threads, n)), work);
   e->uploaded = e->ran = false;
   return MAYA_OK;
 }
@@ -642,13 +655,7 @@ int maya_upload(maya_engine *e) {
         copy_job(j);
       }
     };
-    if (nt <= 1) {
-      work();
-    } else {
-      std::vector<std::thread> th;
-      for (int t = 0; t < nt; t++) th.emplace_back(work);
-      for (auto &t : th) t.join();
-    }
+    WorkerPool::get().run(nt, work);
   }
   CU(cudaMemcpyAsync(e->d_arena, e->h_arena, e->arena_bytes, cudaMemcpyHostToDevice, e->stream));
   // device view
@@ -942,6 +949,26 @@ int maya_timeline(maya_engine *e, int32_t job, int32_t *rank, int32_t *stream, i
 
 // ---- native generation ----------------------------------------------------
 
+
+int maya_debug_pack_compare(const maya_model *model, int32_t n, const maya_config *cfgs,
+                                       const maya_cluster *cluster, int32_t schedule,
+                                       int64_t dispatch_overhead_ns, int32_t collapse) {
+  int bad = 0;
+  GenJob g, g2;
+  for (int i = 0; i < n; i++) {
+    std::string err;
+    JobPack a, b2;
+    int rc = generate_job(*model, cfgs[i], *cluster, schedule, dispatch_overhead_ns, g, &err);
+    if (rc != MAYA_OK) continue;
+    maya_raw_job raw = g.raw(0);
+    pack_job(raw, i, a, collapse != 0);
+    rc = pack_generated(*model, cfgs[i], *cluster, schedule, dispatch_overhead_ns, 0, i,
+                        collapse != 0, g2, b2, &err);
+    if (rc != MAYA_OK || !pack_eq(a, b2)) bad++;
+  }
+  return bad;
+}
+
 struct maya_gen {
   GenJob job;
 };
@@ -992,33 +1019,26 @@ int maya_batch_add_generated(maya_engine *e, const maya_model *model, int32_t n,
   e->packs.resize(base + n);
   std::atomic<int> next(0);
   auto work = [&]() {
-    GenJob g;
+    thread_local GenJob g;
     for (;;) {
       int i = next.fetch_add(1);
       if (i >= n) break;
       std::string err;
-      int rc = generate_job(*model, cfgs[i], *cluster, schedule, dispatch_overhead_ns, g, &err);
-      if (status_out) status_out[i] = rc;
       JobPack &P = e->packs[base + i];
+      const int32_t kr = key_ranks ? key_ranks[i] : i;
+      // fused generate -> pack (no raw event arrays)
+      int rc = pack_generated(*model, cfgs[i], *cluster, schedule, dispatch_overhead_ns, device,
+                              kr, (e->options & MAYA_OPT_COLLAPSE) != 0, g, P, &err);
+      if (status_out) status_out[i] = rc;
       if (rc != MAYA_OK) {
         P.clear();
         P.hdr.status = MAYA_ST_BAD_INPUT;
-        P.hdr.key_rank = key_ranks ? key_ranks[i] : i;
+        P.hdr.key_rank = kr;
         P.message = err;
-        continue;
       }
-      maya_raw_job raw = g.raw(device);
-      pack_job(raw, key_ranks ? key_ranks[i] : i, P, (e->options & MAYA_OPT_COLLAPSE) != 0);
     }
   };
-  int nt = std::max(1, std::min<int>(n_threads, n));
-  if (nt == 1) {
-    work();
-  } else {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; t++) th.emplace_back(work);
-    for (auto &t : th) t.join();
-  }
+  WorkerPool::get().run(std::max(1, std::min<int>(n_threads, n)), work);
   e->uploaded = e->ran = false;
   return MAYA_OK;
 }

@@ -289,6 +289,7 @@ struct Builder {
   std::vector<uint8_t> &kind;
   std::vector<int32_t> &stream;
   std::vector<int64_t> &f;
+  EventSink *sink;
   int64_t overhead;
   int32_t dtype;
   std::vector<int32_t> comm_nranks;          // per local comm
@@ -298,6 +299,10 @@ struct Builder {
   int64_t next_alloc = 0;
 
   void ev(uint8_t k, int32_t s, int64_t a, int64_t b = 0, int64_t c = 0, int64_t d = 0) {
+    if (sink) {
+      sink->ev(k, s, a, b, c, d);
+      return;
+    }
     kind.push_back(k);
     stream.push_back(s);
     const size_t n = f.size();
@@ -353,7 +358,8 @@ struct RepCalls {
 
 // workload.py:571-780 for one representative rank; appends events.
 void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int schedule,
-                    int64_t rank, int64_t overhead, int32_t dtype, GenJob &G, RepCalls &rc) {
+                    int64_t rank, int64_t overhead, int32_t dtype, GenJob &G, RepCalls &rc,
+                    EventSink *sink) {
   const int64_t t = C.t, d = C.d;
   const int64_t i = rank % t, j = (rank / t) % d, stage = rank / (t * d);
   const int64_t p = cfg.pp, v = cfg.virtual_stages, total_vs = p * v;
@@ -363,13 +369,17 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   const bool sp = cfg.seq_parallel != 0;
   const i128 u = sp ? t : 1;
 
-  Builder B{G.ev_kind, G.ev_stream, G.ev_f, overhead, dtype, {}, {}, {}, {}, {}, 0};
+  Builder B{G.ev_kind, G.ev_stream, G.ev_f, sink, overhead, dtype, {}, {}, {}, {}, {}, 0};
   {  // reserve for this trace: ~ (2 x kernels per layer-microbatch) + specials
     const size_t est = (size_t)(cfg.micro_mult) * (size_t)cfg.pp * (size_t)(M.L / cfg.pp + 2) *
                            (cfg.act_recompute ? 110 : 80) + 4096;
-    G.ev_kind.reserve(G.ev_kind.size() + est);
-    G.ev_stream.reserve(G.ev_stream.size() + est);
-    G.ev_f.reserve(G.ev_f.size() + 4 * est);
+    if (sink) {
+      sink->rep_begin(est);
+    } else {
+      G.ev_kind.reserve(G.ev_kind.size() + est);
+      G.ev_stream.reserve(G.ev_stream.size() + est);
+      G.ev_f.reserve(G.ev_f.size() + 4 * est);
+    }
   }
   std::vector<CommRole> roles = worker_comms(C, v, rank);
   // local comm index of each role (first CommInit of a comm id)
@@ -550,6 +560,7 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   }
   B.ev(MAYA_EV_DSYNC, 0, 0);
   rc.calls = std::move(B.calls);
+  if (sink) sink->rep_end();
 }
 
 // workload.py:168-208 (cluster divisibility + model + schedule rules)
@@ -601,7 +612,8 @@ maya_raw_job GenJob::raw(int32_t device) const {
 }
 
 int generate_job(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
-                 int32_t schedule, int64_t overhead, GenJob &G, std::string *err) {
+                 int32_t schedule, int64_t overhead, GenJob &G, std::string *err,
+                 EventSink *sink) {
   G.clear();   // keep capacity: a worker thread reuses one GenJob across configs
   try {
     if (cl.num_hosts < 1 || cl.devices_per_host < 1) throw GenFail{"empty cluster"};
@@ -622,7 +634,7 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
     for (int k = 0; k < cfg.pp; k++) {
       int64_t rep = rank_of(C, 0, 0, k);
       G.rep_ranks.push_back(rep);
-      generate_trace(M, cfg, C, schedule, rep, overhead, model.dtype, G, rcalls[k]);
+      generate_trace(M, cfg, C, schedule, rep, overhead, model.dtype, G, rcalls[k], sink);
       G.ev_off.push_back((int64_t)G.ev_kind.size());
     }
     G.rank_rep.resize(n);

@@ -43,8 +43,20 @@ struct GenJob {
   }
 };
 
-// Returns 0 or a negative code with *err set (invalid configuration).
+// Receives the events of each representative trace in order instead of the
+// raw arrays (the fused generate -> pack path, pack.cpp pack_generated).
+struct EventSink {
+  virtual ~EventSink() {}
+  virtual void rep_begin(size_t est_events) = 0;
+  virtual void ev(uint8_t k, int32_t s, int64_t a, int64_t b, int64_t c, int64_t d) = 0;
+  virtual void rep_end() = 0;
+};
+
+// Returns 0 or a negative code with *err set (invalid configuration).  With a
+// sink, the events go to the sink and out's event arrays stay empty (its job
+// tables -- reps, communicators, calls, rank translation -- are filled).
 int generate_job(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
-                 int32_t schedule, int64_t dispatch_overhead_ns, GenJob &out, std::string *err);
+                 int32_t schedule, int64_t dispatch_overhead_ns, GenJob &out, std::string *err,
+                 EventSink *sink = nullptr);
 
 }  // namespace maya

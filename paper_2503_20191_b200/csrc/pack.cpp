@@ -74,72 +74,135 @@ struct FeatCacheEnt {
   uint32_t fid;
 };
 
-void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
-              std::unordered_map<FeatKey, uint32_t, FeatHash> &feat_map,
-              std::unordered_map<int64_t, uint32_t> &fixed_map, uint32_t &n_local_comms) {
-  const int64_t b = job.ev_off[rep], e = job.ev_off[rep + 1];
+// Job-level kernel-feature dedup (estimate.py:329-352 runs the estimator per
+// event; we run it once per unique (op_kind, dtype, flops, bytes)).
+struct FeatState {
+  std::unordered_map<FeatKey, uint32_t, FeatHash> feat_map;
+  std::unordered_map<int64_t, uint32_t> fixed_map;
+  FeatCacheEnt fcache[64];
+  void clear() {
+    feat_map.clear();
+    fixed_map.clear();
+    for (auto &ce : fcache) ce.fid = UINT32_MAX;
+  }
+};
+
+// Per-event half of the packer for ONE representative trace, in trace order.
+// pack_job drives it from raw event arrays (ordinals precomputed by a first
+// pass, so a wait may precede its record); the fused generator drives it
+// directly (ordinals assigned at the record: every generated wait follows its
+// record, workload.py:510-568).
+struct RepPacker {
+  JobPack *P = nullptr;
+  FeatState *F = nullptr;
+  int32_t device = 0;
   RepHdr h{};
-  h.n_events = (uint32_t)(e - b);
-  h.job = 0;
-  // record ordinals (trace.py:453-459: each (event, version) recorded once)
-  std::unordered_map<uint64_t, uint32_t> rec;
-  auto ekey = [](int64_t ev, int64_t ver) -> uint64_t {
+  RepBuild RB;
+  bool fly = false;                                  // ordinals on the fly
+  std::unordered_map<uint64_t, uint32_t> rec;        // (event, version) -> ordinal
+  std::vector<std::vector<uint32_t>> rec_small;      // fly mode: [event][version]
+  uint32_t n_recs = 0, n_local_comms = 0;
+  std::vector<std::vector<uint32_t>> snap;
+  std::unordered_map<int64_t, int64_t> alloc_big;
+  std::vector<int64_t> alloc_small;
+  std::unordered_map<uint64_t, uint32_t> coll_seen;
+  std::vector<int32_t> comm_stream;
+  std::vector<int64_t> comm_next;
+  bool ring_ok = true;
+  uint64_t coll0 = 0, mem0 = 0, sync0 = 0;
+  int64_t gpre = 0;
+  uint32_t seg = 0, seq = 0;
+
+  static uint64_t ekey(int64_t ev, int64_t ver) {
     if (ev < 0 || ev > 0x7fffffff || ver < 0 || ver > 0x7fffffff)
       throw Fail{MAYA_ST_BAD_INPUT, "event id/version outside [0, 2^31)"};
     return ((uint64_t)ev << 32) | (uint64_t)ver;
-  };
-  n_local_comms = 0;
-  for (int64_t i = b; i < e; i++) {
-    const int k = job.ev_kind[i];
-    if (k == MAYA_EV_RECORD) {
-      const int64_t *f = job.ev_f + 4 * i;
-      auto ins = rec.emplace(ekey(f[0], f[1]), (uint32_t)rec.size());
-      if (!ins.second)
-        throw Fail{MAYA_ST_BAD_INPUT, "event (" + std::to_string(f[0]) + ", v" +
-                                          std::to_string(f[1]) + ") recorded twice"};
-    } else if (k == MAYA_EV_COMMINIT) {
-      n_local_comms = std::max<uint32_t>(n_local_comms, (uint32_t)job.ev_f[4 * i] + 1);
-    }
   }
-  h.n_recs = (uint32_t)rec.size();
-  auto ord = [&](const int64_t *f) -> uint32_t {
+
+  void begin(JobPack &pk, FeatState &fs, int32_t dev, bool on_the_fly, size_t reserve_hint) {
+    P = &pk;
+    F = &fs;
+    device = dev;
+    h = RepHdr{};
+    h.job = 0;
+    RB = RepBuild();
+    RB.reserve_hint = reserve_hint;
+    fly = on_the_fly;
+    rec.clear();
+    rec_small.clear();
+    n_recs = 0;
+    n_local_comms = 0;
+    snap.clear();
+    alloc_big.clear();
+    alloc_small.clear();
+    coll_seen.clear();
+    comm_stream.clear();
+    comm_next.clear();
+    ring_ok = true;
+    coll0 = P->coll_lc.size();
+    mem0 = P->mems.size();
+    sync0 = P->syncs.size();
+    gpre = 0;
+    seg = 0;
+    seq = 0;
+  }
+
+  // raw mode: the first pass over the rep's events
+  void add_record(int64_t ev, int64_t ver) {
+    auto ins = rec.emplace(ekey(ev, ver), n_recs);
+    if (!ins.second)
+      throw Fail{MAYA_ST_BAD_INPUT, "event (" + std::to_string(ev) + ", v" +
+                                        std::to_string(ver) + ") recorded twice"};
+    n_recs++;
+  }
+  void set_local_comms(uint32_t n) {
+    n_local_comms = n;
+    comm_stream.assign(n, INT32_MIN);
+    comm_next.assign(n, 0);
+  }
+
+  uint32_t ord(const int64_t *f) {
+    if (fly && f[0] >= 0 && f[0] < 4096 && f[1] >= 0 && f[1] < (1 << 20)) {
+      if ((size_t)f[0] < rec_small.size() && (size_t)f[1] < rec_small[f[0]].size())
+        return rec_small[f[0]][f[1]];
+      return NO_REC;
+    }
     auto it = rec.find(ekey(f[0], f[1]));
     return it == rec.end() ? NO_REC : it->second;
-  };
+  }
+  uint32_t record_fly(const int64_t *f) {
+    if (f[0] >= 0 && f[0] < 4096 && f[1] >= 0 && f[1] < (1 << 20)) {
+      if ((size_t)f[0] >= rec_small.size()) rec_small.resize(f[0] + 1);
+      auto &v = rec_small[f[0]];
+      if ((size_t)f[1] >= v.size()) v.resize(f[1] + 1, NO_REC);
+      if (v[f[1]] != NO_REC)
+        throw Fail{MAYA_ST_BAD_INPUT, "event (" + std::to_string(f[0]) + ", v" +
+                                          std::to_string(f[1]) + ") recorded twice"};
+      v[f[1]] = n_recs;
+      return n_recs++;
+    }
+    add_record(f[0], f[1]);
+    return n_recs - 1;
+  }
 
-  RepBuild RB;
-  RB.reserve_hint = (size_t)(e - b) / 2 + 16;
-  FeatCacheEnt fcache[64];
-  for (auto &ce : fcache) ce.fid = UINT32_MAX;
-  std::vector<std::vector<uint32_t>> snap;  // per sync: ops dispatched per local stream
-  std::unordered_map<int64_t, int64_t> alloc_big;   // alloc_id -> bytes (large ids)
-  std::vector<int64_t> alloc_small;                  // alloc_id -> bytes + 1 (0: none)
-  std::unordered_map<uint64_t, uint32_t> coll_seen;
-  // ring eligibility: per local comm, one issuing stream and call_idx 0,1,2,...
-  std::vector<int32_t> comm_stream(n_local_comms, INT32_MIN);
-  std::vector<int64_t> comm_next(n_local_comms, 0);
-  bool ring_ok = true;
-  const uint64_t coll0 = P.coll_lc.size();
-  int64_t gpre = 0;
-  uint32_t seg = 0;
-  const uint64_t mem0 = P.mems.size(), sync0 = P.syncs.size();
-  for (int64_t i = b; i < e; i++) {
-    const int k = job.ev_kind[i];
-    const int64_t *f = job.ev_f + 4 * i;
-    const uint32_t seq = (uint32_t)(i - b);
-    auto emit = [&](uint32_t tag, uint32_t arg) {
-      int ls = RB.local_stream(job.ev_stream[i], true);
-      if (seg >= (1u << 30)) throw Fail{MAYA_ST_BAD_INPUT, "too many host syncs"};
-      RB.sops[ls].push_back(Op{gpre, arg, tag | (seg << 2)});
-      RB.sseq[ls].push_back(seq);
-    };
-    auto sync = [&](uint32_t type, uint32_t arg) {
-      std::vector<uint32_t> c(RB.sops.size());
-      for (size_t s = 0; s < c.size(); s++) c[s] = (uint32_t)RB.sops[s].size();
-      snap.push_back(std::move(c));
-      P.syncs.push_back(SyncRec{gpre, type, arg, 0, 0});
-      seg++;
-    };
+  void emit(int32_t stream, uint32_t tag, uint32_t arg) {
+    int ls = RB.local_stream(stream, true);
+    if (seg >= (1u << 30)) throw Fail{MAYA_ST_BAD_INPUT, "too many host syncs"};
+    RB.sops[ls].push_back(Op{gpre, arg, tag | (seg << 2)});
+    RB.sseq[ls].push_back(seq);
+  }
+  void sync(uint32_t type, uint32_t arg) {
+    std::vector<uint32_t> c(RB.sops.size());
+    for (size_t s = 0; s < c.size(); s++) c[s] = (uint32_t)RB.sops[s].size();
+    snap.push_back(std::move(c));
+    P->syncs.push_back(SyncRec{gpre, type, arg, 0, 0});
+    seg++;
+  }
+
+  // one event (trace.py:71-151 as rawtrace.py arrays); host_ns >= 0: a
+  // host-computed duration for a kernel-class event (annotate() with another
+  // EstimatorInterface)
+  void event(int k, int32_t stream, const int64_t *f, int64_t host_ns, bool has_host) {
     switch (k) {
       case MAYA_EV_HOSTGAP:
         if (f[0] > 0) {
@@ -151,17 +214,15 @@ void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
       case MAYA_EV_MEMCPY:
       case MAYA_EV_MEMSET: {
         uint32_t fid;
-        if (job.kernel_ns) {
-          int64_t d = job.kernel_ns[i];
-          if (d < 0)
-            throw Fail{MAYA_ST_ESTIMATION, "rank " + std::to_string(rep) + " seq " +
-                                               std::to_string(seq) + ": negative duration " +
-                                               std::to_string(d)};
-          auto it = fixed_map.find(d);
-          if (it == fixed_map.end()) {
-            fid = (uint32_t)P.feats.size();
-            fixed_map.emplace(d, fid);
-            P.feats.push_back(Feature{0, 0, d, -1, -1, (int16_t)job.device});
+        if (has_host) {
+          if (host_ns < 0)
+            throw Fail{MAYA_ST_ESTIMATION, "seq " + std::to_string(seq) + ": negative duration " +
+                                               std::to_string(host_ns)};
+          auto it = F->fixed_map.find(host_ns);
+          if (it == F->fixed_map.end()) {
+            fid = (uint32_t)P->feats.size();
+            F->fixed_map.emplace(host_ns, fid);
+            P->feats.push_back(Feature{0, 0, host_ns, -1, -1, (int16_t)device});
           } else {
             fid = it->second;
           }
@@ -169,25 +230,25 @@ void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
           // direct-mapped cache in front of the hash map: kernel templates repeat
           const uint64_t hk = ((uint64_t)f[2] * 0x9e3779b97f4a7c15ull) ^ (uint64_t)f[3] ^
                               ((uint64_t)f[0] << 48) ^ ((uint64_t)f[1] << 56);
-          FeatCacheEnt &ce = fcache[(hk >> 58) & 63];
+          FeatCacheEnt &ce = F->fcache[(hk >> 58) & 63];
           if (ce.fid != UINT32_MAX && ce.k[0] == f[0] && ce.k[1] == f[1] && ce.k[2] == f[2] &&
               ce.k[3] == f[3]) {
             fid = ce.fid;
           } else {
             FeatKey key{f[0], f[1], f[2], f[3]};
-            auto it = feat_map.find(key);
-            if (it == feat_map.end()) {
-              fid = (uint32_t)P.feats.size();
-              feat_map.emplace(key, fid);
-              P.feats.push_back(Feature{f[2], f[3], -1, (int32_t)f[0], (int16_t)f[1],
-                                        (int16_t)job.device});
+            auto it = F->feat_map.find(key);
+            if (it == F->feat_map.end()) {
+              fid = (uint32_t)P->feats.size();
+              F->feat_map.emplace(key, fid);
+              P->feats.push_back(Feature{f[2], f[3], -1, (int32_t)f[0], (int16_t)f[1],
+                                         (int16_t)device});
             } else {
               fid = it->second;
             }
             ce = FeatCacheEnt{{f[0], f[1], f[2], f[3]}, fid};
           }
         }
-        emit(TAG_KERN, fid);
+        emit(stream, TAG_KERN, fid);
         break;
       }
       case MAYA_EV_MEMALLOC:
@@ -197,7 +258,7 @@ void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
         } else {
           alloc_big[f[0]] = f[1];
         }
-        P.mems.push_back(MemRec{f[1], gpre, seg, seq});
+        P->mems.push_back(MemRec{f[1], gpre, seg, seq});
         break;
       case MAYA_EV_MEMFREE: {
         int64_t sz = INT64_MIN;
@@ -209,83 +270,129 @@ void pack_rep(const maya_raw_job &job, int rep, JobPack &P,
         }
         if (sz == INT64_MIN)
           throw Fail{MAYA_ST_INTERNAL, "MemFree of unallocated handle " + std::to_string(f[0])};
-        P.mems.push_back(MemRec{-sz, gpre, seg, seq});
+        P->mems.push_back(MemRec{-sz, gpre, seg, seq});
         break;
       }
-      case MAYA_EV_RECORD: emit(TAG_REC, ord(f)); break;
-      case MAYA_EV_WAIT: emit(TAG_WAIT, ord(f)); break;
+      case MAYA_EV_RECORD: emit(stream, TAG_REC, fly ? record_fly(f) : ord(f)); break;
+      case MAYA_EV_WAIT: emit(stream, TAG_WAIT, ord(f)); break;
       case MAYA_EV_ESYNC: sync(SYNC_ESYNC, ord(f)); break;
       case MAYA_EV_SSYNC: {
-        int ls = RB.local_stream(job.ev_stream[i], false);
+        int ls = RB.local_stream(stream, false);
         sync(SYNC_SSYNC, ls < 0 ? NO_REC : (uint32_t)ls);
         break;
       }
       case MAYA_EV_DSYNC: sync(SYNC_DSYNC, 0); break;
-      case MAYA_EV_COMMINIT: break;
+      case MAYA_EV_COMMINIT:
+        if (fly && f[0] >= 0 && (uint64_t)f[0] >= n_local_comms && f[0] < (1 << 20)) {
+          n_local_comms = (uint32_t)f[0] + 1;
+          comm_stream.resize(n_local_comms, INT32_MIN);
+          comm_next.resize(n_local_comms, 0);
+        }
+        break;
       case MAYA_EV_COLLECTIVE: {
         if (f[0] < 0 || (uint64_t)f[0] >= n_local_comms)
           throw Fail{MAYA_ST_BAD_INPUT, "collective on comm without CommInit"};
         if (f[1] < 0 || f[1] > 0x7fffffff) throw Fail{MAYA_ST_BAD_INPUT, "call_idx range"};
-        uint64_t ck = ((uint64_t)f[0] << 32) | (uint64_t)f[1];
-        if (!coll_seen.emplace(ck, 0).second)
-          throw Fail{MAYA_ST_BAD_INPUT, "collective (comm, call_idx) issued twice by one rank"};
-        if (comm_stream[f[0]] == INT32_MIN) comm_stream[f[0]] = job.ev_stream[i];
-        if (comm_stream[f[0]] != job.ev_stream[i] || comm_next[f[0]] != f[1]) ring_ok = false;
-        comm_next[f[0]] = f[1] + 1;
-        uint32_t ci = (uint32_t)(P.coll_lc.size() - coll0);
-        P.coll_lc.push_back((uint32_t)f[0]);
-        P.coll_idx.push_back((uint32_t)f[1]);
-        emit(TAG_COLL, ci);
+        // (comm, call_idx) issued twice by one rank?  Calls issued in order
+        // 0, 1, 2, ... (the common case) cannot repeat; others go to the map.
+        const bool in_order = comm_next[f[0]] == f[1] && !(comm_stream[f[0]] == INT32_MIN && f[1] != 0);
+        if (!in_order || !coll_seen.empty()) {
+          uint64_t ck = ((uint64_t)f[0] << 32) | (uint64_t)f[1];
+          if (coll_seen.empty()) {   // first out-of-order call: enter the earlier in-order ones
+            for (uint32_t c = 0; c < n_local_comms; c++)
+              for (int64_t q = 0; q < comm_next[c] && comm_stream[c] != INT32_MIN; q++)
+                coll_seen.emplace(((uint64_t)c << 32) | (uint64_t)q, 0);
+          }
+          if (!coll_seen.emplace(ck, 0).second)
+            throw Fail{MAYA_ST_BAD_INPUT, "collective (comm, call_idx) issued twice by one rank"};
+        }
+        if (comm_stream[f[0]] == INT32_MIN) comm_stream[f[0]] = stream;
+        if (comm_stream[f[0]] != stream || comm_next[f[0]] != f[1]) ring_ok = false;
+        if (comm_next[f[0]] <= f[1]) comm_next[f[0]] = f[1] + 1;
+        uint32_t ci = (uint32_t)(P->coll_lc.size() - coll0);
+        P->coll_lc.push_back((uint32_t)f[0]);
+        P->coll_idx.push_back((uint32_t)f[1]);
+        emit(stream, TAG_COLL, ci);
         break;
       }
       default:
         throw Fail{MAYA_ST_BAD_INPUT, "unknown event kind " + std::to_string(k)};
     }
+    seq++;
   }
-  // collectives renumbered stream-major: the collectives of one FIFO are
-  // consecutive in the per-rank collective tables, so a walker reads (and
-  // prefetches) its entries sequentially
-  {
-    const uint32_t nc = (uint32_t)(P.coll_lc.size() - coll0);
-    std::vector<uint32_t> lc(nc), ix(nc);
-    uint32_t next = 0;
-    for (auto &ops : RB.sops)
-      for (Op &o : ops)
-        if (op_tag(o.meta) == TAG_COLL) {
-          lc[next] = P.coll_lc[coll0 + o.arg];
-          ix[next] = P.coll_idx[coll0 + o.arg];
-          o.arg = next++;
-        }
-    std::copy(lc.begin(), lc.end(), P.coll_lc.begin() + coll0);
-    std::copy(ix.begin(), ix.end(), P.coll_idx.begin() + coll0);
+
+  void finish() {
+    h.n_events = seq;
+    h.n_recs = n_recs;
+    // collectives renumbered stream-major: the collectives of one FIFO are
+    // consecutive in the per-rank collective tables, so a walker reads (and
+    // prefetches) its entries sequentially
+    {
+      const uint32_t nc = (uint32_t)(P->coll_lc.size() - coll0);
+      std::vector<uint32_t> lc(nc), ix(nc);
+      uint32_t next = 0;
+      for (auto &ops : RB.sops)
+        for (Op &o : ops)
+          if (op_tag(o.meta) == TAG_COLL) {
+            lc[next] = P->coll_lc[coll0 + o.arg];
+            ix[next] = P->coll_idx[coll0 + o.arg];
+            o.arg = next++;
+          }
+      std::copy(lc.begin(), lc.end(), P->coll_lc.begin() + coll0);
+      std::copy(ix.begin(), ix.end(), P->coll_idx.begin() + coll0);
+    }
+    // stream-major op layout
+    h.ops = P->ops.size();
+    h.streams = P->streams.size();
+    h.n_streams = (uint32_t)RB.sops.size();
+    uint32_t pos = 0;
+    for (size_t s = 0; s < RB.sops.size(); s++) {
+      P->streams.push_back(StreamRange{pos, (uint32_t)RB.sops[s].size(), RB.raw_of[s], 0});
+      P->ops.insert(P->ops.end(), RB.sops[s].begin(), RB.sops[s].end());
+      P->op_seq.insert(P->op_seq.end(), RB.sseq[s].begin(), RB.sseq[s].end());
+      pos += (uint32_t)RB.sops[s].size();
+    }
+    h.n_ops = pos;
+    h.colls = coll0;
+    h.n_colls = (uint32_t)(P->coll_lc.size() - coll0);
+    h.syncs = sync0;
+    h.n_syncs = (uint32_t)(P->syncs.size() - sync0);
+    h.counts = P->counts.size();
+    for (size_t k = 0; k < snap.size(); k++) {
+      P->syncs[sync0 + k].cnt = (uint32_t)(P->counts.size() - h.counts);
+      for (uint32_t s = 0; s < h.n_streams; s++)
+        P->counts.push_back(s < snap[k].size() ? snap[k][s] : 0u);
+    }
+    h.mems = mem0;
+    h.n_mems = (uint32_t)(P->mems.size() - mem0);
+    h.gend = gpre;
+    P->reps.push_back(h);
+    P->rep_ring_ok.push_back(ring_ok ? 1 : 0);
   }
-  // stream-major op layout
-  h.ops = P.ops.size();
-  h.streams = P.streams.size();
-  h.n_streams = (uint32_t)RB.sops.size();
-  uint32_t pos = 0;
-  for (size_t s = 0; s < RB.sops.size(); s++) {
-    P.streams.push_back(StreamRange{pos, (uint32_t)RB.sops[s].size(), RB.raw_of[s], 0});
-    P.ops.insert(P.ops.end(), RB.sops[s].begin(), RB.sops[s].end());
-    P.op_seq.insert(P.op_seq.end(), RB.sseq[s].begin(), RB.sseq[s].end());
-    pos += (uint32_t)RB.sops[s].size();
+};
+
+void pack_rep(const maya_raw_job &job, int rep, JobPack &P, FeatState &F, RepPacker &RP,
+              uint32_t &n_local_comms) {
+  const int64_t b = job.ev_off[rep], e = job.ev_off[rep + 1];
+  RP.begin(P, F, job.device, false, (size_t)(e - b) / 2 + 16);
+  // first pass: record ordinals (trace.py:453-459: each (event, version)
+  // recorded once) and the number of local communicators
+  uint32_t nlc = 0;
+  for (int64_t i = b; i < e; i++) {
+    const int k = job.ev_kind[i];
+    if (k == MAYA_EV_RECORD) {
+      const int64_t *f = job.ev_f + 4 * i;
+      RP.add_record(f[0], f[1]);
+    } else if (k == MAYA_EV_COMMINIT) {
+      nlc = std::max<uint32_t>(nlc, (uint32_t)job.ev_f[4 * i] + 1);
+    }
   }
-  h.n_ops = pos;
-  h.colls = coll0;
-  h.n_colls = (uint32_t)(P.coll_lc.size() - coll0);
-  h.syncs = sync0;
-  h.n_syncs = (uint32_t)(P.syncs.size() - sync0);
-  h.counts = P.counts.size();
-  for (size_t k = 0; k < snap.size(); k++) {
-    P.syncs[sync0 + k].cnt = (uint32_t)(P.counts.size() - h.counts);
-    for (uint32_t s = 0; s < h.n_streams; s++)
-      P.counts.push_back(s < snap[k].size() ? snap[k][s] : 0u);
-  }
-  h.mems = mem0;
-  h.n_mems = (uint32_t)(P.mems.size() - mem0);
-  h.gend = gpre;
-  P.reps.push_back(h);
-  P.rep_ring_ok.push_back(ring_ok ? 1 : 0);
+  RP.set_local_comms(nlc);
+  for (int64_t i = b; i < e; i++)
+    RP.event(job.ev_kind[i], job.ev_stream[i], job.ev_f + 4 * i,
+             job.kernel_ns ? job.kernel_ns[i] : -1, job.kernel_ns != nullptr);
+  RP.finish();
+  n_local_comms = nlc;
 }
 
 }  // namespace
@@ -474,7 +581,134 @@ void full_view(const maya_raw_job &job, SimView &V) {
 
 }  // namespace
 
-void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P, bool collapse) {
+namespace {
+
+// Job-level half of the packer: validation, rank classes, communicators, call
+// slots, simulated ranks, per-rank collective tables, walkers.  Reads only the
+// job tables of `job` (not its events); the reps are already in P.
+void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
+               const std::vector<uint32_t> &rep_comms) {
+  JobHdr &H = P.hdr;
+    // validate rank tables
+  for (int r = 0; r < job.num_ranks; r++) {
+    int rep = job.rank_rep[r];
+    if (rep < 0 || rep >= job.n_reps) throw Fail{MAYA_ST_BAD_INPUT, "rank_rep out of range"};
+    int64_t cb = job.rank_comm_off[r], ce = job.rank_comm_off[r + 1];
+    if ((uint64_t)(ce - cb) < rep_comms[rep])
+      throw Fail{MAYA_ST_BAD_INPUT, "rank lacks comm translation"};
+    for (int64_t q = cb; q < ce; q++)
+      if (job.rank_comm[q] < 0 || job.rank_comm[q] >= job.n_comms)
+        throw Fail{MAYA_ST_BAD_INPUT, "rank_comm out of range"};
+  }
+  const int64_t n_calls = job.call_off[job.n_comms];
+  if (n_calls > 0x7fffffff) throw Fail{MAYA_ST_BAD_INPUT, "too many group calls"};
+  // the ranks / communicators the scheduler simulates (collapsed or full)
+  SimView V;
+  P.collapsed = collapse && build_collapsed(job, rep_comms, V);
+  if (!P.collapsed) full_view(job, V);
+  P.rank_orig = V.rank_orig;
+  P.rank_sim = V.rank_sim;
+  // communicators and their call slots (JobTrace.groups / .calls)
+  for (size_t sg = 0; sg < V.comm_real.size(); sg++) {
+    const int g = V.comm_real[sg];
+    CommRec cr{job.comm_nranks[g], job.comm_topo[g], (uint32_t)P.slots.size(),
+               (uint32_t)(job.call_off[g + 1] - job.call_off[g])};
+    if (cr.topo < 0 || cr.topo > 2) throw Fail{MAYA_ST_BAD_INPUT, "topology class"};
+    P.comms.push_back(cr);
+    P.comm_rdv.push_back(V.comm_rdv[sg]);
+    for (int64_t s = job.call_off[g]; s < job.call_off[g + 1]; s++) {
+      int64_t fixed = -1;
+      if (job.wire_ns && job.call_kind[s] >= 0) {
+        fixed = job.wire_ns[s];
+        if (fixed < 0) throw Fail{MAYA_ST_BAD_INPUT, "negative host wire time"};
+      }
+      if (job.call_kind[s] > 4) throw Fail{MAYA_ST_BAD_INPUT, "collective kind"};
+      P.slots.push_back(SlotRec{job.call_bytes[s], fixed, job.call_kind[s], cr.nranks, cr.topo,
+                                job.device});
+    }
+  }
+  // work accounting over ALL ranks (sim.py:183-184)
+  int64_t rank_ops = 0, dev_ops = 0;
+  for (int r = 0; r < job.num_ranks; r++) {
+    const RepHdr &h = P.reps[job.rank_rep[r]];
+    rank_ops += h.n_events;
+    dev_ops += h.n_ops;
+  }
+  // simulated ranks
+  uint64_t fire = 0, delay = 0, walk = 0, tl = 0;
+  for (size_t sr = 0; sr < V.rank_orig.size(); sr++) {
+    const int rep = job.rank_rep[V.rank_orig[sr]];
+    const RepHdr &h = P.reps[rep];
+    RankRec rr{(uint32_t)rep, (uint32_t)P.rank_comm.size(), (uint32_t)fire, (uint32_t)delay,
+               (uint32_t)walk, (uint32_t)tl, 0, 0};
+    for (int32_t g : V.rank_comm[sr]) P.rank_comm.push_back((uint32_t)g);
+    for (uint32_t s = 0; s < h.n_streams; s++) P.walkers.push_back(Walker{(uint32_t)sr, s});
+    P.ranks.push_back(rr);
+    fire += h.n_recs;
+    delay += h.n_syncs + 1;
+    walk += h.n_streams;
+    tl += h.n_ops;
+    if (fire > 0xffffffffull || delay > 0xffffffffull || tl > 0xffffffffull)
+      throw Fail{MAYA_ST_BAD_INPUT, "job too large for 32-bit per-job tables"};
+  }
+  // each collective of a rep must address a real call slot for every rank;
+  // per-rank collective tables (arrivals | comm | call_idx)
+  bool ring = P.comms.size() <= 0xffff;
+  for (uint8_t ok : P.rep_ring_ok) ring = ring && ok;
+  for (size_t sr = 0; sr < P.ranks.size(); sr++) {
+    RankRec &rr = P.ranks[sr];
+    const RepHdr &h = P.reps[rr.rep];
+    rr.rslot = (uint32_t)P.rcolls.size();
+    for (uint32_t c2 = 0; c2 < h.n_colls; c2++) {
+      uint32_t g = P.rank_comm[rr.comm + P.coll_lc[h.colls + c2]];
+      uint32_t idx = P.coll_idx[h.colls + c2];
+      if (idx >= P.comms[g].n_calls || P.slots[P.comms[g].call_base + idx].kind < 0)
+        throw Fail{MAYA_ST_BAD_INPUT, "collective call missing from the job's call table"};
+      int64_t nr = P.comm_rdv[g];
+      if (nr < 1 || nr > 0xffff || g > 0xffff)
+        throw Fail{MAYA_ST_BAD_INPUT, "communicator too large for the engine"};
+      if (ring && (uint64_t)(P.comms[g].n_calls / 2 + 1) * (uint64_t)nr > 0xffffffffull)
+        ring = false;
+      P.rcolls.push_back(((uint64_t)nr << 48) | ((uint64_t)g << 32) | idx);
+    }
+    if (P.rcolls.size() > 0xffffffffull) throw Fail{MAYA_ST_BAD_INPUT, "too many collectives"};
+  }
+  // walkers rank-major: a scheduler warp owns whole ranks
+  P.wids.resize(P.walkers.size());
+  for (size_t w = 0; w < P.walkers.size(); w++) P.wids[w] = (uint32_t)w;
+  H.flags = ring ? JOB_RING : 0;
+  H.n_rcolls = (uint32_t)P.rcolls.size();
+  H.n_fire = (uint32_t)fire;
+  H.n_ranks = (uint32_t)P.ranks.size();
+  H.n_comms = (uint32_t)P.comms.size();
+  H.n_slots = (uint32_t)P.slots.size();
+  H.n_walkers = (uint32_t)P.walkers.size();
+  H.n_feats = (uint32_t)P.feats.size();
+  H.rank_ops = rank_ops;
+  H.dev_ops = dev_ops;
+  P.n_fire = fire;
+  P.n_delay = delay;
+}
+
+void pack_fail(const maya_raw_job &job, JobPack &P, const Fail &f) {
+  JobHdr &H = P.hdr;
+  H.status = f.status;
+  P.message = f.msg;
+  int64_t rank_ops = 0;
+  for (int r = 0; r < job.num_ranks && job.n_reps > 0; r++) {
+    int rep = job.rank_rep[r];
+    if (rep >= 0 && rep < job.n_reps) rank_ops += job.ev_off[rep + 1] - job.ev_off[rep];
+  }
+  // keep nothing else: the scheduler skips jobs whose status is preset
+  JobPack empty;
+  empty.hdr = H;
+  empty.hdr.rank_ops = rank_ops;
+  empty.hdr.n_ranks = 0;
+  empty.message = P.message;
+  P = std::move(empty);
+}
+
+void pack_header(const maya_raw_job &job, int32_t key_rank, JobPack &P) {
   P.clear();
   JobHdr &H = P.hdr;
   H.key_rank = key_rank;
@@ -482,130 +716,89 @@ void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P, bool collap
   H.device = (uint32_t)job.device;
   H.n_ranks = (uint32_t)job.num_ranks;
   H.status = MAYA_ST_OK;
+}
+
+// Generator events straight into the packer (no raw event arrays).
+struct PackSink final : EventSink {
+  JobPack *P;
+  FeatState *F;
+  RepPacker *RP;
+  int32_t device;
+  std::vector<uint32_t> *rep_comms;
+  void rep_begin(size_t est_events) override {
+    RP->begin(*P, *F, device, true, est_events / 2 + 16);
+  }
+  void ev(uint8_t k, int32_t s, int64_t a, int64_t b, int64_t c, int64_t d) override {
+    const int64_t f[4] = {a, b, c, d};
+    RP->event(k, s, f, -1, false);
+  }
+  void rep_end() override {
+    RP->finish();
+    P->reps.back().job = 0;
+    rep_comms->push_back(RP->n_local_comms);
+  }
+};
+
+}  // namespace
+
+void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P, bool collapse) {
+  pack_header(job, key_rank, P);
   try {
     if (job.num_ranks < 0 || job.n_reps < 0) throw Fail{MAYA_ST_BAD_INPUT, "negative sizes"};
-    std::unordered_map<FeatKey, uint32_t, FeatHash> feat_map;
-    std::unordered_map<int64_t, uint32_t> fixed_map;
+    thread_local FeatState F;
+    thread_local RepPacker RP;
+    F.clear();
     std::vector<uint32_t> rep_comms(job.n_reps);
     for (int rep = 0; rep < job.n_reps; rep++) {
-      pack_rep(job, rep, P, feat_map, fixed_map, rep_comms[rep]);
+      pack_rep(job, rep, P, F, RP, rep_comms[rep]);
       P.reps.back().job = 0;
     }
-    // validate rank tables
-    for (int r = 0; r < job.num_ranks; r++) {
-      int rep = job.rank_rep[r];
-      if (rep < 0 || rep >= job.n_reps) throw Fail{MAYA_ST_BAD_INPUT, "rank_rep out of range"};
-      int64_t cb = job.rank_comm_off[r], ce = job.rank_comm_off[r + 1];
-      if ((uint64_t)(ce - cb) < rep_comms[rep])
-        throw Fail{MAYA_ST_BAD_INPUT, "rank lacks comm translation"};
-      for (int64_t q = cb; q < ce; q++)
-        if (job.rank_comm[q] < 0 || job.rank_comm[q] >= job.n_comms)
-          throw Fail{MAYA_ST_BAD_INPUT, "rank_comm out of range"};
-    }
-    const int64_t n_calls = job.call_off[job.n_comms];
-    if (n_calls > 0x7fffffff) throw Fail{MAYA_ST_BAD_INPUT, "too many group calls"};
-    // the ranks / communicators the scheduler simulates (collapsed or full)
-    SimView V;
-    P.collapsed = collapse && build_collapsed(job, rep_comms, V);
-    if (!P.collapsed) full_view(job, V);
-    P.rank_orig = V.rank_orig;
-    P.rank_sim = V.rank_sim;
-    // communicators and their call slots (JobTrace.groups / .calls)
-    for (size_t sg = 0; sg < V.comm_real.size(); sg++) {
-      const int g = V.comm_real[sg];
-      CommRec cr{job.comm_nranks[g], job.comm_topo[g], (uint32_t)P.slots.size(),
-                 (uint32_t)(job.call_off[g + 1] - job.call_off[g])};
-      if (cr.topo < 0 || cr.topo > 2) throw Fail{MAYA_ST_BAD_INPUT, "topology class"};
-      P.comms.push_back(cr);
-      P.comm_rdv.push_back(V.comm_rdv[sg]);
-      for (int64_t s = job.call_off[g]; s < job.call_off[g + 1]; s++) {
-        int64_t fixed = -1;
-        if (job.wire_ns && job.call_kind[s] >= 0) {
-          fixed = job.wire_ns[s];
-          if (fixed < 0) throw Fail{MAYA_ST_BAD_INPUT, "negative host wire time"};
-        }
-        if (job.call_kind[s] > 4) throw Fail{MAYA_ST_BAD_INPUT, "collective kind"};
-        P.slots.push_back(SlotRec{job.call_bytes[s], fixed, job.call_kind[s], cr.nranks, cr.topo,
-                                  job.device});
-      }
-    }
-    // work accounting over ALL ranks (sim.py:183-184)
-    int64_t rank_ops = 0, dev_ops = 0;
-    for (int r = 0; r < job.num_ranks; r++) {
-      const RepHdr &h = P.reps[job.rank_rep[r]];
-      rank_ops += h.n_events;
-      dev_ops += h.n_ops;
-    }
-    // simulated ranks
-    uint64_t fire = 0, delay = 0, walk = 0, tl = 0;
-    for (size_t sr = 0; sr < V.rank_orig.size(); sr++) {
-      const int rep = job.rank_rep[V.rank_orig[sr]];
-      const RepHdr &h = P.reps[rep];
-      RankRec rr{(uint32_t)rep, (uint32_t)P.rank_comm.size(), (uint32_t)fire, (uint32_t)delay,
-                 (uint32_t)walk, (uint32_t)tl, 0, 0};
-      for (int32_t g : V.rank_comm[sr]) P.rank_comm.push_back((uint32_t)g);
-      for (uint32_t s = 0; s < h.n_streams; s++) P.walkers.push_back(Walker{(uint32_t)sr, s});
-      P.ranks.push_back(rr);
-      fire += h.n_recs;
-      delay += h.n_syncs + 1;
-      walk += h.n_streams;
-      tl += h.n_ops;
-      if (fire > 0xffffffffull || delay > 0xffffffffull || tl > 0xffffffffull)
-        throw Fail{MAYA_ST_BAD_INPUT, "job too large for 32-bit per-job tables"};
-    }
-    // each collective of a rep must address a real call slot for every rank;
-    // per-rank collective tables (arrivals | comm | call_idx)
-    bool ring = P.comms.size() <= 0xffff;
-    for (uint8_t ok : P.rep_ring_ok) ring = ring && ok;
-    for (size_t sr = 0; sr < P.ranks.size(); sr++) {
-      RankRec &rr = P.ranks[sr];
-      const RepHdr &h = P.reps[rr.rep];
-      rr.rslot = (uint32_t)P.rcolls.size();
-      for (uint32_t c2 = 0; c2 < h.n_colls; c2++) {
-        uint32_t g = P.rank_comm[rr.comm + P.coll_lc[h.colls + c2]];
-        uint32_t idx = P.coll_idx[h.colls + c2];
-        if (idx >= P.comms[g].n_calls || P.slots[P.comms[g].call_base + idx].kind < 0)
-          throw Fail{MAYA_ST_BAD_INPUT, "collective call missing from the job's call table"};
-        int64_t nr = P.comm_rdv[g];
-        if (nr < 1 || nr > 0xffff || g > 0xffff)
-          throw Fail{MAYA_ST_BAD_INPUT, "communicator too large for the engine"};
-        if (ring && (uint64_t)(P.comms[g].n_calls / 2 + 1) * (uint64_t)nr > 0xffffffffull)
-          ring = false;
-        P.rcolls.push_back(((uint64_t)nr << 48) | ((uint64_t)g << 32) | idx);
-      }
-      if (P.rcolls.size() > 0xffffffffull) throw Fail{MAYA_ST_BAD_INPUT, "too many collectives"};
-    }
-    // walkers rank-major: a scheduler warp owns whole ranks
-    P.wids.resize(P.walkers.size());
-    for (size_t w = 0; w < P.walkers.size(); w++) P.wids[w] = (uint32_t)w;
-    H.flags = ring ? JOB_RING : 0;
-    H.n_rcolls = (uint32_t)P.rcolls.size();
-    H.n_fire = (uint32_t)fire;
-    H.n_ranks = (uint32_t)P.ranks.size();
-    H.n_comms = (uint32_t)P.comms.size();
-    H.n_slots = (uint32_t)P.slots.size();
-    H.n_walkers = (uint32_t)P.walkers.size();
-    H.n_feats = (uint32_t)P.feats.size();
-    H.rank_ops = rank_ops;
-    H.dev_ops = dev_ops;
-    P.n_fire = fire;
-    P.n_delay = delay;
+    pack_tail(job, P, collapse, rep_comms);
   } catch (const Fail &f) {
-    H.status = f.status;
-    P.message = f.msg;
-    int64_t rank_ops = 0;
-    for (int r = 0; r < job.num_ranks && job.n_reps > 0; r++) {
-      int rep = job.rank_rep[r];
-      if (rep >= 0 && rep < job.n_reps) rank_ops += job.ev_off[rep + 1] - job.ev_off[rep];
-    }
-    // keep nothing else: the scheduler skips jobs whose status is preset
-    JobPack empty;
-    empty.hdr = H;
-    empty.hdr.rank_ops = rank_ops;
-    empty.hdr.n_ranks = 0;
-    empty.message = P.message;
-    P = std::move(empty);
+    pack_fail(job, P, f);
   }
+}
+
+int pack_generated(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
+                   int32_t schedule, int64_t overhead, int32_t device, int32_t key_rank,
+                   bool collapse, GenJob &G, JobPack &P, std::string *err) {
+  thread_local FeatState F;
+  thread_local RepPacker RP;
+  F.clear();
+  std::vector<uint32_t> rep_comms;
+  P.clear();
+  PackSink sink;
+  sink.P = &P;
+  sink.F = &F;
+  sink.RP = &RP;
+  sink.device = device;
+  sink.rep_comms = &rep_comms;
+  int rc;
+  try {
+    rc = generate_job(model, cfg, cl, schedule, overhead, G, err, &sink);
+  } catch (const Fail &f) {   // packer error inside the generator's event stream
+    maya_raw_job raw = G.raw(device);
+    pack_header(raw, key_rank, P);
+    pack_fail(raw, P, f);
+    if (err) *err = f.msg;
+    return MAYA_OK;
+  }
+  if (rc != MAYA_OK) return rc;
+  maya_raw_job raw = G.raw(device);
+  // keep the packed reps: pack_header clears P, so set the header by hand
+  JobHdr &H = P.hdr;
+  H = JobHdr{};
+  H.key_rank = key_rank;
+  H.capacity = raw.capacity;
+  H.device = (uint32_t)device;
+  H.n_ranks = (uint32_t)raw.num_ranks;
+  H.status = MAYA_ST_OK;
+  try {
+    pack_tail(raw, P, collapse, rep_comms);
+  } catch (const Fail &f) {
+    pack_fail(raw, P, f);
+  }
+  return MAYA_OK;
 }
 
 }  // namespace maya

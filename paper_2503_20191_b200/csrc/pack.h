@@ -4,6 +4,7 @@
 #include <vector>
 
 #include "../../include/maya_b200.h"
+#include "gen.h"
 #include "soa.h"
 
 namespace maya {
@@ -49,5 +50,13 @@ struct JobPack {
 
 // Pack one job.  Never throws; input problems become hdr.status + message.
 void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &out, bool collapse);
+
+// Generate one configuration (gen.cpp) and pack it in the same pass: the
+// generator's events go straight into the per-rep packer, never through raw
+// event arrays.  Same JobPack as generate_job + pack_job (tests/test_gen.py).
+// Returns generate_job's code (invalid configuration: <0 with *err set).
+int pack_generated(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
+                   int32_t schedule, int64_t overhead, int32_t device, int32_t key_rank,
+                   bool collapse, GenJob &scratch, JobPack &out, std::string *err);
 
 }  // namespace maya

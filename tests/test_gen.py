@@ -84,3 +84,37 @@ def test_generator_event_level_vs_reference():
         ref = from_reference(collate(tr, ex, cl))
         got = W.generate_job(model, cfg, cl, schedule=s, dispatch_overhead_ns=777)
         assert raw_digest(ref) == raw_digest(got), (cfg, s)
+
+
+def _pack_compare(model, cfgs, cluster, collapse, schedule=None, overhead=5000):
+    import ctypes as C
+    from paper_2503_20191_b200.workload import (ConfigC, cluster_c, config_c, model_c,
+                                                schedule_code, _gen_lib)
+    L = _gen_lib()
+    L.maya_debug_pack_compare.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                          C.c_int32, C.c_int64, C.c_int32]
+    arr = (ConfigC * len(cfgs))(*[config_c(c) for c in cfgs])
+    m, cl = model_c(model), cluster_c(cluster)
+    return L.maya_debug_pack_compare(C.byref(m), len(cfgs), arr, C.byref(cl),
+                                     schedule_code(schedule), overhead, int(collapse))
+
+
+@pytest.mark.parametrize("collapse", [True, False])
+def test_fused_generate_pack_equals_generate_then_pack(collapse):
+    """engine's maya_batch_add_generated packs generator events on the fly
+    (pack.cpp pack_generated); it must produce byte-identical JobPacks to
+    generate_job + pack_job on the C2 lattice and the C3/C4 golden configs."""
+    model, cluster, cfgs = c2_space()
+    assert _pack_compare(model, cfgs, cluster, collapse) == 0
+    with open(os.path.join(GOLDEN, "scale_results.json")) as f:
+        rows = json.load(f)
+    for r in rows[::3]:
+        m = W.ModelSpec(*r["model"])
+        cl = W.ClusterSpec(r["ranks"] // 8, 8, 80 * 2 ** 30, W.load_device_preset("fast"))
+        assert _pack_compare(m, [W.ConfigPoint(*r["key"])], cl, collapse) == 0, r["key"]
+    # small lattices, every schedule, odd overheads
+    m = W.ModelSpec("t", 8, 128, 64, 512)
+    cl = W.ClusterSpec(2, 8, 2 ** 34, W.load_device_preset("fast"))
+    small = W.enumerate_space(W.SearchSpace(global_batch=64), m, cl)
+    assert _pack_compare(m, small, cl, collapse, overhead=777) == 0
+    assert _pack_compare(m, small, cl, collapse, overhead=0) == 0

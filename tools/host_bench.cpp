@@ -44,5 +44,18 @@ done:
   }
   printf("%zu configs, %zu events: gen %.1f ms (%.1f ns/ev), pack %.1f ms (%.1f ns/ev)\n",
          cfgs.size(), ev, tg * 1e3, tg * 1e9 / ev, tp * 1e3, tp * 1e9 / ev);
+  double tf = 0;
+  for (int it = 0; it < 2; it++) {
+    tf = 0;
+    GenJob g;
+    for (auto &c : cfgs) {
+      JobPack P;
+      std::string err;
+      auto t0 = clk::now();
+      pack_generated(m, c, cl, -1, 5000, 0, 0, true, g, P, &err);
+      tf += std::chrono::duration<double>(clk::now() - t0).count();
+    }
+  }
+  printf("fused generate+pack %.1f ms (%.1f ns/ev)\n", tf * 1e3, tf * 1e9 / ev);
   return 0;
 }
