@@ -134,6 +134,8 @@ int maya_batch_num_jobs(maya_engine *eng);
 #define MAYA_OPT_COLLAPSE 1   /* exact rank-class collapse (default on) */
 #define MAYA_OPT_WARP_SCHED 2 /* schedule every job with the warp-window kernel instead of
                                  the lane-parallel kernel (A/B and parity testing) */
+#define MAYA_OPT_NO_FOLD 8    /* keep one scheduler op per trace op (no affine run folding;
+                                 A/B testing -- runs are never folded when a timeline is recorded) */
 #define MAYA_OPT_LANE_SCHED 4 /* schedule every job that fits with the lane-parallel kernel
                                  (default: per job, by the shape of its FIFOs) */
 int maya_set_options(maya_engine *eng, int32_t options);

@@ -94,7 +94,8 @@ struct maya_engine {
   // segments
   Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_slots, s_walkers, s_reps, s_ops, s_streams,
       s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
-      s_lane_jobs, s_lane_wslot, s_lane_perm;
+      s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks;
+  Seg x_clen, x_ccounts, x_chunk_cnt;
   Seg x_exec, x_rcw, x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
       x_results, x_err, x_topk, x_topk_out, x_topk_n;
   uint64_t n_tl = 0;
@@ -366,7 +367,7 @@ int maya_upload(maya_engine *e) {
   // totals
   size_t n_ranks = 0, n_rank_comm = 0, n_comms = 0, n_slots = 0, n_walkers = 0, n_reps = 0,
          n_ops = 0, n_streams = 0, n_colls = 0, n_syncs = 0, n_counts = 0, n_mems = 0,
-         n_feats = 0, n_fire = 0, n_delay = 0, n_wstate = 0, n_rcolls = 0;
+         n_feats = 0, n_fire = 0, n_delay = 0, n_wstate = 0, n_rcolls = 0, n_chunks = 0;
   uint64_t n_tl = 0;
   e->job_tl.resize(nj);
   e->job_ops.resize(nj);
@@ -389,6 +390,7 @@ int maya_upload(maya_engine *e) {
     n_fire += P.n_fire;
     n_delay += P.n_delay;
     n_rcolls += P.rcolls.size();
+    for (const StreamRange &sr : P.streams) n_chunks += (sr.len + FOLD_CHUNK - 1) / FOLD_CHUNK;
     {
       const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
                                          (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0,
@@ -448,10 +450,14 @@ int maya_upload(maya_engine *e) {
   seg(e->s_lane_jobs, nj * sizeof(LaneJob));
   seg(e->s_lane_wslot, n_walkers * sizeof(uint32_t));
   seg(e->s_lane_perm, n_perm * sizeof(uint32_t));
+  seg(e->s_chunks, n_chunks * sizeof(FoldChunk));
   e->arena_bytes = off;
   // scratch layout
   off = 0;
   seg(e->x_exec, n_ops * sizeof(ExecOp));
+  seg(e->x_clen, n_streams * sizeof(uint32_t));
+  seg(e->x_chunk_cnt, n_chunks * sizeof(uint32_t));
+  seg(e->x_ccounts, n_counts * sizeof(uint32_t));
   seg(e->x_rcw, n_rcolls * sizeof(RCX));
   seg(e->x_feat_ns, n_feats * 8);
   seg(e->x_wire, n_slots * 8);
@@ -556,6 +562,23 @@ int maya_upload(maya_engine *e) {
       if (!L.on_chip) b.wstate += spill_bytes(P.walkers.size(), P.ranks.size());
     }
   }
+  {  // run-folding work items: one per 1,024 ops of every FIFO
+    FoldChunk *fcs = (FoldChunk *)(H + e->s_chunks.off);
+    size_t q = 0;
+    for (size_t j = 0; j < nj; j++) {
+      const JobPack &P = e->packs[j];
+      for (size_t r = 0; r < P.reps.size(); r++) {
+        const RepHdr &h = P.reps[r];
+        for (uint32_t st = 0; st < h.n_streams; st++) {
+          const uint32_t len = P.streams[h.streams + st].len;
+          const uint32_t first = (uint32_t)q;
+          for (uint32_t c = 0; c * FOLD_CHUNK < len; c++)
+            fcs[q++] = FoldChunk{(uint32_t)(bases[j].reps + r), st, c, first};
+        }
+      }
+    }
+  }
+  if (n_chunks >= 0xffffffffull) return fail(MAYA_EINVAL, "too many fold chunks in batch");
   auto copy_job = [&](size_t j) {
     const JobPack &P = e->packs[j];
     const Base &B = bases[j];
@@ -667,6 +690,8 @@ int maya_upload(maya_engine *e) {
   db.lane_jobs = (const LaneJob *)(D + e->s_lane_jobs.off);
   db.lane_wslot = (const uint32_t *)(D + e->s_lane_wslot.off);
   db.lane_perm = (const uint32_t *)(D + e->s_lane_perm.off);
+  db.chunks = (const FoldChunk *)(D + e->s_chunks.off);
+  db.n_chunks = (uint32_t)n_chunks;
   db.ranks = (const RankRec *)(D + e->s_ranks.off);
   db.rank_comm = (const uint32_t *)(D + e->s_rank_comm.off);
   db.comms = (const CommRec *)(D + e->s_comms.off);
@@ -759,6 +784,11 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
     e->db.tl_end = db.tl_end;
   }
   char *X = (char *)e->d_scratch;
+  // runs fold (fold_kernel) unless a per-op timeline is recorded
+  const bool fold = !record_timeline && !(e->options & MAYA_OPT_NO_FOLD);
+  db.clen = fold ? (uint32_t *)(X + e->x_clen.off) : nullptr;
+  db.chunk_cnt = (uint32_t *)(X + e->x_chunk_cnt.off);
+  db.ccounts = fold ? (uint32_t *)(X + e->x_ccounts.off) : nullptr;
   CU(cudaEventRecord(e->ev[0], e->stream));
   CU(cudaMemsetAsync(X + e->x_err.off, 0, 16, e->stream));
   launch_estimate(db, e->tables, e->stream);
@@ -839,8 +869,9 @@ int maya_results(maya_engine *e, maya_job_result *out) {
       bool bad = false;
       for (size_t f = 0; f < P.feats.size(); f++) bad |= fns[fb + f] < 0;
       for (size_t s = 0; s < P.slots.size(); s++) bad |= wns[sb + s] < 0;
-      if (bad && out[j].status == MAYA_ST_OK) out[j].status = MAYA_ST_ESTIMATION;
-      if (bad && out[j].status == MAYA_ST_DEADLOCK) out[j].status = MAYA_ST_ESTIMATION;
+      // annotate() raises before simulate() runs (estimate.py:344-347): any
+      // failed estimate of the job decides its status, whatever the schedule did
+      if (bad && out[j].status != MAYA_ST_BAD_INPUT) out[j].status = MAYA_ST_ESTIMATION;
       fb += P.feats.size();
       sb += P.slots.size();
     }

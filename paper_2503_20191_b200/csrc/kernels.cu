@@ -41,8 +41,24 @@ __device__ __forceinline__ bool mul_u128_u64(u128 a, uint64_t b, u128 *r) {
   return true;
 }
 
-// ceil(a / b) into int64; false on overflow
+// ceil(a / b) into int64; false on overflow.  Fast path for a, b < 2^64 and a
+// quotient < 2^52: a double-precision estimate corrected exactly with 128-bit
+// products (the estimate is within +-2 of the true quotient); otherwise the
+// exact 128-bit division.
 __device__ __forceinline__ bool ceil_div_i64(u128 a, u128 b, int64_t *out) {
+  if ((a >> 64) == 0 && (b >> 64) == 0 && (uint64_t)b != 0) {
+    const uint64_t x = (uint64_t)a, y = (uint64_t)b;
+    const double qd = (double)x / (double)y;
+    if (qd < 4503599627370496.0) {   // 2^52
+      uint64_t q = (uint64_t)qd;
+      u128 p = (u128)q * y;
+      while (p > (u128)x) { q--; p -= y; }
+      while (p + y <= (u128)x) { q++; p += y; }
+      if (p != (u128)x) q++;
+      *out = (int64_t)q;
+      return true;
+    }
+  }
   u128 q = a / b;
   if (q * b != a) q += 1;
   if (q > (u128)INT64_MAX) return false;
@@ -262,8 +278,8 @@ __device__ __forceinline__ void load_ctx(const DevBatch &b, const JobHdr &J, uin
   c.fire = fire_job + rr.fire;
   c.delay = b.delay + J.delay + rr.delay;
   c.rc = rcx_job + rr.rslot;
-  c.cnt = b.counts + h.counts + wk.stream;
-  c.len = sr.len;
+  c.cnt = (b.clen ? b.ccounts : b.counts) + h.counts + wk.stream;
+  c.len = b.clen ? b.clen[h.streams + wk.stream] : sr.len;
   c.rank = wk.rank;
   c.ns = h.n_streams;
   c.nsync = h.n_syncs;
@@ -541,6 +557,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
         int64_t dd = 0;
         if (qtag == TAG_KERN) {
           if (qw == EXEC_BAD) { stc = STEP_ERR; eno = MAYA_ST_ESTIMATION; }
+          else if (qw == EXEC_OVF) { stc = STEP_ERR; eno = MAYA_ST_OVERFLOW; }
           dd = (int64_t)qpay;
         }
         if (stc == STEP_OK && qtag == TAG_KERN) {
@@ -686,7 +703,7 @@ __device__ bool host_step(const DevBatch &b, const JobSh &sh, uint32_t r, int64_
         if (s.arg == NO_REC) { s0 = s1 = 0; } else { s0 = s.arg; s1 = s.arg + 1; }
       }
       for (uint32_t ls = s0; ls < s1; ls++) {
-        const uint32_t cnt = b.counts[h.counts + s.cnt + ls];
+        const uint32_t cnt = (b.clen ? b.ccounts : b.counts)[h.counts + s.cnt + ls];
         if (cnt == 0) continue;
         const WSt &ws = sh.st[sh.wid[rr.walker + ls]];
         if (ws.i < cnt) { ok = false; break; }
@@ -915,8 +932,9 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
   for (uint32_t w = tid; w < W; w += nt) {
     const Walker wk = b.walkers[J.walkers + w];
     const RankRec rr = b.ranks[J.ranks + wk.rank];
-    const StreamRange sr = b.streams[b.reps[rr.rep].streams + wk.stream];
-    if (sh.st[w].i < sr.len) s_incomplete = 1;
+    const uint64_t si = b.reps[rr.rep].streams + wk.stream;
+    const uint32_t len = b.clen ? b.clen[si] : b.streams[si].len;
+    if (sh.st[w].i < len) s_incomplete = 1;
   }
   // epilogue: host end time, peak memory, first OOM (sim.py:235-242, 365-366)
   for (uint32_t r = tid; r < R; r += nt) {
@@ -975,8 +993,302 @@ int sched_variant(uint32_t W, uint32_t R) {
   return nw == 4 ? 0 : nw == 8 ? 1 : 2;
 }
 
+// ---------------------------------------------------------------------------
+// Affine run folding (the resolve pass of runs without a timeline).
+//
+// A kernel op is the max-plus map x -> max(x + d, disp + delay + d); a run of
+// kernel ops of one FIFO inside one host-sync segment (one `delay`) composes
+// to ONE such map, x -> max(x + A, B0 + delay) with A = sum d and
+// B0 = fold of (disp + d).  The fold is written as a kernel op with
+// d' = A, disp' = B0 - A, so both schedulers consume it unchanged and produce
+// identical times (same maps, composed earlier).  One warp per FIFO streams
+// its 16-byte ops once (segmented warp scan of the (A, B0) pairs), writes the
+// folded FIFO in place of the ExecOp array (same base), its length (clen) and
+// the per-sync dispatch counts in folded indices (ccounts: counts[k][s] =
+// number of ops with segment <= k, so a segment change is a fold boundary).
+// Runs are cut every 1,024 ops and only durations < 2^40 fold, so A < 2^50.
+// Per-op fold eligibility and run starts of one 32-op window.  Eligibility
+// reads the op only (a kernel whose gap prefix is < 2^61), so the counting
+// pass does not gather durations; the writing pass saturates the composite at
+// 2^62 and writes EXEC_OVF when it leaves int64 (every op time of the run
+// does too: done >= sum of durations, done >= B0), and a failed estimate
+// saturates as well (the job's status is ESTIMATION whatever the schedule).
+static constexpr int64_t FOLD_SAT = (int64_t)1 << 62;
+__device__ __forceinline__ int64_t sat_add(int64_t x, int64_t y) {   // x, y in [0, FOLD_SAT]
+  const int64_t s = x + y;
+  return s > FOLD_SAT ? FOLD_SAT : s;
+}
+
+// Both passes give each lane 32 consecutive ops of the 1,024-op chunk and walk
+// them sequentially (a few instructions per op, not a warp scan per 32 ops);
+// the warp combines the 32 lane results once per chunk.
+__device__ __forceinline__ bool op_foldable(const Op &o) {
+  return op_tag(o.meta) == TAG_KERN && o.disp < ((int64_t)1 << 61);
+}
+
+// pass 1: folded ops per chunk
+static constexpr uint32_t FOLD_WARPS = 2;             // warps (chunks) per CTA
+static constexpr uint32_t FOLD_PAD = FOLD_CHUNK + FOLD_CHUNK / 32;   // one pad op per 32
+
+// Coalesced copy of a chunk into shared memory, padded so that lane L's 32
+// consecutive ops (L*33 + t) spread over the banks.
+__device__ __forceinline__ void fold_stage(const Op *in, uint32_t lo, uint32_t hi, Op *sm,
+                                           uint32_t lane) {
+  // every load in flight at once (LDGSTS), then one wait
+  for (uint32_t j = lane; lo + j < hi; j += 32) {
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm[j + (j >> 5)]);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(in + lo + j)
+                 : "memory");
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+}
+__device__ __forceinline__ const Op &fold_at(const Op *sm, uint32_t j) { return sm[j + (j >> 5)]; }
+
+__global__ void __launch_bounds__(FOLD_WARPS * 32) fold_count_kernel(DevBatch b) {
+  __shared__ Op sm_all[FOLD_WARPS][FOLD_PAD];
+  const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const uint32_t c = blockIdx.x * FOLD_WARPS + wp;
+  if (c >= b.n_chunks) return;
+  Op *sm = sm_all[wp];
+  const FoldChunk fc = b.chunks[c];
+  const RepHdr &h = b.reps[fc.rep];
+  const StreamRange sr = b.streams[h.streams + fc.st];
+  const Op *in = b.ops + h.ops + sr.begin;
+  const uint32_t lo = fc.chunk * FOLD_CHUNK, hi = min(sr.len, lo + FOLD_CHUNK);
+  fold_stage(in, lo, hi, sm, lane);
+  const uint32_t k0 = lo + lane * 32u, k1 = min(hi, k0 + 32u);
+  uint32_t cnt = 0;
+  if (k0 < hi) {
+    uint32_t pseg = 0;
+    bool pfold = false;
+    if (k0 > lo) {
+      const Op &p = fold_at(sm, k0 - 1 - lo);
+      pseg = op_seg(p.meta);
+      pfold = op_foldable(p);
+    }
+    for (uint32_t i = k0; i < k1; i++) {
+      const Op &o = fold_at(sm, i - lo);
+      const bool f = op_foldable(o);
+      const uint32_t sg = op_seg(o.meta);
+      cnt += (i == lo || !f || !pfold || sg != pseg) ? 1u : 0u;
+      pseg = sg;
+      pfold = f;
+    }
+  }
+  cnt = __reduce_add_sync(FULL, cnt);
+  if (lane == 0) b.chunk_cnt[c] = cnt;
+}
+
+// pass 2: fold and write each chunk at its offset; sync counts; lengths.
+// 128-op windows, 4 consecutive ops per lane: a lane composes its 4 maps
+// sequentially (branch-free), the warp scans the 32 lane composites once, and
+// each lane writes the runs that end among its ops.
+__global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= b.n_chunks) return;
+  const FoldChunk fc = b.chunks[c];
+  const RepHdr &h = b.reps[fc.rep];
+  const uint32_t ns = h.n_streams, nsync = h.n_syncs;
+  const StreamRange sr = b.streams[h.streams + fc.st];
+  const Op *in = b.ops + h.ops + sr.begin;
+  ExecOp *out = b.exec + h.ops + sr.begin;
+  uint32_t *cc = b.ccounts + h.counts + fc.st;
+  const uint32_t n = sr.len;
+  const uint32_t lo = fc.chunk * FOLD_CHUNK, hi = min(n, lo + FOLD_CHUNK);
+  uint32_t outpos = 0;   // folded ops of the FIFO before this window
+  for (uint32_t q = fc.first + lane; q < c; q += 32) outpos += b.chunk_cnt[q];
+  outpos = __reduce_add_sync(FULL, outpos);
+  // carry from the previous window: last op's segment / foldability, open run
+  uint32_t cseg = lo > 0 ? op_seg(in[lo - 1].meta) : 0;
+  bool cfold = false;            // the chunk's first op always starts a run
+  int64_t cA = 0, cB = 0;        // composite of the run open at the window edge
+  for (uint32_t base = lo; base < hi; base += 128) {
+    const uint32_t j0 = base + lane * 4u;
+    Op o[4];
+    int64_t d[4];
+    bool v[4], f[4], st[4];
+    uint32_t sg[4];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      v[t] = j0 + t < hi;
+      o[t] = v[t] ? in[j0 + t] : Op{0, 0, 0};
+      sg[t] = op_seg(o[t].meta);
+      f[t] = v[t] && op_foldable(o[t]);
+      d[t] = 0;
+      if (v[t] && op_tag(o[t].meta) == TAG_KERN) d[t] = b.feat_ns[o[t].arg];
+    }
+    // previous op of each of the lane's ops
+    uint32_t psg = __shfl_up_sync(FULL, sg[3], 1);
+    bool pf = __shfl_up_sync(FULL, f[3], 1);
+    if (lane == 0) {
+      psg = cseg;
+      pf = cfold;
+    }
+    uint32_t nst = 0;   // starts among the lane's ops
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const uint32_t ps = t ? sg[t - 1] : psg;
+      const bool pfo = t ? f[t - 1] : pf;
+      st[t] = v[t] && (j0 + t == lo || !f[t] || !pfo || sg[t] != ps);
+      nst += st[t] ? 1u : 0u;
+    }
+    // lane composite of its last run (restarts at each start), affine pairs
+    int64_t A = 0, B = 0;
+    bool hs = false;     // the lane has a start
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      if (!v[t]) continue;
+      const int64_t de = (d[t] < 0 || d[t] > FOLD_SAT) ? FOLD_SAT : d[t];
+      const int64_t a = f[t] ? de : 0, bb = f[t] ? sat_add(o[t].disp, de) : 0;
+      if (st[t]) {
+        A = a;
+        B = bb;
+        hs = true;
+      } else {
+        const int64_t nb = sat_add(B, a);
+        B = nb > bb ? nb : bb;
+        A = sat_add(A, a);
+      }
+    }
+    // output index base of the lane: exclusive scan of start counts
+    uint32_t incl = nst;
+#pragma unroll
+    for (uint32_t off = 1; off < 32; off <<= 1) {
+      const uint32_t x = __shfl_up_sync(FULL, incl, off);
+      if (lane >= off) incl += x;
+    }
+    const uint32_t obase = outpos + incl - nst;
+    // incoming composite of the run open at the lane's first op
+    int64_t sA = A, sB = B;
+    bool sfl = hs || !v[0];
+    if (lane == 0 && !hs) {   // continue the carried run
+      const int64_t nb = sat_add(cB, sA);
+      sB = nb > sB ? nb : sB;
+      sA = sat_add(cA, sA);
+      sfl = true;
+    }
+#pragma unroll
+    for (uint32_t off = 1; off < 32; off <<= 1) {
+      const int64_t A2 = __shfl_up_sync(FULL, sA, off);
+      const int64_t B2 = __shfl_up_sync(FULL, sB, off);
+      const bool f2 = __shfl_up_sync(FULL, sfl, off);
+      if (lane >= off && !sfl) {
+        const int64_t nb = sat_add(B2, sA);
+        sB = nb > sB ? nb : sB;
+        sA = sat_add(A2, sA);
+        sfl = f2;
+      }
+    }
+    int64_t iA = __shfl_up_sync(FULL, sA, 1), iB = __shfl_up_sync(FULL, sB, 1);
+    if (lane == 0) {
+      iA = cA;
+      iB = cB;
+    }
+    // start flag of the op after the lane's last op
+    bool nxt = __shfl_down_sync(FULL, st[0], 1);
+    if (lane == 31 || j0 + 4 >= hi) nxt = true;   // window / chunk edge: resolved below
+    // walk the lane's ops: write runs that end here, sync counts
+    uint32_t oidx = obase - 1;
+    int64_t rA = iA, rB = iB;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      if (!v[t]) continue;
+      const int64_t de = (d[t] < 0 || d[t] > FOLD_SAT) ? FOLD_SAT : d[t];
+      const int64_t a = f[t] ? de : 0, bb = f[t] ? sat_add(o[t].disp, de) : 0;
+      if (st[t]) {
+        oidx++;
+        rA = a;
+        rB = bb;
+        const uint32_t ps = t ? sg[t - 1] : psg;
+        if (sg[t] != ps)
+          for (uint32_t k = ps; k < sg[t] && k < nsync; k++) cc[(size_t)k * ns] = oidx;
+      } else {
+        const int64_t nb = sat_add(rB, a);
+        rB = nb > bb ? nb : bb;
+        rA = sat_add(rA, a);
+      }
+      const bool ends = t < 3 ? (!v[t + 1] || st[t + 1]) : nxt;
+      // a foldable run reaching the window edge (not the chunk end) stays open
+      const bool edge = (t == 3 || !v[t + 1]) && (lane == 31 || j0 + t + 1 >= base + 128) &&
+                        j0 + t + 1 < hi;
+      if (ends && !(f[t] && edge)) {
+        if (f[t]) {
+          out[oidx] = (rA >= FOLD_SAT || rB >= FOLD_SAT)
+                          ? ExecOp{0, EXEC_OVF}
+                          : ExecOp{rB - rA, ((uint64_t)rA << 2) | TAG_KERN};
+        } else {
+          const uint32_t tag = op_tag(o[t].meta);
+          const bool bad = d[t] < 0 || d[t] >= (int64_t)(EXEC_BAD >> 2);
+          uint64_t pay;
+          if (tag == TAG_KERN) pay = bad ? (EXEC_BAD >> 2) : (uint64_t)d[t];
+          else pay = (o[t].arg == NO_REC) ? (EXEC_NONE >> 2) : (uint64_t)o[t].arg;
+          out[oidx] = ExecOp{o[t].disp, (pay << 2) | tag};
+        }
+      }
+    }
+    // carry to the next window: the last valid op of the window
+    const uint32_t nwin = min(128u, hi - base);
+    const uint32_t ll = (nwin - 1) >> 2, lt = (nwin - 1) & 3;
+    const uint32_t sgl = lt == 0 ? sg[0] : lt == 1 ? sg[1] : lt == 2 ? sg[2] : sg[3];
+    const bool fl = lt == 0 ? f[0] : lt == 1 ? f[1] : lt == 2 ? f[2] : f[3];
+    const uint32_t lseg = __shfl_sync(FULL, sgl, ll);
+    const bool lfold = __shfl_sync(FULL, fl, ll);
+    const int64_t lA = __shfl_sync(FULL, rA, ll), lB = __shfl_sync(FULL, rB, ll);
+    const uint32_t ltotal = __shfl_sync(FULL, incl, 31);
+    // the next window's first op decides whether the carried run ends
+    const bool more = base + 128 < hi;
+    bool next_start = true;
+    if (more) {
+      const Op on = in[base + 128];
+      next_start = !op_foldable(on) || !lfold || op_seg(on.meta) != lseg;
+    }
+    if (lfold && lane == 0) {
+      if (!more || next_start) {
+        const uint32_t last_idx = outpos + ltotal - 1;
+        out[last_idx] = (lA >= FOLD_SAT || lB >= FOLD_SAT)
+                              ? ExecOp{0, EXEC_OVF}
+                              : ExecOp{lB - lA, ((uint64_t)lA << 2) | TAG_KERN};
+      }
+    }
+    cseg = lseg;
+    cfold = lfold && more && !next_start;
+    cA = lA;
+    cB = lB;
+    outpos += ltotal;
+  }
+  if (hi == n) {   // the FIFO's last chunk: counts of the remaining syncs, length
+    const uint32_t last_seg = n > 0 ? cseg : 0;
+    for (uint32_t k = last_seg + lane; k < nsync; k += 32) cc[(size_t)k * ns] = outpos;
+    if (lane == 0) b.clen[h.streams + fc.st] = outpos;
+  }
+}
+
+// FIFOs without ops have no chunk: their counts are 0, their length 0
+__global__ void fold_empty_kernel(DevBatch b) {
+  const uint32_t rep = blockIdx.x * blockDim.y + threadIdx.y;
+  if (rep >= b.n_reps) return;
+  const RepHdr &h = b.reps[rep];
+  for (uint32_t st = 0; st < h.n_streams; st++) {
+    if (b.streams[h.streams + st].len) continue;
+    for (uint32_t k = threadIdx.x; k < h.n_syncs; k += 32)
+      b.ccounts[h.counts + (size_t)k * h.n_streams + st] = 0;
+    if (threadIdx.x == 0) b.clen[h.streams + st] = 0;
+  }
+}
+
 void launch_resolve(const DevBatch &b, cudaStream_t s) {
-  if (b.n_ops) resolve_kernel<<<(unsigned)((b.n_ops + 255) / 256), 256, 0, s>>>(b);
+  if (b.clen) {
+    if (b.n_chunks) {
+      const unsigned g = (b.n_chunks + FOLD_WARPS - 1) / FOLD_WARPS;
+      fold_count_kernel<<<g, FOLD_WARPS * 32, 0, s>>>(b);
+      fold_write_kernel<<<(unsigned)((b.n_chunks * 32ull + 127) / 128), 128, 0, s>>>(b);
+    }
+    if (b.n_reps) fold_empty_kernel<<<(b.n_reps + 7) / 8, dim3(32, 8), 0, s>>>(b);
+  } else if (b.n_ops) {
+    resolve_kernel<<<(unsigned)((b.n_ops + 255) / 256), 256, 0, s>>>(b);
+  }
   if (b.n_rcolls)
     resolve_colls_kernel<<<(unsigned)((b.n_rcolls + 255) / 256), 256, 0, s>>>(b);
 }

@@ -11,6 +11,8 @@ namespace maya {
 // ExecOp.w sentinels
 static const uint64_t EXEC_BAD = ~0ull << 2;             // KERN whose estimator failed
 static const uint64_t EXEC_NONE = ((~0ull) >> 2) << 2;   // WAIT on a never-recorded event
+static const uint64_t EXEC_OVF = EXEC_BAD - 4;           // folded kernel run whose composite
+                                                         // leaves int64 (the run's times do too)
 
 // Device view of one uploaded batch (all pointers into the device arena).
 struct DevBatch {
@@ -49,6 +51,11 @@ struct DevBatch {
   const LaneJob *lane_jobs;   // per job: lane-scheduler layout choice
   const uint32_t *lane_wslot; // per walker: ring slot word (soa.h)
   const uint32_t *lane_perm;  // per job: lane -> FIFO tables
+  const FoldChunk *chunks;    // fold work items (one per 1,024 ops of a FIFO)
+  uint32_t *chunk_cnt;        // folded ops per chunk
+  uint32_t n_chunks;
+  uint32_t *clen;             // folded FIFO lengths (fold_kernel) or null: unfolded ops
+  uint32_t *ccounts;          // host-sync dispatch counts in folded indices (with clen)
   int32_t *err_flag;          // any estimator failure
   uint32_t n_jobs, n_reps, n_feats, n_slots;
   uint64_t n_ops, n_rcolls;

@@ -586,9 +586,31 @@ namespace {
 // Job-level half of the packer: validation, rank classes, communicators, call
 // slots, simulated ranks, per-rank collective tables, walkers.  Reads only the
 // job tables of `job` (not its events); the reps are already in P.
+// Kernel features renumbered in stream-major first use: consecutive kernel ops
+// of a FIFO then read consecutive duration entries on the device (the fold
+// pass gathers one per op), which matters when features are mostly unique.
+void renumber_features(JobPack &P) {
+  const uint32_t nf = (uint32_t)P.feats.size();
+  if (nf < 2) return;
+  std::vector<uint32_t> nid(nf, UINT32_MAX);
+  uint32_t next = 0;
+  for (Op &o : P.ops) {
+    if (op_tag(o.meta) != TAG_KERN) continue;
+    uint32_t &m = nid[o.arg];
+    if (m == UINT32_MAX) m = next++;
+    o.arg = m;
+  }
+  for (uint32_t f = 0; f < nf; f++)
+    if (nid[f] == UINT32_MAX) nid[f] = next++;   // unused (cannot happen; keep total)
+  std::vector<Feature> nf2(nf);
+  for (uint32_t f = 0; f < nf; f++) nf2[nid[f]] = P.feats[f];
+  P.feats.swap(nf2);
+}
+
 void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
                const std::vector<uint32_t> &rep_comms) {
   JobHdr &H = P.hdr;
+  renumber_features(P);
     // validate rank tables
   for (int r = 0; r < job.num_ranks; r++) {
     int rep = job.rank_rep[r];

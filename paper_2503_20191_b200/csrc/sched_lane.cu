@@ -308,6 +308,7 @@ __device__ __forceinline__ int lane_step(const DevBatch &b, const LaneSh &sh, co
   int64_t done;
   if (tag == TAG_KERN) {
     if (wv == EXEC_BAD) { err = MAYA_ST_ESTIMATION; return ADV_IDLE; }
+    if (wv == EXEC_OVF) { err = MAYA_ST_OVERFLOW; return ADV_IDLE; }
     const int64_t d = (int64_t)pay;
     if (d > INT64_MAX - ready) { err = MAYA_ST_OVERFLOW; return ADV_IDLE; }
     done = ready + d;
@@ -422,7 +423,7 @@ __device__ bool lane_host_step(const DevBatch &b, const LaneSh &sh, uint32_t r) 
         if (s.arg == NO_REC) { s0 = s1 = 0; } else { s0 = s.arg; s1 = s.arg + 1; }
       }
       for (uint32_t ls = s0; ls < s1; ls++) {
-        const uint32_t cnt = b.counts[h.counts + s.cnt + ls];
+        const uint32_t cnt = (b.clen ? b.ccounts : b.counts)[h.counts + s.cnt + ls];
         if (cnt == 0) continue;
         const LSt &ws = sh.st[rr.walker + ls];
         if (ws.i < cnt) { ok = false; break; }
@@ -490,9 +491,9 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
     const StreamRange sr = b.streams[h.streams + wk.stream];
     LCtx c;
     c.ops = b.exec + h.ops + sr.begin;
-    c.cnt = b.counts + h.counts + wk.stream;
+    c.cnt = (b.clen ? b.ccounts : b.counts) + h.counts + wk.stream;
     c.tl = J.timeline + rr.tl + sr.begin;
-    c.len = sr.len;
+    c.len = b.clen ? b.clen[h.streams + wk.stream] : sr.len;
     c.rank = wk.rank;
     c.ns = h.n_streams;
     c.nsync = h.n_syncs;

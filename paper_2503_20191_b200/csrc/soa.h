@@ -150,6 +150,16 @@ __host__ __device__ inline LaneLayout lane_layout(uint32_t W, uint32_t R, uint32
   return L;
 }
 
+// One 1,024-op chunk of one FIFO for the run-folding pass (kernels.cu):
+// runs are cut at chunk starts, so chunks fold independently.
+static const uint32_t FOLD_CHUNK = 1024;
+struct FoldChunk {
+  uint32_t rep;        // batch rep index
+  uint32_t st;         // local stream
+  uint32_t chunk;      // chunk index within the FIFO
+  uint32_t first;      // batch chunk id of the FIFO's chunk 0
+};
+
 // 16-byte device op record.
 struct alignas(16) Op {
   int64_t disp;    // sum of host gaps before this op in host order (ns)

@@ -100,7 +100,8 @@ class Timeline:
 class Engine:
     """One engine per CUDA device (C ABI: maya_open ... maya_close)."""
 
-    def __init__(self, device: int = 0, collapse: bool = True, sched: str = "auto"):
+    def __init__(self, device: int = 0, collapse: bool = True, sched: str = "auto",
+                 fold: bool = True):
         L = lib()
         self._h = C.c_void_p()
         _check(L.maya_open(int(device), C.byref(self._h)))
@@ -108,6 +109,7 @@ class Engine:
             raise ValueError(f"sched must be 'auto', 'lane' or 'warp', not {sched!r}")
         self._collapse = bool(collapse)
         self._sched = sched
+        self._fold = bool(fold)
         self._apply_options()
         self.device = device
         self.batch: Batch | None = None
@@ -128,7 +130,7 @@ class Engine:
 
     def _apply_options(self) -> None:
         opts = ((1 if self._collapse else 0) | (2 if self._sched == "warp" else 0)
-                | (4 if self._sched == "lane" else 0))
+                | (4 if self._sched == "lane" else 0) | (0 if self._fold else 8))
         _check(lib().maya_set_options(self._h, opts))
 
     def collapsed(self) -> np.ndarray:
