@@ -83,7 +83,12 @@ def key_ranks(configs):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons around and during the timed region.
+
+    nvidia-smi runs from start() with a 10 ms period; a reader thread stamps
+    every line with the host clock, and stop(t0, t1) keeps the samples taken
+    inside [t0, t1].  A region shorter than the sampling period falls back to
+    the samples that bracket it (marked so)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -92,38 +97,53 @@ class ClockSampler:
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
-        self.path = None
+        self.rows = []
+        self.thread = None
 
     def start(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "--format=csv,noheader,nounits", "-lms", "10"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
         except OSError:
             self.proc = None
+            return
 
-    def stop(self) -> dict:
+        def reader():
+            for line in self.proc.stdout:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 9:
+                    self.rows.append((time.perf_counter(), p))
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        t_end = time.perf_counter() + 2.0   # wait for the first sample
+        while not self.rows and time.perf_counter() < t_end:
+            time.sleep(0.01)
+
+    def stop(self, t0: float, t1: float) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
         self.proc.terminate()
         self.proc.wait()
-        rows = []
-        for line in open(self.path):
-            p = [x.strip() for x in line.split(",")]
-            if len(p) >= 9:
-                rows.append(p)
-        os.unlink(self.path)
-        if not rows:
+        if self.thread:
+            self.thread.join(timeout=1.0)
+        inside = [p for t, p in self.rows if t0 <= t <= t1]
+        window = "timed region"
+        if not inside:
+            before = [p for t, p in self.rows if t < t0][-1:]
+            after = [p for t, p in self.rows if t > t1][:1]
+            inside = before + after
+            window = "samples bracketing the timed region (shorter than the 10 ms period)"
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        smax = max(float(r[2]) for r in rows)
+        sm = [float(r[1]) for r in inside if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in inside)
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        reasons = sorted({names[i] for r in inside for i in range(4) if r[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(inside), "window": window}
 
 
 def load_golden_c2():
@@ -355,6 +375,7 @@ def bench_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    t_region0 = time.perf_counter()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     sched_ms = []
@@ -369,8 +390,9 @@ def bench_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    t_region1 = time.perf_counter()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    clocks = sampler.stop()
+    clocks = sampler.stop(t_region0, t_region1)
     ms = sum(step_ms) / len(step_ms)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:

@@ -163,8 +163,18 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
   if (W > 16 * LANE_MAX_THREADS) return pl;
   const bool warp_job = W <= LANE_WARP_JOB_MAX_FIFOS;
   if (!warp_job) budget = LANE_SMEM_CAP;
-  std::vector<uint32_t> lens(W);
-  for (uint32_t w = 0; w < W; w++) lens[w] = lane_fifo_len(P, w);
+  std::vector<uint32_t> lens(W);   // ring sizing: the folded FIFO (what the kernel stages)
+  for (uint32_t w = 0; w < W; w++) {
+    const Walker wk = P.walkers[w];
+    const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
+    lens[w] = P.streams[h.streams + wk.stream].folded;
+  }
+  const uint32_t nthreads = warp_job ? 32u : [&] {
+    uint32_t nw = 2;
+    while (nw * 32 < W && nw * 32 < LANE_MAX_THREADS) nw <<= 1;
+    return nw * 32;
+  }();
+  const uint32_t ctxf = W > nthreads ? LANE_CTX_SMEM : 0u;
   // record-time cache when the table stays global: 8 live records per rank
   uint32_t fc = 0;
   while ((1u << fc) < 8 * R && fc < 12) fc++;
@@ -178,7 +188,7 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
       uint64_t slots = 0;
       for (uint32_t w = 0; w < W; w++) slots += lane_slots_of(lens[w], t.lgd);
       if (slots >= (1u << 28)) continue;
-      const uint32_t fl = ring | t.flags;
+      const uint32_t fl = ring | t.flags | ctxf;
       const LaneLayout L =
           lane_layout(W, R, nc, fl, (uint32_t)slots, P.hdr.n_fire, P.hdr.n_rcolls, fc);
       if (L.bytes > cap) continue;
@@ -642,7 +652,7 @@ int maya_upload(maya_engine *e) {
       for (size_t w = 0; w < P.walkers.size(); w++) {
         const Walker wk = P.walkers[w];
         const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
-        const uint32_t n = pl.variant >= 3 ? lane_slots_of(P.streams[h.streams + wk.stream].len,
+        const uint32_t n = pl.variant >= 3 ? lane_slots_of(P.streams[h.streams + wk.stream].folded,
                                                            pl.lgd_max)
                                            : 0;
         uint32_t lg = 0;

@@ -347,7 +347,22 @@ struct RepPacker {
     h.n_streams = (uint32_t)RB.sops.size();
     uint32_t pos = 0;
     for (size_t s = 0; s < RB.sops.size(); s++) {
-      P->streams.push_back(StreamRange{pos, (uint32_t)RB.sops[s].size(), RB.raw_of[s], 0});
+      // ops the scheduler sees after the device folds kernel runs (kernels.cu
+      // fold_count_kernel: same rule), for sizing its staging rings
+      uint32_t folded = 0;
+      {
+        bool pf = false;
+        uint32_t ps = 0;
+        const auto &v = RB.sops[s];
+        for (size_t i = 0; i < v.size(); i++) {
+          const bool f = op_tag(v[i].meta) == TAG_KERN && v[i].disp < ((int64_t)1 << 61);
+          const uint32_t sg = op_seg(v[i].meta);
+          folded += (i % FOLD_CHUNK == 0 || !f || !pf || sg != ps) ? 1u : 0u;
+          pf = f;
+          ps = sg;
+        }
+      }
+      P->streams.push_back(StreamRange{pos, (uint32_t)RB.sops[s].size(), RB.raw_of[s], folded});
       P->ops.insert(P->ops.end(), RB.sops[s].begin(), RB.sops[s].end());
       P->op_seq.insert(P->op_seq.end(), RB.sseq[s].begin(), RB.sseq[s].end());
       pos += (uint32_t)RB.sops[s].size();

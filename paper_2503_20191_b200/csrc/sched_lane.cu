@@ -120,6 +120,9 @@ enum : uint32_t {
 static_assert(sizeof(LSt) == 48, "LSt");
 
 enum { ADV_IDLE = 0, ADV_PROG = 1, ADV_DATA = 2 };
+#ifndef LANE_SUBSTEPS
+#define LANE_SUBSTEPS 1
+#endif
 
 #ifdef MAYA_PROFILE
 // [0] loop cycles [1] group steps [2] data-only steps [3] step cycles
@@ -252,7 +255,7 @@ __device__ __forceinline__ int lane_step(const DevBatch &b, const LaneSh &sh, co
   }
   longlong2 v;
   const bool ring = c.lgd != 0xffu;
-  if (ring && (s.i & SMASK) != 0 && !sh.record) {
+  if (ring && (s.i & SMASK) != 0 && !sh.record && !b.clen) {   // folded runs: no prelude
     // kernel prelude: up to 3 kernel ops of the staged chunk, operands < 2^61
     // (no sum can leave int64), before the one general op below
     constexpr int64_t LIM = (int64_t)1 << 61;
@@ -442,7 +445,7 @@ __device__ bool lane_host_step(const DevBatch &b, const LaneSh &sh, uint32_t r) 
 
 // Set up the job's shared-memory region (group-strided: tid in [0, nt)).
 __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_t tid,
-                           uint32_t nt, LaneSh &sh, int record) {
+                           uint32_t nt, LaneSh &sh, int record, LCtx &own) {
   const JobHdr &J = b.jobs[j];
   const LaneJob LJ = b.lane_jobs[j];
   const uint32_t W = J.n_walkers, R = J.n_ranks;
@@ -457,7 +460,7 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
     for (uint32_t q = tid; q < 2 * J.n_comms; q += nt) sh.ring[q] = CollSlot{0, 0, 0};
   sh.hostk = (uint32_t *)(base + L.hostk);
   sh.st = (LSt *)(base + L.state);
-  sh.ctx = (LCtx *)(base + L.ctx);
+  sh.ctx = (LJ.flags & LANE_CTX_SMEM) ? (LCtx *)(base + L.ctx) : nullptr;
   sh.bars = (uint64_t *)(base + L.bars);
   sh.rdata = (ExecOp *)(base + L.rdata);
   sh.fire_sm = (LJ.flags & LANE_FIRE_SMEM) != 0;
@@ -504,7 +507,8 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
     c.rc = rr.rslot;
     c.delay = rr.delay;
     c.pad = 0;
-    sh.ctx[w] = c;
+    if (sh.ctx) sh.ctx[w] = c;
+    if (w == tid) own = c;   // one FIFO per lane: the context stays in registers
     LSt s{};
     s.bound = c.nsync ? c.cnt[0] : c.len;
     sh.st[w] = s;
@@ -522,10 +526,11 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
 
 // Wait for every bulk copy still targeting the region (no copy may land in
 // shared memory after the job's CTA has exited); flag unfinished FIFOs.
-__device__ bool lane_drain(const LaneSh &sh, uint32_t W, uint32_t tid, uint32_t nt) {
+__device__ bool lane_drain(const LaneSh &sh, uint32_t W, uint32_t tid, uint32_t nt,
+                           const LCtx &own) {
   bool incomplete = false;
   for (uint32_t w = tid; w < W; w += nt) {
-    const LCtx c = sh.ctx[w];
+    const LCtx c = sh.ctx ? sh.ctx[w] : own;
     const LSt s = sh.st[w];
     if (s.i < c.len) incomplete = true;
     if (c.lgd == 0xffu) continue;
@@ -572,10 +577,19 @@ __device__ __forceinline__ void fifos_step(const DevBatch &b, const LaneSh &sh, 
                                            uint32_t nt, LaneFifos &f, int64_t &tmax, int &err,
                                            bool &prog, bool &data, bool full) {
   if (f.one) {
-    if (!f.valid) return;
-    const int a = lane_step(b, sh, f.c, f.s, tmax, err, full, sh.rcx_sm ? nullptr : &f.pf);
-    prog |= a == ADV_PROG;
-    data |= a == ADV_DATA;
+    // LANE_SUBSTEPS lockstep sub-steps per group step: a hand-off between
+    // FIFOs of the warp (record -> wait, last collective arrival) resolves
+    // within one step; the __syncwarp orders the sub-steps' shared-memory
+    // accesses across lanes
+#pragma unroll 1
+    for (int m = 0; m < LANE_SUBSTEPS; m++) {
+      int a = ADV_IDLE;
+      if (f.valid) a = lane_step(b, sh, f.c, f.s, tmax, err, full && m == 0,
+                                 sh.rcx_sm ? nullptr : &f.pf);
+      prog |= a == ADV_PROG;
+      data |= a == ADV_DATA;
+      __syncwarp();
+    }
     return;
   }
   for (uint32_t k = 0; k < sh.K; k++) {
@@ -664,14 +678,15 @@ __device__ __forceinline__ int64_t warp_max64(int64_t v) {
   return v;
 }
 
-__device__ __forceinline__ void fifos_init(const LaneSh &sh, uint32_t tid, LaneFifos &f) {
+__device__ __forceinline__ void fifos_init(const LaneSh &sh, uint32_t tid, LaneFifos &f,
+                                           const LCtx &own) {
   f.one = sh.K == 1;
   f.valid = false;
   f.pf.key = 0xffffffffu;
   if (f.one) {
-    const uint32_t w = sh.perm[tid];
+    const uint32_t w = sh.perm[tid];   // == tid (identity table when K == 1)
     f.valid = w != 0xffffffffu;
-    if (f.valid) f.c = sh.ctx[w];
+    if (f.valid) f.c = own;
   }
 }
 
@@ -680,7 +695,10 @@ __device__ __forceinline__ void fifos_init(const LaneSh &sh, uint32_t tid, LaneF
 // ---------------------------------------------------------------------------
 // warp jobs: CTA = blockDim/32 independent jobs, one shared-memory region each
 
-__global__ void __launch_bounds__(256) sched_lane_warp_kernel(DevBatch b, const int32_t *order,
+#ifndef LANE_WARP_MINB
+#define LANE_WARP_MINB 2
+#endif
+__global__ void __launch_bounds__(256, LANE_WARP_MINB) sched_lane_warp_kernel(DevBatch b, const int32_t *order,
                                                               uint32_t n_jobs, uint32_t region,
                                                               int record) {
   extern __shared__ __align__(128) uint8_t dsm[];
@@ -698,10 +716,11 @@ __global__ void __launch_bounds__(256) sched_lane_warp_kernel(DevBatch b, const 
 #ifdef MAYA_PROFILE
   const long long tstart = clock64();
 #endif
-  lane_setup(b, j, dsm + wp * region, lane, 32, sh, record);
+  LCtx own{};
+  lane_setup(b, j, dsm + wp * region, lane, 32, sh, record, own);
   __syncwarp();
   LaneFifos f;
-  fifos_init(sh, lane, f);
+  fifos_init(sh, lane, f, own);
   const uint32_t R = J.n_ranks;
   int64_t tmax = 0;
   int err = 0;
@@ -749,7 +768,7 @@ __global__ void __launch_bounds__(256) sched_lane_warp_kernel(DevBatch b, const 
 #ifdef MAYA_PROFILE
   if (lane == 0) atomicAdd(&g_lprof[0], (unsigned long long)(clock64() - tstart));
 #endif
-  bool incomplete = lane_drain(sh, J.n_walkers, lane, 32);
+  bool incomplete = lane_drain(sh, J.n_walkers, lane, 32, own);
   __syncwarp();
   EpiVals v{tmax, INT64_MAX, 0, INT32_MAX, incomplete};
   epi_ranks(b, sh, lane, 32, v);
@@ -788,7 +807,8 @@ __global__ void __launch_bounds__(LANE_MAX_THREADS, 1)
     return;
   }
   LaneSh sh;
-  lane_setup(b, j, dsm, tid, nt, sh, record);
+  LCtx own{};
+  lane_setup(b, j, dsm, tid, nt, sh, record, own);
   if (tid == 0) {
     s_tmax = 0;
     s_err = 0;
@@ -799,7 +819,7 @@ __global__ void __launch_bounds__(LANE_MAX_THREADS, 1)
   }
   __syncthreads();
   LaneFifos f;
-  fifos_init(sh, tid, f);
+  fifos_init(sh, tid, f, own);
   const uint32_t R = J.n_ranks;
   int64_t tmax = 0;
   int err = 0;
@@ -845,7 +865,7 @@ __global__ void __launch_bounds__(LANE_MAX_THREADS, 1)
     if (vld(&s_err) != 0) progress = 0;
     if (!__syncthreads_or(progress)) break;
   }
-  if (lane_drain(sh, J.n_walkers, tid, nt)) s_incomplete = 1;
+  if (lane_drain(sh, J.n_walkers, tid, nt, own)) s_incomplete = 1;
   EpiVals v{tmax, INT64_MAX, 0, INT32_MAX, false};
   epi_ranks(b, sh, tid, nt, v);
   if (v.incomplete) s_incomplete = 1;

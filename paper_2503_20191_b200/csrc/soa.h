@@ -106,6 +106,7 @@ enum LaneFlags : uint32_t {
   LANE_COLL_RING = 1,   // collectives rendezvous in shared-memory rings
   LANE_FIRE_SMEM = 2,   // record times in shared memory
   LANE_RCX_SMEM = 4,    // per-rank collective table in shared memory
+  LANE_CTX_SMEM = 8,    // FIFO contexts in shared memory (lanes own several FIFOs)
 };
 struct LaneJob {
   uint32_t flags;       // LaneFlags
@@ -135,7 +136,7 @@ __host__ __device__ inline LaneLayout lane_layout(uint32_t W, uint32_t R, uint32
   L.state = (uint32_t)off;
   off += 48ull * W;
   L.ctx = (uint32_t)off;
-  off += 64ull * W;
+  if (flags & LANE_CTX_SMEM) off += 64ull * W;
   L.bars = (uint32_t)off;
   off = (off + 8ull * n_slots + 127) & ~127ull;
   L.rdata = (uint32_t)off;
@@ -175,7 +176,7 @@ struct StreamRange {
   uint32_t begin;  // rep-local op index
   uint32_t len;
   int32_t raw;     // stream handle in the trace
-  uint32_t pad;
+  uint32_t folded; // ops after the device folds kernel runs (ring sizing)
 };
 
 struct SyncRec {
