@@ -96,6 +96,27 @@ def test_evaluate_space_topk_is_reference_ranking():
     assert got == ranked[:8]
 
 
+@gpu
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_gen_pipeline_matches_reference(chunks):
+    """api.GenPipeline (the bench's e2e path): results in config order and the
+    merged top-k equal the reference's C2 results and _rank order."""
+    from paper_2503_20191_b200.api import GenPipeline
+    W, model, cluster = _c2()
+    gold = json.load(open(os.path.join(GOLDEN, "c2_results.json")))
+    cfgs = W.enumerate_space(W.SearchSpace(global_batch=512), model, cluster)[:512]
+    pipe = GenPipeline(0, chunks=chunks)
+    res, top, st = pipe.evaluate(model, cfgs, cluster, k=8, dispatch_overhead_ns=5000)
+    pipe.close()
+    assert (st == 0).all()
+    for r, g in zip(res, gold):
+        assert (int(r["total_ns"]), int(r["peak_mem_bytes"]), bool(r["oom"])) == \
+            (g["total_ns"], g["peak_mem_bytes"], g["oom"])
+    ok = sorted((g for g in gold if not g["oom"]), key=lambda g: (g["total_ns"], tuple(g["key"])))
+    assert [(int(t[0]), tuple(cfgs[int(t[2])].key())) for t in top] == \
+        [(g["total_ns"], tuple(g["key"])) for g in ok[:8]]
+
+
 @pytest.mark.parametrize("name", ["unit", "multirank", "workload"])
 def test_refmirror_round_trip(golden, name):
     """Host-only: the mirror objects flatten back to the same raw job."""
