@@ -679,7 +679,8 @@ int maya_upload(maya_engine *e) {
 #undef CPY
   };
   {
-    int nt = (int)std::min<size_t>(8, std::max<size_t>(1, nj / 64));
+    int nt = (int)std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()),
+                                   std::max<size_t>(1, nj / 16));
     std::atomic<size_t> next(0);
     auto work = [&]() {
       for (;;) {

@@ -44,12 +44,28 @@ struct Fail {
 
 inline bool add_overflows(int64_t a, int64_t b) { return b > 0 && a > INT64_MAX - b; }
 
+// Per-stream op lists of one rep.  Reused across reps by a thread's packer:
+// reset() keeps every list's capacity (no regrowth per rep).
 struct RepBuild {
   std::vector<int32_t> raw_of;                 // local stream -> raw handle
-  std::vector<std::vector<Op>> sops;           // per local stream
+  std::vector<std::vector<Op>> sops;           // per local stream (first n_live used)
   std::vector<std::vector<uint32_t>> sseq;
+  size_t n_live = 0;
   int last_raw = INT32_MIN, last_local = -1;
   size_t reserve_hint = 0;
+
+  void reset(size_t hint) {
+    raw_of.clear();
+    for (size_t i = 0; i < n_live; i++) {
+      sops[i].clear();
+      sseq[i].clear();
+    }
+    n_live = 0;
+    last_raw = INT32_MIN;
+    last_local = -1;
+    reserve_hint = hint;
+  }
+  size_t size() const { return n_live; }
 
   int local_stream(int32_t raw, bool create) {
     if (raw == last_raw) return last_local;
@@ -57,11 +73,14 @@ struct RepBuild {
       if (raw_of[i] == raw) { last_raw = raw; last_local = (int)i; return (int)i; }
     if (!create) return -1;
     raw_of.push_back(raw);
-    sops.emplace_back();
-    sseq.emplace_back();
-    if (sops.size() == 1) {   // the first stream is usually the compute stream
-      sops.back().reserve(reserve_hint);
-      sseq.back().reserve(reserve_hint);
+    if (n_live == sops.size()) {
+      sops.emplace_back();
+      sseq.emplace_back();
+    }
+    n_live++;
+    if (n_live == 1 && sops[0].capacity() < reserve_hint) {   // usually the compute stream
+      sops[0].reserve(reserve_hint);
+      sseq[0].reserve(reserve_hint);
     }
     last_raw = raw;
     last_local = (int)raw_of.size() - 1;
@@ -125,8 +144,7 @@ struct RepPacker {
     device = dev;
     h = RepHdr{};
     h.job = 0;
-    RB = RepBuild();
-    RB.reserve_hint = reserve_hint;
+    RB.reset(reserve_hint);
     fly = on_the_fly;
     rec.clear();
     rec_small.clear();
@@ -192,7 +210,7 @@ struct RepPacker {
     RB.sseq[ls].push_back(seq);
   }
   void sync(uint32_t type, uint32_t arg) {
-    std::vector<uint32_t> c(RB.sops.size());
+    std::vector<uint32_t> c(RB.size());
     for (size_t s = 0; s < c.size(); s++) c[s] = (uint32_t)RB.sops[s].size();
     snap.push_back(std::move(c));
     P->syncs.push_back(SyncRec{gpre, type, arg, 0, 0});
@@ -331,8 +349,8 @@ struct RepPacker {
       const uint32_t nc = (uint32_t)(P->coll_lc.size() - coll0);
       std::vector<uint32_t> lc(nc), ix(nc);
       uint32_t next = 0;
-      for (auto &ops : RB.sops)
-        for (Op &o : ops)
+      for (size_t si = 0; si < RB.size(); si++)
+        for (Op &o : RB.sops[si])
           if (op_tag(o.meta) == TAG_COLL) {
             lc[next] = P->coll_lc[coll0 + o.arg];
             ix[next] = P->coll_idx[coll0 + o.arg];
@@ -344,9 +362,9 @@ struct RepPacker {
     // stream-major op layout
     h.ops = P->ops.size();
     h.streams = P->streams.size();
-    h.n_streams = (uint32_t)RB.sops.size();
+    h.n_streams = (uint32_t)RB.size();
     uint32_t pos = 0;
-    for (size_t s = 0; s < RB.sops.size(); s++) {
+    for (size_t s = 0; s < RB.size(); s++) {
       // ops the scheduler sees after the device folds kernel runs (kernels.cu
       // fold_count_kernel: same rule), for sizing its staging rings
       uint32_t folded = 0;
