@@ -325,6 +325,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
   const uint32_t hk = sh.hostk[c.rank];
   const uint32_t limit = hk < c.nsync ? c.cnt[hk * c.ns] : c.len;
   bool adv = false;
+  bool streaming = false;   // the last window committed 32 ops: try 128-op windows
   s.wk = WAKE_ROUND;   // until something else is known: wait for the next round
   while (s.i < limit) {
     PROF_T(t_win);
@@ -343,7 +344,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
     // the next 2 KB of this FIFO into L1 while this window computes (one line per lane)
     if (lane < 16 && s.i + 128u + lane * 8u < c.len)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(c.ops + s.i + 128u + lane * 8u));
-    if (end - s.i >= 128u && s.x < LIM_T) {
+    if (streaming && end - s.i >= 128u && s.x < LIM_T) {
       int64_t A4[4], B4[4], rd4[4];
       uint32_t rec4 = 0;
       bool blk = false;
@@ -427,6 +428,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
         s.wk = WAKE_ROUND;
         continue;
       }
+      streaming = false;
     }
     const uint32_t n = min(32u, end - s.i);
     const bool valid = lane < n;
@@ -657,6 +659,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
 #ifdef MAYA_PROFILE
     if (lane == 0) PROF_ADD(7, commit);
 #endif
+    streaming = !blocked && commit == 32u;
     if (commit > 0) {
       s.x = __shfl_sync(FULL, d, commit - 1);
       s.i += commit;
