@@ -95,7 +95,7 @@ struct maya_engine {
   Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_slots, s_walkers, s_reps, s_ops, s_streams,
       s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
       s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks;
-  Seg x_clen, x_ccounts, x_chunk_cnt;
+  Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst;
   Seg x_exec, x_rcw, x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
       x_results, x_err, x_topk, x_topk_out, x_topk_n;
   uint64_t n_tl = 0;
@@ -174,7 +174,10 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
     while (nw * 32 < W && nw * 32 < LANE_MAX_THREADS) nw <<= 1;
     return nw * 32;
   }();
-  const uint32_t ctxf = W > nthreads ? LANE_CTX_SMEM : 0u;
+  const bool multi = W > nthreads;   // lanes own several FIFOs
+  // FIFO contexts / states: shared memory first, global memory when the job's
+  // FIFOs do not fit (thousands of ranks)
+  const uint32_t place[3] = {multi ? LANE_CTX_SMEM : 0u, 0u, LANE_ST_GLOBAL};
   // record-time cache when the table stays global: 8 live records per rank
   uint32_t fc = 0;
   while ((1u << fc) < 8 * R && fc < 12) fc++;
@@ -184,6 +187,9 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
                        {1, LANE_FIRE_SMEM}, {1, 0}, {0xff, LANE_FIRE_SMEM}, {0xff, 0}};
   for (int pass = 0; pass < 2; pass++) {
     const uint32_t cap = pass == 0 ? budget : LANE_SMEM_CAP;
+    for (uint32_t pc = 0; pc < 3; pc++) {
+    if (pc > 0 && !multi) break;
+    const uint32_t ctxf = place[pc];
     for (const Try &t : tries) {
       uint64_t slots = 0;
       for (uint32_t w = 0; w < W; w++) slots += lane_slots_of(lens[w], t.lgd);
@@ -211,6 +217,7 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
       pl.per_lane = (W + pl.threads - 1) / pl.threads;
       if (pl.per_lane == 0) pl.per_lane = 1;
       return pl;
+    }
     }
   }
   return pl;
@@ -467,6 +474,8 @@ int maya_upload(maya_engine *e) {
   seg(e->x_exec, n_ops * sizeof(ExecOp));
   seg(e->x_clen, n_streams * sizeof(uint32_t));
   seg(e->x_chunk_cnt, n_chunks * sizeof(uint32_t));
+  seg(e->x_lctx, n_walkers * 64);
+  seg(e->x_lst, n_walkers * 48);
   seg(e->x_ccounts, n_counts * sizeof(uint32_t));
   seg(e->x_rcw, n_rcolls * sizeof(RCX));
   seg(e->x_feat_ns, n_feats * 8);
@@ -798,6 +807,8 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   // runs fold (fold_kernel) unless a per-op timeline is recorded
   const bool fold = !record_timeline && !(e->options & MAYA_OPT_NO_FOLD);
   db.clen = fold ? (uint32_t *)(X + e->x_clen.off) : nullptr;
+  db.lane_gctx = (uint8_t *)(X + e->x_lctx.off);
+  db.lane_gst = (uint8_t *)(X + e->x_lst.off);
   db.chunk_cnt = (uint32_t *)(X + e->x_chunk_cnt.off);
   db.ccounts = fold ? (uint32_t *)(X + e->x_ccounts.off) : nullptr;
   CU(cudaEventRecord(e->ev[0], e->stream));

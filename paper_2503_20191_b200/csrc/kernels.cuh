@@ -51,6 +51,8 @@ struct DevBatch {
   const LaneJob *lane_jobs;   // per job: lane-scheduler layout choice
   const uint32_t *lane_wslot; // per walker: ring slot word (soa.h)
   const uint32_t *lane_perm;  // per job: lane -> FIFO tables
+  uint8_t *lane_gctx;         // per walker: 64 B FIFO context when not in shared memory
+  uint8_t *lane_gst;          // per walker: 48 B FIFO state when LANE_ST_GLOBAL
   const FoldChunk *chunks;    // fold work items (one per 1,024 ops of a FIFO)
   uint32_t *chunk_cnt;        // folded ops per chunk
   uint32_t n_chunks;

@@ -459,8 +459,13 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
   if (sh.ring)
     for (uint32_t q = tid; q < 2 * J.n_comms; q += nt) sh.ring[q] = CollSlot{0, 0, 0};
   sh.hostk = (uint32_t *)(base + L.hostk);
-  sh.st = (LSt *)(base + L.state);
-  sh.ctx = (LJ.flags & LANE_CTX_SMEM) ? (LCtx *)(base + L.ctx) : nullptr;
+  sh.st = (LJ.flags & LANE_ST_GLOBAL) ? (LSt *)(b.lane_gst + (size_t)J.walkers * 48)
+                                      : (LSt *)(base + L.state);
+  // several FIFOs per lane: contexts in shared memory, else in global memory
+  // (one FIFO per lane keeps its context in registers)
+  sh.ctx = (LJ.flags & LANE_CTX_SMEM) ? (LCtx *)(base + L.ctx)
+           : LJ.per_lane > 1          ? (LCtx *)(b.lane_gctx + (size_t)J.walkers * 64)
+                                      : nullptr;
   sh.bars = (uint64_t *)(base + L.bars);
   sh.rdata = (ExecOp *)(base + L.rdata);
   sh.fire_sm = (LJ.flags & LANE_FIRE_SMEM) != 0;

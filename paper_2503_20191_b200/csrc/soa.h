@@ -107,6 +107,7 @@ enum LaneFlags : uint32_t {
   LANE_FIRE_SMEM = 2,   // record times in shared memory
   LANE_RCX_SMEM = 4,    // per-rank collective table in shared memory
   LANE_CTX_SMEM = 8,    // FIFO contexts in shared memory (lanes own several FIFOs)
+  LANE_ST_GLOBAL = 16,  // FIFO states in global memory (jobs with thousands of FIFOs)
 };
 struct LaneJob {
   uint32_t flags;       // LaneFlags
@@ -134,7 +135,7 @@ __host__ __device__ inline LaneLayout lane_layout(uint32_t W, uint32_t R, uint32
   L.hostk = (uint32_t)off;
   off = (off + 4ull * R + 15) & ~15ull;
   L.state = (uint32_t)off;
-  off += 48ull * W;
+  if (!(flags & LANE_ST_GLOBAL)) off += 48ull * W;
   L.ctx = (uint32_t)off;
   if (flags & LANE_CTX_SMEM) off += 64ull * W;
   L.bars = (uint32_t)off;
