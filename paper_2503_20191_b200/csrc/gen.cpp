@@ -639,32 +639,55 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
     }
     G.rank_rep.resize(n);
     for (int64_t r = 0; r < n; r++) G.rank_rep[r] = (int32_t)(r / (C.t * C.d));
-    // communicators: every role of every rank (collate.py:297-322)
+    // communicators: every role of every rank (collate.py:297-322).  Roles are
+    // keyed by integers; each communicator's name is built once (the global
+    // comm order is the reference's: sorted by name)
+    auto role_key = [](const CommRole &r) -> uint64_t {
+      return ((uint64_t)r.type << 60) | ((uint64_t)r.a << 40) | ((uint64_t)r.b << 20) |
+             (uint64_t)r.c;
+    };
     struct CInfo {
       CommRole role;
       int32_t stage_of_first;  // stage of position-0 rank
       int32_t lc_of_first;     // local comm index of the role in that rank's rep
     };
-    std::unordered_map<std::string, CInfo> comms;
-    std::vector<std::vector<std::string>> names_by_rank(n);
+    std::unordered_map<uint64_t, int32_t> idx_of;   // role key -> comm (discovery order)
+    std::vector<CInfo> infos;
+    std::vector<uint64_t> keys_by_rank;            // per rank, per local comm
+    std::vector<int64_t> rk_off(n + 1, 0);
     for (int64_t r = 0; r < n; r++) {
-      std::vector<CommRole> roles = worker_comms(C, cfg.virtual_stages, r);
+      const std::vector<CommRole> roles = worker_comms(C, cfg.virtual_stages, r);
       for (size_t q = 0; q < roles.size(); q++) {
-        std::string nm = comm_name(roles[q]);
-        names_by_rank[r].push_back(nm);
-        if (roles[q].my_rank == 0 && !comms.count(nm))
-          comms.emplace(nm, CInfo{roles[q], (int32_t)(r / (C.t * C.d)), (int32_t)q});
+        const uint64_t key = role_key(roles[q]);
+        keys_by_rank.push_back(key);
+        auto it = idx_of.find(key);
+        if (it == idx_of.end()) {
+          idx_of.emplace(key, (int32_t)infos.size());
+          infos.push_back(CInfo{roles[q], -1, -1});
+          it = idx_of.find(key);
+        }
+        CInfo &ci = infos[it->second];
+        if (roles[q].my_rank == 0 && ci.stage_of_first < 0) {
+          ci.role = roles[q];
+          ci.stage_of_first = (int32_t)(r / (C.t * C.d));
+          ci.lc_of_first = (int32_t)q;
+        }
       }
+      rk_off[r + 1] = (int64_t)keys_by_rank.size();
     }
-    std::vector<std::string> names;
-    names.reserve(comms.size());
-    for (auto &kv : comms) names.push_back(kv.first);
-    std::sort(names.begin(), names.end());
-    std::unordered_map<std::string, int32_t> gid;
+    std::vector<std::string> names(infos.size());
+    for (size_t g = 0; g < infos.size(); g++) names[g] = comm_name(infos[g].role);
+    std::vector<int32_t> order(infos.size());
+    for (size_t g = 0; g < order.size(); g++) order[g] = (int32_t)g;
+    std::sort(order.begin(), order.end(),
+              [&](int32_t x, int32_t y) { return names[x] < names[y]; });
+    std::vector<int32_t> gid_of(infos.size());
     G.call_off.push_back(0);
-    for (size_t g = 0; g < names.size(); g++) {
-      gid[names[g]] = (int32_t)g;
-      const CInfo &ci = comms[names[g]];
+    for (size_t gi = 0; gi < order.size(); gi++) {
+      const int32_t g0 = order[gi];
+      gid_of[g0] = (int32_t)gi;
+      const CInfo &ci = infos[g0];
+      if (ci.stage_of_first < 0) throw GenFail{"communicator without a position-0 member"};
       std::vector<int64_t> mem = comm_members(C, ci.role);
       std::vector<int64_t> hosts;
       for (int64_t r : mem) hosts.push_back(r / cl.devices_per_host);
@@ -672,7 +695,7 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
       std::sort(uh.begin(), uh.end());
       uh.erase(std::unique(uh.begin(), uh.end()), uh.end());
       int8_t topo = uh.size() == 1 ? 0 : (uh.size() == hosts.size() ? 1 : 2);
-      G.comm_names.push_back(names[g]);
+      G.comm_names.push_back(names[g0]);
       G.comm_nranks.push_back(ci.role.nranks);
       G.comm_topo.push_back(topo);
       const auto &cl2 = rcalls[ci.stage_of_first].calls[ci.lc_of_first];
@@ -681,12 +704,13 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
         G.call_bytes.push_back(kb.second);
       }
       G.call_off.push_back((int64_t)G.call_kind.size());
-      G.comm_blob += names[g];
+      G.comm_blob += names[g0];
       G.comm_blob += '\n';
     }
     G.rank_comm_off.push_back(0);
     for (int64_t r = 0; r < n; r++) {
-      for (const std::string &nm : names_by_rank[r]) G.rank_comm.push_back(gid.at(nm));
+      for (int64_t q = rk_off[r]; q < rk_off[r + 1]; q++)
+        G.rank_comm.push_back(gid_of[idx_of.at(keys_by_rank[q])]);
       G.rank_comm_off.push_back((int64_t)G.rank_comm.size());
     }
   } catch (const GenFail &f) {
