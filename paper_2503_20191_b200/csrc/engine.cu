@@ -69,7 +69,7 @@ struct maya_engine {
   // scheduler launch groups: 0-2 warp-window kernel (4/8/16 warps), 3-10 lane
   // kernel warp jobs (by shared-memory region class), 11-14 lane kernel CTA
   // jobs (2/4/8/16 warps); each group runs on its own stream (fork/join)
-  static const int NVAR = 15;
+  static const int NVAR = 16;   // 15: grid jobs (cooperative launch over their parts)
   cudaStream_t vstream[NVAR] = {};
   cudaEvent_t vev[NVAR + 1] = {};
   uint32_t var_n[NVAR] = {};        // jobs per group (order segments)
@@ -94,8 +94,11 @@ struct maya_engine {
   // segments
   Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_slots, s_walkers, s_reps, s_ops, s_streams,
       s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
-      s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks;
-  Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst;
+      s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks, s_grid_parts;
+  Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst, x_gsync;
+  std::vector<GridPart> grid_parts;        // host copy (launch grouping)
+  std::vector<std::pair<uint32_t, uint32_t>> grid_launches;   // part ranges per launch
+  uint32_t grid_smem = 0;
   Seg x_exec, x_rcw, x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
       x_results, x_err, x_topk, x_topk_out, x_topk_n;
   uint64_t n_tl = 0;
@@ -122,6 +125,7 @@ static const uint32_t LANE_WARP_JOB_MAX_FIFOS = 128;   // 4 FIFOs per lane
 struct LanePlan {
   int variant = -1;
   uint32_t flags = 0, n_slots = 0, smem = 0, lgd_max = 0, threads = 32, per_lane = 1, fc_log2 = 0;
+  std::vector<GridPart> parts;   // variant 15: the job's CTAs (job/wslot/first filled at upload)
 };
 
 uint32_t lane_slots_of(uint32_t len, uint32_t lgd_max) {
@@ -136,6 +140,68 @@ uint32_t lane_fifo_len(const JobPack &P, uint32_t w) {
   const Walker wk = P.walkers[w];
   const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
   return P.streams[h.streams + wk.stream].len;
+}
+
+static const uint32_t GRID_PART_FIFOS = 256;   // one FIFO per thread of a grid-job CTA
+
+// A job with more FIFOs than a CTA has threads runs as a grid job: rank-aligned
+// parts of <= 256 FIFOs, one CTA each, rings sized by folded FIFO length.
+bool plan_grid(const JobPack &P, LanePlan &pl) {
+  const uint32_t W = (uint32_t)P.walkers.size(), R = (uint32_t)P.ranks.size();
+  const uint32_t nc = (uint32_t)P.comms.size();
+  std::vector<GridPart> parts;
+  uint32_t w = 0;
+  for (uint32_t r = 0; r < R;) {
+    GridPart g{};
+    g.r0 = r;
+    g.w0 = w;
+    while (r < R) {
+      const uint32_t ns = P.reps[P.ranks[r].rep].n_streams;
+      if (w + ns - g.w0 > GRID_PART_FIFOS && r > g.r0) break;
+      w += ns;
+      r++;
+    }
+    g.r1 = r;
+    g.w1 = w;
+    parts.push_back(g);
+  }
+  if (w != W) return false;
+  uint32_t smem_max = 0;
+  for (GridPart &g : parts) {
+    uint32_t fc = 0;
+    while ((1u << fc) < 8 * (g.r1 - g.r0) && fc < 12) fc++;
+    bool ok = false;
+    for (uint32_t lgd : {2u, 1u, 0xffu}) {
+      uint64_t slots = 0;
+      for (uint32_t q = g.w0; q < g.w1; q++) {
+        const Walker wk = P.walkers[q];
+        const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
+        slots += lane_slots_of(P.streams[h.streams + wk.stream].folded, lgd);
+      }
+      const LaneLayout L = lane_layout(g.w1 - g.w0, g.r1 - g.r0, nc, 0, (uint32_t)slots,
+                                       P.hdr.n_fire, P.hdr.n_rcolls, fc);
+      if (L.bytes > LANE_SMEM_CAP) continue;
+      g.flags = 0;
+      g.n_slots = (uint32_t)slots;
+      g.fc_log2 = fc;
+      g.wslot = lgd;   // ring depth, replaced by the batch index at upload
+      smem_max = std::max(smem_max, L.bytes);
+      ok = true;
+      break;
+    }
+    if (!ok) return false;
+  }
+  for (GridPart &g : parts) {
+    g.part = (uint32_t)(&g - parts.data());
+    g.n_parts = (uint32_t)parts.size();
+    g.warps_total = (uint32_t)parts.size() * (GRID_PART_FIFOS / 32);
+  }
+  pl.variant = 15;
+  pl.parts = std::move(parts);
+  pl.smem = smem_max;
+  pl.threads = GRID_PART_FIFOS;
+  pl.per_lane = 1;
+  return true;
 }
 
 LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
@@ -160,7 +226,10 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
   }
   const uint32_t nc = (uint32_t)P.comms.size();
   const uint32_t ring = (P.hdr.flags & JOB_RING) && nc <= RING_MAX_COMMS ? LANE_COLL_RING : 0;
-  if (W > 16 * LANE_MAX_THREADS) return pl;
+  if (W > LANE_MAX_THREADS) {   // a grid job: several co-resident CTAs
+    if (!plan_grid(P, pl)) pl = LanePlan();
+    return pl;
+  }
   const bool warp_job = W <= LANE_WARP_JOB_MAX_FIFOS;
   if (!warp_job) budget = LANE_SMEM_CAP;
   std::vector<uint32_t> lens(W);   // ring sizing: the folded FIFO (what the kernel stages)
@@ -431,7 +500,8 @@ int maya_upload(maya_engine *e) {
     for (size_t j = 0; j < nj; j++) {
       if (!(e->options & MAYA_OPT_WARP_SCHED))
         plans[j] = plan_lane(e->packs[j], (uint32_t)budget, (e->options & MAYA_OPT_LANE_SCHED) != 0);
-      if (plans[j].variant >= 0) n_perm += (size_t)plans[j].per_lane * plans[j].threads;
+      if (plans[j].variant >= 0 && plans[j].variant != 15)
+        n_perm += (size_t)plans[j].per_lane * plans[j].threads;
     }
   }
   if (n_reps > 0xffffffffull) return fail(MAYA_EINVAL, "too many representatives in batch");
@@ -468,6 +538,9 @@ int maya_upload(maya_engine *e) {
   seg(e->s_lane_wslot, n_walkers * sizeof(uint32_t));
   seg(e->s_lane_perm, n_perm * sizeof(uint32_t));
   seg(e->s_chunks, n_chunks * sizeof(FoldChunk));
+  size_t n_parts = 0;
+  for (size_t j = 0; j < nj; j++) n_parts += plans[j].parts.size();
+  seg(e->s_grid_parts, n_parts * sizeof(GridPart));
   e->arena_bytes = off;
   // scratch layout
   off = 0;
@@ -476,6 +549,7 @@ int maya_upload(maya_engine *e) {
   seg(e->x_chunk_cnt, n_chunks * sizeof(uint32_t));
   seg(e->x_lctx, n_walkers * 64);
   seg(e->x_lst, n_walkers * 48);
+  seg(e->x_gsync, nj * sizeof(GridSync));
   seg(e->x_ccounts, n_counts * sizeof(uint32_t));
   seg(e->x_rcw, n_rcolls * sizeof(RCX));
   seg(e->x_feat_ns, n_feats * 8);
@@ -534,7 +608,7 @@ int maya_upload(maya_engine *e) {
     for (int v = 0; v < maya_engine::NVAR; v++) e->var_n[v] = e->var_smem[v] = 0;
     for (size_t j = 0; j < nj; j++) {
       e->var_n[var[j]]++;
-      if (var[j] >= 3) {
+      if (var[j] >= 3) {   // lane kernels (15: grid jobs, smem per part)
         const uint32_t need = (plans[j].smem + 127u) & ~127u;
         if (need > e->var_smem[var[j]]) e->var_smem[var[j]] = need;
         continue;
@@ -574,7 +648,8 @@ int maya_upload(maya_engine *e) {
       b.fire += P.n_fire;
       b.delay += P.n_delay;
       b.rcolls += P.rcolls.size();
-      if (plans[j].variant >= 0) b.perm += (size_t)plans[j].per_lane * plans[j].threads;
+      if (plans[j].variant >= 0 && plans[j].variant != 15)
+        b.perm += (size_t)plans[j].per_lane * plans[j].threads;
       const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
                                          (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0,
                                          P.hdr.n_fire, P.hdr.n_rcolls, sched_smem_cap());
@@ -598,6 +673,38 @@ int maya_upload(maya_engine *e) {
     }
   }
   if (n_chunks >= 0xffffffffull) return fail(MAYA_EINVAL, "too many fold chunks in batch");
+  {  // grid jobs: their parts, grouped into cooperative launches that fit co-resident
+    e->grid_parts.clear();
+    e->grid_launches.clear();
+    e->grid_smem = e->var_smem[15];
+    for (size_t j = 0; j < nj; j++) {
+      if (plans[j].variant != 15) continue;
+      const uint32_t first = (uint32_t)e->grid_parts.size();
+      for (GridPart g : plans[j].parts) {
+        g.job = (uint32_t)j;
+        g.first = first;
+        g.wslot = bases[j].walkers + g.w0;
+        e->grid_parts.push_back(g);
+      }
+    }
+    if (!e->grid_parts.empty()) {
+      const uint32_t cap = (uint32_t)std::max(1, grid_max_ctas(e->grid_smem));
+      uint32_t p = 0;
+      while (p < e->grid_parts.size()) {
+        uint32_t q = p;
+        while (q < e->grid_parts.size()) {
+          const uint32_t np = e->grid_parts[q].n_parts;
+          if (q + np - p > cap && q > p) break;
+          if (np > cap) return fail(MAYA_EINVAL, "grid job larger than the co-resident CTAs");
+          q += np;
+        }
+        e->grid_launches.push_back({p, q});
+        p = q;
+      }
+    }
+    if (!e->grid_parts.empty())
+      memcpy(H + e->s_grid_parts.off, e->grid_parts.data(), e->grid_parts.size() * sizeof(GridPart));
+  }
   auto copy_job = [&](size_t j) {
     const JobPack &P = e->packs[j];
     const Base &B = bases[j];
@@ -654,15 +761,22 @@ int maya_upload(maya_engine *e) {
       const LanePlan &pl = plans[j];
       LaneJob lj{pl.flags, pl.n_slots, B.walkers, B.perm, pl.per_lane, pl.fc_log2};
       memcpy(H + e->s_lane_jobs.off + j * sizeof(LaneJob), &lj, sizeof lj);
-      if (pl.variant >= 0 && P.hdr.status == MAYA_ST_OK)
+      if (pl.variant >= 0 && pl.variant != 15 && P.hdr.status == MAYA_ST_OK)
         lane_perm_fill(P, pl, (uint32_t *)(H + e->s_lane_perm.off) + B.perm);
       uint32_t *ws = (uint32_t *)(H + e->s_lane_wslot.off) + B.walkers;
       uint32_t slot = 0;
+      size_t part = 0;
       for (size_t w = 0; w < P.walkers.size(); w++) {
+        uint32_t lgd_max = pl.lgd_max;
+        if (pl.variant == 15) {   // grid job: ring slots are part-local
+          while (part + 1 < pl.parts.size() && w >= pl.parts[part + 1].w0) part++;
+          if (w == pl.parts[part].w0) slot = 0;
+          lgd_max = (uint32_t)pl.parts[part].wslot;
+        }
         const Walker wk = P.walkers[w];
         const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
         const uint32_t n = pl.variant >= 3 ? lane_slots_of(P.streams[h.streams + wk.stream].folded,
-                                                           pl.lgd_max)
+                                                           lgd_max)
                                            : 0;
         uint32_t lg = 0;
         while ((1u << lg) < n) lg++;
@@ -711,6 +825,7 @@ int maya_upload(maya_engine *e) {
   db.lane_wslot = (const uint32_t *)(D + e->s_lane_wslot.off);
   db.lane_perm = (const uint32_t *)(D + e->s_lane_perm.off);
   db.chunks = (const FoldChunk *)(D + e->s_chunks.off);
+  db.grid_parts = (const GridPart *)(D + e->s_grid_parts.off);
   db.n_chunks = (uint32_t)n_chunks;
   db.ranks = (const RankRec *)(D + e->s_ranks.off);
   db.rank_comm = (const uint32_t *)(D + e->s_rank_comm.off);
@@ -809,6 +924,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   db.clen = fold ? (uint32_t *)(X + e->x_clen.off) : nullptr;
   db.lane_gctx = (uint8_t *)(X + e->x_lctx.off);
   db.lane_gst = (uint8_t *)(X + e->x_lst.off);
+  db.gsync = (GridSync *)(X + e->x_gsync.off);
   db.chunk_cnt = (uint32_t *)(X + e->x_chunk_cnt.off);
   db.ccounts = fold ? (uint32_t *)(X + e->x_ccounts.off) : nullptr;
   CU(cudaEventRecord(e->ev[0], e->stream));
@@ -818,6 +934,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   CU(cudaEventRecord(e->ev[1], e->stream));
   CU(cudaMemsetAsync(X + e->x_fire.off, 0xff, e->x_fire.bytes, e->stream));
   CU(cudaMemsetAsync(X + e->x_cslots.off, 0, e->x_cslots.bytes, e->stream));
+  if (!e->grid_parts.empty()) CU(cudaMemsetAsync(X + e->x_gsync.off, 0, e->x_gsync.bytes, e->stream));
   launch_memscan(db, e->stream);
   CU(cudaGetLastError());
   launch_resolve(db, e->stream);
@@ -830,7 +947,13 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
     for (int v = 0; v < maya_engine::NVAR; v++) {
       if (!e->var_n[v]) continue;
       CU(cudaStreamWaitEvent(e->vstream[v], e->vev[maya_engine::NVAR], 0));
-      if (v < 3) {
+      if (v == 15) {   // grid jobs: one cooperative launch per group of co-resident parts
+        for (auto &pr : e->grid_launches)
+          if (launch_schedule_grid(db, pr.first, pr.second, record_timeline ? 1 : 0,
+                                   e->grid_smem, e->vstream[v]) != 0)
+            return fail(MAYA_ECUDA, std::string("cooperative launch: ") +
+                                        cudaGetErrorString(cudaGetLastError()));
+      } else if (v < 3) {
         launch_schedule_variant(db, v, db.order + off, e->var_n[v], record_timeline ? 1 : 0,
                                 e->var_smem[v], e->vstream[v]);
       } else if (v <= 10) {

@@ -51,6 +51,8 @@ struct DevBatch {
   const LaneJob *lane_jobs;   // per job: lane-scheduler layout choice
   const uint32_t *lane_wslot; // per walker: ring slot word (soa.h)
   const uint32_t *lane_perm;  // per job: lane -> FIFO tables
+  const GridPart *grid_parts; // grid jobs: one entry per part (CTA)
+  GridSync *gsync;            // per job (grid jobs only)
   uint8_t *lane_gctx;         // per walker: 64 B FIFO context when not in shared memory
   uint8_t *lane_gst;          // per walker: 48 B FIFO state when LANE_ST_GLOBAL
   const FoldChunk *chunks;    // fold work items (one per 1,024 ops of a FIFO)
@@ -83,6 +85,10 @@ void launch_schedule_lane_warp(const DevBatch &b, const int32_t *order, uint32_t
                                cudaStream_t s);
 void launch_schedule_lane(const DevBatch &b, const int32_t *order, uint32_t n, uint32_t threads,
                           int record, uint32_t smem, cudaStream_t s);
+// grid jobs: parts [p0, p1) of b.grid_parts in one cooperative launch
+int launch_schedule_grid(const DevBatch &b, uint32_t p0, uint32_t p1, int record, uint32_t smem,
+                         cudaStream_t s);
+int grid_max_ctas(uint32_t smem);   // co-resident CTAs of the grid kernel at this smem
 int prof_read(unsigned long long *out8, int reset);   // MAYA_PROFILE builds only
 int lane_prof_read(unsigned long long *out8, int reset);
 void launch_topk(const DevBatch &b, int k, maya_topk_entry *out, int32_t *n_out, void *scratch,

@@ -149,8 +149,9 @@ struct LaneSh {
   uint32_t fmask;             // cache entries - 1
   const RCX *rcx;             // smem or global collective table
   int64_t *delay;             // job's host-delay table (global)
-  const uint32_t *perm;       // lane -> FIFOs (K per lane, stride = group threads)
+  const uint32_t *perm;       // lane -> FIFOs (K per lane, stride = group threads); null: w0 + lane
   uint32_t K;
+  uint32_t w0, w1;            // the FIFOs of this group (a grid job's part; else the job)
   int record;
   bool fire_sm, rcx_sm;       // fire / rcx tables in shared memory
 };
@@ -444,13 +445,14 @@ __device__ bool lane_host_step(const DevBatch &b, const LaneSh &sh, uint32_t r) 
 }
 
 // Set up the job's shared-memory region (group-strided: tid in [0, nt)).
+// The FIFOs [w0, w1) and ranks [r0, r1) of job j (the whole job, or one part of
+// a grid job); state and host-sync arrays are indexed with job-local numbers.
 __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_t tid,
-                           uint32_t nt, LaneSh &sh, int record, LCtx &own) {
+                           uint32_t nt, LaneSh &sh, int record, LCtx &own, const LaneJob &LJ,
+                           uint32_t w0, uint32_t w1, uint32_t r0, uint32_t r1) {
   const JobHdr &J = b.jobs[j];
-  const LaneJob LJ = b.lane_jobs[j];
-  const uint32_t W = J.n_walkers, R = J.n_ranks;
-  const LaneLayout L = lane_layout(W, R, J.n_comms, LJ.flags, LJ.n_slots, J.n_fire, J.n_rcolls,
-                                   LJ.fc_log2);
+  const LaneLayout L = lane_layout(w1 - w0, r1 - r0, J.n_comms, LJ.flags, LJ.n_slots, J.n_fire,
+                                   J.n_rcolls, LJ.fc_log2);
   sh.J = &J;
   sh.ring = (LJ.flags & LANE_COLL_RING) ? (CollSlot *)(base + L.ring) : nullptr;
   uint32_t *cb = (uint32_t *)(base + L.cb);
@@ -458,9 +460,11 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
   sh.cb = cb;
   if (sh.ring)
     for (uint32_t q = tid; q < 2 * J.n_comms; q += nt) sh.ring[q] = CollSlot{0, 0, 0};
-  sh.hostk = (uint32_t *)(base + L.hostk);
+  sh.hostk = (uint32_t *)(base + L.hostk) - r0;
   sh.st = (LJ.flags & LANE_ST_GLOBAL) ? (LSt *)(b.lane_gst + (size_t)J.walkers * 48)
-                                      : (LSt *)(base + L.state);
+                                      : (LSt *)(base + L.state) - w0;
+  sh.w0 = w0;
+  sh.w1 = w1;
   // several FIFOs per lane: contexts in shared memory, else in global memory
   // (one FIFO per lane keeps its context in registers)
   sh.ctx = (LJ.flags & LANE_CTX_SMEM) ? (LCtx *)(base + L.ctx)
@@ -487,12 +491,12 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
     RCX *dst = (RCX *)(base + L.rcx);
     for (uint32_t q = tid; q < J.n_rcolls; q += nt) dst[q] = src[q];
   }
-  for (uint32_t r = tid; r < R; r += nt) {
+  for (uint32_t r = r0 + tid; r < r1; r += nt) {
     sh.delay[b.ranks[J.ranks + r].delay] = 0;
     sh.hostk[r] = 0;
   }
-  const uint32_t *wslot = b.lane_wslot + LJ.wslot;
-  for (uint32_t w = tid; w < W; w += nt) {
+  const uint32_t *wslot = b.lane_wslot + LJ.wslot - w0;
+  for (uint32_t w = w0 + tid; w < w1; w += nt) {
     const Walker wk = b.walkers[J.walkers + w];
     const RankRec rr = b.ranks[J.ranks + wk.rank];
     const RepHdr &h = b.reps[rr.rep];
@@ -513,7 +517,7 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
     c.delay = rr.delay;
     c.pad = 0;
     if (sh.ctx) sh.ctx[w] = c;
-    if (w == tid) own = c;   // one FIFO per lane: the context stays in registers
+    if (w == w0 + tid) own = c;   // one FIFO per lane: the context stays in registers
     LSt s{};
     s.bound = c.nsync ? c.cnt[0] : c.len;
     sh.st[w] = s;
@@ -531,10 +535,9 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
 
 // Wait for every bulk copy still targeting the region (no copy may land in
 // shared memory after the job's CTA has exited); flag unfinished FIFOs.
-__device__ bool lane_drain(const LaneSh &sh, uint32_t W, uint32_t tid, uint32_t nt,
-                           const LCtx &own) {
+__device__ bool lane_drain(const LaneSh &sh, uint32_t tid, uint32_t nt, const LCtx &own) {
   bool incomplete = false;
-  for (uint32_t w = tid; w < W; w += nt) {
+  for (uint32_t w = sh.w0 + tid; w < sh.w1; w += nt) {
     const LCtx c = sh.ctx ? sh.ctx[w] : own;
     const LSt s = sh.st[w];
     if (s.i < c.len) incomplete = true;
@@ -562,7 +565,7 @@ __device__ __forceinline__ void fifos_begin_round(const LaneSh &sh, uint32_t tid
                                                   LaneFifos &f) {
   if (f.one) {
     if (f.valid) {
-      f.s = sh.st[sh.perm[tid]];
+      f.s = sh.st[sh.w0 + tid];
       f.s.lim = fifo_limit(sh, f.c);
     }
     return;
@@ -575,7 +578,7 @@ __device__ __forceinline__ void fifos_begin_round(const LaneSh &sh, uint32_t tid
 }
 
 __device__ __forceinline__ void fifos_end_round(const LaneSh &sh, uint32_t tid, LaneFifos &f) {
-  if (f.one && f.valid) sh.st[sh.perm[tid]] = f.s;
+  if (f.one && f.valid) sh.st[sh.w0 + tid] = f.s;
 }
 
 __device__ __forceinline__ void fifos_step(const DevBatch &b, const LaneSh &sh, uint32_t tid,
@@ -620,9 +623,9 @@ struct EpiVals {       // per-thread partials of the job epilogue
 };
 
 __device__ void epi_ranks(const DevBatch &b, const LaneSh &sh, uint32_t tid, uint32_t nt,
-                          EpiVals &v) {
+                          EpiVals &v, uint32_t r0, uint32_t r1) {
   const JobHdr &J = *sh.J;
-  for (uint32_t r = tid; r < J.n_ranks; r += nt) {
+  for (uint32_t r = r0 + tid; r < r1; r += nt) {
     const RankRec rr = b.ranks[J.ranks + r];
     const RepHdr &h = b.reps[rr.rep];
     const uint32_t k = sh.hostk[r];
@@ -689,8 +692,8 @@ __device__ __forceinline__ void fifos_init(const LaneSh &sh, uint32_t tid, LaneF
   f.valid = false;
   f.pf.key = 0xffffffffu;
   if (f.one) {
-    const uint32_t w = sh.perm[tid];   // == tid (identity table when K == 1)
-    f.valid = w != 0xffffffffu;
+    const uint32_t w = sh.perm ? sh.perm[tid] : (sh.w0 + tid < sh.w1 ? sh.w0 + tid : 0xffffffffu);
+    f.valid = w != 0xffffffffu;   // (identity: w == w0 + tid when K == 1)
     if (f.valid) f.c = own;
   }
 }
@@ -722,7 +725,9 @@ __global__ void __launch_bounds__(256, LANE_WARP_MINB) sched_lane_warp_kernel(De
   const long long tstart = clock64();
 #endif
   LCtx own{};
-  lane_setup(b, j, dsm + wp * region, lane, 32, sh, record, own);
+  const LaneJob LJ = b.lane_jobs[j];
+  lane_setup(b, j, dsm + wp * region, lane, 32, sh, record, own, LJ, 0, J.n_walkers, 0,
+             J.n_ranks);
   __syncwarp();
   LaneFifos f;
   fifos_init(sh, lane, f, own);
@@ -773,10 +778,10 @@ __global__ void __launch_bounds__(256, LANE_WARP_MINB) sched_lane_warp_kernel(De
 #ifdef MAYA_PROFILE
   if (lane == 0) atomicAdd(&g_lprof[0], (unsigned long long)(clock64() - tstart));
 #endif
-  bool incomplete = lane_drain(sh, J.n_walkers, lane, 32, own);
+  bool incomplete = lane_drain(sh, lane, 32, own);
   __syncwarp();
   EpiVals v{tmax, INT64_MAX, 0, INT32_MAX, incomplete};
-  epi_ranks(b, sh, lane, 32, v);
+  epi_ranks(b, sh, lane, 32, v, 0, J.n_ranks);
   incomplete = __any_sync(FULL, v.incomplete);
   const int64_t tm = warp_max64(v.tmax);
   const int64_t pk = warp_max64(v.peak);
@@ -813,7 +818,8 @@ __global__ void __launch_bounds__(LANE_MAX_THREADS, 1)
   }
   LaneSh sh;
   LCtx own{};
-  lane_setup(b, j, dsm, tid, nt, sh, record, own);
+  const LaneJob LJ = b.lane_jobs[j];
+  lane_setup(b, j, dsm, tid, nt, sh, record, own, LJ, 0, J.n_walkers, 0, J.n_ranks);
   if (tid == 0) {
     s_tmax = 0;
     s_err = 0;
@@ -870,9 +876,9 @@ __global__ void __launch_bounds__(LANE_MAX_THREADS, 1)
     if (vld(&s_err) != 0) progress = 0;
     if (!__syncthreads_or(progress)) break;
   }
-  if (lane_drain(sh, J.n_walkers, tid, nt, own)) s_incomplete = 1;
+  if (lane_drain(sh, tid, nt, own)) s_incomplete = 1;
   EpiVals v{tmax, INT64_MAX, 0, INT32_MAX, false};
-  epi_ranks(b, sh, tid, nt, v);
+  epi_ranks(b, sh, tid, nt, v, 0, J.n_ranks);
   if (v.incomplete) s_incomplete = 1;
   atomicMax(&s_tmax, (unsigned long long)v.tmax);
   atomicMax(&s_peak, (long long)v.peak);
@@ -882,6 +888,175 @@ __global__ void __launch_bounds__(LANE_MAX_THREADS, 1)
   __syncthreads();
   if (tid == 0)
     write_result(b, J, res, s_err, s_incomplete != 0, (int64_t)s_tmax, s_peak, s_oom_rank, rounds);
+}
+
+
+// ---------------------------------------------------------------------------
+// grid jobs: a job too large for one CTA runs on several co-resident CTAs
+// (rank-aligned FIFO ranges, one FIFO per thread).  The round protocol of the
+// CTA kernel is lifted to the job: one job-wide counter of walking warps in
+// global memory, collectives through global slots, and a job-wide barrier
+// between rounds (host syncs, termination and deadlock decided there).
+
+static constexpr uint32_t GRID_THREADS = 256;
+
+__device__ void grid_barrier(GridSync *gs, uint32_t n_parts, int reset_active) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = vld(&gs->gen);
+    __threadfence();
+    if (atomicAdd(&gs->arrive, 1u) == n_parts - 1) {
+      vst(&gs->arrive, 0u);
+      if (reset_active >= 0) {
+        vst(&gs->active, reset_active);
+        vst(&gs->progress, 0);
+      }
+      __threadfence();
+      atomicAdd(&gs->gen, 1u);
+    } else {
+      while (vld(&gs->gen) == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(GRID_THREADS, 1)
+    sched_lane_grid_kernel(DevBatch b, uint32_t p0, int record) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ unsigned long long s_tmax;
+  __shared__ int s_err, s_incomplete, s_oom_rank, s_any;
+  __shared__ long long s_peak, s_oom_t;
+  const GridPart P = b.grid_parts[p0 + blockIdx.x];
+  const uint32_t j = P.job;
+  const JobHdr &J = b.jobs[j];
+  GridSync *gs = b.gsync + j;
+  const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+  LaneJob LJ{};
+  LJ.flags = P.flags;
+  LJ.n_slots = P.n_slots;
+  LJ.wslot = P.wslot;
+  LJ.per_lane = 1;
+  LJ.fc_log2 = P.fc_log2;
+  LaneSh sh;
+  LCtx own{};
+  lane_setup(b, j, dsm, tid, nt, sh, record, own, LJ, P.w0, P.w1, P.r0, P.r1);
+  sh.perm = nullptr;
+  sh.K = 1;
+  if (tid == 0) {
+    s_tmax = 0;
+    s_err = 0;
+    s_incomplete = 0;
+    s_peak = 0;
+    s_oom_t = INT64_MAX;
+    s_oom_rank = INT32_MAX;
+  }
+  LaneFifos f;
+  fifos_init(sh, tid, f, own);
+  if (P.part == 0 && tid == 0) {   // the job-wide minima start at +inf (scratch is zeroed)
+    vst(&gs->oom_t, (long long)INT64_MAX);
+    vst(&gs->oom_rank, (int)INT32_MAX);
+  }
+  grid_barrier(gs, P.n_parts, (int)P.warps_total);
+  int64_t tmax = 0;
+  int err = 0;
+  int64_t rounds = 0;
+  for (;;) {
+    int progress = 0;
+    for (uint32_t r = P.r0 + tid; r < P.r1; r += nt) progress |= lane_host_step(b, sh, r);
+    __syncthreads();
+    fifos_begin_round(sh, tid, nt, f);
+    bool idle = false;
+    for (uint32_t spin = 0;; spin++) {
+      bool prog = false, data = false;
+      fifos_step(b, sh, tid, nt, f, tmax, err, prog, data, spin == 0 && !idle);
+      if (__any_sync(FULL, err != 0)) {
+        if (err && lane == 0) atomicMax(&gs->err, err);
+        if (err) atomicMax(&s_err, err);
+        __syncwarp();
+      }
+      if (vld(&gs->err) != 0) {
+        if (!idle && lane == 0) atomicSub(&gs->active, 1);
+        break;
+      }
+      if (__any_sync(FULL, prog)) {
+        progress = 1;
+        if (idle) {
+          if (lane == 0) atomicAdd(&gs->active, 1);
+          idle = false;
+        }
+        spin = 0;
+        continue;
+      }
+      if (__any_sync(FULL, data)) continue;     // bytes in flight: not idle
+      if (!idle) {
+        if (lane == 0) atomicSub(&gs->active, 1);
+        idle = true;
+      }
+      __syncwarp();
+      if (vld(&gs->active) <= 0) break;         // every warp of the job is idle
+      if (spin > 16) __nanosleep(128);
+    }
+    fifos_end_round(sh, tid, f);
+    rounds++;
+    if (__syncthreads_or(progress) && tid == 0) atomicOr(&gs->progress, 1);
+    grid_barrier(gs, P.n_parts, -1);            // the round is over everywhere
+    if (tid == 0) s_any = vld(&gs->progress) && !vld(&gs->err);
+    grid_barrier(gs, P.n_parts, (int)P.warps_total);   // read; reset for the next round
+    if (!s_any) break;
+  }
+  if (lane_drain(sh, tid, nt, own)) s_incomplete = 1;
+  EpiVals v{tmax, INT64_MAX, 0, INT32_MAX, false};
+  epi_ranks(b, sh, tid, nt, v, P.r0, P.r1);
+  if (v.incomplete) s_incomplete = 1;
+  atomicMax(&s_tmax, (unsigned long long)v.tmax);
+  atomicMax(&s_peak, (long long)v.peak);
+  if (v.oom_rank != INT32_MAX) atomicMin(&s_oom_t, (long long)v.oom_t);
+  __syncthreads();
+  if (tid == 0) {
+    atomicMax(&gs->tmax, s_tmax);
+    atomicMax(&gs->peak, s_peak);
+    atomicMin(&gs->oom_t, s_oom_t);
+    if (s_incomplete) atomicOr(&gs->incomplete, 1);
+  }
+  grid_barrier(gs, P.n_parts, -1);
+  const long long got = vld(&gs->oom_t);
+  if (v.oom_rank != INT32_MAX && v.oom_t == got) atomicMin(&s_oom_rank, v.oom_rank);
+  __syncthreads();
+  if (tid == 0 && s_oom_rank != INT32_MAX) atomicMin(&gs->oom_rank, s_oom_rank);
+  grid_barrier(gs, P.n_parts, -1);
+  if (P.part == 0 && tid == 0)
+    write_result(b, J, b.results + j, vld(&gs->err), vld(&gs->incomplete) != 0,
+                 (int64_t)vld(&gs->tmax), vld(&gs->peak), vld(&gs->oom_rank), rounds);
+}
+
+int grid_max_ctas(uint32_t smem) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sched_lane_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)LANE_SMEM_CAP);
+    attr = true;
+  }
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sched_lane_grid_kernel, GRID_THREADS,
+                                                smem);
+  return per_sm * sms;
+}
+
+int launch_schedule_grid(const DevBatch &b, uint32_t p0, uint32_t p1, int record, uint32_t smem,
+                         cudaStream_t s) {
+  if (p1 <= p0) return 0;
+  grid_max_ctas(smem);   // sets the shared-memory attribute
+  DevBatch bb = b;
+  uint32_t pp = p0;
+  int rec = record;
+  void *args[] = {&bb, &pp, &rec};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void *)sched_lane_grid_kernel,
+                                                    dim3(p1 - p0), dim3(GRID_THREADS), args,
+                                                    smem, s);
+  return e == cudaSuccess ? 0 : -1;
 }
 
 int lane_prof_read(unsigned long long *out8, int reset) {

@@ -117,6 +117,25 @@ struct LaneJob {
   uint32_t per_lane;    // FIFOs per lane (table is per_lane x group threads, 0xFFFFFFFF pad)
   uint32_t fc_log2;     // record-time cache entries (log2; 0: none) when LANE_FIRE_SMEM is off
 };
+// One CTA of a grid job (a job too large for one CTA): a rank-aligned range
+// of its FIFOs.  All parts of a grid job are co-resident (cooperative launch);
+// collectives rendezvous in global slots and rounds end at a job-wide barrier.
+struct GridPart {
+  uint32_t job, part, n_parts, warps_total;   // warps_total: all parts of the job
+  uint32_t w0, w1, r0, r1;                    // job-local FIFO and rank ranges
+  uint32_t flags, n_slots, fc_log2, first;    // first: batch index of the job's part 0
+  uint64_t wslot;                             // batch index of the part's ring words
+};
+// Job-wide synchronisation of a grid job (scratch, zeroed every run).
+struct GridSync {
+  unsigned arrive, gen;
+  int active, progress;
+  int err, incomplete;
+  int oom_rank, rounds;
+  unsigned long long tmax;
+  long long peak, oom_t;
+};
+
 // per-walker ring word: first slot (job-local, 28 bits) | log2(slots) << 28
 // (0xF << 28: the FIFO reads global memory directly)
 struct LaneLayout {
