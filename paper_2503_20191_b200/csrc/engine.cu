@@ -94,7 +94,7 @@ struct maya_engine {
   // segments
   Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_slots, s_walkers, s_reps, s_ops, s_streams,
       s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
-      s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks, s_grid_parts;
+      s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks, s_grid_parts, s_comm_part;
   Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst, x_gsync;
   std::vector<GridPart> grid_parts;        // host copy (launch grouping)
   std::vector<std::pair<uint32_t, uint32_t>> grid_launches;   // part ranges per launch
@@ -178,10 +178,12 @@ bool plan_grid(const JobPack &P, LanePlan &pl) {
         const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
         slots += lane_slots_of(P.streams[h.streams + wk.stream].folded, lgd);
       }
-      const LaneLayout L = lane_layout(g.w1 - g.w0, g.r1 - g.r0, nc, 0, (uint32_t)slots,
+      const uint32_t ringf =
+          (P.hdr.flags & JOB_RING) && nc <= RING_MAX_COMMS ? LANE_COLL_RING : 0u;
+      const LaneLayout L = lane_layout(g.w1 - g.w0, g.r1 - g.r0, nc, ringf, (uint32_t)slots,
                                        P.hdr.n_fire, P.hdr.n_rcolls, fc);
       if (L.bytes > LANE_SMEM_CAP) continue;
-      g.flags = 0;
+      g.flags = ringf;
       g.n_slots = (uint32_t)slots;
       g.fc_log2 = fc;
       g.wslot = lgd;   // ring depth, replaced by the batch index at upload
@@ -212,17 +214,46 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
     // Lockstep lanes pay off when many FIFOs carry work; a few long FIFOs
     // (compute streams) are serial chains the warp-window kernel scans 32 ops
     // per step.
-    // Criterion: the 16th longest FIFO is at least a quarter of the longest,
-    // and no FIFO is longer than 8k ops.
-    if (W < 16) return pl;
+    // Criterion: the 32nd longest FIFO is at least a quarter of the longest
+    // (a warp's worth of busy FIFOs; a pipeline's per-stage compute streams
+    // are fewer), and no folded FIFO is longer than 8k ops.
+    if (W < 32) return pl;
     std::vector<uint32_t> l(W);
     for (uint32_t w = 0; w < W; w++) l[w] = lane_fifo_len(P, w);
-    std::nth_element(l.begin(), l.begin() + 15, l.end(), std::greater<uint32_t>());
-    const uint32_t mx = *std::max_element(l.begin(), l.begin() + 16);
-    if (l[15] < 64 || 4ull * l[15] < mx) return pl;
-    // very long FIFOs: the warp-window scan's 32 ops per step win even when
-    // many of them are busy (C5 at 100k ops/rank, C4's 16-stage pipelines)
-    if (mx > 8192) return pl;
+    std::nth_element(l.begin(), l.begin() + 31, l.end(), std::greater<uint32_t>());
+    const uint32_t mx = *std::max_element(l.begin(), l.begin() + 32);
+    if (l[31] < 64 || 4ull * l[31] < mx) return pl;
+    // very long FIFOs after run folding: the warp-window scan's 32 ops per
+    // step win even when many of them are busy (C4's 16-stage pipelines)
+    uint32_t mxf = 0, wl = 0;
+    for (uint32_t w = 0; w < W; w++) {
+      const Walker wk = P.walkers[w];
+      const uint32_t f = P.streams[P.reps[P.ranks[wk.rank].rep].streams + wk.stream].folded;
+      if (f > mxf) { mxf = f; wl = w; }
+    }
+    if (mxf > 8192) return pl;
+    // ... and the same when the longest FIFO rarely blocks: waits and
+    // multi-member collectives (sampled over its first 4k ops) more than 128
+    // ops apart leave long affine runs for the scan
+    {
+      const Walker wk = P.walkers[wl];
+      const RankRec &rr = P.ranks[wk.rank];
+      const RepHdr &h = P.reps[rr.rep];
+      const StreamRange &sr = P.streams[h.streams + wk.stream];
+      const uint32_t n = std::min<uint32_t>(sr.len, 4096);
+      uint32_t blockers = 0;
+      for (uint32_t q = 0; q < n; q++) {
+        const Op &o = P.ops[h.ops + sr.begin + q];
+        const uint32_t tg = op_tag(o.meta);
+        if (tg == TAG_WAIT) {
+          blockers++;
+        } else if (tg == TAG_COLL) {
+          const uint32_t g = P.rank_comm[rr.comm + P.coll_lc[h.colls + o.arg]];
+          blockers += P.comm_rdv[g] > 1 ? 1u : 0u;
+        }
+      }
+      if (blockers == 0 || n / blockers > 128) return pl;
+    }
   }
   const uint32_t nc = (uint32_t)P.comms.size();
   const uint32_t ring = (P.hdr.flags & JOB_RING) && nc <= RING_MAX_COMMS ? LANE_COLL_RING : 0;
@@ -541,6 +572,7 @@ int maya_upload(maya_engine *e) {
   size_t n_parts = 0;
   for (size_t j = 0; j < nj; j++) n_parts += plans[j].parts.size();
   seg(e->s_grid_parts, n_parts * sizeof(GridPart));
+  seg(e->s_comm_part, n_comms * sizeof(uint32_t));
   e->arena_bytes = off;
   // scratch layout
   off = 0;
@@ -784,6 +816,28 @@ int maya_upload(maya_engine *e) {
         slot += n;
       }
     }
+    {  // grid jobs: the part holding all members of each communicator (else ~0)
+      uint32_t *cp = (uint32_t *)(H + e->s_comm_part.off) + B.comms;
+      for (size_t g = 0; g < P.comms.size(); g++) cp[g] = 0xffffffffu;
+      const LanePlan &pl = plans[j];
+      if (pl.variant == 15) {
+        std::vector<uint32_t> owner(P.comms.size(), 0xfffffffeu);   // unset
+        size_t part = 0;
+        for (size_t r = 0; r < P.ranks.size(); r++) {
+          while (part + 1 < pl.parts.size() && r >= pl.parts[part + 1].r0) part++;
+          const RankRec &rr = P.ranks[r];
+          const uint32_t nlc = (r + 1 < P.ranks.size() ? P.ranks[r + 1].comm
+                                                        : (uint32_t)P.rank_comm.size()) - rr.comm;
+          for (uint32_t q = 0; q < nlc; q++) {
+            const uint32_t g = P.rank_comm[rr.comm + q];
+            owner[g] = owner[g] == 0xfffffffeu ? (uint32_t)part
+                       : owner[g] == (uint32_t)part ? owner[g] : 0xffffffffu;
+          }
+        }
+        for (size_t g = 0; g < P.comms.size(); g++)
+          cp[g] = owner[g] == 0xfffffffeu ? 0xffffffffu : owner[g];
+      }
+    }
     {  // batch-global call slot of every rank-collective entry
       uint32_t *dst = (uint32_t *)(H + e->s_rcslot.off) + B.rcolls;
       for (size_t q = 0; q < P.rcolls.size(); q++) {
@@ -826,6 +880,7 @@ int maya_upload(maya_engine *e) {
   db.lane_perm = (const uint32_t *)(D + e->s_lane_perm.off);
   db.chunks = (const FoldChunk *)(D + e->s_chunks.off);
   db.grid_parts = (const GridPart *)(D + e->s_grid_parts.off);
+  db.comm_part = (const uint32_t *)(D + e->s_comm_part.off);
   db.n_chunks = (uint32_t)n_chunks;
   db.ranks = (const RankRec *)(D + e->s_ranks.off);
   db.rank_comm = (const uint32_t *)(D + e->s_rank_comm.off);

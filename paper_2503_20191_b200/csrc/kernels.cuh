@@ -53,6 +53,7 @@ struct DevBatch {
   const uint32_t *lane_perm;  // per job: lane -> FIFO tables
   const GridPart *grid_parts; // grid jobs: one entry per part (CTA)
   GridSync *gsync;            // per job (grid jobs only)
+  const uint32_t *comm_part;  // per comm: the grid part holding all its members, else ~0
   uint8_t *lane_gctx;         // per walker: 64 B FIFO context when not in shared memory
   uint8_t *lane_gst;          // per walker: 48 B FIFO state when LANE_ST_GLOBAL
   const FoldChunk *chunks;    // fold work items (one per 1,024 ops of a FIFO)

@@ -152,6 +152,8 @@ struct LaneSh {
   const uint32_t *perm;       // lane -> FIFOs (K per lane, stride = group threads); null: w0 + lane
   uint32_t K;
   uint32_t w0, w1;            // the FIFOs of this group (a grid job's part; else the job)
+  const uint32_t *comm_part;  // grid jobs: part holding all members of each comm (else global slots)
+  uint32_t part;
   int record;
   bool fire_sm, rcx_sm;       // fire / rcx tables in shared memory
 };
@@ -245,7 +247,7 @@ __device__ __forceinline__ int lane_step(const DevBatch &b, const LaneSh &sh, co
     if (fire_load(sh, s.wtgt, full) < 0) return ADV_IDLE;
     s.flags &= ~ST_WFIRE;
   } else if (s.flags & ST_WCOUNT) {
-    const uint32_t cnt = sh.ring ? (uint32_t)ld_vol_shared_u32(s.waddr) : vld(s.waddr);
+    const uint32_t cnt = __isShared(s.waddr) ? (uint32_t)ld_vol_shared_u32(s.waddr) : vld(s.waddr);
     if (cnt < s.wtgt) return ADV_IDLE;
     s.flags &= ~ST_WCOUNT;
   }
@@ -341,7 +343,7 @@ __device__ __forceinline__ int lane_step(const DevBatch &b, const LaneSh &sh, co
     } else {
       CollSlot *cs;
       uint32_t target;
-      if (sh.ring) {
+      if (sh.ring && (!sh.comm_part || sh.comm_part[g] == sh.part)) {   // on-chip rendezvous
         cs = sh.ring + 2 * g + (idx & 1u);
         target = ((idx >> 1) + 1u) * nr;
       } else {
@@ -465,6 +467,8 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
                                       : (LSt *)(base + L.state) - w0;
   sh.w0 = w0;
   sh.w1 = w1;
+  sh.comm_part = nullptr;
+  sh.part = 0;
   // several FIFOs per lane: contexts in shared memory, else in global memory
   // (one FIFO per lane keeps its context in registers)
   sh.ctx = (LJ.flags & LANE_CTX_SMEM) ? (LCtx *)(base + L.ctx)
@@ -943,6 +947,10 @@ __global__ void __launch_bounds__(GRID_THREADS, 1)
   lane_setup(b, j, dsm, tid, nt, sh, record, own, LJ, P.w0, P.w1, P.r0, P.r1);
   sh.perm = nullptr;
   sh.K = 1;
+  if (sh.ring) {   // communicators whose members all live in this part meet on chip
+    sh.comm_part = b.comm_part + J.comms;
+    sh.part = P.part;
+  }
   if (tid == 0) {
     s_tmax = 0;
     s_err = 0;
