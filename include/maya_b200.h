@@ -163,6 +163,12 @@ int maya_timeline_size(maya_engine *eng, int32_t job, int64_t *n);
 int maya_timeline(maya_engine *eng, int32_t job, int32_t *rank, int32_t *stream,
                   int32_t *seq, int64_t *start, int64_t *end);
 
+/* Per-rank statistics of _report (sim.py:406-426, RankStats sim.py:50-56) of
+ * one job after maya_run(record_timeline=1), computed on the device from the
+ * recorded timeline (segmented sort + union scans, stats.cu).  out is
+ * [num_ranks][5]: compute_busy_ns, comm_busy_ns, exposed_comm_ns, idle_ns,
+ * peak_mem_bytes, in the job's original rank numbering. */
+int maya_rank_stats(maya_engine *eng, int32_t job, int32_t num_ranks, int64_t *out);
 /* The engine's CUDA stream (cudaStream_t) so callers can time on it. */
 int maya_get_stream(maya_engine *eng, void **stream);
 

@@ -120,58 +120,6 @@ def _is_default_roofline(est) -> bool:
 
 # --- simulate() ----------------------------------------------------------------------
 
-def _rank_stats(tl, total: int, n_ranks: int, peaks) -> dict:
-    """Per-rank busy/exposed/idle from the GPU timeline (sim.py:406-473)."""
-    T = _ref_types()
-    out = {}
-    timed = tl.timed()
-    for r in range(n_ranks):
-        m = timed.rank == r
-        a, b, tag = timed.start[m], timed.end[m], timed.tag[m]
-        comp = _merge(a[tag == 0], b[tag == 0])
-        comm = _merge(a[tag == 1], b[tag == 1])
-        busy = _merge(a, b)
-        out[r] = T["RankStats"](
-            compute_busy_ns=int(sum(y - x for x, y in comp)),
-            comm_busy_ns=int(sum(y - x for x, y in comm)),
-            exposed_comm_ns=_subtract_len(comm, comp),
-            idle_ns=int(total - sum(y - x for x, y in busy)),
-            peak_mem_bytes=int(peaks[r]))
-    return out
-
-
-def _merge(a, b):
-    out = []
-    for x, y in sorted(zip(a.tolist(), b.tolist())):
-        if y <= x:
-            continue
-        if out and x <= out[-1][1]:
-            if y > out[-1][1]:
-                out[-1] = (out[-1][0], y)
-        else:
-            out.append((x, y))
-    return out
-
-
-def _subtract_len(base, cut) -> int:
-    total, ci = 0, 0
-    for a, b in base:
-        pos = a
-        while ci < len(cut) and cut[ci][1] <= pos:
-            ci += 1
-        k = ci
-        while pos < b:
-            if k >= len(cut) or cut[k][0] >= b:
-                total += b - pos
-                break
-            ca, cb = cut[k]
-            if ca > pos:
-                total += ca - pos
-            pos = max(pos, cb)
-            k += 1
-    return total
-
-
 def simulate_raw(jobs: Sequence[RawJob], device: int = 0, record_timeline: bool = False,
                  efficiency: Mapping[str, float] | None = None,
                  overhead_ns: int = DEFAULT_KERNEL_OVERHEAD_NS):
@@ -188,44 +136,25 @@ def simulate(annotated, cluster=None, record_timeline: bool = False, device: int
     res, eng = simulate_raw([raw], device, record_timeline=True)
     r = res[0]
     _raise_for(int(r["status"]))
-    tl = eng.timeline(0)
-    rep_peak = _rep_peaks(raw)
-    peaks = [rep_peak[raw.rank_rep[q]] for q in range(raw.num_ranks)]
-    per_rank = _rank_stats(tl, int(r["total_ns"]), raw.num_ranks, peaks)
+    T = _ref_types()
+    # per-rank busy / exposed / idle / peak: segmented sort + union scans on the
+    # device over the recorded timeline (stats.cu, _report sim.py:406-426)
+    per_rank = {q: T["RankStats"](compute_busy_ns=int(x[0]), comm_busy_ns=int(x[1]),
+                                  exposed_comm_ns=int(x[2]), idle_ns=int(x[3]),
+                                  peak_mem_bytes=int(x[4]))
+                for q, x in enumerate(eng.rank_stats(0, raw.num_ranks))}
     timeline = []
     if record_timeline:
         names = _timeline_names(raw, eng)
-        timed = tl.timed()
+        timed = eng.timeline(0).timed()
         order = np.lexsort((timed.start, timed.end, timed.rank))
         timeline = [(int(timed.rank[i]), int(timed.stream[i]), names(timed, i),
                      int(timed.start[i]), int(timed.end[i])) for i in order]
-    T = _ref_types()
     return T["SimReport"](
         total_ns=int(r["total_ns"]), per_rank=per_rank, oom=bool(r["oom"]),
         first_oom=((int(r["first_oom_rank"]), int(r["first_oom_seq"])) if r["oom"] else None),
         dispatched_ops=int(r["dispatched_ops"]), completed_ops=int(r["completed_ops"]),
         timeline=timeline)
-
-
-def _rep_peaks(raw: RawJob) -> list:
-    from .rawtrace import EV_MEMALLOC, EV_MEMFREE
-    out = []
-    for rep in range(raw.n_reps):
-        sl = raw.rep_events(rep)
-        kinds, f = raw.ev_kind[sl], raw.ev_f[sl]
-        alloc = {}
-        mem = peak = 0
-        for k, row in zip(kinds.tolist(), f.tolist()):
-            if k == EV_MEMALLOC:
-                alloc[row[0]] = row[1]
-                mem += row[1]
-            elif k == EV_MEMFREE:
-                mem -= alloc[row[0]]
-            else:
-                continue
-            peak = max(peak, mem)
-        out.append(peak)
-    return out
 
 
 def _timeline_names(raw: RawJob, eng):

@@ -104,6 +104,12 @@ struct maya_engine {
   uint64_t n_tl = 0;
   std::vector<uint64_t> job_tl;      // per job timeline base
   std::vector<uint64_t> job_ops;     // per job batch op base (for op_seq/streams)
+  std::vector<uint32_t> job_rank0;   // per job batch index of its first simulated rank
+  std::vector<uint64_t> rank_seg;    // per batch rank: timeline base (n_ranks + 1 entries)
+  void *d_stats = nullptr;           // rank_seg + per-rank stats + sort scratch (timeline runs)
+  size_t d_stats_cap = 0;
+  int64_t *d_rstats = nullptr;       // [n_ranks][4] compute, comm, busy, peak
+  bool stats_ok = false;
   float last_ms[3] = {0, 0, 0};
   int64_t run_launches = 0, topk_launches = 0;
   int32_t options = MAYA_OPT_COLLAPSE;
@@ -408,6 +414,7 @@ int maya_close(maya_engine *e) {
   if (e->h_arena) cudaFreeHost(e->h_arena);
   if (e->d_arena) cudaFree(e->d_arena);
   if (e->d_scratch) cudaFree(e->d_scratch);
+  if (e->d_stats) cudaFree(e->d_stats);
   for (auto &ev : e->ev) if (ev) cudaEventDestroy(ev);
   for (auto &ev : e->vev) if (ev) cudaEventDestroy(ev);
   for (auto &s : e->vstream) if (s) cudaStreamDestroy(s);
@@ -488,8 +495,11 @@ int maya_upload(maya_engine *e) {
   uint64_t n_tl = 0;
   e->job_tl.resize(nj);
   e->job_ops.resize(nj);
+  e->job_rank0.resize(nj);
+  e->rank_seg.clear();
   for (size_t j = 0; j < nj; j++) {
     const JobPack &P = e->packs[j];
+    e->job_rank0[j] = (uint32_t)n_ranks;
     n_ranks += P.ranks.size();
     n_rank_comm += P.rank_comm.size();
     n_comms += P.comms.size();
@@ -515,8 +525,12 @@ int maya_upload(maya_engine *e) {
       if (!L.on_chip) n_wstate += spill_bytes(P.walkers.size(), P.ranks.size());
     }
     e->job_tl[j] = n_tl;
-    for (const RankRec &rr : P.ranks) n_tl += P.reps[rr.rep].n_ops;
+    for (const RankRec &rr : P.ranks) {
+      e->rank_seg.push_back(n_tl);
+      n_tl += P.reps[rr.rep].n_ops;
+    }
   }
+  e->rank_seg.push_back(n_tl);
   // scheduler plans (lane kernel unless disabled or the job does not fit it)
   std::vector<LanePlan> plans(nj);
   size_t n_perm = 0;
@@ -1028,10 +1042,35 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
     }
   }
   CU(cudaEventRecord(e->ev[3], e->stream));
+  e->stats_ok = false;
+  if (record_timeline) {
+    // per-rank busy statistics (_report, sim.py:406-426) from the recorded timeline
+    const uint32_t nr = (uint32_t)(e->rank_seg.size() - 1);
+    if (e->n_tl >= 0x7fffffffull) return fail(MAYA_EINVAL, "timeline too large for rank stats");
+    const size_t seg_b = align_up(e->rank_seg.size() * 8, 256), out_b = align_up(nr * 32ull, 256);
+    const size_t tmp_b = rank_stats_scratch_bytes(e->n_tl, nr);
+    const size_t need = seg_b + out_b + tmp_b;
+    if (need > e->d_stats_cap) {
+      CU(cudaStreamSynchronize(e->stream));
+      if (e->d_stats) cudaFree(e->d_stats);
+      e->d_stats = nullptr;
+      CU(cudaMalloc(&e->d_stats, need));
+      e->d_stats_cap = need;
+    }
+    char *S = (char *)e->d_stats;
+    CU(cudaMemcpyAsync(S, e->rank_seg.data(), e->rank_seg.size() * 8, cudaMemcpyHostToDevice,
+                       e->stream));
+    e->d_rstats = (int64_t *)(S + seg_b);
+    if (launch_rank_stats(db, (const uint64_t *)S, nr, e->n_tl, S + seg_b + out_b, tmp_b,
+                          e->d_rstats, e->stream) != 0)
+      return fail(MAYA_ECUDA, std::string("rank stats: ") + cudaGetErrorString(cudaGetLastError()));
+    e->stats_ok = true;
+  }
   {
     int64_t n = (db.n_feats ? 1 : 0) + (db.n_slots ? 1 : 0) + (db.n_reps ? 1 : 0) +
                 (db.n_ops ? 1 : 0) + (db.n_rcolls ? 1 : 0);
     for (int v = 0; v < maya_engine::NVAR; v++) n += e->var_n[v] ? 1 : 0;
+    if (e->stats_ok) n += 3;   // keys, segmented sort (cub), unions
     e->run_launches = n;
   }
   e->ran = true;
@@ -1174,6 +1213,31 @@ int maya_timeline(maya_engine *e, int32_t job, int32_t *rank, int32_t *stream, i
         end[t] = en[src];
       }
     }
+  }
+  return MAYA_OK;
+}
+
+int maya_rank_stats(maya_engine *e, int32_t job, int32_t num_ranks, int64_t *out) {
+  if (!e->recorded || !e->stats_ok) return fail(MAYA_ESTATE, "no timeline recorded");
+  if (job < 0 || (size_t)job >= e->packs.size()) return fail(MAYA_EINVAL, "job index");
+  const JobPack &P = e->packs[job];
+  if (num_ranks != (int32_t)P.rank_sim.size()) return fail(MAYA_EINVAL, "num_ranks of the job");
+  CU(cudaSetDevice(e->device));
+  const size_t ns = P.ranks.size();
+  std::vector<int64_t> st(4 * ns);
+  maya_job_result r{};
+  if (ns)
+    CU(cudaMemcpyAsync(st.data(), e->d_rstats + 4ull * e->job_rank0[job], 32 * ns,
+                       cudaMemcpyDeviceToHost, e->stream));
+  CU(cudaMemcpyAsync(&r, e->db.results + job, sizeof r, cudaMemcpyDeviceToHost, e->stream));
+  CU(cudaStreamSynchronize(e->stream));
+  for (int32_t q = 0; q < num_ranks; q++) {
+    const int64_t *x = st.data() + 4 * (size_t)P.rank_sim[q];
+    out[5 * q + 0] = x[0];              // compute_busy_ns
+    out[5 * q + 1] = x[1];              // comm_busy_ns
+    out[5 * q + 2] = x[2] - x[0];       // exposed_comm_ns = |comm u compute| - |compute|
+    out[5 * q + 3] = r.total_ns - x[2]; // idle_ns
+    out[5 * q + 4] = x[3];              // peak_mem_bytes
   }
   return MAYA_OK;
 }

@@ -95,5 +95,11 @@ int lane_prof_read(unsigned long long *out8, int reset);
 void launch_topk(const DevBatch &b, int k, maya_topk_entry *out, int32_t *n_out, void *scratch,
                  cudaStream_t s);
 size_t topk_scratch_bytes(uint32_t n_jobs, int k);
+// per-rank busy statistics from a recorded timeline (stats.cu): out[4 * rank] =
+// compute, comm, busy (unions), peak memory
+size_t rank_stats_scratch_bytes(uint64_t n_tl, uint32_t n_ranks);
+int launch_rank_stats(const DevBatch &b, const uint64_t *rank_seg, uint32_t n_ranks,
+                      uint64_t n_tl, void *scratch, size_t scratch_bytes, int64_t *out,
+                      cudaStream_t s);
 
 }  // namespace maya

@@ -30,7 +30,7 @@ EXPORTED = (
     "maya_get_stream", "maya_arena_bytes", "maya_gen_job", "maya_gen_view_of", "maya_gen_free",
     "maya_gen_op_kind_name", "maya_gen_dtype_name", "maya_batch_add_generated",
     "maya_batch_stats", "maya_set_options", "maya_batch_collapsed", "maya_prof_read",
-    "maya_debug_pack_compare",
+    "maya_debug_pack_compare", "maya_rank_stats",
 )
 
 
@@ -72,6 +72,7 @@ def lib():
     L.maya_batch_stats.argtypes = [vp, P(C.c_int64)]
     L.maya_set_options.argtypes = [vp, C.c_int32]
     L.maya_batch_collapsed.argtypes = [vp, P(C.c_uint8)]
+    L.maya_rank_stats.argtypes = [vp, C.c_int32, C.c_int32, P(C.c_int64)]
     _lib = L
     return L
 
@@ -213,6 +214,14 @@ class Engine:
                                start.ctypes.data_as(P(C.c_int64)),
                                end.ctypes.data_as(P(C.c_int64))))
         return Timeline(rank[:n], stream[:n], seq[:n] >> 2, seq[:n] & 3, start[:n], end[:n])
+
+    def rank_stats(self, job: int, num_ranks: int) -> np.ndarray:
+        """Per-rank (compute_busy, comm_busy, exposed_comm, idle, peak_mem) of one
+        job, computed on the device after run(record_timeline=True)."""
+        out = np.zeros((max(num_ranks, 1), 5), np.int64)
+        _check(lib().maya_rank_stats(self._h, int(job), int(num_ranks),
+                                     out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out[:num_ranks]
 
     def stream_handle(self) -> int:
         s = C.c_void_p()
