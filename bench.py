@@ -475,8 +475,11 @@ def bench_ours(args):
         n_total = N_CONFIGS * world
         value = n_total / (ms_max / 1000)
         rank_ops = stats["rank_ops"]
-        # algorithmic bytes of one scheduler launch
-        alg_bytes = (16 * stats["rep_events"] + 4 * stats["rank_comms"]
+        # algorithmic bytes of one step: the packed input read
+        # once -- 16 B per device op record (a kernel block is one record, plus 16 B
+        # per interned block and 4 B per block feature id) -- and the tables
+        alg_bytes = (16 * stats["device_ops"] + 16 * stats["kernel_blocks"]
+                     + 4 * stats["block_fids"] + 4 * stats["rank_comms"]
                      + 16 * (stats["features"] + stats["slots"]) + 24 * stats["jobs"])
         sched = statistics.median(sched_ms)
         peak, peak_kind = measured_peak_hbm()
@@ -509,7 +512,8 @@ def bench_ours(args):
                          "frac": round(achieved / peak, 5), "traffic": ncu_traffic(),
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "kernel_ms": round(sched, 4), "peak_source": peak_kind,
-                         "note": "C2 is latency-bound (dedup makes compulsory bytes << work)"},
+                         "note": "C2 is latency-bound (dedup and kernel blocks make the "
+                                 "compulsory bytes << work)"},
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "rounds": {"max": int(res["rounds"].max()), "median": float(np.median(res["rounds"]))},

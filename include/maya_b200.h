@@ -138,6 +138,9 @@ int maya_batch_num_jobs(maya_engine *eng);
                                  A/B testing -- runs are never folded when a timeline is recorded) */
 #define MAYA_OPT_LANE_SCHED 4 /* schedule every job that fits with the lane-parallel kernel
                                  (default: per job, by the shape of its FIFOs) */
+#define MAYA_OPT_NO_BLOCKS 16 /* generated jobs: one op per kernel launch instead of interned
+                                 kernel blocks (runs of launches of one stream, folded on the
+                                 device); required to record a timeline of generated jobs */
 int maya_set_options(maya_engine *eng, int32_t options);
 /* Per staged job: 1 if it is simulated as rank classes. */
 int maya_batch_collapsed(maya_engine *eng, uint8_t *out);
@@ -177,10 +180,11 @@ int64_t maya_arena_bytes(maya_engine *eng);
 
 /* Batch totals of the staged batch: [0] jobs, [1] sum of rep trace events,
  * [2] sum over ranks of rep CommInits, [3] kernel features, [4] group-call
- * slots, [5] device ops (stream-major records), [6] rank-ops, [7] arena bytes,
- * [8] ranks, [9] reps, [10] kernels launched by the last maya_run,
- * [11] kernels launched by the last maya_topk. */
-int maya_batch_stats(maya_engine *eng, int64_t *out12);
+ * slots, [5] device op records (stream-major; a kernel block is one record),
+ * [6] rank-ops, [7] arena bytes, [8] ranks, [9] reps, [10] kernels launched by
+ * the last maya_run, [11] kernels launched by the last maya_topk, [12] kernel
+ * blocks, [13] block feature ids. */
+int maya_batch_stats(maya_engine *eng, int64_t *out14);
 
 /* Scheduler phase counters of instrumented builds (-DMAYA_PROFILE); returns
  * 0 (and leaves out8 untouched) in product builds. */

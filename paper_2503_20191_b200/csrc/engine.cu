@@ -94,11 +94,14 @@ struct maya_engine {
   // segments
   Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_slots, s_walkers, s_reps, s_ops, s_streams,
       s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
-      s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks, s_grid_parts, s_comm_part;
+      s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks, s_grid_parts, s_comm_part, s_blocks,
+      s_blk_fids;
   Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst, x_gsync;
   std::vector<GridPart> grid_parts;        // host copy (launch grouping)
   std::vector<std::pair<uint32_t, uint32_t>> grid_launches;   // part ranges per launch
   uint32_t grid_smem = 0;
+  Seg x_blk_ab;
+  bool has_blocks = false;             // staged jobs carry kernel blocks (must run folded)
   Seg x_exec, x_rcw, x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
       x_results, x_err, x_topk, x_topk_out, x_topk_n;
   uint64_t n_tl = 0;
@@ -142,10 +145,12 @@ uint32_t lane_slots_of(uint32_t len, uint32_t lgd_max) {
   return 1u << lg;
 }
 
+// device events of a FIFO (a kernel block counts its launches): the shape the
+// kernel-choice thresholds below were tuned on
 uint32_t lane_fifo_len(const JobPack &P, uint32_t w) {
   const Walker wk = P.walkers[w];
   const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
-  return P.streams[h.streams + wk.stream].len;
+  return P.stream_events[h.streams + wk.stream];
 }
 
 static const uint32_t GRID_PART_FIFOS = 256;   // one FIFO per thread of a grid-job CTA
@@ -246,11 +251,11 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
       const RankRec &rr = P.ranks[wk.rank];
       const RepHdr &h = P.reps[rr.rep];
       const StreamRange &sr = P.streams[h.streams + wk.stream];
-      const uint32_t n = std::min<uint32_t>(sr.len, 4096);
-      uint32_t blockers = 0;
-      for (uint32_t q = 0; q < n; q++) {
+      uint32_t n = 0, blockers = 0;   // over the first ~4k device events
+      for (uint32_t q = 0; q < sr.len && n < 4096; q++) {
         const Op &o = P.ops[h.ops + sr.begin + q];
         const uint32_t tg = op_tag(o.meta);
+        n += (tg == TAG_KERN && (o.arg & KBLOCK)) ? P.blocks[o.arg & ~KBLOCK].n : 1u;
         if (tg == TAG_WAIT) {
           blockers++;
         } else if (tg == TAG_COLL) {
@@ -379,6 +384,8 @@ bool pack_eq(const JobPack &a, const JobPack &b) {
          vec_eq(a.walkers, b.walkers) && vec_eq(a.wids, b.wids) && vec_eq(a.rcolls, b.rcolls) &&
          vec_eq(a.rep_ring_ok, b.rep_ring_ok) && vec_eq(a.comm_rdv, b.comm_rdv) &&
          vec_eq(a.rank_orig, b.rank_orig) && vec_eq(a.rank_sim, b.rank_sim) &&
+         vec_eq(a.stream_events, b.stream_events) && vec_eq(a.blocks, b.blocks) &&
+         vec_eq(a.blk_fids, b.blk_fids) &&
          a.collapsed == b.collapsed && a.n_fire == b.n_fire && a.n_delay == b.n_delay;
 }
 }  // namespace
@@ -491,7 +498,8 @@ int maya_upload(maya_engine *e) {
   // totals
   size_t n_ranks = 0, n_rank_comm = 0, n_comms = 0, n_slots = 0, n_walkers = 0, n_reps = 0,
          n_ops = 0, n_streams = 0, n_colls = 0, n_syncs = 0, n_counts = 0, n_mems = 0,
-         n_feats = 0, n_fire = 0, n_delay = 0, n_wstate = 0, n_rcolls = 0, n_chunks = 0;
+         n_feats = 0, n_fire = 0, n_delay = 0, n_wstate = 0, n_rcolls = 0, n_chunks = 0,
+         n_blocks = 0, n_blk_fids = 0;
   uint64_t n_tl = 0;
   e->job_tl.resize(nj);
   e->job_ops.resize(nj);
@@ -514,6 +522,8 @@ int maya_upload(maya_engine *e) {
     n_counts += P.counts.size();
     n_mems += P.mems.size();
     n_feats += P.feats.size();
+    n_blocks += P.blocks.size();
+    n_blk_fids += P.blk_fids.size();
     n_fire += P.n_fire;
     n_delay += P.n_delay;
     n_rcolls += P.rcolls.size();
@@ -551,6 +561,8 @@ int maya_upload(maya_engine *e) {
   }
   if (n_reps > 0xffffffffull) return fail(MAYA_EINVAL, "too many representatives in batch");
   if (n_feats >= 0xffffffffull) return fail(MAYA_EINVAL, "too many kernel features in batch");
+  if (n_blocks >= KBLOCK) return fail(MAYA_EINVAL, "too many kernel blocks in batch");
+  e->has_blocks = n_blocks > 0;
   if (n_slots >= 0xffffffffull) return fail(MAYA_EINVAL, "too many collective calls in batch");
   e->n_tl = n_tl;
   // arena layout
@@ -587,6 +599,8 @@ int maya_upload(maya_engine *e) {
   for (size_t j = 0; j < nj; j++) n_parts += plans[j].parts.size();
   seg(e->s_grid_parts, n_parts * sizeof(GridPart));
   seg(e->s_comm_part, n_comms * sizeof(uint32_t));
+  seg(e->s_blocks, n_blocks * sizeof(KBlock));
+  seg(e->s_blk_fids, n_blk_fids * sizeof(uint32_t));
   e->arena_bytes = off;
   // scratch layout
   off = 0;
@@ -599,6 +613,7 @@ int maya_upload(maya_engine *e) {
   seg(e->x_ccounts, n_counts * sizeof(uint32_t));
   seg(e->x_rcw, n_rcolls * sizeof(RCX));
   seg(e->x_feat_ns, n_feats * 8);
+  seg(e->x_blk_ab, n_blocks * 16);
   seg(e->x_wire, n_slots * 8);
   seg(e->x_fire, n_fire * 8);
   seg(e->x_delay, n_delay * 8);
@@ -670,7 +685,7 @@ int maya_upload(maya_engine *e) {
   // per-job bases (serial prefix), then parallel copy
   struct Base {
     size_t ranks, rank_comm, comms, slots, walkers, reps, ops, streams, colls, syncs, counts,
-        mems, feats, fire, delay, wstate, rcolls, perm;
+        mems, feats, fire, delay, wstate, rcolls, perm, blocks, blk_fids;
   };
   std::vector<Base> bases(nj);
   {
@@ -691,6 +706,8 @@ int maya_upload(maya_engine *e) {
       b.counts += P.counts.size();
       b.mems += P.mems.size();
       b.feats += P.feats.size();
+      b.blocks += P.blocks.size();
+      b.blk_fids += P.blk_fids.size();
       b.fire += P.n_fire;
       b.delay += P.n_delay;
       b.rcolls += P.rcolls.size();
@@ -766,6 +783,9 @@ int maya_upload(maya_engine *e) {
     h.wstate = B.wstate;
     h.timeline = e->job_tl[j];
     h.rcolls = B.rcolls;
+    h.blocks = B.blocks;
+    h.blk_fids = B.blk_fids;
+    h.n_blocks = (uint32_t)P.blocks.size();
     memcpy(H + e->s_jobs.off + j * sizeof(JobHdr), &h, sizeof h);
     RankRec *rk = (RankRec *)(H + e->s_ranks.off) + B.ranks;
     for (size_t r = 0; r < P.ranks.size(); r++) {
@@ -794,13 +814,23 @@ int maya_upload(maya_engine *e) {
     CPY(s_slots, slots, B.slots)
     CPY(s_walkers, walkers, B.walkers)
     CPY(s_wids, wids, B.walkers)
-    {  // ops: KERN args become batch-global feature ids
+    {  // ops: KERN args become batch-global feature (or kernel block) ids
       Op *dst = (Op *)(H + e->s_ops.off) + B.ops;
       for (size_t q = 0; q < P.ops.size(); q++) {
         Op o = P.ops[q];
-        if (op_tag(o.meta) == TAG_KERN) o.arg += (uint32_t)B.feats;
+        if (op_tag(o.meta) == TAG_KERN)
+          o.arg = (o.arg & KBLOCK) ? (KBLOCK | ((o.arg & ~KBLOCK) + (uint32_t)B.blocks))
+                                   : o.arg + (uint32_t)B.feats;
         dst[q] = o;
       }
+      KBlock *kb = (KBlock *)(H + e->s_blocks.off) + B.blocks;
+      for (size_t q = 0; q < P.blocks.size(); q++) {
+        KBlock x = P.blocks[q];
+        x.fid0 += (uint32_t)B.blk_fids;
+        kb[q] = x;
+      }
+      uint32_t *bf = (uint32_t *)(H + e->s_blk_fids.off) + B.blk_fids;
+      for (size_t q = 0; q < P.blk_fids.size(); q++) bf[q] = P.blk_fids[q] + (uint32_t)B.feats;
     }
     CPY(s_rcolls, rcolls, B.rcolls)
     {  // lane-scheduler plan and per-walker ring words
@@ -911,6 +941,9 @@ int maya_upload(maya_engine *e) {
   db.counts = (const uint32_t *)(D + e->s_counts.off);
   db.mems = (const MemRec *)(D + e->s_mems.off);
   db.feats = (const Feature *)(D + e->s_feats.off);
+  db.blocks = (const KBlock *)(D + e->s_blocks.off);
+  db.blk_fids = (const uint32_t *)(D + e->s_blk_fids.off);
+  db.n_blocks = (uint32_t)n_blocks;
   db.rcolls = (const RankColl *)(D + e->s_rcolls.off);
   db.rcslot = (const uint32_t *)(D + e->s_rcslot.off);
   db.rcx = (RCX *)(X + e->x_rcw.off);
@@ -955,6 +988,9 @@ int maya_upload(maya_engine *e) {
 
 int maya_run(maya_engine *e, int32_t record_timeline) {
   if (!e->uploaded) return fail(MAYA_ESTATE, "maya_run before maya_upload");
+  if (e->has_blocks && (record_timeline || (e->options & MAYA_OPT_NO_FOLD)))
+    return fail(MAYA_ESTATE, "batch staged with kernel blocks runs folded only: set "
+                             "MAYA_OPT_NO_BLOCKS before staging to record a timeline");
   CU(cudaSetDevice(e->device));
   DevBatch db = e->db;
   if (record_timeline) {
@@ -991,6 +1027,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   // runs fold (fold_kernel) unless a per-op timeline is recorded
   const bool fold = !record_timeline && !(e->options & MAYA_OPT_NO_FOLD);
   db.clen = fold ? (uint32_t *)(X + e->x_clen.off) : nullptr;
+  db.blk_ab = (int64_t *)(X + e->x_blk_ab.off);
   db.lane_gctx = (uint8_t *)(X + e->x_lctx.off);
   db.lane_gst = (uint8_t *)(X + e->x_lst.off);
   db.gsync = (GridSync *)(X + e->x_gsync.off);
@@ -1134,7 +1171,7 @@ int maya_get_stream(maya_engine *e, void **stream) {
 int64_t maya_arena_bytes(maya_engine *e) { return (int64_t)e->arena_bytes; }
 
 int maya_batch_stats(maya_engine *e, int64_t *o) {
-  for (int i = 0; i < 12; i++) o[i] = 0;
+  for (int i = 0; i < 14; i++) o[i] = 0;
   o[10] = e->run_launches;
   o[11] = e->topk_launches;
   o[0] = (int64_t)e->packs.size();
@@ -1148,6 +1185,8 @@ int maya_batch_stats(maya_engine *e, int64_t *o) {
     o[6] += P.hdr.rank_ops;
     o[8] += (int64_t)P.ranks.size();
     o[9] += (int64_t)P.reps.size();
+    o[12] += (int64_t)P.blocks.size();
+    o[13] += (int64_t)P.blk_fids.size();
   }
   o[7] = (int64_t)e->arena_bytes;
   return MAYA_OK;
@@ -1323,7 +1362,8 @@ int maya_batch_add_generated(maya_engine *e, const maya_model *model, int32_t n,
       const int32_t kr = key_ranks ? key_ranks[i] : i;
       // fused generate -> pack (no raw event arrays)
       int rc = pack_generated(*model, cfgs[i], *cluster, schedule, dispatch_overhead_ns, device,
-                              kr, (e->options & MAYA_OPT_COLLAPSE) != 0, g, P, &err);
+                              kr, (e->options & MAYA_OPT_COLLAPSE) != 0, g, P, &err,
+                              !(e->options & MAYA_OPT_NO_BLOCKS));
       if (status_out) status_out[i] = rc;
       if (rc != MAYA_OK) {
         P.clear();

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <unordered_map>
 
 namespace maya {
@@ -52,10 +53,6 @@ inline int64_t fdiv(i128 a, i128 b) {
   return chk(q);
 }
 
-struct KSpec {
-  int op;
-  int64_t flops, bytes;
-};
 
 KSpec gemm(i128 m, i128 n, i128 k, i128 esz) {  // workload.py:316-318
   return KSpec{OK_GEMM, chk(2 * m * n * k), chk(esz * (m * k + k * n + m * n))};
@@ -297,9 +294,19 @@ struct Builder {
   std::vector<std::vector<std::pair<int8_t, int64_t>>> calls;  // per local comm
   std::vector<int64_t> next_version, last_version;   // by event id (small)
   int64_t next_alloc = 0;
+  // kernel blocks (sinks that take them): the open run of kernel launches
+  bool blocks = false;
+  int32_t run_stream = 0;
+  std::vector<KSpec> run;
 
+  void flush() {
+    if (run.empty()) return;
+    sink->kernel_block(run_stream, run.data(), run.size(), overhead > 0 ? overhead : 0, dtype);
+    run.clear();
+  }
   void ev(uint8_t k, int32_t s, int64_t a, int64_t b = 0, int64_t c = 0, int64_t d = 0) {
     if (sink) {
+      if (!run.empty()) flush();
       sink->ev(k, s, a, b, c, d);
       return;
     }
@@ -317,6 +324,12 @@ struct Builder {
     if (overhead > 0) ev(MAYA_EV_HOSTGAP, 0, overhead);
   }
   void kernel(int32_t s, const KSpec &k) {
+    if (blocks) {   // [HostGap, KernelLaunch] joins the open run of stream s
+      if (!run.empty() && run_stream != s) flush();
+      run_stream = s;
+      run.push_back(k);
+      return;
+    }
     gap();
     ev(MAYA_EV_KERNEL, s, k.op, dtype, k.flops, k.bytes);
   }
@@ -370,6 +383,7 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   const i128 u = sp ? t : 1;
 
   Builder B{G.ev_kind, G.ev_stream, G.ev_f, sink, overhead, dtype, {}, {}, {}, {}, {}, 0};
+  B.blocks = sink && sink->takes_blocks();
   {  // reserve for this trace: ~ (2 x kernels per layer-microbatch) + specials
     const size_t est = (size_t)(cfg.micro_mult) * (size_t)cfg.pp * (size_t)(M.L / cfg.pp + 2) *
                            (cfg.act_recompute ? 110 : 80) + 4096;
@@ -382,20 +396,20 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
     }
   }
   std::vector<CommRole> roles = worker_comms(C, v, rank);
-  // local comm index of each role (first CommInit of a comm id)
-  std::map<std::string, int> local;
+  // local comm index of each role (first CommInit of a comm id); keyed by the
+  // role's integer fields, which comm_name spells out one to one
+  std::map<std::tuple<int, int64_t, int64_t, int64_t>, int> local;
   for (const CommRole &r : roles) {
-    std::string nm = comm_name(r);
     int lc = (int)B.comm_nranks.size();
-    if (!local.emplace(nm, lc).second) throw GenFail{"duplicate communicator"};
+    if (!local.emplace(std::make_tuple(r.type, r.a, r.b, r.c), lc).second)
+      throw GenFail{"duplicate communicator"};
     B.comm_nranks.push_back(r.nranks);
     B.call_idx.push_back(0);
     B.calls.emplace_back();
     B.ev(MAYA_EV_COMMINIT, 0, lc, r.nranks, r.my_rank);
   }
   auto lc_of = [&](int type, int64_t a, int64_t b2, int64_t c2) {
-    CommRole r{type, a, b2, c2, 0, 0};
-    auto it = local.find(comm_name(r));
+    auto it = local.find(std::make_tuple(type, a, b2, c2));
     if (it == local.end()) throw GenFail{"communicator missing from worker_comms"};
     return it->second;
   };

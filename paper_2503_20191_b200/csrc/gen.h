@@ -43,6 +43,12 @@ struct GenJob {
   }
 };
 
+// One kernel launch of the generator's inventory (workload.py:316-378).
+struct KSpec {
+  int op;
+  int64_t flops, bytes;
+};
+
 // Receives the events of each representative trace in order instead of the
 // raw arrays (the fused generate -> pack path, pack.cpp pack_generated).
 struct EventSink {
@@ -50,6 +56,11 @@ struct EventSink {
   virtual void rep_begin(size_t est_events) = 0;
   virtual void ev(uint8_t k, int32_t s, int64_t a, int64_t b, int64_t c, int64_t d) = 0;
   virtual void rep_end() = 0;
+  // A sink that takes kernel blocks receives each maximal run of kernel
+  // launches on one stream (with nothing else in between) as ONE call: the
+  // events [HostGap(gap) if gap > 0, KernelLaunch(ks[i], dtype)] for i < n.
+  virtual bool takes_blocks() const { return false; }
+  virtual void kernel_block(int32_t, const KSpec *, size_t, int64_t, int32_t) {}
 };
 
 // Returns 0 or a negative code with *err set (invalid configuration).  With a

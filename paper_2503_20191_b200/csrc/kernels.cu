@@ -1029,6 +1029,59 @@ __device__ __forceinline__ bool op_foldable(const Op &o) {
   return op_tag(o.meta) == TAG_KERN && o.disp < ((int64_t)1 << 61);
 }
 
+// Kernel blocks (soa.h KBLOCK): the composite of a block's n kernels, kernel k
+// dispatched k*gap after the first, relative to the first kernel's disp:
+// A = sum d_k, Brel = fold of (k*gap + d_k) -- the same saturating maps the
+// fold pass composes op by op, composed once per interned block (affine
+// max-plus composition is associative, so the folded FIFO is identical up to
+// where runs are cut, and the schedule is exact either way).  One warp per
+// block: each lane composes a contiguous slice, then a shuffle tree.
+__global__ void block_compose_kernel(DevBatch b) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= b.n_blocks) return;
+  const KBlock kb = b.blocks[i];
+  const uint32_t *fp = b.blk_fids + kb.fid0;
+  const uint32_t per = (kb.n + 31) / 32, k0 = lane * per, k1 = min(kb.n, k0 + per);
+  int64_t A = 0, B = 0;
+  bool any = false;
+  for (uint32_t k = k0; k < k1; k++) {
+    const int64_t d = b.feat_ns[fp[k]];
+    const int64_t de = (d < 0 || d > FOLD_SAT) ? FOLD_SAT : d;
+    const int64_t bk = sat_add((int64_t)k * kb.gap, de);   // k * gap < 2^61 (packer)
+    if (!any) {
+      A = de;
+      B = bk;
+      any = true;
+    } else {
+      const int64_t nb = sat_add(B, de);
+      B = nb > bk ? nb : bk;
+      A = sat_add(A, de);
+    }
+  }
+  // left-to-right tree: lane L absorbs lane L + off (identity: empty slice)
+#pragma unroll
+  for (uint32_t off = 1; off < 32; off <<= 1) {
+    const int64_t A2 = __shfl_down_sync(FULL, A, off), B2 = __shfl_down_sync(FULL, B, off);
+    const bool any2 = __shfl_down_sync(FULL, any, off);
+    if ((lane & (2 * off - 1)) == 0 && lane + off < 32 && any2) {
+      if (any) {
+        const int64_t nb = sat_add(B, A2);
+        B = nb > B2 ? nb : B2;
+        A = sat_add(A, A2);
+      } else {
+        A = A2;
+        B = B2;
+        any = true;
+      }
+    }
+  }
+  if (lane == 0) {
+    b.blk_ab[2 * (size_t)i] = A;
+    b.blk_ab[2 * (size_t)i + 1] = B;
+  }
+}
+
 // pass 1: folded ops per chunk
 static constexpr uint32_t FOLD_WARPS = 2;             // warps (chunks) per CTA
 static constexpr uint32_t FOLD_PAD = FOLD_CHUNK + FOLD_CHUNK / 32;   // one pad op per 32
@@ -1110,7 +1163,7 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
   for (uint32_t base = lo; base < hi; base += 128) {
     const uint32_t j0 = base + lane * 4u;
     Op o[4];
-    int64_t d[4];
+    int64_t d[4], bx[4];   // bx >= 0: a kernel block's Brel (d is its A)
     bool v[4], f[4], st[4];
     uint32_t sg[4];
 #pragma unroll
@@ -1120,7 +1173,17 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
       sg[t] = op_seg(o[t].meta);
       f[t] = v[t] && op_foldable(o[t]);
       d[t] = 0;
-      if (v[t] && op_tag(o[t].meta) == TAG_KERN) d[t] = b.feat_ns[o[t].arg];
+      bx[t] = -1;
+      if (v[t] && op_tag(o[t].meta) == TAG_KERN) {
+        if (o[t].arg & KBLOCK) {
+          const longlong2 ab =
+              *reinterpret_cast<const longlong2 *>(b.blk_ab + 2 * (size_t)(o[t].arg & ~KBLOCK));
+          d[t] = ab.x;
+          bx[t] = ab.y;
+        } else {
+          d[t] = b.feat_ns[o[t].arg];
+        }
+      }
     }
     // previous op of each of the lane's ops
     uint32_t psg = __shfl_up_sync(FULL, sg[3], 1);
@@ -1144,7 +1207,7 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
     for (int t = 0; t < 4; t++) {
       if (!v[t]) continue;
       const int64_t de = (d[t] < 0 || d[t] > FOLD_SAT) ? FOLD_SAT : d[t];
-      const int64_t a = f[t] ? de : 0, bb = f[t] ? sat_add(o[t].disp, de) : 0;
+      const int64_t a = f[t] ? de : 0, bb = f[t] ? sat_add(o[t].disp, bx[t] >= 0 ? bx[t] : de) : 0;
       if (st[t]) {
         A = a;
         B = bb;
@@ -1199,7 +1262,7 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
     for (int t = 0; t < 4; t++) {
       if (!v[t]) continue;
       const int64_t de = (d[t] < 0 || d[t] > FOLD_SAT) ? FOLD_SAT : d[t];
-      const int64_t a = f[t] ? de : 0, bb = f[t] ? sat_add(o[t].disp, de) : 0;
+      const int64_t a = f[t] ? de : 0, bb = f[t] ? sat_add(o[t].disp, bx[t] >= 0 ? bx[t] : de) : 0;
       if (st[t]) {
         oidx++;
         rA = a;
@@ -1225,7 +1288,8 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
           const uint32_t tag = op_tag(o[t].meta);
           const bool bad = d[t] < 0 || d[t] >= (int64_t)(EXEC_BAD >> 2);
           uint64_t pay;
-          if (tag == TAG_KERN) pay = bad ? (EXEC_BAD >> 2) : (uint64_t)d[t];
+          if (tag == TAG_KERN && bx[t] >= 0) pay = EXEC_OVF >> 2;   // blocks always fold (packer)
+          else if (tag == TAG_KERN) pay = bad ? (EXEC_BAD >> 2) : (uint64_t)d[t];
           else pay = (o[t].arg == NO_REC) ? (EXEC_NONE >> 2) : (uint64_t)o[t].arg;
           out[oidx] = ExecOp{o[t].disp, (pay << 2) | tag};
         }
@@ -1283,6 +1347,8 @@ __global__ void fold_empty_kernel(DevBatch b) {
 
 void launch_resolve(const DevBatch &b, cudaStream_t s) {
   if (b.clen) {
+    if (b.n_blocks)
+      block_compose_kernel<<<(unsigned)((b.n_blocks * 32ull + 255) / 256), 256, 0, s>>>(b);
     if (b.n_chunks) {
       const unsigned g = (b.n_chunks + FOLD_WARPS - 1) / FOLD_WARPS;
       fold_count_kernel<<<g, FOLD_WARPS * 32, 0, s>>>(b);

@@ -32,6 +32,9 @@ struct DevBatch {
   const uint32_t *counts;
   const MemRec *mems;
   const Feature *feats;
+  const KBlock *blocks;       // kernel blocks (batch-global fid lists)
+  const uint32_t *blk_fids;
+  int64_t *blk_ab;            // per block: (A, Brel) composite after the estimator
   const RankColl *rcolls;
   const uint32_t *rcslot;     // batch-global call slot of each rank-collective entry
   RCX *rcx;                   // entry + wire time of each rank-collective entry (resolve)
@@ -62,7 +65,7 @@ struct DevBatch {
   uint32_t *clen;             // folded FIFO lengths (fold_kernel) or null: unfolded ops
   uint32_t *ccounts;          // host-sync dispatch counts in folded indices (with clen)
   int32_t *err_flag;          // any estimator failure
-  uint32_t n_jobs, n_reps, n_feats, n_slots;
+  uint32_t n_jobs, n_reps, n_feats, n_slots, n_blocks;
   uint64_t n_ops, n_rcolls;
 };
 

@@ -50,12 +50,14 @@ struct RepBuild {
   std::vector<int32_t> raw_of;                 // local stream -> raw handle
   std::vector<std::vector<Op>> sops;           // per local stream (first n_live used)
   std::vector<std::vector<uint32_t>> sseq;
+  std::vector<uint32_t> sev;                   // per local stream: device events (blocks expanded)
   size_t n_live = 0;
   int last_raw = INT32_MIN, last_local = -1;
   size_t reserve_hint = 0;
 
   void reset(size_t hint) {
     raw_of.clear();
+    sev.clear();
     for (size_t i = 0; i < n_live; i++) {
       sops[i].clear();
       sseq[i].clear();
@@ -73,6 +75,7 @@ struct RepBuild {
       if (raw_of[i] == raw) { last_raw = raw; last_local = (int)i; return (int)i; }
     if (!create) return -1;
     raw_of.push_back(raw);
+    sev.push_back(0);
     if (n_live == sops.size()) {
       sops.emplace_back();
       sseq.emplace_back();
@@ -98,10 +101,22 @@ struct FeatCacheEnt {
 struct FeatState {
   std::unordered_map<FeatKey, uint32_t, FeatHash> feat_map;
   std::unordered_map<int64_t, uint32_t> fixed_map;
+  std::unordered_map<uint64_t, uint32_t> blk_map;    // launch-list hash -> kernel block id
+  struct BlkKey {
+    size_t spec0;
+    uint32_t n;
+    int32_t dtype;
+    int64_t gap;
+  };
+  std::vector<BlkKey> blk_keys;                      // per block id: its launch list
+  std::vector<KSpec> blk_specs;
   FeatCacheEnt fcache[64];
   void clear() {
     feat_map.clear();
     fixed_map.clear();
+    blk_map.clear();
+    blk_keys.clear();
+    blk_specs.clear();
     for (auto &ce : fcache) ce.fid = UINT32_MAX;
   }
 };
@@ -130,7 +145,7 @@ struct RepPacker {
   bool ring_ok = true;
   uint64_t coll0 = 0, mem0 = 0, sync0 = 0;
   int64_t gpre = 0;
-  uint32_t seg = 0, seq = 0;
+  uint32_t seg = 0, seq = 0, n_devev = 0;
 
   static uint64_t ekey(int64_t ev, int64_t ver) {
     if (ev < 0 || ev > 0x7fffffff || ver < 0 || ver > 0x7fffffff)
@@ -163,6 +178,7 @@ struct RepPacker {
     gpre = 0;
     seg = 0;
     seq = 0;
+    n_devev = 0;
   }
 
   // raw mode: the first pass over the rep's events
@@ -208,6 +224,8 @@ struct RepPacker {
     if (seg >= (1u << 30)) throw Fail{MAYA_ST_BAD_INPUT, "too many host syncs"};
     RB.sops[ls].push_back(Op{gpre, arg, tag | (seg << 2)});
     RB.sseq[ls].push_back(seq);
+    RB.sev[ls]++;
+    n_devev++;
   }
   void sync(uint32_t type, uint32_t arg) {
     std::vector<uint32_t> c(RB.size());
@@ -215,6 +233,89 @@ struct RepPacker {
     snap.push_back(std::move(c));
     P->syncs.push_back(SyncRec{gpre, type, arg, 0, 0});
     seg++;
+  }
+
+  // job-local id of roofline feature (op kind, dtype, flops, bytes)
+  uint32_t feature(const int64_t *f) {
+    // direct-mapped cache in front of the hash map: kernel templates repeat
+    const uint64_t hk = ((uint64_t)f[2] * 0x9e3779b97f4a7c15ull) ^ (uint64_t)f[3] ^
+                        ((uint64_t)f[0] << 48) ^ ((uint64_t)f[1] << 56);
+    FeatCacheEnt &ce = F->fcache[(hk >> 58) & 63];
+    if (ce.fid != UINT32_MAX && ce.k[0] == f[0] && ce.k[1] == f[1] && ce.k[2] == f[2] &&
+        ce.k[3] == f[3])
+      return ce.fid;
+    uint32_t fid;
+    FeatKey key{f[0], f[1], f[2], f[3]};
+    auto it = F->feat_map.find(key);
+    if (it == F->feat_map.end()) {
+      fid = (uint32_t)P->feats.size();
+      F->feat_map.emplace(key, fid);
+      P->feats.push_back(Feature{f[2], f[3], -1, (int32_t)f[0], (int16_t)f[1], (int16_t)device});
+    } else {
+      fid = it->second;
+    }
+    ce = FeatCacheEnt{{f[0], f[1], f[2], f[3]}, fid};
+    return fid;
+  }
+
+  // A run of n kernel launches on one stream, each after a host gap of `gap`
+  // (the events [HostGap(gap) if gap > 0, KernelLaunch] x n): ONE KBLOCK op
+  // whose disp is the first kernel's, the block interned per job.  Single
+  // kernels, and runs reaching the fold limit of the gap prefix (2^61), go
+  // through the per-event path (kernels.cu op_foldable).
+  void kernel_block(int32_t stream, const KSpec *ks, size_t n, int64_t gap, int32_t dtype) {
+    const bool fits = gap >= 0 && n >= 2 && n < (1u << 24) &&
+                      (gap == 0 || (int64_t)n <= (((int64_t)1 << 61) - 1 - gpre) / gap);
+    if (!fits) {
+      for (size_t i = 0; i < n; i++) {
+        if (gap > 0) {
+          const int64_t g[4] = {gap, 0, 0, 0};
+          event(MAYA_EV_HOSTGAP, 0, g, -1, false);
+        }
+        const int64_t f[4] = {ks[i].op, dtype, ks[i].flops, ks[i].bytes};
+        event(MAYA_EV_KERNEL, stream, f, -1, false);
+      }
+      return;
+    }
+    // intern by the launch list itself: a repeated layer body costs a hash
+    // and a compare, no per-kernel feature lookups
+    uint64_t hsh = (1469598103934665603ull ^ (uint64_t)gap) * 1099511628211ull;
+    hsh = (hsh ^ ((uint64_t)n << 8 | (uint32_t)dtype)) * 1099511628211ull;
+    for (size_t i = 0; i < n; i++) {
+      hsh = (hsh ^ (uint64_t)ks[i].op) * 1099511628211ull;
+      hsh = (hsh ^ (uint64_t)ks[i].flops) * 1099511628211ull;
+      hsh = (hsh ^ (uint64_t)ks[i].bytes) * 1099511628211ull;
+    }
+    uint32_t id = UINT32_MAX;
+    auto it = F->blk_map.find(hsh);
+    if (it != F->blk_map.end()) {
+      const FeatState::BlkKey &bk = F->blk_keys[it->second];
+      bool same = bk.n == n && bk.gap == gap && bk.dtype == dtype;
+      for (size_t i = 0; same && i < n; i++) {
+        const KSpec &x = F->blk_specs[bk.spec0 + i];
+        same = x.op == ks[i].op && x.flops == ks[i].flops && x.bytes == ks[i].bytes;
+      }
+      if (same) id = it->second;
+    }
+    if (id == UINT32_MAX) {
+      id = (uint32_t)P->blocks.size();
+      if (id >= KBLOCK) throw Fail{MAYA_ST_BAD_INPUT, "too many kernel blocks"};
+      P->blocks.push_back(KBlock{(uint32_t)P->blk_fids.size(), (uint32_t)n, gap});
+      F->blk_keys.push_back(FeatState::BlkKey{F->blk_specs.size(), (uint32_t)n, dtype, gap});
+      for (size_t i = 0; i < n; i++) {
+        const int64_t f[4] = {ks[i].op, dtype, ks[i].flops, ks[i].bytes};
+        P->blk_fids.push_back(feature(f));
+        F->blk_specs.push_back(ks[i]);
+      }
+      F->blk_map.emplace(hsh, id);   // first block of this hash stays the interned one
+    }
+    gpre += gap;                     // the first kernel's gap
+    seq += gap > 0 ? 1 : 0;
+    emit(stream, TAG_KERN, KBLOCK | id);
+    gpre += (int64_t)(n - 1) * gap;
+    seq += (uint32_t)((n - 1) * (gap > 0 ? 2 : 1) + 1);
+    n_devev += (uint32_t)(n - 1);
+    RB.sev[RB.local_stream(stream, false)] += (uint32_t)(n - 1);
   }
 
   // one event (trace.py:71-151 as rawtrace.py arrays); host_ns >= 0: a
@@ -245,26 +346,7 @@ struct RepPacker {
             fid = it->second;
           }
         } else {
-          // direct-mapped cache in front of the hash map: kernel templates repeat
-          const uint64_t hk = ((uint64_t)f[2] * 0x9e3779b97f4a7c15ull) ^ (uint64_t)f[3] ^
-                              ((uint64_t)f[0] << 48) ^ ((uint64_t)f[1] << 56);
-          FeatCacheEnt &ce = F->fcache[(hk >> 58) & 63];
-          if (ce.fid != UINT32_MAX && ce.k[0] == f[0] && ce.k[1] == f[1] && ce.k[2] == f[2] &&
-              ce.k[3] == f[3]) {
-            fid = ce.fid;
-          } else {
-            FeatKey key{f[0], f[1], f[2], f[3]};
-            auto it = F->feat_map.find(key);
-            if (it == F->feat_map.end()) {
-              fid = (uint32_t)P->feats.size();
-              F->feat_map.emplace(key, fid);
-              P->feats.push_back(Feature{f[2], f[3], -1, (int32_t)f[0], (int16_t)f[1],
-                                         (int16_t)device});
-            } else {
-              fid = it->second;
-            }
-            ce = FeatCacheEnt{{f[0], f[1], f[2], f[3]}, fid};
-          }
+          fid = feature(f);
         }
         emit(stream, TAG_KERN, fid);
         break;
@@ -341,6 +423,7 @@ struct RepPacker {
 
   void finish() {
     h.n_events = seq;
+    h.n_devev = n_devev;
     h.n_recs = n_recs;
     // collectives renumbered stream-major: the collectives of one FIFO are
     // consecutive in the per-rank collective tables, so a walker reads (and
@@ -381,6 +464,7 @@ struct RepPacker {
         }
       }
       P->streams.push_back(StreamRange{pos, (uint32_t)RB.sops[s].size(), RB.raw_of[s], folded});
+      P->stream_events.push_back(RB.sev[s]);
       P->ops.insert(P->ops.end(), RB.sops[s].begin(), RB.sops[s].end());
       P->op_seq.insert(P->op_seq.end(), RB.sseq[s].begin(), RB.sseq[s].end());
       pos += (uint32_t)RB.sops[s].size();
@@ -624,7 +708,7 @@ namespace {
 // pass gathers one per op), which matters when features are mostly unique.
 void renumber_features(JobPack &P) {
   const uint32_t nf = (uint32_t)P.feats.size();
-  if (nf < 2) return;
+  if (nf < 2 || !P.blocks.empty()) return;   // block jobs: few per-op gathers remain
   std::vector<uint32_t> nid(nf, UINT32_MAX);
   uint32_t next = 0;
   for (Op &o : P.ops) {
@@ -687,7 +771,7 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
   for (int r = 0; r < job.num_ranks; r++) {
     const RepHdr &h = P.reps[job.rank_rep[r]];
     rank_ops += h.n_events;
-    dev_ops += h.n_ops;
+    dev_ops += h.n_devev;
   }
   // simulated ranks
   uint64_t fire = 0, delay = 0, walk = 0, tl = 0;
@@ -780,6 +864,11 @@ struct PackSink final : EventSink {
   RepPacker *RP;
   int32_t device;
   std::vector<uint32_t> *rep_comms;
+  bool blocks = false;
+  bool takes_blocks() const override { return blocks; }
+  void kernel_block(int32_t s, const KSpec *ks, size_t n, int64_t gap, int32_t dtype) override {
+    RP->kernel_block(s, ks, n, gap, dtype);
+  }
   void rep_begin(size_t est_events) override {
     RP->begin(*P, *F, device, true, est_events / 2 + 16);
   }
@@ -816,7 +905,7 @@ void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P, bool collap
 
 int pack_generated(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
                    int32_t schedule, int64_t overhead, int32_t device, int32_t key_rank,
-                   bool collapse, GenJob &G, JobPack &P, std::string *err) {
+                   bool collapse, GenJob &G, JobPack &P, std::string *err, bool blocks) {
   thread_local FeatState F;
   thread_local RepPacker RP;
   F.clear();
@@ -828,6 +917,7 @@ int pack_generated(const maya_model &model, const maya_config &cfg, const maya_c
   sink.RP = &RP;
   sink.device = device;
   sink.rep_comms = &rep_comms;
+  sink.blocks = blocks;
   int rc;
   try {
     rc = generate_job(model, cfg, cl, schedule, overhead, G, err, &sink);

@@ -16,11 +16,14 @@ struct JobPack {
   std::vector<Op> ops;
   std::vector<uint32_t> op_seq;        // event seq of each op (timeline)
   std::vector<StreamRange> streams;
+  std::vector<uint32_t> stream_events; // host only: device events per stream (blocks expanded)
   std::vector<uint32_t> coll_lc, coll_idx;
   std::vector<SyncRec> syncs;
   std::vector<uint32_t> counts;
   std::vector<MemRec> mems;
   std::vector<Feature> feats;
+  std::vector<KBlock> blocks;          // interned kernel blocks (soa.h KBLOCK)
+  std::vector<uint32_t> blk_fids;      // their feature ids, job-local
   std::vector<CommRec> comms;
   std::vector<SlotRec> slots;
   std::vector<RankRec> ranks;
@@ -38,8 +41,9 @@ struct JobPack {
 
   void clear() {   // keeps capacity (see engine.cu PackPool)
     hdr = JobHdr{};
-    reps.clear(); ops.clear(); op_seq.clear(); streams.clear(); coll_lc.clear();
+    reps.clear(); ops.clear(); op_seq.clear(); streams.clear(); stream_events.clear(); coll_lc.clear();
     coll_idx.clear(); syncs.clear(); counts.clear(); mems.clear(); feats.clear(); comms.clear();
+    blocks.clear(); blk_fids.clear();
     slots.clear(); ranks.clear(); rank_comm.clear(); walkers.clear(); wids.clear();
     rcolls.clear(); rep_ring_ok.clear(); comm_rdv.clear(); rank_orig.clear(); rank_sim.clear();
     collapsed = false;
@@ -55,8 +59,11 @@ void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &out, bool coll
 // generator's events go straight into the per-rep packer, never through raw
 // event arrays.  Same JobPack as generate_job + pack_job (tests/test_gen.py).
 // Returns generate_job's code (invalid configuration: <0 with *err set).
+// With blocks, runs of kernel launches become interned kernel blocks (one
+// KBLOCK op each): the batch must then be run folded (no timeline).
 int pack_generated(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
                    int32_t schedule, int64_t overhead, int32_t device, int32_t key_rank,
-                   bool collapse, GenJob &scratch, JobPack &out, std::string *err);
+                   bool collapse, GenJob &scratch, JobPack &out, std::string *err,
+                   bool blocks = false);
 
 }  // namespace maya

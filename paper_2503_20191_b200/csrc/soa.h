@@ -31,6 +31,17 @@ enum OpTag : uint32_t { TAG_KERN = 0, TAG_COLL = 1, TAG_REC = 2, TAG_WAIT = 3 };
 enum SyncType : uint32_t { SYNC_ESYNC = 0, SYNC_SSYNC = 1, SYNC_DSYNC = 2 };
 
 static const uint32_t NO_REC = 0xFFFFFFFFu;
+// Op.arg flag of a KERN op that stands for a kernel BLOCK: n consecutive
+// kernel launches of one stream, each after a host gap of `gap` ns, with no
+// other event in between (the generator's layer bodies).  Blocks are interned
+// per job (KBlock); the device folds each into one affine map after the
+// estimator (kernels.cu block_compose_kernel).  Only in batches that fold.
+static const uint32_t KBLOCK = 0x80000000u;
+struct KBlock {
+  uint32_t fid0;       // job-local index of its first feature id in the job's block fid list
+  uint32_t n;          // kernels (>= 2)
+  int64_t gap;         // host gap before each kernel (ns)
+};
 // On-chip layout of one job inside a scheduler CTA (shared by the engine,
 // which sizes dynamic shared memory, and the kernel).  When the whole layout
 // does not fit the CTA's dynamic shared memory, host-sync counters and walker
@@ -225,6 +236,9 @@ struct RepHdr {
   int64_t gend;        // total host gaps of the trace
   uint32_t n_ops, n_streams, n_recs, n_colls, n_syncs, n_mems;
   uint32_t n_events, job;
+  uint32_t n_devev;    // device events (kernel-class, collective, record, wait): n_ops
+                       // plus the kernels hidden in blocks
+  uint32_t pad3;
 };
 
 // Kernel feature (one per unique (op kind, dtype, flops, bytes) of a job, or a
@@ -299,7 +313,9 @@ struct JobHdr {
   uint32_t flags;      // JobFlags
   uint32_t n_rcolls;
   uint32_t n_fire;     // record-time entries of the simulated ranks
-  uint32_t pad2;
+  uint32_t n_blocks;   // kernel blocks (KBlock) of the job
+  uint64_t blocks;     // batch KBlock index
+  uint64_t blk_fids;   // batch index into the block feature-id list
 };
 
 // per-(rank, rep collective) entry with its wire time (resolve_colls_kernel)

@@ -102,7 +102,7 @@ class Engine:
     """One engine per CUDA device (C ABI: maya_open ... maya_close)."""
 
     def __init__(self, device: int = 0, collapse: bool = True, sched: str = "auto",
-                 fold: bool = True):
+                 fold: bool = True, blocks: bool = True):
         L = lib()
         self._h = C.c_void_p()
         _check(L.maya_open(int(device), C.byref(self._h)))
@@ -111,6 +111,7 @@ class Engine:
         self._collapse = bool(collapse)
         self._sched = sched
         self._fold = bool(fold)
+        self._blocks = bool(blocks)
         self._apply_options()
         self.device = device
         self.batch: Batch | None = None
@@ -129,9 +130,17 @@ class Engine:
         self._sched = sched
         self._apply_options()
 
+    def set_blocks(self, on: bool) -> None:
+        """Generated jobs carry interned kernel blocks (runs of launches of one
+        stream, folded on the device).  Off: one op per launch, which a
+        timeline recording of generated jobs needs."""
+        self._blocks = bool(on)
+        self._apply_options()
+
     def _apply_options(self) -> None:
         opts = ((1 if self._collapse else 0) | (2 if self._sched == "warp" else 0)
-                | (4 if self._sched == "lane" else 0) | (0 if self._fold else 8))
+                | (4 if self._sched == "lane" else 0) | (0 if self._fold else 8)
+                | (16 if not (self._blocks and self._fold) else 0))
         _check(lib().maya_set_options(self._h, opts))
 
     def collapsed(self) -> np.ndarray:
@@ -229,10 +238,11 @@ class Engine:
         return s.value or 0
 
     def batch_stats(self) -> dict:
-        o = (C.c_int64 * 12)()
+        o = (C.c_int64 * 14)()
         _check(lib().maya_batch_stats(self._h, o))
         keys = ("jobs", "rep_events", "rank_comms", "features", "slots", "device_ops",
-                "rank_ops", "arena_bytes", "ranks", "reps", "run_launches", "topk_launches")
+                "rank_ops", "arena_bytes", "ranks", "reps", "run_launches", "topk_launches",
+                "kernel_blocks", "block_fids")
         return {k: int(v) for k, v in zip(keys, o)}
 
     def arena_bytes(self) -> int:

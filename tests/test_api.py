@@ -130,3 +130,35 @@ def test_refmirror_round_trip(golden, name):
         if raw.kernel_ns is not None:
             assert np.array_equal(back.kernel_ns, raw.kernel_ns)
             assert np.array_equal(back.wire_ns, raw.wire_ns)
+
+
+@gpu
+@pytest.mark.parametrize("sched", ["auto", "lane", "warp"])
+def test_c2_kernel_blocks_match_per_launch_ops(sched):
+    """Generated jobs with interned kernel blocks (soa.h KBLOCK, folded on the
+    device by block_compose_kernel) give the same results as one op per
+    launch, on all 512 C2 configs and on each schedule of a 16-rank cluster."""
+    from paper_2503_20191_b200.engine import Engine
+    W, model, cluster = _c2()
+    cfgs = W.enumerate_space(W.SearchSpace(global_batch=512), model, cluster)[:512]
+    cl16 = W.ClusterSpec(2, 8, 80 * 2 ** 30, W.load_device_preset("fast"))
+    cfgs16 = W.enumerate_space(W.SearchSpace(global_batch=256), model, cl16)[::7][:96]
+    out = {}
+    for blocks in (True, False):
+        eng = Engine(0, sched=sched, blocks=blocks)
+        rows = []
+        for cl, cs in ((cluster, cfgs), (cl16, cfgs16)):
+            for schedule in ((None,) if cl is cluster else ("gpipe", "1f1b", "interleaved")):
+                st = eng.stage_generated(model, cs, cl, schedule=schedule,
+                                         dispatch_overhead_ns=5000)
+                eng.upload()
+                eng.run()
+                r = eng.results()
+                rows.append(np.stack([st, r["status"], r["total_ns"], r["peak_mem_bytes"],
+                                      r["oom"], r["dispatched_ops"], r["rank_ops"]]))
+        eng.close()
+        out[blocks] = rows
+    for a, b in zip(out[True], out[False]):
+        assert np.array_equal(a, b)
+    ok = out[True][0][1] == 0
+    assert ok.sum() >= 500

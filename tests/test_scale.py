@@ -43,10 +43,13 @@ def test_scale_generator_digests_match_reference():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("collapse", [True, False])
-def test_scale_engine_matches_reference(collapse):
+@pytest.mark.parametrize("blocks", [True, False])
+def test_scale_engine_matches_reference(collapse, blocks):
+    """C3/C4-shaped configs at 64-256 ranks against the reference's results,
+    with and without kernel blocks (interned launch runs, soa.h KBLOCK)."""
     from paper_2503_20191_b200.engine import Engine
     rs = rows()
-    eng = Engine(0, collapse=collapse)
+    eng = Engine(0, collapse=collapse, blocks=blocks)
     bad = []
     groups = {}
     for i, r in enumerate(rs):

@@ -8,7 +8,8 @@ from paper_2503_20191_b200.engine import Engine
 model = W.ModelSpec("gpt3-1.3b", 24, 2048, 2048, 51200)
 cluster = W.ClusterSpec(1, 8, 80 * 2 ** 30, W.load_device_preset("fast"))
 cfgs = W.enumerate_space(W.SearchSpace(global_batch=512), model, cluster)[:512]
-eng = Engine(0, collapse=("--full" not in sys.argv), sched=os.environ.get("SCHED", "auto"))
+eng = Engine(0, collapse=("--full" not in sys.argv), sched=os.environ.get("SCHED", "auto"),
+             blocks=os.environ.get("BLOCKS", "1") == "1")
 
 def run(sub, reps=5):
     eng.stage_generated(model, sub, cluster, dispatch_overhead_ns=5000)

@@ -57,5 +57,23 @@ done:
     }
   }
   printf("fused generate+pack %.1f ms (%.1f ns/ev)\n", tf * 1e3, tf * 1e9 / ev);
+  size_t recs = 0, blks = 0, bf = 0, ops0 = 0;
+  for (int it = 0; it < 2; it++) {
+    tf = 0;
+    recs = blks = bf = ops0 = 0;
+    GenJob g;
+    for (auto &c : cfgs) {
+      JobPack P;
+      std::string err;
+      auto t0 = clk::now();
+      pack_generated(m, c, cl, -1, 5000, 0, 0, true, g, P, &err, true);
+      tf += std::chrono::duration<double>(clk::now() - t0).count();
+      recs += P.ops.size();
+      blks += P.blocks.size();
+      bf += P.blk_fids.size();
+    }
+  }
+  printf("fused generate+pack, kernel blocks %.1f ms (%.1f ns/ev): %zu op records, %zu blocks, "
+         "%zu block fids\n", tf * 1e3, tf * 1e9 / ev, recs, blks, bf);
   return 0;
 }

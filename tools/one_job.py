@@ -9,7 +9,7 @@ model = W.ModelSpec("gpt3-1.3b", 24, 2048, 2048, 51200)
 cluster = W.ClusterSpec(1, 8, 80 * 2 ** 30, W.load_device_preset("fast"))
 cfgs = [c for c in W.enumerate_space(W.SearchSpace(global_batch=512), model, cluster)[:512]
         if c.label() == label]
-eng = Engine(0, sched=os.environ.get("SCHED", "auto"))
+eng = Engine(0, sched=os.environ.get("SCHED", "auto"), blocks=os.environ.get("BLOCKS", "1") == "1")
 eng.stage_generated(model, cfgs, cluster, dispatch_overhead_ns=5000)
 print(eng.batch_stats())
 eng.upload()
