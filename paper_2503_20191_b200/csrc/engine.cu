@@ -602,6 +602,20 @@ int maya_upload(maya_engine *e) {
   seg(e->s_blocks, n_blocks * sizeof(KBlock));
   seg(e->s_blk_fids, n_blk_fids * sizeof(uint32_t));
   e->arena_bytes = off;
+  if (getenv("MAYA_DEBUG_ARENA")) {
+    const Seg *sg[] = {&e->s_jobs, &e->s_order, &e->s_ranks, &e->s_rank_comm, &e->s_comms,
+                       &e->s_slots, &e->s_walkers, &e->s_wids, &e->s_reps, &e->s_ops,
+                       &e->s_streams, &e->s_coll_lc, &e->s_coll_idx, &e->s_syncs, &e->s_counts,
+                       &e->s_mems, &e->s_feats, &e->s_rcolls, &e->s_rcslot, &e->s_lane_jobs,
+                       &e->s_lane_wslot, &e->s_lane_perm, &e->s_chunks, &e->s_grid_parts,
+                       &e->s_comm_part, &e->s_blocks, &e->s_blk_fids};
+    const char *nm[] = {"jobs", "order", "ranks", "rank_comm", "comms", "slots", "walkers",
+                        "wids", "reps", "ops", "streams", "coll_lc", "coll_idx", "syncs",
+                        "counts", "mems", "feats", "rcolls", "rcslot", "lane_jobs", "lane_wslot",
+                        "lane_perm", "chunks", "grid_parts", "comm_part", "blocks", "blk_fids"};
+    for (size_t q = 0; q < sizeof(sg) / sizeof(sg[0]); q++)
+      fprintf(stderr, "arena %-10s %12zu\n", nm[q], sg[q]->bytes);
+  }
   // scratch layout
   off = 0;
   seg(e->x_exec, n_ops * sizeof(ExecOp));
