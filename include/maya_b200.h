@@ -239,6 +239,31 @@ int maya_gen_job(const maya_model *model, const maya_config *cfg, const maya_clu
 int maya_gen_view_of(const maya_gen *g, maya_gen_view *view);
 int maya_gen_free(maya_gen *g);
 
+/* ---- text traces and job manifests (trace.py:282-495, collate.py:256-431) --
+ * Native parse_trace / serialize_trace / validate_trace and save_job /
+ * load_job + collate.  Errors return MAYA_EINVAL with maya_last_error() set to
+ * the reference's exception message and maya_last_error_kind() to its class. */
+#define MAYA_ERR_PARSE 1        /* TraceParseError (trace.py:209-212) */
+#define MAYA_ERR_VALIDATION 2   /* TraceValidationError (trace.py:215-220) */
+#define MAYA_ERR_COLLATION 3    /* CollationError (collate.py:42) */
+#define MAYA_ERR_RANGE 4        /* an integer the engine's int64/int32 fields cannot hold */
+#define MAYA_ERR_IO 5           /* file missing / unwritable (FileNotFoundError) */
+int maya_last_error_kind(void);
+typedef struct maya_trace maya_trace;
+/* parse_trace + validate_trace of one rank_<r>.trace text (universal newlines). */
+int maya_trace_parse(const char *text, int64_t len, maya_trace **out);
+/* [0] global rank, [1] host, [2] device, [3] events */
+int maya_trace_info(const maya_trace *t, int64_t *out4);
+/* serialize_trace; the text is owned by t (valid until the next call or free). */
+int maya_trace_serialize(maya_trace *t, const char **text, int64_t *len);
+int maya_trace_free(maya_trace *t);
+/* load_job(manifest, cluster): the rank traces, dup expansion and collate, into
+ * a raw job (maya_gen_view_of; string tables via maya_gen_names). */
+int maya_job_load(const char *manifest_path, const maya_cluster *cluster, maya_gen **out);
+/* save_job of a loaded job: rank_<r>.trace per representative + manifest. */
+int maya_job_save(const maya_gen *g, const char *out_dir, const char *manifest_name);
+/* '\n'-joined op-kind (which 0) or dtype (which 1) names of a job's ev_f ids. */
+int maya_gen_names(const maya_gen *g, int32_t which, const char **blob, int32_t *n);
 /* Generate + pack n configs straight into the engine batch (no host round
  * trip through arrays).  status_out[i] receives 0 or MAYA_EINVAL for an
  * invalid configuration (ConfigError, workload.py:168-208); such jobs are

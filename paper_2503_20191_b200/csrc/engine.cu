@@ -18,16 +18,24 @@
 #include "gen.h"
 #include "pack.h"
 #include "pool.h"
+#include "traceio.h"
 
 using namespace maya;
 
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_err_kind = 0;
 
 int fail(int code, const std::string &msg) {
   g_err = msg;
+  g_err_kind = 0;
   return code;
+}
+int fail_trace(const TraceFail &f) {
+  g_err = f.msg;
+  g_err_kind = f.kind;
+  return MAYA_EINVAL;
 }
 
 #define CU(x)                                                                        \
@@ -1319,7 +1327,104 @@ int maya_debug_pack_compare(const maya_model *model, int32_t n, const maya_confi
 
 struct maya_gen {
   GenJob job;
+  std::unique_ptr<LoadedJob> loaded;   // jobs read by maya_job_load (their text form)
+  std::string op_blob, dtype_blob;
 };
+
+struct maya_trace {
+  ParsedTrace t;
+  std::string text;
+};
+
+int maya_last_error_kind(void) { return g_err_kind; }
+
+int maya_trace_parse(const char *text, int64_t len, maya_trace **out) {
+  if (!text || len < 0) return fail(MAYA_EINVAL, "null text");
+  maya_trace *h = new maya_trace();
+  try {
+    parse_trace(text, (size_t)len, h->t);
+  } catch (const TraceFail &f) {
+    delete h;
+    return fail_trace(f);
+  } catch (const std::exception &x) {
+    delete h;
+    return fail(MAYA_EINVAL, x.what());
+  }
+  *out = h;
+  return MAYA_OK;
+}
+
+int maya_trace_info(const maya_trace *h, int64_t *out4) {
+  out4[0] = h->t.rank;
+  out4[1] = h->t.host;
+  out4[2] = h->t.device;
+  out4[3] = (int64_t)h->t.ev.size();
+  return MAYA_OK;
+}
+
+int maya_trace_serialize(maya_trace *h, const char **text, int64_t *len) {
+  h->text = serialize_trace(h->t);
+  *text = h->text.c_str();
+  *len = (int64_t)h->text.size();
+  return MAYA_OK;
+}
+
+int maya_trace_free(maya_trace *h) {
+  delete h;
+  return MAYA_OK;
+}
+
+int maya_job_load(const char *manifest_path, const maya_cluster *cluster, maya_gen **out) {
+  if (!manifest_path || !cluster) return fail(MAYA_EINVAL, "null argument");
+  if (cluster->num_hosts < 1 || cluster->devices_per_host < 1)
+    return fail(MAYA_EINVAL, "cluster must have at least one host and device");
+  maya_gen *g = new maya_gen();
+  g->loaded.reset(new LoadedJob());
+  try {
+    load_job(manifest_path, cluster->num_hosts, cluster->devices_per_host,
+             cluster->device_memory_bytes, g->job, *g->loaded);
+  } catch (const TraceFail &f) {
+    delete g;
+    return fail_trace(f);
+  } catch (const std::exception &x) {
+    delete g;
+    return fail(MAYA_EINVAL, x.what());
+  }
+  for (size_t q = 0; q < g->loaded->op_names.size(); q++)
+    g->op_blob += (q ? "\n" : "") + g->loaded->op_names[q];
+  for (size_t q = 0; q < g->loaded->dtype_names.size(); q++)
+    g->dtype_blob += (q ? "\n" : "") + g->loaded->dtype_names[q];
+  *out = g;
+  return MAYA_OK;
+}
+
+int maya_job_save(const maya_gen *g, const char *out_dir, const char *manifest_name) {
+  if (!g->loaded) return fail(MAYA_EINVAL, "only jobs read by maya_job_load keep their text form");
+  try {
+    save_job(*g->loaded, out_dir, manifest_name ? manifest_name : "job.manifest");
+  } catch (const TraceFail &f) {
+    return fail_trace(f);
+  }
+  return MAYA_OK;
+}
+
+int maya_gen_names(const maya_gen *g, int32_t which, const char **blob, int32_t *n) {
+  if (which != 0 && which != 1) return fail(MAYA_EINVAL, "which: 0 op kinds, 1 dtypes");
+  if (g->loaded) {
+    *blob = which == 0 ? g->op_blob.c_str() : g->dtype_blob.c_str();
+    *n = (int32_t)(which == 0 ? g->loaded->op_names.size() : g->loaded->dtype_names.size());
+  } else {
+    static std::string ob, db;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      for (int q = 0; q < 12; q++) ob += (q ? "\n" : "") + std::string(GEN_OP_KINDS[q]);
+      for (int q = 0; q < 3; q++) db += (q ? "\n" : "") + std::string(GEN_DTYPES[q]);
+    });
+    *blob = which == 0 ? ob.c_str() : db.c_str();
+    *n = which == 0 ? 12 : 3;
+  }
+  return MAYA_OK;
+}
 
 const char *maya_gen_op_kind_name(int32_t id) {
   return (id >= 0 && id < 12) ? GEN_OP_KINDS[id] : nullptr;

@@ -30,7 +30,9 @@ EXPORTED = (
     "maya_get_stream", "maya_arena_bytes", "maya_gen_job", "maya_gen_view_of", "maya_gen_free",
     "maya_gen_op_kind_name", "maya_gen_dtype_name", "maya_batch_add_generated",
     "maya_batch_stats", "maya_set_options", "maya_batch_collapsed", "maya_prof_read",
-    "maya_debug_pack_compare", "maya_rank_stats",
+    "maya_debug_pack_compare", "maya_rank_stats", "maya_last_error_kind", "maya_trace_parse",
+    "maya_trace_info", "maya_trace_serialize", "maya_trace_free", "maya_job_load",
+    "maya_job_save", "maya_gen_names",
 )
 
 
