@@ -911,10 +911,12 @@ __global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, cons
             break;
           }
           if (vload(&s_active) <= 0) break;
+#ifndef MAYA_POLL_SPIN
           if (poll >= 32) {
             __nanosleep(ns);
             if (ns < 256) ns <<= 1;
           }
+#endif
         }
         if (wake && lane == 0) atomicAdd(&s_active, 1);
         wake = __shfl_sync(FULL, wake, 0);

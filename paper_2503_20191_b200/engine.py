@@ -19,7 +19,7 @@ from .rawtrace import RawJob
 from .workload import ConfigC
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmaya_b200.so")
+LIB_PATH = os.environ.get("MAYA_LIB_PATH") or os.path.join(_HERE, "libmaya_b200.so")
 _lib = None
 
 EXPORTED = (
