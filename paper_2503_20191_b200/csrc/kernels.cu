@@ -215,6 +215,9 @@ static constexpr unsigned FULL = 0xffffffffu;
 // [3] sweeps (skip checks + ctx), [4] windows, [5] slow-op calls, [6] wakes, [7] passes
 // accumulated per thread (lane 0 of each warp) and flushed once at kernel exit
 __device__ unsigned long long g_prof[8];
+// window sub-phases (lane 0): [0] segment advance + wide attempt, [1] load + classify
+// (to the blocker ballot), [2] scan, [3] blockers + commit
+__device__ unsigned long long g_prof_sub[4];
 #define PROF_T(v) long long v = clock64()
 #define PROF_ADD(i, v) (prof_acc[i] += (unsigned long long)(v))
 #else
@@ -430,6 +433,9 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
       }
       streaming = false;
     }
+#ifdef MAYA_PROFILE
+    long long t_a = clock64();
+#endif
     const uint32_t n = min(32u, end - s.i);
     const bool valid = lane < n;
     ExecOp e{0, 0};
@@ -490,6 +496,9 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
       }
     }
     const uint32_t bmask = __ballot_sync(FULL, blocker);
+#ifdef MAYA_PROFILE
+    long long t_b = clock64();
+#endif
     if (blocker) { A = 0; B = NEG; }
     bool flag = (lane == 0) || ((bmask >> (lane - 1)) & 1u);
 #pragma unroll
@@ -504,6 +513,9 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
         flag = f2;
       }
     }
+#ifdef MAYA_PROFILE
+    long long t_c = clock64();
+#endif
     // finalize segments; apply blockers in order
     int64_t xin = s.x, d = 0;
     uint32_t p = 0, commit = n, spec = bmask;
@@ -658,6 +670,15 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
     }
 #ifdef MAYA_PROFILE
     if (lane == 0) PROF_ADD(7, commit);
+#endif
+#ifdef MAYA_PROFILE
+    if (lane == 0) {
+      const long long t_d = clock64();
+      atomicAdd(&g_prof_sub[0], (unsigned long long)(t_a - t_win));
+      atomicAdd(&g_prof_sub[1], (unsigned long long)(t_b - t_a));
+      atomicAdd(&g_prof_sub[2], (unsigned long long)(t_c - t_b));
+      atomicAdd(&g_prof_sub[3], (unsigned long long)(t_d - t_c));
+    }
 #endif
     streaming = !blocked && commit == 32u;
     if (commit > 0) {
@@ -1388,6 +1409,22 @@ void launch_schedule_variant(const DevBatch &b, int variant, const int32_t *orde
 }
 
 uint32_t sched_smem_cap() { return SCHED_SMEM_CAP; }
+
+extern "C" int maya_prof_read_sub(unsigned long long *out4, int reset) {
+#ifdef MAYA_PROFILE
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out4, g_prof_sub, sizeof(unsigned long long) * 4);
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_prof_sub, z, sizeof z);
+  }
+  return 1;
+#else
+  (void)out4;
+  (void)reset;
+  return 0;
+#endif
+}
 
 int prof_read(unsigned long long *out8, int reset) {
 #ifdef MAYA_PROFILE
