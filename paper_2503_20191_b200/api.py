@@ -446,6 +446,45 @@ class GenPipeline:
         return res, top, status
 
 
+    def evaluate_stream(self, model, batches, cluster, k: int = 8, key_orders=None,
+                        dispatch_overhead_ns: int = 0, schedule=None, threads: int = 8,
+                        efficiency: Mapping[str, float] | None = None,
+                        overhead_ns: int = DEFAULT_KERNEL_OVERHEAD_NS):
+        """Evaluate a stream of config batches (a search's successive
+        populations), yielding (results, top-k rows, status) per batch in
+        order.  Batch q+1 is generated and packed on the host threads while
+        batch q's H2D, kernels and D2H run on the device (the two engines
+        alternate), so a long search runs at the speed of the slower side
+        instead of the sum.  Every batch still goes through generation, H2D,
+        the kernels, the D2H of its results and the top-k."""
+        from ._abi import RESULT_DTYPE
+
+        def collect(item):
+            e, n, st = item
+            res = np.zeros(n, dtype=RESULT_DTYPE)
+            res[:] = e.results()
+            top = merge_topk(np.array([(int(t["time_ns"]), int(t["key_rank"]), int(t["job"]))
+                                       for t in e.topk(k)], dtype=np.int64).reshape(-1, 3), k)
+            return res, top, st
+
+        pending = None
+        for q, configs in enumerate(batches):
+            e = self.engines[q % 2]
+            kr = (key_ranks(configs) if key_orders is None or key_orders[q] is None
+                  else np.asarray(key_orders[q]))
+            st = e.stage_generated(model, configs, cluster, schedule=schedule,
+                                   dispatch_overhead_ns=dispatch_overhead_ns,
+                                   efficiency=efficiency, overhead_ns=overhead_ns,
+                                   key_ranks=kr, threads=threads)
+            e.upload()
+            e.run()
+            if pending is not None:
+                yield collect(pending)
+            pending = (e, len(configs), st)
+        if pending is not None:
+            yield collect(pending)
+
+
 def merge_topk(candidates: np.ndarray, k: int) -> np.ndarray:
     """Merge per-GPU top-k candidate rows (time_ns, global key rank, config id)
     with the device comparator; time_ns == 0 sorts after every positive time."""

@@ -162,3 +162,23 @@ def test_c2_kernel_blocks_match_per_launch_ops(sched):
         assert np.array_equal(a, b)
     ok = out[True][0][1] == 0
     assert ok.sum() >= 500
+
+
+@gpu
+def test_gen_pipeline_stream_matches_single_batches():
+    """evaluate_stream (host work of batch q+1 overlapping device work of
+    batch q) returns, batch by batch, exactly what evaluate returns."""
+    from paper_2503_20191_b200.api import GenPipeline
+    W, model, cluster = _c2()
+    cfgs = W.enumerate_space(W.SearchSpace(global_batch=512), model, cluster)[:512]
+    batches = [cfgs[:200], cfgs[200:512], cfgs[:512:3]]
+    pipe = GenPipeline(0)
+    want = [pipe.evaluate(model, b, cluster, k=8, dispatch_overhead_ns=5000) for b in batches]
+    got = list(pipe.evaluate_stream(model, batches, cluster, k=8, dispatch_overhead_ns=5000))
+    pipe.close()
+    assert len(got) == len(want)
+    for (r1, t1, s1), (r2, t2, s2) in zip(want, got):
+        for f in ("status", "total_ns", "peak_mem_bytes", "oom"):
+            assert np.array_equal(r1[f], r2[f]), f
+        assert np.array_equal(np.asarray(t1), np.asarray(t2))
+        assert np.array_equal(s1, s2)
