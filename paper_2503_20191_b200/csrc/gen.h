@@ -44,8 +44,8 @@ struct GenJob {
 };
 
 // One kernel launch of the generator's inventory (workload.py:316-378).
-struct KSpec {
-  int op;
+struct KSpec {          // no padding: launch lists compare with memcmp (pack.cpp)
+  int64_t op;
   int64_t flops, bytes;
 };
 

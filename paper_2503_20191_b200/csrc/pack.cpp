@@ -279,23 +279,21 @@ struct RepPacker {
     }
     // intern by the launch list itself: a repeated layer body costs a hash
     // and a compare, no per-kernel feature lookups
-    uint64_t hsh = (1469598103934665603ull ^ (uint64_t)gap) * 1099511628211ull;
-    hsh = (hsh ^ ((uint64_t)n << 8 | (uint32_t)dtype)) * 1099511628211ull;
-    for (size_t i = 0; i < n; i++) {
-      hsh = (hsh ^ (uint64_t)ks[i].op) * 1099511628211ull;
-      hsh = (hsh ^ (uint64_t)ks[i].flops) * 1099511628211ull;
-      hsh = (hsh ^ (uint64_t)ks[i].bytes) * 1099511628211ull;
+    uint64_t h0 = 1469598103934665603ull ^ (uint64_t)gap, h1 = (uint64_t)n << 8 | (uint32_t)dtype,
+             h2 = 0x9e3779b97f4a7c15ull;
+    for (size_t i = 0; i < n; i++) {   // three independent multiply chains
+      h0 = (h0 ^ (uint64_t)ks[i].op) * 1099511628211ull;
+      h1 = (h1 ^ (uint64_t)ks[i].flops) * 0xff51afd7ed558ccdull;
+      h2 = (h2 ^ (uint64_t)ks[i].bytes) * 0xc4ceb9fe1a85ec53ull;
     }
+    const uint64_t hsh = h0 ^ (h1 >> 1) ^ (h2 << 1) ^ (h1 * 31) ^ (h2 >> 7);
     uint32_t id = UINT32_MAX;
     auto it = F->blk_map.find(hsh);
     if (it != F->blk_map.end()) {
       const FeatState::BlkKey &bk = F->blk_keys[it->second];
-      bool same = bk.n == n && bk.gap == gap && bk.dtype == dtype;
-      for (size_t i = 0; same && i < n; i++) {
-        const KSpec &x = F->blk_specs[bk.spec0 + i];
-        same = x.op == ks[i].op && x.flops == ks[i].flops && x.bytes == ks[i].bytes;
-      }
-      if (same) id = it->second;
+      if (bk.n == n && bk.gap == gap && bk.dtype == dtype &&
+          memcmp(F->blk_specs.data() + bk.spec0, ks, n * sizeof(KSpec)) == 0)
+        id = it->second;
     }
     if (id == UINT32_MAX) {
       id = (uint32_t)P->blocks.size();
@@ -305,8 +303,8 @@ struct RepPacker {
       for (size_t i = 0; i < n; i++) {
         const int64_t f[4] = {ks[i].op, dtype, ks[i].flops, ks[i].bytes};
         P->blk_fids.push_back(feature(f));
-        F->blk_specs.push_back(ks[i]);
       }
+      F->blk_specs.insert(F->blk_specs.end(), ks, ks + n);
       F->blk_map.emplace(hsh, id);   // first block of this hash stays the interned one
     }
     gpre += gap;                     // the first kernel's gap
