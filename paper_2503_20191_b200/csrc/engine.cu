@@ -1126,9 +1126,15 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
     e->stats_ok = true;
   }
   {
+    // kernels this run launched: estimators, memscan, resolve/fold, schedulers
     int64_t n = (db.n_feats ? 1 : 0) + (db.n_slots ? 1 : 0) + (db.n_reps ? 1 : 0) +
-                (db.n_ops ? 1 : 0) + (db.n_rcolls ? 1 : 0);
-    for (int v = 0; v < maya_engine::NVAR; v++) n += e->var_n[v] ? 1 : 0;
+                (db.n_rcolls ? 1 : 0);
+    if (fold)
+      n += (db.n_blocks ? 1 : 0) + (db.n_chunks ? 2 : 0) + (db.n_reps ? 1 : 0);
+    else
+      n += db.n_ops ? 1 : 0;
+    for (int v = 0; v < maya_engine::NVAR; v++)
+      n += v == 15 ? (int64_t)e->grid_launches.size() : (e->var_n[v] ? 1 : 0);
     if (e->stats_ok) n += 3;   // keys, segmented sort (cub), unions
     e->run_launches = n;
   }
