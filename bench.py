@@ -484,7 +484,7 @@ def bench_ours(args):
         # per interned block and 4 B per block feature id) -- and the tables
         alg_bytes = (16 * stats["device_ops"] + 16 * stats["kernel_blocks"]
                      + 4 * stats["block_fids"] + 4 * stats["rank_comms"]
-                     + 16 * (stats["features"] + stats["slots"]) + 24 * stats["jobs"])
+                     + 32 * (stats["features"] + stats["wire_features"]) + 24 * stats["jobs"])
         sched = statistics.median(sched_ms)
         peak, peak_kind = measured_peak_hbm()
         achieved = alg_bytes / (sched / 1000) / 1e9

@@ -183,8 +183,9 @@ int64_t maya_arena_bytes(maya_engine *eng);
  * slots, [5] device op records (stream-major; a kernel block is one record),
  * [6] rank-ops, [7] arena bytes, [8] ranks, [9] reps, [10] kernels launched by
  * the last maya_run, [11] kernels launched by the last maya_topk, [12] kernel
- * blocks, [13] block feature ids. */
-int maya_batch_stats(maya_engine *eng, int64_t *out14);
+ * blocks, [13] block feature ids, [14] wire features (unique call records),
+ * [15] reserved. */
+int maya_batch_stats(maya_engine *eng, int64_t *out16);
 
 /* Scheduler phase counters of instrumented builds (-DMAYA_PROFILE); returns
  * 0 (and leaves out8 untouched) in product builds. */

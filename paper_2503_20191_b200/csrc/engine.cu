@@ -100,7 +100,7 @@ struct maya_engine {
   DevBatch db{};
   DevTables tables{};
   // segments
-  Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_slots, s_walkers, s_reps, s_ops, s_streams,
+  Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_wfeats, s_walkers, s_reps, s_ops, s_streams,
       s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
       s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks, s_grid_parts, s_comm_part, s_blocks,
       s_blk_fids;
@@ -393,6 +393,7 @@ bool pack_eq(const JobPack &a, const JobPack &b) {
          vec_eq(a.rep_ring_ok, b.rep_ring_ok) && vec_eq(a.comm_rdv, b.comm_rdv) &&
          vec_eq(a.rank_orig, b.rank_orig) && vec_eq(a.rank_sim, b.rank_sim) &&
          vec_eq(a.stream_events, b.stream_events) && vec_eq(a.blocks, b.blocks) &&
+         vec_eq(a.wfeats, b.wfeats) && vec_eq(a.slot_wf, b.slot_wf) &&
          vec_eq(a.blk_fids, b.blk_fids) &&
          a.collapsed == b.collapsed && a.n_fire == b.n_fire && a.n_delay == b.n_delay;
 }
@@ -507,7 +508,7 @@ int maya_upload(maya_engine *e) {
   size_t n_ranks = 0, n_rank_comm = 0, n_comms = 0, n_slots = 0, n_walkers = 0, n_reps = 0,
          n_ops = 0, n_streams = 0, n_colls = 0, n_syncs = 0, n_counts = 0, n_mems = 0,
          n_feats = 0, n_fire = 0, n_delay = 0, n_wstate = 0, n_rcolls = 0, n_chunks = 0,
-         n_blocks = 0, n_blk_fids = 0;
+         n_blocks = 0, n_blk_fids = 0, n_wfeats = 0;
   uint64_t n_tl = 0;
   e->job_tl.resize(nj);
   e->job_ops.resize(nj);
@@ -520,6 +521,7 @@ int maya_upload(maya_engine *e) {
     n_rank_comm += P.rank_comm.size();
     n_comms += P.comms.size();
     n_slots += P.slots.size();
+    n_wfeats += P.wfeats.size();
     n_walkers += P.walkers.size();
     n_reps += P.reps.size();
     e->job_ops[j] = n_ops;
@@ -585,7 +587,7 @@ int maya_upload(maya_engine *e) {
   seg(e->s_ranks, n_ranks * sizeof(RankRec));
   seg(e->s_rank_comm, n_rank_comm * sizeof(uint32_t));
   seg(e->s_comms, n_comms * sizeof(CommRec));
-  seg(e->s_slots, n_slots * sizeof(SlotRec));
+  seg(e->s_wfeats, n_wfeats * sizeof(SlotRec));
   seg(e->s_walkers, n_walkers * sizeof(Walker));
   seg(e->s_wids, n_walkers * sizeof(uint32_t));
   seg(e->s_reps, n_reps * sizeof(RepHdr));
@@ -612,12 +614,12 @@ int maya_upload(maya_engine *e) {
   e->arena_bytes = off;
   if (getenv("MAYA_DEBUG_ARENA")) {
     const Seg *sg[] = {&e->s_jobs, &e->s_order, &e->s_ranks, &e->s_rank_comm, &e->s_comms,
-                       &e->s_slots, &e->s_walkers, &e->s_wids, &e->s_reps, &e->s_ops,
+                       &e->s_wfeats, &e->s_walkers, &e->s_wids, &e->s_reps, &e->s_ops,
                        &e->s_streams, &e->s_coll_lc, &e->s_coll_idx, &e->s_syncs, &e->s_counts,
                        &e->s_mems, &e->s_feats, &e->s_rcolls, &e->s_rcslot, &e->s_lane_jobs,
                        &e->s_lane_wslot, &e->s_lane_perm, &e->s_chunks, &e->s_grid_parts,
                        &e->s_comm_part, &e->s_blocks, &e->s_blk_fids};
-    const char *nm[] = {"jobs", "order", "ranks", "rank_comm", "comms", "slots", "walkers",
+    const char *nm[] = {"jobs", "order", "ranks", "rank_comm", "comms", "wfeats", "walkers",
                         "wids", "reps", "ops", "streams", "coll_lc", "coll_idx", "syncs",
                         "counts", "mems", "feats", "rcolls", "rcslot", "lane_jobs", "lane_wslot",
                         "lane_perm", "chunks", "grid_parts", "comm_part", "blocks", "blk_fids"};
@@ -636,7 +638,7 @@ int maya_upload(maya_engine *e) {
   seg(e->x_rcw, n_rcolls * sizeof(RCX));
   seg(e->x_feat_ns, n_feats * 8);
   seg(e->x_blk_ab, n_blocks * 16);
-  seg(e->x_wire, n_slots * 8);
+  seg(e->x_wire, n_wfeats * 8);
   seg(e->x_fire, n_fire * 8);
   seg(e->x_delay, n_delay * 8);
   seg(e->x_wstate, n_wstate);
@@ -707,7 +709,7 @@ int maya_upload(maya_engine *e) {
   // per-job bases (serial prefix), then parallel copy
   struct Base {
     size_t ranks, rank_comm, comms, slots, walkers, reps, ops, streams, colls, syncs, counts,
-        mems, feats, fire, delay, wstate, rcolls, perm, blocks, blk_fids;
+        mems, feats, fire, delay, wstate, rcolls, perm, blocks, blk_fids, wfeats;
   };
   std::vector<Base> bases(nj);
   {
@@ -719,6 +721,7 @@ int maya_upload(maya_engine *e) {
       b.rank_comm += P.rank_comm.size();
       b.comms += P.comms.size();
       b.slots += P.slots.size();
+      b.wfeats += P.wfeats.size();
       b.walkers += P.walkers.size();
       b.reps += P.reps.size();
       b.ops += P.ops.size();
@@ -833,7 +836,7 @@ int maya_upload(maya_engine *e) {
            P.VEC.size() * sizeof(P.VEC[0]));
     CPY(s_rank_comm, rank_comm, B.rank_comm)
     CPY(s_comms, comms, B.comms)
-    CPY(s_slots, slots, B.slots)
+    CPY(s_wfeats, wfeats, B.wfeats)
     CPY(s_walkers, walkers, B.walkers)
     CPY(s_wids, wids, B.walkers)
     {  // ops: KERN args become batch-global feature (or kernel block) ids
@@ -909,7 +912,7 @@ int maya_upload(maya_engine *e) {
       for (size_t q = 0; q < P.rcolls.size(); q++) {
         const RankColl ent = P.rcolls[q];
         const uint32_t g = (uint32_t)(ent >> 32) & 0xffffu, idx = (uint32_t)ent;
-        dst[q] = (uint32_t)(B.slots + P.comms[g].call_base + idx);
+        dst[q] = (uint32_t)(B.wfeats + P.slot_wf[P.comms[g].call_base + idx]);
       }
     }
     CPY(s_streams, streams, B.streams)
@@ -951,7 +954,8 @@ int maya_upload(maya_engine *e) {
   db.ranks = (const RankRec *)(D + e->s_ranks.off);
   db.rank_comm = (const uint32_t *)(D + e->s_rank_comm.off);
   db.comms = (const CommRec *)(D + e->s_comms.off);
-  db.slots = (const SlotRec *)(D + e->s_slots.off);
+  db.wfeats = (const SlotRec *)(D + e->s_wfeats.off);
+  db.n_wfeats = (uint32_t)n_wfeats;
   db.walkers = (const Walker *)(D + e->s_walkers.off);
   db.wids = (const uint32_t *)(D + e->s_wids.off);
   db.reps = (const RepHdr *)(D + e->s_reps.off);
@@ -1127,7 +1131,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   }
   {
     // kernels this run launched: estimators, memscan, resolve/fold, schedulers
-    int64_t n = (db.n_feats ? 1 : 0) + (db.n_slots ? 1 : 0) + (db.n_reps ? 1 : 0) +
+    int64_t n = (db.n_feats ? 1 : 0) + (db.n_wfeats ? 1 : 0) + (db.n_reps ? 1 : 0) +
                 (db.n_rcolls ? 1 : 0);
     if (fold)
       n += (db.n_blocks ? 1 : 0) + (db.n_chunks ? 2 : 0) + (db.n_reps ? 1 : 0);
@@ -1164,7 +1168,7 @@ int maya_results(maya_engine *e, maya_job_result *out) {
   if (err_flag) {
     // Estimation errors are raised by annotate() for ANY event, before the
     // simulation (estimate.py:344-347): attribute failed features to jobs.
-    std::vector<int64_t> fns(e->db.n_feats), wns(e->db.n_slots);
+    std::vector<int64_t> fns(e->db.n_feats), wns(e->db.n_wfeats);
     CU(cudaMemcpy(fns.data(), e->db.feat_ns, fns.size() * 8, cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(wns.data(), e->db.wire, wns.size() * 8, cudaMemcpyDeviceToHost));
     size_t fb = 0, sb = 0;
@@ -1172,12 +1176,12 @@ int maya_results(maya_engine *e, maya_job_result *out) {
       const JobPack &P = e->packs[j];
       bool bad = false;
       for (size_t f = 0; f < P.feats.size(); f++) bad |= fns[fb + f] < 0;
-      for (size_t s = 0; s < P.slots.size(); s++) bad |= wns[sb + s] < 0;
+      for (size_t s = 0; s < P.wfeats.size(); s++) bad |= wns[sb + s] < 0;
       // annotate() raises before simulate() runs (estimate.py:344-347): any
       // failed estimate of the job decides its status, whatever the schedule did
       if (bad && out[j].status != MAYA_ST_BAD_INPUT) out[j].status = MAYA_ST_ESTIMATION;
       fb += P.feats.size();
-      sb += P.slots.size();
+      sb += P.wfeats.size();
     }
   }
   return MAYA_OK;
@@ -1199,7 +1203,7 @@ int maya_get_stream(maya_engine *e, void **stream) {
 int64_t maya_arena_bytes(maya_engine *e) { return (int64_t)e->arena_bytes; }
 
 int maya_batch_stats(maya_engine *e, int64_t *o) {
-  for (int i = 0; i < 14; i++) o[i] = 0;
+  for (int i = 0; i < 16; i++) o[i] = 0;
   o[10] = e->run_launches;
   o[11] = e->topk_launches;
   o[0] = (int64_t)e->packs.size();
@@ -1215,6 +1219,7 @@ int maya_batch_stats(maya_engine *e, int64_t *o) {
     o[9] += (int64_t)P.reps.size();
     o[12] += (int64_t)P.blocks.size();
     o[13] += (int64_t)P.blk_fids.size();
+    o[14] += (int64_t)P.wfeats.size();
   }
   o[7] = (int64_t)e->arena_bytes;
   return MAYA_OK;

@@ -104,8 +104,8 @@ __global__ void estimate_features_kernel(DevBatch b, DevTables t) {
 
 __global__ void estimate_wire_kernel(DevBatch b, DevTables t) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= b.n_slots) return;
-  SlotRec s = b.slots[i];
+  if (i >= b.n_wfeats) return;
+  SlotRec s = b.wfeats[i];
   if (s.kind < 0) { b.wire[i] = 0; return; }
   if (s.fixed >= 0) { b.wire[i] = s.fixed; return; }
   int64_t n = s.nranks;
@@ -128,7 +128,7 @@ __global__ void estimate_wire_kernel(DevBatch b, DevTables t) {
 
 void launch_estimate(const DevBatch &b, const DevTables &t, cudaStream_t s) {
   if (b.n_feats) estimate_features_kernel<<<(b.n_feats + 255) / 256, 256, 0, s>>>(b, t);
-  if (b.n_slots) estimate_wire_kernel<<<(b.n_slots + 255) / 256, 256, 0, s>>>(b, t);
+  if (b.n_wfeats) estimate_wire_kernel<<<(b.n_wfeats + 255) / 256, 256, 0, s>>>(b, t);
 }
 
 // ---------------------------------------------------------------------------
@@ -1163,6 +1163,9 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) fold_count_kernel(DevBatch b)
 // 128-op windows, 4 consecutive ops per lane: a lane composes its 4 maps
 // sequentially (branch-free), the warp scans the 32 lane composites once, and
 // each lane writes the runs that end among its ops.
+// BLOCKS: the batch has kernel blocks (KBLOCK ops enter as their composites);
+// without, the kernel is the plain per-op fold.
+template <bool BLOCKS>
 __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1198,7 +1201,7 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
       d[t] = 0;
       bx[t] = -1;
       if (v[t] && op_tag(o[t].meta) == TAG_KERN) {
-        if (o[t].arg & KBLOCK) {
+        if (BLOCKS && (o[t].arg & KBLOCK)) {
           const longlong2 ab =
               *reinterpret_cast<const longlong2 *>(b.blk_ab + 2 * (size_t)(o[t].arg & ~KBLOCK));
           d[t] = ab.x;
@@ -1230,7 +1233,8 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
     for (int t = 0; t < 4; t++) {
       if (!v[t]) continue;
       const int64_t de = (d[t] < 0 || d[t] > FOLD_SAT) ? FOLD_SAT : d[t];
-      const int64_t a = f[t] ? de : 0, bb = f[t] ? sat_add(o[t].disp, bx[t] >= 0 ? bx[t] : de) : 0;
+      const int64_t a = f[t] ? de : 0,
+                    bb = f[t] ? sat_add(o[t].disp, (BLOCKS && bx[t] >= 0) ? bx[t] : de) : 0;
       if (st[t]) {
         A = a;
         B = bb;
@@ -1285,7 +1289,8 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
     for (int t = 0; t < 4; t++) {
       if (!v[t]) continue;
       const int64_t de = (d[t] < 0 || d[t] > FOLD_SAT) ? FOLD_SAT : d[t];
-      const int64_t a = f[t] ? de : 0, bb = f[t] ? sat_add(o[t].disp, bx[t] >= 0 ? bx[t] : de) : 0;
+      const int64_t a = f[t] ? de : 0,
+                    bb = f[t] ? sat_add(o[t].disp, (BLOCKS && bx[t] >= 0) ? bx[t] : de) : 0;
       if (st[t]) {
         oidx++;
         rA = a;
@@ -1311,7 +1316,7 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
           const uint32_t tag = op_tag(o[t].meta);
           const bool bad = d[t] < 0 || d[t] >= (int64_t)(EXEC_BAD >> 2);
           uint64_t pay;
-          if (tag == TAG_KERN && bx[t] >= 0) pay = EXEC_OVF >> 2;   // blocks always fold (packer)
+          if (BLOCKS && tag == TAG_KERN && bx[t] >= 0) pay = EXEC_OVF >> 2;   // blocks always fold
           else if (tag == TAG_KERN) pay = bad ? (EXEC_BAD >> 2) : (uint64_t)d[t];
           else pay = (o[t].arg == NO_REC) ? (EXEC_NONE >> 2) : (uint64_t)o[t].arg;
           out[oidx] = ExecOp{o[t].disp, (pay << 2) | tag};
@@ -1375,7 +1380,9 @@ void launch_resolve(const DevBatch &b, cudaStream_t s) {
     if (b.n_chunks) {
       const unsigned g = (b.n_chunks + FOLD_WARPS - 1) / FOLD_WARPS;
       fold_count_kernel<<<g, FOLD_WARPS * 32, 0, s>>>(b);
-      fold_write_kernel<<<(unsigned)((b.n_chunks * 32ull + 127) / 128), 128, 0, s>>>(b);
+      const unsigned gw = (unsigned)((b.n_chunks * 32ull + 127) / 128);
+      if (b.n_blocks) fold_write_kernel<true><<<gw, 128, 0, s>>>(b);
+      else fold_write_kernel<false><<<gw, 128, 0, s>>>(b);
     }
     if (b.n_reps) fold_empty_kernel<<<(b.n_reps + 7) / 8, dim3(32, 8), 0, s>>>(b);
   } else if (b.n_ops) {

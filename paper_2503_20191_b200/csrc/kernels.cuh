@@ -20,7 +20,7 @@ struct DevBatch {
   const RankRec *ranks;
   const uint32_t *rank_comm;
   const CommRec *comms;
-  const SlotRec *slots;
+  const SlotRec *wfeats;      // unique call records (wire features)
   const Walker *walkers;      // heaviest stream first
   const uint32_t *wids;       // rank-major (rank, stream) -> walker index
   const RepHdr *reps;
@@ -65,7 +65,7 @@ struct DevBatch {
   uint32_t *clen;             // folded FIFO lengths (fold_kernel) or null: unfolded ops
   uint32_t *ccounts;          // host-sync dispatch counts in folded indices (with clen)
   int32_t *err_flag;          // any estimator failure
-  uint32_t n_jobs, n_reps, n_feats, n_slots, n_blocks;
+  uint32_t n_jobs, n_reps, n_feats, n_slots, n_blocks, n_wfeats;
   uint64_t n_ops, n_rcolls;
 };
 

@@ -764,6 +764,35 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
                                 job.device});
     }
   }
+  // wire features: the unique call records of the job (collective_estimate
+  // depends on kind, bytes, nranks, topology and device only), one wire time
+  // each on the device; slots keep an index
+  {
+    struct WK {
+      int64_t bytes, fixed;
+      int32_t kind, nranks, topo, device;
+      bool operator==(const WK &o) const {
+        return bytes == o.bytes && fixed == o.fixed && kind == o.kind && nranks == o.nranks &&
+               topo == o.topo && device == o.device;
+      }
+    };
+    struct WH {
+      size_t operator()(const WK &k) const {
+        return std::hash<int64_t>()(k.bytes * 0x9E3779B97F4A7C15ll ^ k.fixed ^
+                                    ((int64_t)k.kind << 40) ^ ((int64_t)k.nranks << 20) ^
+                                    ((int64_t)k.topo << 56) ^ ((int64_t)k.device << 60));
+      }
+    };
+    std::unordered_map<WK, uint32_t, WH> wmap;
+    P.slot_wf.resize(P.slots.size());
+    for (size_t q = 0; q < P.slots.size(); q++) {
+      const SlotRec &r = P.slots[q];
+      auto it = wmap.emplace(WK{r.bytes, r.fixed, r.kind, r.nranks, r.topo, r.device},
+                             (uint32_t)P.wfeats.size());
+      if (it.second) P.wfeats.push_back(r);
+      P.slot_wf[q] = it.first->second;
+    }
+  }
   // work accounting over ALL ranks (sim.py:183-184)
   int64_t rank_ops = 0, dev_ops = 0;
   for (int r = 0; r < job.num_ranks; r++) {

@@ -25,7 +25,9 @@ struct JobPack {
   std::vector<KBlock> blocks;          // interned kernel blocks (soa.h KBLOCK)
   std::vector<uint32_t> blk_fids;      // their feature ids, job-local
   std::vector<CommRec> comms;
-  std::vector<SlotRec> slots;
+  std::vector<SlotRec> slots;          // host only: one per (comm, call_idx) group call
+  std::vector<SlotRec> wfeats;         // unique call records of the job (uploaded)
+  std::vector<uint32_t> slot_wf;       // per slot: its wire feature
   std::vector<RankRec> ranks;
   std::vector<uint32_t> rank_comm;
   std::vector<Walker> walkers;         // rank-major (rank, local stream)
@@ -44,7 +46,7 @@ struct JobPack {
     reps.clear(); ops.clear(); op_seq.clear(); streams.clear(); stream_events.clear(); coll_lc.clear();
     coll_idx.clear(); syncs.clear(); counts.clear(); mems.clear(); feats.clear(); comms.clear();
     blocks.clear(); blk_fids.clear();
-    slots.clear(); ranks.clear(); rank_comm.clear(); walkers.clear(); wids.clear();
+    slots.clear(); wfeats.clear(); slot_wf.clear(); ranks.clear(); rank_comm.clear(); walkers.clear(); wids.clear();
     rcolls.clear(); rep_ring_ok.clear(); comm_rdv.clear(); rank_orig.clear(); rank_sim.clear();
     collapsed = false;
     n_fire = n_delay = 0;

@@ -240,11 +240,11 @@ class Engine:
         return s.value or 0
 
     def batch_stats(self) -> dict:
-        o = (C.c_int64 * 14)()
+        o = (C.c_int64 * 16)()
         _check(lib().maya_batch_stats(self._h, o))
         keys = ("jobs", "rep_events", "rank_comms", "features", "slots", "device_ops",
                 "rank_ops", "arena_bytes", "ranks", "reps", "run_launches", "topk_launches",
-                "kernel_blocks", "block_fids")
+                "kernel_blocks", "block_fids", "wire_features")
         return {k: int(v) for k, v in zip(keys, o)}
 
     def arena_bytes(self) -> int:
