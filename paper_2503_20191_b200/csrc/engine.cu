@@ -100,6 +100,7 @@ struct maya_engine {
   DevBatch db{};
   DevTables tables{};
   // segments
+  Seg s_fmeta;
   Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_wfeats, s_walkers, s_reps, s_ops, s_streams,
       s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
       s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks, s_grid_parts, s_comm_part, s_blocks,
@@ -387,7 +388,7 @@ bool pack_eq(const JobPack &a, const JobPack &b) {
          vec_eq(a.ops, b.ops) && vec_eq(a.op_seq, b.op_seq) && vec_eq(a.streams, b.streams) &&
          vec_eq(a.coll_lc, b.coll_lc) && vec_eq(a.coll_idx, b.coll_idx) &&
          vec_eq(a.syncs, b.syncs) && vec_eq(a.counts, b.counts) && vec_eq(a.mems, b.mems) &&
-         vec_eq(a.feats, b.feats) && vec_eq(a.comms, b.comms) && vec_eq(a.slots, b.slots) &&
+         vec_eq(a.feats, b.feats) && vec_eq(a.feat_meta, b.feat_meta) && vec_eq(a.comms, b.comms) && vec_eq(a.slots, b.slots) &&
          vec_eq(a.ranks, b.ranks) && vec_eq(a.rank_comm, b.rank_comm) &&
          vec_eq(a.walkers, b.walkers) && vec_eq(a.wids, b.wids) && vec_eq(a.rcolls, b.rcolls) &&
          vec_eq(a.rep_ring_ok, b.rep_ring_ok) && vec_eq(a.comm_rdv, b.comm_rdv) &&
@@ -599,6 +600,7 @@ int maya_upload(maya_engine *e) {
   seg(e->s_counts, n_counts * sizeof(uint32_t));
   seg(e->s_mems, n_mems * sizeof(MemRec));
   seg(e->s_feats, n_feats * sizeof(Feature));
+  seg(e->s_fmeta, n_feats * sizeof(uint32_t));
   seg(e->s_rcolls, n_rcolls * sizeof(RankColl));
   seg(e->s_rcslot, n_rcolls * sizeof(uint32_t));
   seg(e->s_lane_jobs, nj * sizeof(LaneJob));
@@ -922,6 +924,7 @@ int maya_upload(maya_engine *e) {
     CPY(s_counts, counts, B.counts)
     CPY(s_mems, mems, B.mems)
     CPY(s_feats, feats, B.feats)
+    CPY(s_fmeta, feat_meta, B.feats)
 #undef CPY
   };
   {
@@ -967,6 +970,7 @@ int maya_upload(maya_engine *e) {
   db.counts = (const uint32_t *)(D + e->s_counts.off);
   db.mems = (const MemRec *)(D + e->s_mems.off);
   db.feats = (const Feature *)(D + e->s_feats.off);
+  db.feat_meta = (const uint32_t *)(D + e->s_fmeta.off);
   db.blocks = (const KBlock *)(D + e->s_blocks.off);
   db.blk_fids = (const uint32_t *)(D + e->s_blk_fids.off);
   db.n_blocks = (uint32_t)n_blocks;

@@ -72,8 +72,11 @@ __device__ __forceinline__ bool ceil_div_i64(u128 a, u128 b, int64_t *out) {
 __global__ void estimate_features_kernel(DevBatch b, DevTables t) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= b.n_feats) return;
-  Feature f = b.feats[i];
-  if (f.fixed >= 0) { b.feat_ns[i] = f.fixed; return; }
+  const longlong2 fv = __ldg(reinterpret_cast<const longlong2 *>(b.feats) + i);
+  const uint32_t meta = __ldg(b.feat_meta + i);
+  if (meta & FMETA_FIXED) { b.feat_ns[i] = fv.x; return; }
+  struct { int64_t flops, bytes; int32_t op_kind, dtype, device; } f{
+      fv.x, fv.y, fmeta_op(meta), fmeta_dtype(meta), fmeta_device(meta)};
   const maya_device_params &dev = t.devs[f.device];
   int64_t compute = 0, memory = 0;
   bool ok = true;
@@ -500,17 +503,19 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
     long long t_b = clock64();
 #endif
     if (blocker) { A = 0; B = NEG; }
-    bool flag = (lane == 0) || ((bmask >> (lane - 1)) & 1u);
+    // segmented inclusive scan; segments start at lane 0 and after each
+    // blocker: lane L absorbs lane L - off while that lane is in its segment
+    // (L - off >= start of L's segment), so no flag travels with the values
+    const uint32_t starts = (bmask << 1) | 1u;
+    const int32_t seg0 = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
 #pragma unroll
     for (uint32_t off = 1; off < 32; off <<= 1) {
       const int64_t A2 = __shfl_up_sync(FULL, A, off);
       const int64_t B2 = __shfl_up_sync(FULL, B, off);
-      const bool f2 = __shfl_up_sync(FULL, flag, off);
-      if (lane >= off && !flag) {
+      if ((int32_t)lane - (int32_t)off >= seg0) {
         const int64_t nb = B2 + A;
         B = nb > B ? nb : B;
         A = A2 + A;
-        flag = f2;
       }
     }
 #ifdef MAYA_PROFILE
@@ -543,11 +548,13 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
         b.tl_start[c.tl + s.i + lane] = rdisp > prev ? rdisp : prev;
         b.tl_end[c.tl + s.i + lane] = d;
       }
-      if (__any_sync(FULL, in_seg && fx)) {
+      // one warp reduction for both: side effects made (bit 0), error (bit 1)
+      const uint32_t ev = __reduce_or_sync(FULL, ((in_seg && fx) ? 1u : 0u) | (err != 0 ? 2u : 0u));
+      if (ev & 1u) {
         adv = true;
         __threadfence_block();
       }
-      if (__any_sync(FULL, err != 0)) {
+      if (ev & 2u) {
         err = __reduce_max_sync(FULL, (unsigned)err);
         blocked = true;
         commit = q;

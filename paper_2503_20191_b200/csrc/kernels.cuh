@@ -32,6 +32,7 @@ struct DevBatch {
   const uint32_t *counts;
   const MemRec *mems;
   const Feature *feats;
+  const uint32_t *feat_meta;
   const KBlock *blocks;       // kernel blocks (batch-global fid lists)
   const uint32_t *blk_fids;
   int64_t *blk_ab;            // per block: (A, Brel) composite after the estimator

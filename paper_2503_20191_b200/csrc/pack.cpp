@@ -250,7 +250,10 @@ struct RepPacker {
     if (it == F->feat_map.end()) {
       fid = (uint32_t)P->feats.size();
       F->feat_map.emplace(key, fid);
-      P->feats.push_back(Feature{f[2], f[3], -1, (int32_t)f[0], (int16_t)f[1], (int16_t)device});
+      if (f[0] < 0 || f[0] > 0xfff || f[1] < 0 || f[1] > 0xff || device < 0 || device > 0xff)
+        throw Fail{MAYA_ST_BAD_INPUT, "op kind / dtype / device id outside the feature meta word"};
+      P->feats.push_back(Feature{f[2], f[3]});
+      P->feat_meta.push_back(fmeta((int32_t)f[0], (int32_t)f[1], device));
     } else {
       fid = it->second;
     }
@@ -339,7 +342,8 @@ struct RepPacker {
           if (it == F->fixed_map.end()) {
             fid = (uint32_t)P->feats.size();
             F->fixed_map.emplace(host_ns, fid);
-            P->feats.push_back(Feature{0, 0, host_ns, -1, -1, (int16_t)device});
+            P->feats.push_back(Feature{host_ns, 0});
+            P->feat_meta.push_back(FMETA_FIXED | fmeta(0, 0, device));
           } else {
             fid = it->second;
           }
@@ -718,8 +722,13 @@ void renumber_features(JobPack &P) {
   for (uint32_t f = 0; f < nf; f++)
     if (nid[f] == UINT32_MAX) nid[f] = next++;   // unused (cannot happen; keep total)
   std::vector<Feature> nf2(nf);
-  for (uint32_t f = 0; f < nf; f++) nf2[nid[f]] = P.feats[f];
+  std::vector<uint32_t> nm2(nf);
+  for (uint32_t f = 0; f < nf; f++) {
+    nf2[nid[f]] = P.feats[f];
+    nm2[nid[f]] = P.feat_meta[f];
+  }
   P.feats.swap(nf2);
+  P.feat_meta.swap(nm2);
 }
 
 void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,

@@ -22,6 +22,7 @@ struct JobPack {
   std::vector<uint32_t> counts;
   std::vector<MemRec> mems;
   std::vector<Feature> feats;
+  std::vector<uint32_t> feat_meta;     // fmeta() per feature (soa.h)
   std::vector<KBlock> blocks;          // interned kernel blocks (soa.h KBLOCK)
   std::vector<uint32_t> blk_fids;      // their feature ids, job-local
   std::vector<CommRec> comms;
@@ -44,7 +45,7 @@ struct JobPack {
   void clear() {   // keeps capacity (see engine.cu PackPool)
     hdr = JobHdr{};
     reps.clear(); ops.clear(); op_seq.clear(); streams.clear(); stream_events.clear(); coll_lc.clear();
-    coll_idx.clear(); syncs.clear(); counts.clear(); mems.clear(); feats.clear(); comms.clear();
+    coll_idx.clear(); syncs.clear(); counts.clear(); mems.clear(); feats.clear(); feat_meta.clear(); comms.clear();
     blocks.clear(); blk_fids.clear();
     slots.clear(); wfeats.clear(); slot_wf.clear(); ranks.clear(); rank_comm.clear(); walkers.clear(); wids.clear();
     rcolls.clear(); rep_ring_ok.clear(); comm_rdv.clear(); rank_orig.clear(); rank_sim.clear();

@@ -242,15 +242,20 @@ struct RepHdr {
 };
 
 // Kernel feature (one per unique (op kind, dtype, flops, bytes) of a job, or a
-// host-provided duration).
+// host-provided duration): 16 B of operands plus a 4 B meta word in a parallel
+// array, so the estimator streams 20 B per feature.
 struct Feature {
-  int64_t flops;
+  int64_t flops;       // FMETA_FIXED: the host duration
   int64_t bytes;
-  int64_t fixed;       // >= 0: host duration; -1: roofline
-  int32_t op_kind;
-  int16_t dtype;
-  int16_t device;
 };
+static const uint32_t FMETA_FIXED = 0x80000000u;
+__host__ __device__ inline uint32_t fmeta(int32_t op_kind, int32_t dtype, int32_t device) {
+  return ((uint32_t)op_kind & 0xfffu) | (((uint32_t)dtype & 0xffu) << 12) |
+         (((uint32_t)device & 0xffu) << 20);
+}
+__host__ __device__ inline int32_t fmeta_op(uint32_t m) { return (int32_t)(m & 0xfffu); }
+__host__ __device__ inline int32_t fmeta_dtype(uint32_t m) { return (int32_t)((m >> 12) & 0xffu); }
+__host__ __device__ inline int32_t fmeta_device(uint32_t m) { return (int32_t)((m >> 20) & 0xffu); }
 
 struct CommRec {
   int32_t nranks;
