@@ -1006,6 +1006,13 @@ int maya_upload(maya_engine *e) {
     t.eff_den[i] = e->eff_den[i];
   }
   t.overhead_ns = e->overhead_ns;
+  for (int d = 0; d < t.n_devs && d < 8; d++) {
+    for (int q = 0; q < MAYA_MAX_DTYPES; q++)
+      t.inv_peak[d][q] = t.devs[d].peak_flops[q] > 0 ? 1.0 / (double)t.devs[d].peak_flops[q] : 0.0;
+    t.inv_hbm[d] = t.devs[d].hbm_bytes_per_s > 0 ? 1.0 / (double)t.devs[d].hbm_bytes_per_s : 0.0;
+  }
+  for (int q = 0; q < t.n_op_kinds && q < 64; q++)
+    t.inv_num[q] = t.eff_num[q] > 0 ? 1.0 / (double)t.eff_num[q] : 0.0;
   for (size_t j = 0; j < nj; j++) {
     const JobPack &P = e->packs[j];
     if (P.hdr.status == MAYA_ST_OK && (int)P.hdr.device >= t.n_devs && !P.feats.empty())

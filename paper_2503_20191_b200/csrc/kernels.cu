@@ -66,6 +66,35 @@ __device__ __forceinline__ bool ceil_div_i64(u128 a, u128 b, int64_t *out) {
   return true;
 }
 
+// ceil(a / b) for a, b < 2^64 with a reciprocal estimate inv ~ 1/b: the
+// double quotient a * inv is within a few units of the true one when it is
+// below 2^50, then corrected exactly with 64 x 64 -> 128-bit products;
+// anything else goes through ceil_div_i64.
+__device__ __forceinline__ bool ceil_div_inv(uint64_t x, uint64_t y, double inv, int64_t *out) {
+  const double qd = (double)x * inv;
+  if (inv > 0.0 && qd < 1125899906842624.0) {   // 2^50
+    uint64_t q = (uint64_t)qd;
+    // p = q * y as (hi, lo); fix q until q * y <= x < (q + 1) * y
+    uint64_t lo = q * y, hi = __umul64hi(q, y);
+    while (hi != 0 || lo > x) {
+      q--;
+      const uint64_t nlo = lo - y;
+      hi -= (nlo > lo) ? 1u : 0u;
+      lo = nlo;
+    }
+    while (true) {   // (q + 1) * y <= x ?
+      const uint64_t nlo = lo + y;
+      if (nlo < lo || nlo > x) break;
+      lo = nlo;
+      q++;
+    }
+    if (lo != x) q++;
+    *out = (int64_t)q;
+    return true;
+  }
+  return ceil_div_i64((u128)x, (u128)y, out);
+}
+
 // ---------------------------------------------------------------------------
 // estimators
 
@@ -89,12 +118,19 @@ __global__ void estimate_features_kernel(DevBatch b, DevTables t) {
       ok = mul_u128_u64((u128)(uint64_t)f.flops * 1000000000ull, (uint64_t)t.eff_den[f.op_kind],
                         &num);
       den = (u128)(uint64_t)peak * (uint64_t)t.eff_num[f.op_kind];
-      if (ok) ok = ceil_div_i64(num, den, &compute);
+      if (ok && (num >> 64) == 0 && (den >> 64) == 0)
+        ok = ceil_div_inv((uint64_t)num, (uint64_t)den,
+                          t.inv_peak[f.device][f.dtype] * t.inv_num[f.op_kind], &compute);
+      else if (ok)
+        ok = ceil_div_i64(num, den, &compute);
     }
   }
-  if (ok && f.bytes > 0)
-    ok = ceil_div_i64((u128)(uint64_t)f.bytes * 1000000000ull, (u128)(uint64_t)dev.hbm_bytes_per_s,
-                      &memory);
+  if (ok && f.bytes > 0) {
+    const u128 mb = (u128)(uint64_t)f.bytes * 1000000000ull;
+    ok = (mb >> 64) == 0
+             ? ceil_div_inv((uint64_t)mb, (uint64_t)dev.hbm_bytes_per_s, t.inv_hbm[f.device], &memory)
+             : ceil_div_i64(mb, (u128)(uint64_t)dev.hbm_bytes_per_s, &memory);
+  }
   int64_t m = compute > memory ? compute : memory;
   if (ok && m > INT64_MAX - t.overhead_ns) ok = false;
   if (!ok) {

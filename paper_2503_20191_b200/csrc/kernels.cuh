@@ -76,6 +76,11 @@ struct DevTables {
   int64_t eff_den[64];
   int32_t n_devs, n_op_kinds;
   int64_t overhead_ns;
+  // reciprocals for the quotient estimates of the roofline (corrected exactly):
+  // 1 / peak_flops[dtype], 1 / eff_num[op], 1 / hbm_bytes_per_s (0: none)
+  double inv_peak[8][MAYA_MAX_DTYPES];
+  double inv_num[64];
+  double inv_hbm[8];
 };
 
 void launch_estimate(const DevBatch &b, const DevTables &t, cudaStream_t s);
