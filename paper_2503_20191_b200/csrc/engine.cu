@@ -1011,8 +1011,12 @@ int maya_upload(maya_engine *e) {
       t.inv_peak[d][q] = t.devs[d].peak_flops[q] > 0 ? 1.0 / (double)t.devs[d].peak_flops[q] : 0.0;
     t.inv_hbm[d] = t.devs[d].hbm_bytes_per_s > 0 ? 1.0 / (double)t.devs[d].hbm_bytes_per_s : 0.0;
   }
-  for (int q = 0; q < t.n_op_kinds && q < 64; q++)
+  for (int q = 0; q < t.n_op_kinds && q < 64; q++) {
     t.inv_num[q] = t.eff_num[q] > 0 ? 1.0 / (double)t.eff_num[q] : 0.0;
+    const unsigned __int128 scale = (unsigned __int128)1000000000ull * (uint64_t)t.eff_den[q];
+    t.max_flops[q] = (t.eff_den[q] > 0 && (scale >> 64) == 0) ? UINT64_MAX / (uint64_t)scale : 0;
+    t.max_peak[q] = t.eff_num[q] > 0 ? UINT64_MAX / (uint64_t)t.eff_num[q] : 0;
+  }
   for (size_t j = 0; j < nj; j++) {
     const JobPack &P = e->packs[j];
     if (P.hdr.status == MAYA_ST_OK && (int)P.hdr.device >= t.n_devs && !P.feats.empty())

@@ -113,6 +113,11 @@ __global__ void estimate_features_kernel(DevBatch b, DevTables t) {
     int64_t peak = (f.dtype >= 0 && f.dtype < MAYA_MAX_DTYPES) ? dev.peak_flops[f.dtype] : 0;
     if (peak <= 0 || f.op_kind < 0 || f.op_kind >= t.n_op_kinds) {
       ok = false;  // EstimationError: no peak rate for dtype (estimate.py:124-127)
+    } else if ((uint64_t)f.flops <= t.max_flops[f.op_kind] && (uint64_t)peak <= t.max_peak[f.op_kind]) {
+      // 64-bit fast path: flops * 1e9 * den and peak * num both fit (host bounds)
+      ok = ceil_div_inv((uint64_t)f.flops * (1000000000ull * (uint64_t)t.eff_den[f.op_kind]),
+                        (uint64_t)peak * (uint64_t)t.eff_num[f.op_kind],
+                        t.inv_peak[f.device][f.dtype] * t.inv_num[f.op_kind], &compute);
     } else {
       u128 num, den;
       ok = mul_u128_u64((u128)(uint64_t)f.flops * 1000000000ull, (uint64_t)t.eff_den[f.op_kind],
