@@ -110,6 +110,11 @@ struct FeatState {
   };
   std::vector<BlkKey> blk_keys;                      // per block id: its launch list
   std::vector<KSpec> blk_specs;
+  struct BlkCacheEnt {
+    uint64_t h;
+    uint32_t id;
+  };
+  BlkCacheEnt bcache[256];                           // direct-mapped, in front of blk_map
   FeatCacheEnt fcache[64];
   void clear() {
     feat_map.clear();
@@ -117,6 +122,7 @@ struct FeatState {
     blk_map.clear();
     blk_keys.clear();
     blk_specs.clear();
+    for (auto &e : bcache) e.id = UINT32_MAX;
     for (auto &ce : fcache) ce.fid = UINT32_MAX;
   }
 };
@@ -290,13 +296,21 @@ struct RepPacker {
       h2 = (h2 ^ (uint64_t)ks[i].bytes) * 0xc4ceb9fe1a85ec53ull;
     }
     const uint64_t hsh = h0 ^ (h1 >> 1) ^ (h2 << 1) ^ (h1 * 31) ^ (h2 >> 7);
-    uint32_t id = UINT32_MAX;
-    auto it = F->blk_map.find(hsh);
-    if (it != F->blk_map.end()) {
-      const FeatState::BlkKey &bk = F->blk_keys[it->second];
+    uint32_t id = UINT32_MAX, cand = UINT32_MAX;
+    FeatState::BlkCacheEnt &ce = F->bcache[(hsh ^ (hsh >> 29)) & 255];
+    if (ce.id != UINT32_MAX && ce.h == hsh) {
+      cand = ce.id;
+    } else {
+      auto it = F->blk_map.find(hsh);
+      if (it != F->blk_map.end()) cand = it->second;
+    }
+    if (cand != UINT32_MAX) {
+      const FeatState::BlkKey &bk = F->blk_keys[cand];
       if (bk.n == n && bk.gap == gap && bk.dtype == dtype &&
-          memcmp(F->blk_specs.data() + bk.spec0, ks, n * sizeof(KSpec)) == 0)
-        id = it->second;
+          memcmp(F->blk_specs.data() + bk.spec0, ks, n * sizeof(KSpec)) == 0) {
+        id = cand;
+        ce = FeatState::BlkCacheEnt{hsh, cand};
+      }
     }
     if (id == UINT32_MAX) {
       id = (uint32_t)P->blocks.size();
@@ -308,7 +322,8 @@ struct RepPacker {
         P->blk_fids.push_back(feature(f));
       }
       F->blk_specs.insert(F->blk_specs.end(), ks, ks + n);
-      F->blk_map.emplace(hsh, id);   // first block of this hash stays the interned one
+      if (F->blk_map.emplace(hsh, id).second) ce = FeatState::BlkCacheEnt{hsh, id};
+      // (a colliding hash keeps its first block interned; later ones stay unshared)
     }
     gpre += gap;                     // the first kernel's gap
     seq += gap > 0 ? 1 : 0;
