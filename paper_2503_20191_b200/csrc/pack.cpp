@@ -790,31 +790,49 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
   }
   // wire features: the unique call records of the job (collective_estimate
   // depends on kind, bytes, nranks, topology and device only), one wire time
-  // each on the device; slots keep an index
+  // each on the device; slots keep an index.  A job has a handful: the last
+  // match, then a scan of the (short) list, then a hash map past 32 entries.
   {
-    struct WK {
-      int64_t bytes, fixed;
-      int32_t kind, nranks, topo, device;
-      bool operator==(const WK &o) const {
-        return bytes == o.bytes && fixed == o.fixed && kind == o.kind && nranks == o.nranks &&
-               topo == o.topo && device == o.device;
-      }
+    auto same = [](const SlotRec &a, const SlotRec &b) {
+      return a.bytes == b.bytes && a.fixed == b.fixed && a.kind == b.kind &&
+             a.nranks == b.nranks && a.topo == b.topo && a.device == b.device;
     };
     struct WH {
-      size_t operator()(const WK &k) const {
+      size_t operator()(const SlotRec &k) const {
         return std::hash<int64_t>()(k.bytes * 0x9E3779B97F4A7C15ll ^ k.fixed ^
                                     ((int64_t)k.kind << 40) ^ ((int64_t)k.nranks << 20) ^
                                     ((int64_t)k.topo << 56) ^ ((int64_t)k.device << 60));
       }
     };
-    std::unordered_map<WK, uint32_t, WH> wmap;
+    struct WE {
+      bool operator()(const SlotRec &a, const SlotRec &b) const {
+        return a.bytes == b.bytes && a.fixed == b.fixed && a.kind == b.kind &&
+               a.nranks == b.nranks && a.topo == b.topo && a.device == b.device;
+      }
+    };
+    std::unordered_map<SlotRec, uint32_t, WH, WE> wmap;
     P.slot_wf.resize(P.slots.size());
+    uint32_t last = UINT32_MAX;
     for (size_t q = 0; q < P.slots.size(); q++) {
       const SlotRec &r = P.slots[q];
-      auto it = wmap.emplace(WK{r.bytes, r.fixed, r.kind, r.nranks, r.topo, r.device},
-                             (uint32_t)P.wfeats.size());
-      if (it.second) P.wfeats.push_back(r);
-      P.slot_wf[q] = it.first->second;
+      uint32_t id = UINT32_MAX;
+      if (last != UINT32_MAX && same(P.wfeats[last], r)) {
+        id = last;
+      } else if (P.wfeats.size() <= 32) {
+        for (uint32_t w = 0; w < P.wfeats.size(); w++)
+          if (same(P.wfeats[w], r)) { id = w; break; }
+        if (id == UINT32_MAX && P.wfeats.size() == 32)   // switching to the map
+          for (uint32_t w = 0; w < 32; w++) wmap.emplace(P.wfeats[w], w);
+      } else {
+        auto it = wmap.find(r);
+        if (it != wmap.end()) id = it->second;
+      }
+      if (id == UINT32_MAX) {
+        id = (uint32_t)P.wfeats.size();
+        P.wfeats.push_back(r);
+        if (P.wfeats.size() > 32) wmap.emplace(r, id);
+      }
+      P.slot_wf[q] = last = id;
     }
   }
   // work accounting over ALL ranks (sim.py:183-184)
