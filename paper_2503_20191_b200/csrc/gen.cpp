@@ -333,6 +333,16 @@ struct Builder {
     gap();
     ev(MAYA_EV_KERNEL, s, k.op, dtype, k.flops, k.bytes);
   }
+  // n consecutive launches on stream s (one append to the open run in block mode)
+  void kernels(int32_t s, const KSpec *k, size_t n) {
+    if (blocks) {
+      if (!run.empty() && run_stream != s) flush();
+      run_stream = s;
+      run.insert(run.end(), k, k + n);
+      return;
+    }
+    for (size_t i = 0; i < n; i++) kernel(s, k[i]);
+  }
   void memcpy_h2d(int32_t s, int64_t n) {
     gap();
     ev(MAYA_EV_MEMCPY, s, OK_MEMCPY_H2D, DT_FP32, 0, n);
@@ -467,19 +477,22 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
     if (t > 1 && sp) B.collective(STREAM_COMPUTE, tp_lc, K_ALLGATHER, tp_coll_bytes);
   };
   auto emit_layer_fwd = [&]() {
+    if (t == 1) {   // no tensor-parallel collectives between the launches
+      B.kernels(STREAM_COMPUTE, lks.data(), 12);
+      return;
+    }
     B.kernel(STREAM_COMPUTE, lks[0]);
     tp_gather_fwd();
-    for (int q = 1; q < 6; q++) B.kernel(STREAM_COMPUTE, lks[q]);
+    B.kernels(STREAM_COMPUTE, &lks[1], 5);
     tp_pair_fwd();
-    B.kernel(STREAM_COMPUTE, lks[6]);
-    B.kernel(STREAM_COMPUTE, lks[7]);
+    B.kernels(STREAM_COMPUTE, &lks[6], 2);
     tp_gather_fwd();
-    for (int q = 8; q < 11; q++) B.kernel(STREAM_COMPUTE, lks[q]);
+    B.kernels(STREAM_COMPUTE, &lks[8], 3);
     tp_pair_fwd();
     B.kernel(STREAM_COMPUTE, lks[11]);
   };
   auto emit_layer_fwd_compute_only = [&]() {
-    for (const KSpec &k : lks) B.kernel(STREAM_COMPUTE, k);
+    B.kernels(STREAM_COMPUTE, lks.data(), lks.size());
   };
   auto emit_head_fwd = [&](bool compute_only) {
     B.kernel(STREAM_COMPUTE, hks[0]);
@@ -490,10 +503,10 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   };
   auto emit_layer_bwd = [&]() {
     if (t > 1) B.collective(STREAM_COMPUTE, tp_lc, sp ? K_ALLGATHER : K_ALLREDUCE, tp_coll_bytes);
-    for (const KSpec &k : mlp_bwd) B.kernel(STREAM_COMPUTE, k);
+    B.kernels(STREAM_COMPUTE, mlp_bwd.data(), mlp_bwd.size());
     if (t > 1 && sp) B.collective(STREAM_COMPUTE, tp_lc, K_REDUCESCATTER, tp_coll_bytes);
     if (t > 1) B.collective(STREAM_COMPUTE, tp_lc, sp ? K_ALLGATHER : K_ALLREDUCE, tp_coll_bytes);
-    for (const KSpec &k : attn_bwd) B.kernel(STREAM_COMPUTE, k);
+    B.kernels(STREAM_COMPUTE, attn_bwd.data(), attn_bwd.size());
     if (t > 1 && sp) B.collective(STREAM_COMPUTE, tp_lc, K_REDUCESCATTER, tp_coll_bytes);
   };
   auto emit_forward = [&](int64_t mb, int chunk_id) {
@@ -533,7 +546,7 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
       if (ch.has_head) emit_head_fwd(true);
     }
     if (ch.has_head)
-      for (const KSpec &k : head_bwd) B.kernel(STREAM_COMPUTE, k);
+      B.kernels(STREAM_COMPUTE, head_bwd.data(), head_bwd.size());
     for (int64_t l = 0; l < ch.layers; l++) emit_layer_bwd();
     if (ch.has_embed) B.kernel(STREAM_COMPUTE, eks);
     if (vs > 0) {
