@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <tuple>
 #include <unordered_map>
 
@@ -239,9 +240,9 @@ std::string comm_name(const CommRole &r) {
   return buf;
 }
 
-std::vector<CommRole> worker_comms(const Coords &C, int64_t v, int64_t rank) {
+void worker_comms(const Coords &C, int64_t v, int64_t rank, std::vector<CommRole> &out) {
   const int64_t i = rank % C.t, j = (rank / C.t) % C.d, k = rank / (C.t * C.d);
-  std::vector<CommRole> out;
+  out.clear();
   if (C.t > 1) out.push_back({C_TP, k, j, 0, (int32_t)C.t, (int32_t)i});
   if (C.d > 1) out.push_back({C_DP, i, k, 0, (int32_t)C.d, (int32_t)j});
   const int64_t total_vs = C.p * v;
@@ -256,7 +257,6 @@ std::vector<CommRole> worker_comms(const Coords &C, int64_t v, int64_t rank) {
       out.push_back({C_PB, vs, i, j, 2, 1});
     }
   }
-  return out;
 }
 
 // members of a communicator by position (resolved by collate from CommInits)
@@ -278,6 +278,63 @@ std::vector<int64_t> comm_members(const Coords &C, const CommRole &r) {
       m.push_back(rank_of(C, r.b, r.c, r.a % C.p));
   }
   return m;
+}
+
+// Rank of x's decimal string among the decimal strings of 0..65535 (string
+// order: "1" < "10" < "11" < "2"); a monotone map of the name order of one
+// numeric field, built once per process.
+const uint16_t *decimal_string_rank() {
+  static std::vector<uint16_t> rank;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    std::vector<std::pair<std::string, uint32_t>> v(65536);
+    for (uint32_t x = 0; x < 65536; x++) v[x] = {std::to_string(x), x};
+    std::sort(v.begin(), v.end());
+    rank.resize(65536);
+    for (uint32_t q = 0; q < 65536; q++) rank[v[q].second] = (uint16_t)q;
+  });
+  return rank.data();
+}
+
+// Sort key equal to the order of comm_name(r) strings.  Field separators are
+// '.' (below every digit) and each name kind has a fixed shape, so comparing
+// names = comparing (kind, field ranks) lexicographically.
+uint64_t comm_order_key(const CommRole &r) {
+  const uint16_t *R = decimal_string_rank();
+  auto f = [&](int64_t x) -> uint64_t {
+    if (x < 0 || x > 65535) throw GenFail{"communicator coordinate beyond 65535"};
+    return R[x];
+  };
+  switch (r.type) {   // "dp" < "pb" < "pf" < "tp"
+    case C_DP: return (0ull << 48) | (f(r.a) << 32) | (f(r.b) << 16);
+    case C_PB: return (1ull << 48) | (f(r.a) << 32) | (f(r.b) << 16) | f(r.c);
+    case C_PF: return (2ull << 48) | (f(r.a) << 32) | (f(r.b) << 16) | f(r.c);
+    default: return (3ull << 48) | (f(r.a) << 32) | (f(r.b) << 16);
+  }
+}
+
+// topology_of over the communicator's members (cluster.py:85-92), no lists kept
+int8_t comm_topology(const Coords &C, const CommRole &r, int64_t dph, std::vector<int64_t> &hosts) {
+  hosts.clear();
+  switch (r.type) {
+    case C_TP:
+      for (int64_t i = 0; i < C.t; i++) hosts.push_back(rank_of(C, i, r.b, r.a) / dph);
+      break;
+    case C_DP:
+      for (int64_t j = 0; j < C.d; j++) hosts.push_back(rank_of(C, r.a, j, r.b) / dph);
+      break;
+    case C_PF:
+      hosts.push_back(rank_of(C, r.b, r.c, r.a % C.p) / dph);
+      hosts.push_back(rank_of(C, r.b, r.c, (r.a + 1) % C.p) / dph);
+      break;
+    default:
+      hosts.push_back(rank_of(C, r.b, r.c, (r.a + 1) % C.p) / dph);
+      hosts.push_back(rank_of(C, r.b, r.c, r.a % C.p) / dph);
+  }
+  const size_t n = hosts.size();
+  std::sort(hosts.begin(), hosts.end());
+  const size_t u = (size_t)(std::unique(hosts.begin(), hosts.end()) - hosts.begin());
+  return u == 1 ? 0 : (u == n ? 1 : 2);
 }
 
 // -- _TraceBuilder (workload.py:510-568)
@@ -405,7 +462,8 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
       G.ev_f.reserve(G.ev_f.size() + 4 * est);
     }
   }
-  std::vector<CommRole> roles = worker_comms(C, v, rank);
+  std::vector<CommRole> roles;
+  worker_comms(C, v, rank, roles);
   // local comm index of each role (first CommInit of a comm id); keyed by the
   // role's integer fields, which comm_name spells out one to one
   std::map<std::tuple<int, int64_t, int64_t, int64_t>, int> local;
@@ -678,66 +736,80 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
       int32_t stage_of_first;  // stage of position-0 rank
       int32_t lc_of_first;     // local comm index of the role in that rank's rep
     };
-    std::unordered_map<uint64_t, int32_t> idx_of;   // role key -> comm (discovery order)
+    // role key -> comm (discovery order): open addressing, sized for every
+    // (rank, role) pair, so the table never grows
     std::vector<CInfo> infos;
-    std::vector<uint64_t> keys_by_rank;            // per rank, per local comm
+    std::vector<int32_t> comm_of;                  // per rank, per local comm: discovery index
     std::vector<int64_t> rk_off(n + 1, 0);
+    const size_t roles_per_rank = 2 + 4 * (size_t)cfg.virtual_stages;
+    size_t cap = 64;
+    while (cap < 2 * (size_t)n * roles_per_rank) cap <<= 1;
+    std::vector<uint64_t> hkey(cap, ~0ull);
+    std::vector<int32_t> hval(cap, -1);
+    auto slot_of = [&](uint64_t key) {
+      size_t h = (size_t)((key * 0x9E3779B97F4A7C15ull) >> 20) & (cap - 1);
+      while (hkey[h] != key && hkey[h] != ~0ull) h = (h + 1) & (cap - 1);
+      return h;
+    };
+    std::vector<CommRole> roles;
     for (int64_t r = 0; r < n; r++) {
-      const std::vector<CommRole> roles = worker_comms(C, cfg.virtual_stages, r);
+      worker_comms(C, cfg.virtual_stages, r, roles);
       for (size_t q = 0; q < roles.size(); q++) {
         const uint64_t key = role_key(roles[q]);
-        keys_by_rank.push_back(key);
-        auto it = idx_of.find(key);
-        if (it == idx_of.end()) {
-          idx_of.emplace(key, (int32_t)infos.size());
+        const size_t h = slot_of(key);
+        if (hkey[h] == ~0ull) {
+          hkey[h] = key;
+          hval[h] = (int32_t)infos.size();
           infos.push_back(CInfo{roles[q], -1, -1});
-          it = idx_of.find(key);
         }
-        CInfo &ci = infos[it->second];
+        comm_of.push_back(hval[h]);
+        CInfo &ci = infos[hval[h]];
         if (roles[q].my_rank == 0 && ci.stage_of_first < 0) {
           ci.role = roles[q];
           ci.stage_of_first = (int32_t)(r / (C.t * C.d));
           ci.lc_of_first = (int32_t)q;
         }
       }
-      rk_off[r + 1] = (int64_t)keys_by_rank.size();
+      rk_off[r + 1] = (int64_t)comm_of.size();
     }
-    std::vector<std::string> names(infos.size());
-    for (size_t g = 0; g < infos.size(); g++) names[g] = comm_name(infos[g].role);
+    // JobTrace.groups order = sorted by name (collate.py:323).  The names are
+    // "dp.t<i>.p<k>" < "pb<v>.t<i>.d<j>" < "pf<v>.t<i>.d<j>" < "tp.p<k>.d<j>", so the
+    // string order is the order of (kind, decimal-string rank of each field):
+    // an integer key per communicator, no names needed (built only for the
+    // raw-job path, which exports them)
+    std::vector<uint64_t> okey(infos.size());
+    for (size_t g = 0; g < infos.size(); g++) okey[g] = comm_order_key(infos[g].role);
     std::vector<int32_t> order(infos.size());
     for (size_t g = 0; g < order.size(); g++) order[g] = (int32_t)g;
     std::sort(order.begin(), order.end(),
-              [&](int32_t x, int32_t y) { return names[x] < names[y]; });
+              [&](int32_t x, int32_t y) { return okey[x] < okey[y]; });
     std::vector<int32_t> gid_of(infos.size());
+    std::vector<int64_t> hosts_buf;
     G.call_off.push_back(0);
     for (size_t gi = 0; gi < order.size(); gi++) {
       const int32_t g0 = order[gi];
       gid_of[g0] = (int32_t)gi;
       const CInfo &ci = infos[g0];
       if (ci.stage_of_first < 0) throw GenFail{"communicator without a position-0 member"};
-      std::vector<int64_t> mem = comm_members(C, ci.role);
-      std::vector<int64_t> hosts;
-      for (int64_t r : mem) hosts.push_back(r / cl.devices_per_host);
-      std::vector<int64_t> uh = hosts;
-      std::sort(uh.begin(), uh.end());
-      uh.erase(std::unique(uh.begin(), uh.end()), uh.end());
-      int8_t topo = uh.size() == 1 ? 0 : (uh.size() == hosts.size() ? 1 : 2);
-      G.comm_names.push_back(names[g0]);
       G.comm_nranks.push_back(ci.role.nranks);
-      G.comm_topo.push_back(topo);
+      G.comm_topo.push_back(comm_topology(C, ci.role, cl.devices_per_host, hosts_buf));
       const auto &cl2 = rcalls[ci.stage_of_first].calls[ci.lc_of_first];
       for (auto &kb : cl2) {
         G.call_kind.push_back(kb.first);
         G.call_bytes.push_back(kb.second);
       }
       G.call_off.push_back((int64_t)G.call_kind.size());
-      G.comm_blob += names[g0];
-      G.comm_blob += '\n';
+      if (!sink) {
+        const std::string nm = comm_name(ci.role);
+        G.comm_names.push_back(nm);
+        G.comm_blob += nm;
+        G.comm_blob += '\n';
+      }
     }
     G.rank_comm_off.push_back(0);
     for (int64_t r = 0; r < n; r++) {
       for (int64_t q = rk_off[r]; q < rk_off[r + 1]; q++)
-        G.rank_comm.push_back(gid_of[idx_of.at(keys_by_rank[q])]);
+        G.rank_comm.push_back(gid_of[comm_of[q]]);
       G.rank_comm_off.push_back((int64_t)G.rank_comm.size());
     }
   } catch (const GenFail &f) {

@@ -152,6 +152,7 @@ struct RepPacker {
   uint64_t coll0 = 0, mem0 = 0, sync0 = 0;
   int64_t gpre = 0;
   uint32_t seg = 0, seq = 0, n_devev = 0;
+  bool keep_seq = true;   // event seq per op, for timelines (not kept with kernel blocks)
 
   static uint64_t ekey(int64_t ev, int64_t ver) {
     if (ev < 0 || ev > 0x7fffffff || ver < 0 || ver > 0x7fffffff)
@@ -160,6 +161,7 @@ struct RepPacker {
   }
 
   void begin(JobPack &pk, FeatState &fs, int32_t dev, bool on_the_fly, size_t reserve_hint) {
+    keep_seq = true;
     P = &pk;
     F = &fs;
     device = dev;
@@ -229,7 +231,7 @@ struct RepPacker {
     int ls = RB.local_stream(stream, true);
     if (seg >= (1u << 30)) throw Fail{MAYA_ST_BAD_INPUT, "too many host syncs"};
     RB.sops[ls].push_back(Op{gpre, arg, tag | (seg << 2)});
-    RB.sseq[ls].push_back(seq);
+    if (keep_seq) RB.sseq[ls].push_back(seq);
     RB.sev[ls]++;
     n_devev++;
   }
@@ -483,7 +485,7 @@ struct RepPacker {
       P->streams.push_back(StreamRange{pos, (uint32_t)RB.sops[s].size(), RB.raw_of[s], folded});
       P->stream_events.push_back(RB.sev[s]);
       P->ops.insert(P->ops.end(), RB.sops[s].begin(), RB.sops[s].end());
-      P->op_seq.insert(P->op_seq.end(), RB.sseq[s].begin(), RB.sseq[s].end());
+      if (keep_seq) P->op_seq.insert(P->op_seq.end(), RB.sseq[s].begin(), RB.sseq[s].end());
       pos += (uint32_t)RB.sops[s].size();
     }
     h.n_ops = pos;
@@ -583,9 +585,14 @@ bool build_collapsed(const maya_raw_job &job, const std::vector<uint32_t> &rep_c
     }
     ncol = (int)m.size();
   }
+  // per iteration: communicator signatures (topology, sorted member colours),
+  // then each rank's signature (colour, comm signatures by local index) laid
+  // out flat; equal signatures (hash, then exact) get one new colour
+  std::vector<uint64_t> csig(G), sig, rh(R);
+  std::vector<int64_t> soff(R + 1);
+  std::vector<int32_t> buf, ncolor(R), first_of, next_of(R);
+  std::unordered_map<uint64_t, int32_t> head;   // signature hash -> first rank
   for (int iter = 0; iter < 64; iter++) {
-    std::vector<uint64_t> csig(G);
-    std::vector<int32_t> buf;
     for (int g = 0; g < G; g++) {
       buf.clear();
       for (int32_t m : members[g]) buf.push_back(color[m]);
@@ -594,28 +601,35 @@ bool build_collapsed(const maya_raw_job &job, const std::vector<uint32_t> &rep_c
       for (int32_t x : buf) h = mix64(h, (uint64_t)x);
       csig[g] = h;
     }
-    // exact signature: (colour, [(comm signature) per local index]); hashed
-    // signatures are confirmed by full comparison
-    std::unordered_map<uint64_t, std::vector<int32_t>> buckets;
-    std::vector<int32_t> ncolor(R, -1);
-    int n2 = 0;
-    auto sig_of = [&](int r) {
-      std::vector<uint64_t> s;
-      s.push_back((uint64_t)color[r]);
-      for (int64_t q = job.rank_comm_off[r]; q < job.rank_comm_off[r + 1]; q++)
-        s.push_back(csig[job.rank_comm[q]]);
-      return s;
-    };
-    std::vector<std::vector<uint64_t>> sigs(R);
+    sig.clear();
     for (int r = 0; r < R; r++) {
-      sigs[r] = sig_of(r);
+      soff[r] = (int64_t)sig.size();
+      sig.push_back((uint64_t)color[r]);
+      for (int64_t q = job.rank_comm_off[r]; q < job.rank_comm_off[r + 1]; q++)
+        sig.push_back(csig[job.rank_comm[q]]);
       uint64_t h = 0x9e37;
-      for (uint64_t v : sigs[r]) h = mix64(h, v);
-      auto &bk = buckets[h];
+      for (int64_t q = soff[r]; q < (int64_t)sig.size(); q++) h = mix64(h, sig[q]);
+      rh[r] = h;
+    }
+    soff[R] = (int64_t)sig.size();
+    auto same_sig = [&](int a, int b2) {
+      const int64_t la = soff[a + 1] - soff[a], lb = soff[b2 + 1] - soff[b2];
+      return la == lb && std::equal(sig.begin() + soff[a], sig.begin() + soff[a + 1],
+                                    sig.begin() + soff[b2]);
+    };
+    head.clear();
+    int n2 = 0;
+    for (int r = 0; r < R; r++) {
+      next_of[r] = -1;
+      auto ins = head.emplace(rh[r], r);
       int found = -1;
-      for (int32_t o : bk)
-        if (sigs[o] == sigs[r]) { found = ncolor[o]; break; }
-      if (found < 0) { found = n2++; bk.push_back(r); }
+      if (!ins.second) {   // walk the ranks already seen with this hash
+        int o = ins.first->second, last = o;
+        for (; o >= 0; last = o, o = next_of[o])
+          if (same_sig(o, r)) { found = ncolor[o]; break; }
+        if (found < 0) next_of[last] = r;
+      }
+      if (found < 0) found = n2++;
       ncolor[r] = found;
     }
     bool stable = n2 == ncol;
@@ -940,6 +954,7 @@ struct PackSink final : EventSink {
   }
   void rep_begin(size_t est_events) override {
     RP->begin(*P, *F, device, true, est_events / 2 + 16);
+    RP->keep_seq = !blocks;   // block batches never record a timeline (engine.cu)
   }
   void ev(uint8_t k, int32_t s, int64_t a, int64_t b, int64_t c, int64_t d) override {
     const int64_t f[4] = {a, b, c, d};
