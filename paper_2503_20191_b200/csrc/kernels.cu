@@ -261,7 +261,7 @@ static constexpr unsigned FULL = 0xffffffffu;
 __device__ unsigned long long g_prof[8];
 // window sub-phases (lane 0): [0] segment advance + wide attempt, [1] load + classify
 // (to the blocker ballot), [2] scan, [3] blockers + commit
-__device__ unsigned long long g_prof_sub[4];
+__device__ unsigned long long g_prof_sub[8];   // [4] wide attempts, [5] failed wide cycles
 #define PROF_T(v) long long v = clock64()
 #define PROF_ADD(i, v) (prof_acc[i] += (unsigned long long)(v))
 #else
@@ -373,6 +373,8 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
   const uint32_t limit = hk < c.nsync ? c.cnt[hk * c.ns] : c.len;
   bool adv = false;
   bool streaming = false;   // the last window committed 32 ops: try 128-op windows
+  bool wide_ok = true;      // no 128-op window has failed in this walk (a failed one costs
+                            // a 2 KB load and its dependent gathers: ~2.5 k cycles)
   s.wk = WAKE_ROUND;   // until something else is known: wait for the next round
   while (s.i < limit) {
     PROF_T(t_win);
@@ -392,6 +394,10 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
     if (lane < 16 && s.i + 128u + lane * 8u < c.len)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(c.ops + s.i + 128u + lane * 8u));
     if (streaming && end - s.i >= 128u && s.x < LIM_T) {
+#ifdef MAYA_PROFILE
+      const long long t_wide = clock64();
+      if (lane == 0) atomicAdd(&g_prof_sub[4], 1ull);
+#endif
       int64_t A4[4], B4[4], rd4[4];
       uint32_t rec4 = 0;
       bool blk = false;
@@ -476,6 +482,10 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
         continue;
       }
       streaming = false;
+      wide_ok = false;
+#ifdef MAYA_PROFILE
+      if (lane == 0) atomicAdd(&g_prof_sub[5], (unsigned long long)(clock64() - t_wide));
+#endif
     }
 #ifdef MAYA_PROFILE
     long long t_a = clock64();
@@ -728,7 +738,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
       atomicAdd(&g_prof_sub[3], (unsigned long long)(t_d - t_c));
     }
 #endif
-    streaming = !blocked && commit == 32u;
+    streaming = wide_ok && !blocked && commit == 32u;
     if (commit > 0) {
       s.x = __shfl_sync(FULL, d, commit - 1);
       s.i += commit;
@@ -1468,9 +1478,9 @@ uint32_t sched_smem_cap() { return SCHED_SMEM_CAP; }
 extern "C" int maya_prof_read_sub(unsigned long long *out4, int reset) {
 #ifdef MAYA_PROFILE
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out4, g_prof_sub, sizeof(unsigned long long) * 4);
+  cudaMemcpyFromSymbol(out4, g_prof_sub, sizeof(unsigned long long) * 8);
   if (reset) {
-    unsigned long long z[4] = {0, 0, 0, 0};
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_prof_sub, z, sizeof z);
   }
   return 1;

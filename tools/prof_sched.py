@@ -21,13 +21,13 @@ for label in (sys.argv[1:] if len(sys.argv) > 1 else ([] if os.environ.get("C5")
     L.maya_prof_read(buf, 1)
     eng.run(); r = eng.results()
     L.maya_prof_read(buf, 1)
-    sub = (C.c_ulonglong * 4)()
+    sub = (C.c_ulonglong * 8)()
     if hasattr(L, "maya_prof_read_sub"):
         L.maya_prof_read_sub(sub, 1)
         eng.run(); eng.results()
         L.maya_prof_read_sub(sub, 1)
     print(label, "sched ms", round(eng.last_timings_ms()[2], 3), dict(zip(names, list(buf))),
-          "window sub-phases (seg/wide, load+classify, scan, blockers+commit):", list(sub))
+          "window sub-phases (seg/wide, load+classify, scan, blockers+commit, wide attempts, failed-wide cycles):", list(sub))
 
 if os.environ.get("C5"):
     from paper_2503_20191_b200.synth import c5_job
