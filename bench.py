@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 lattice sub-line")
     ap.add_argument("--c5", default="8x10000x4096",
                     help="C5 synthetic sweep point RANKSxOPSxCONFIGS for the HBM-roofline line "
                          "('' to skip)")
@@ -331,6 +332,57 @@ def c5_sweep(spec: str, steps: int, dev_index: int) -> dict:
                                  "estimators + fold + schedulers"}}
 
 
+def c3_lattice(dev_index: int, threads: int) -> dict:
+    """C3 (BASELINE configs[2]): GPT-3 18.4B, all 4,088 configs of the
+    64-1,024-rank lattices (act_recompute on, global batch 1,024 / 2,048), on one
+    GPU.  device: kernel time of each lattice batch with its trace resident (median
+    of 3 runs, summed); e2e: generation + packing + H2D + kernels + D2H + top-k per
+    batch on a warm engine (arenas already sized), summed."""
+    from paper_2503_20191_b200 import workload as W
+    from paper_2503_20191_b200.engine import Engine
+    model = W.ModelSpec("gpt3-18.4b", 40, 6144, 2048, 51200, "bf16")
+    fast = W.load_device_preset("fast")
+    batches = []
+    for n in (64, 128, 256, 512, 1024):
+        cl = W.ClusterSpec(n // 8, 8, 80 * 2 ** 30, fast)
+        for gb in (1024, 2048):
+            batches.append((cl, W.enumerate_space(
+                W.SearchSpace(act_recompute=(True,), global_batch=gb), model, cl)))
+    eng = Engine(dev_index)
+
+    def once(cl, cfgs):
+        eng.stage_generated(model, cfgs, cl, dispatch_overhead_ns=5000, threads=threads)
+        eng.upload()
+        eng.run()
+        r = eng.results()
+        eng.topk(TOPK)
+        return r
+    for cl, cfgs in batches:          # warm: size the arenas once
+        once(cl, cfgs)
+    e2e_s, dev_ms, n_cfg, n_ok, rank_ops = 0.0, 0.0, 0, 0, 0
+    for cl, cfgs in batches:
+        t0 = time.perf_counter()
+        r = once(cl, cfgs)
+        e2e_s += time.perf_counter() - t0
+        ks = []
+        for _ in range(3):
+            eng.run()
+            eng.results()
+            ks.append(sum(eng.last_timings_ms()))
+        dev_ms += statistics.median(ks)
+        n_cfg += len(cfgs)
+        n_ok += int((r["status"] == 0).sum())
+        rank_ops += eng.batch_stats()["rank_ops"]
+    eng.close()
+    return {"workload": "C3: GPT-3 18.4B (40 x 6144, seq 2048), 64-1,024 ranks (8 per host), "
+                        "SearchSpace(act_recompute=(True,), global_batch=1024|2048), 5 us gaps, "
+                        "RooflineEstimator; 10 lattice batches",
+            "configs": n_cfg, "ok": n_ok,
+            "device_configs_per_s": round(n_cfg / (dev_ms / 1000), 1),
+            "e2e_configs_per_s": round(n_cfg / e2e_s, 1),
+            "rank_ops_per_s_device": round(rank_ops / (dev_ms / 1000), 1)}
+
+
 def bench_ours(args):
     import numpy as np
     import torch
@@ -531,6 +583,8 @@ def bench_ours(args):
         }
         if world == 1 and args.c5:
             line["c5"] = c5_sweep(args.c5, args.steps, local)
+        if world == 1 and not args.no_c3:
+            line["c3"] = c3_lattice(local, threads)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(model, cluster, configs, args.cpu_seconds,
                                                 host_threads())
