@@ -257,7 +257,7 @@ class Engine:
         """Generate + pack configs natively into the batch (no RawJob round trip).
         Returns per-config generation status (0 ok, <0 invalid config)."""
         from .rawtrace import DeviceParams
-        from .workload import _gen_lib, cluster_c, config_c, model_c, schedule_code
+        from .workload import _gen_lib, cluster_c, configs_array, model_c, schedule_code
         L = _gen_lib()
         b = Batch([], efficiency, overhead_ns)
         b.devices.append(DeviceParams.from_reference(cluster.device))
@@ -268,7 +268,8 @@ class Engine:
         _check(L.maya_batch_reset(self._h))
         _check(L.maya_batch_set_devices(self._h, 1, b.c_devices))
         _check(L.maya_batch_set_roofline(self._h, C.byref(b.c_roof)))
-        cfgs = (ConfigC * max(n, 1))(*[config_c(c) for c in configs])
+        cfgs_np = configs_array(configs)
+        cfgs = cfgs_np.ctypes.data_as(C.POINTER(ConfigC))
         kr = (np.arange(n, dtype=np.int32) if key_ranks is None
               else np.ascontiguousarray(key_ranks, dtype=np.int32))
         st = np.zeros(max(n, 1), dtype=np.int32)

@@ -265,6 +265,23 @@ def config_c(cfg) -> ConfigC:
                    int(bool(cfg.dist_optimizer)), 0, int(cfg.global_batch))
 
 
+CONFIG_DTYPE = np.dtype([("tp", "<i4"), ("pp", "<i4"), ("micro_mult", "<i4"),
+                         ("virtual_stages", "<i4"), ("act_recompute", "<i4"),
+                         ("seq_parallel", "<i4"), ("dist_optimizer", "<i4"), ("pad", "<i4"),
+                         ("global_batch", "<i8")])
+
+
+def configs_array(configs) -> np.ndarray:
+    """maya_config[n] (ConfigC layout) for a config list, built in one pass
+    (ctypes structs one by one cost ~3 us per config)."""
+    a = np.zeros(max(len(configs), 1), dtype=CONFIG_DTYPE)
+    if configs:
+        a[:len(configs)] = [(c.tp, c.pp, c.micro_mult, c.virtual_stages, bool(c.act_recompute),
+                             bool(c.seq_parallel), bool(c.dist_optimizer), 0, c.global_batch)
+                            for c in configs]
+    return a
+
+
 def cluster_c(cluster) -> ClusterC:
     return ClusterC(int(cluster.num_hosts), int(cluster.devices_per_host),
                     int(cluster.device_memory_bytes))
