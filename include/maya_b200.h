@@ -160,6 +160,10 @@ int maya_results(maya_engine *eng, maya_job_result *out);
  * then time_ns == 0 jobs (their MFU is 0.0, search.py:784 / sim.py:493-494). */
 int maya_topk(maya_engine *eng, int32_t k, maya_topk_entry *out, int32_t *n_out);
 
+/* Enqueue the same reduction after the last maya_run without waiting; the
+ * next maya_topk with the same k returns its result (stream order keeps it
+ * behind the run, so a host can stage the next batch meanwhile). */
+int maya_topk_async(maya_engine *eng, int32_t k);
 /* Timeline of one job after maya_run(record_timeline=1): per timed op
  * (rank, stream, seq, start, end), ordered by rank then stream then FIFO. */
 int maya_timeline_size(maya_engine *eng, int32_t job, int64_t *n);

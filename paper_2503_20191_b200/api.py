@@ -478,6 +478,7 @@ class GenPipeline:
                                    key_ranks=kr, threads=threads)
             e.upload()
             e.run()
+            e.topk_async(k)                    # behind the run on its stream: no wait
             if pending is not None:
                 yield collect(pending)
             pending = (e, len(configs), st)

@@ -124,6 +124,8 @@ struct maya_engine {
   bool stats_ok = false;
   float last_ms[3] = {0, 0, 0};
   int64_t run_launches = 0, topk_launches = 0;
+  maya_topk_entry *h_topk = nullptr;   // pinned: 64 entries + count (maya_topk_async)
+  int32_t topk_pending = 0;            // k of an enqueued, not yet read top-k
   int32_t options = MAYA_OPT_COLLAPSE;
 };
 
@@ -432,6 +434,7 @@ int maya_close(maya_engine *e) {
   if (e->d_arena) cudaFree(e->d_arena);
   if (e->d_scratch) cudaFree(e->d_scratch);
   if (e->d_stats) cudaFree(e->d_stats);
+  if (e->h_topk) cudaFreeHost(e->h_topk);
   for (auto &ev : e->ev) if (ev) cudaEventDestroy(ev);
   for (auto &ev : e->vev) if (ev) cudaEventDestroy(ev);
   for (auto &s : e->vstream) if (s) cudaStreamDestroy(s);
@@ -1028,6 +1031,7 @@ int maya_upload(maya_engine *e) {
 }
 
 int maya_run(maya_engine *e, int32_t record_timeline) {
+  e->topk_pending = 0;
   if (!e->uploaded) return fail(MAYA_ESTATE, "maya_run before maya_upload");
   if (e->has_blocks && (record_timeline || (e->options & MAYA_OPT_NO_FOLD)))
     return fail(MAYA_ESTATE, "batch staged with kernel blocks runs folded only: set "
@@ -1245,10 +1249,35 @@ int maya_last_timings(maya_engine *e, float *ms3) {
   return MAYA_OK;
 }
 
+int maya_topk_async(maya_engine *e, int32_t k) {
+  if (!e->ran) return fail(MAYA_ESTATE, "maya_topk_async before maya_run");
+  if (k < 1 || k > 64) return fail(MAYA_EINVAL, "k must be in [1, 64]");
+  CU(cudaSetDevice(e->device));
+  if (!e->h_topk) CU(cudaMallocHost(&e->h_topk, 65 * sizeof(maya_topk_entry)));
+  char *X = (char *)e->d_scratch;
+  maya_topk_entry *d_out = (maya_topk_entry *)(X + e->x_topk_out.off);
+  int32_t *d_n = (int32_t *)(X + e->x_topk_n.off);
+  launch_topk(e->db, k, d_out, d_n, X + e->x_topk.off, e->stream);
+  e->topk_launches = e->db.n_jobs ? 2 : 0;
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(e->h_topk + 64, d_n, sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
+  CU(cudaMemcpyAsync(e->h_topk, d_out, k * sizeof(maya_topk_entry), cudaMemcpyDeviceToHost,
+                     e->stream));
+  e->topk_pending = k;
+  return MAYA_OK;
+}
+
 int maya_topk(maya_engine *e, int32_t k, maya_topk_entry *out, int32_t *n_out) {
   if (!e->ran) return fail(MAYA_ESTATE, "maya_topk before maya_run");
   if (k < 1 || k > 64) return fail(MAYA_EINVAL, "k must be in [1, 64]");
   CU(cudaSetDevice(e->device));
+  if (e->topk_pending == k) {   // enqueued by maya_topk_async after this run
+    CU(cudaStreamSynchronize(e->stream));
+    e->topk_pending = 0;
+    *n_out = *(const int32_t *)(e->h_topk + 64);
+    memcpy(out, e->h_topk, k * sizeof(maya_topk_entry));
+    return MAYA_OK;
+  }
   char *X = (char *)e->d_scratch;
   maya_topk_entry *d_out = (maya_topk_entry *)(X + e->x_topk_out.off);
   int32_t *d_n = (int32_t *)(X + e->x_topk_n.off);

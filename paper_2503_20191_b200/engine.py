@@ -32,7 +32,7 @@ EXPORTED = (
     "maya_batch_stats", "maya_set_options", "maya_batch_collapsed", "maya_prof_read",
     "maya_debug_pack_compare", "maya_rank_stats", "maya_last_error_kind", "maya_trace_parse",
     "maya_trace_info", "maya_trace_serialize", "maya_trace_free", "maya_job_load",
-    "maya_job_save", "maya_gen_names",
+    "maya_job_save", "maya_gen_names", "maya_topk_async",
 )
 
 
@@ -75,6 +75,7 @@ def lib():
     L.maya_set_options.argtypes = [vp, C.c_int32]
     L.maya_batch_collapsed.argtypes = [vp, P(C.c_uint8)]
     L.maya_rank_stats.argtypes = [vp, C.c_int32, C.c_int32, P(C.c_int64)]
+    L.maya_topk_async.argtypes = [vp, C.c_int32]
     _lib = L
     return L
 
@@ -225,6 +226,10 @@ class Engine:
                                start.ctypes.data_as(P(C.c_int64)),
                                end.ctypes.data_as(P(C.c_int64))))
         return Timeline(rank[:n], stream[:n], seq[:n] >> 2, seq[:n] & 3, start[:n], end[:n])
+
+    def topk_async(self, k: int) -> None:
+        """Enqueue the top-k after the last run; the next topk(k) returns it."""
+        _check(lib().maya_topk_async(self._h, int(k)))
 
     def rank_stats(self, job: int, num_ranks: int) -> np.ndarray:
         """Per-rank (compute_busy, comm_busy, exposed_comm, idle, peak_mem) of one
