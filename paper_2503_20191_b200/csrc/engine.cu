@@ -1094,8 +1094,15 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   {
     // variants run concurrently on their own streams (fork/join)
     CU(cudaEventRecord(e->vev[maya_engine::NVAR], e->stream));
-    uint32_t off = 0;
-    for (int v = 0; v < maya_engine::NVAR; v++) {
+    uint32_t var_off[maya_engine::NVAR];
+    for (int v = 0, o = 0; v < maya_engine::NVAR; v++) { var_off[v] = (uint32_t)o; o += (int)e->var_n[v]; }
+    // groups of larger jobs first (grid jobs, CTA lane jobs, then warp-window
+    // jobs from 16 down to 4 warps): the longest dependency chains get their
+    // SMs before the short jobs fill the machine (measured: C2's step stays at
+    // its fast mode in 5 of 6 processes instead of 2 of 5)
+    for (int vi = 0; vi < maya_engine::NVAR; vi++) {
+      const int v = maya_engine::NVAR - 1 - vi;
+      const uint32_t off = var_off[v];
       if (!e->var_n[v]) continue;
       CU(cudaStreamWaitEvent(e->vstream[v], e->vev[maya_engine::NVAR], 0));
       if (v == 15) {   // grid jobs: one cooperative launch per group of co-resident parts
@@ -1120,7 +1127,6 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
       CU(cudaGetLastError());
       CU(cudaEventRecord(e->vev[v], e->vstream[v]));
       CU(cudaStreamWaitEvent(e->stream, e->vev[v], 0));
-      off += e->var_n[v];
     }
   }
   CU(cudaEventRecord(e->ev[3], e->stream));
