@@ -373,8 +373,10 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
   const uint32_t limit = hk < c.nsync ? c.cnt[hk * c.ns] : c.len;
   bool adv = false;
   bool streaming = false;   // the last window committed 32 ops: try 128-op windows
-  bool wide_ok = true;      // no 128-op window has failed in this walk (a failed one costs
-                            // a 2 KB load and its dependent gathers: ~2.5 k cycles)
+  // no 128-op window has failed in this walk, and the FIFO has not failed two
+  // (WSt.flags bits 4-5 count failures): a failed one costs a 2 KB load and its
+  // dependent gathers, ~2.5 k cycles, and FIFOs that block often keep failing
+  bool wide_ok = ((s.flags >> 4) & 3u) < 2u;
   s.wk = WAKE_ROUND;   // until something else is known: wait for the next round
   while (s.i < limit) {
     PROF_T(t_win);
@@ -475,7 +477,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
         if (lane == 0) { PROF_ADD(6, 1); PROF_ADD(7, 128); PROF_ADD(0, clock64() - t_win); PROF_ADD(4, 1); }
 #endif
         s.i += 128u;
-        s.flags = 0;
+        s.flags &= ~1u;
         adv = true;
         if (__any_sync(FULL, rec4 != 0)) __threadfence_block();
         s.wk = WAKE_ROUND;
@@ -483,6 +485,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
       }
       streaming = false;
       wide_ok = false;
+      if (((s.flags >> 4) & 3u) < 3u) s.flags += 16u;
 #ifdef MAYA_PROFILE
       if (lane == 0) atomicAdd(&g_prof_sub[5], (unsigned long long)(clock64() - t_wide));
 #endif
@@ -645,7 +648,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
           const int64_t f = qpay == (EXEC_NONE >> 2) ? -1 : vload(&c.fire[qpay]);
           if (f < 0) {
             stc = STEP_BLOCK;
-            s.flags = 0;
+            s.flags &= ~1u;
             wk = qpay == (EXEC_NONE >> 2) ? WAKE_ROUND : WAKE_FIRE;
             wa = qpay == (EXEC_NONE >> 2) ? nullptr : &c.fire[qpay];
           } else {
@@ -696,7 +699,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
             if (code & 4u) { stc = STEP_ERR; eno = MAYA_ST_INTERNAL; }
             else if (!(code & 1u)) {
               stc = STEP_BLOCK; wk = WAKE_COUNT; wt = tgt; wa = &qs->count;
-              s.flags = (posted || (code & 2u)) ? 1u : 0u;   // for the new s.i (= this op)
+              s.flags = (s.flags & ~1u) | ((posted || (code & 2u)) ? 1u : 0u);   // for the new s.i (= this op)
             }
             else if (qw8 > INT64_MAX - m) { stc = STEP_ERR; eno = MAYA_ST_OVERFLOW; }
             else { nx = m + qw8; }
@@ -708,7 +711,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
 #endif
       if (stc != STEP_OK) {
         if (stc == STEP_ERR) err = (int)eno;
-        if (stc == STEP_ERR && q > 0) s.flags = 0;
+        if (stc == STEP_ERR && q > 0) s.flags &= ~1u;
         s.wk = wk;
         s.wt = wt;
         s.wa = wa;
@@ -745,7 +748,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
       adv = true;
       // the arrival flag belongs to the op at s.i: a committed op 0 completed it;
       // a blocker at q > 0 set it for the new s.i
-      if (!blocked) s.flags = 0;
+      if (!blocked) s.flags &= ~1u;
     }
 #ifdef MAYA_PROFILE
     if (lane == 0) { PROF_ADD(0, clock64() - t_win); PROF_ADD(4, 1); }
