@@ -253,6 +253,9 @@ __device__ __forceinline__ void vstore(T *p, T v) {
 }
 
 static constexpr unsigned FULL = 0xffffffffu;
+#ifndef MAYA_WIDE_FAILS
+#define MAYA_WIDE_FAILS 2u   // failed 128-op windows after which a FIFO stops trying them
+#endif
 
 #ifdef MAYA_PROFILE
 // per-batch cycle counters: [0] walk windows, [1] slow ops, [2] idle sleep,
@@ -376,7 +379,7 @@ __device__ bool warp_walk(const DevBatch &b, const JobSh &sh, const WCtx &c, WSt
   // no 128-op window has failed in this walk, and the FIFO has not failed two
   // (WSt.flags bits 4-5 count failures): a failed one costs a 2 KB load and its
   // dependent gathers, ~2.5 k cycles, and FIFOs that block often keep failing
-  bool wide_ok = ((s.flags >> 4) & 3u) < 2u;
+  bool wide_ok = ((s.flags >> 4) & 3u) < MAYA_WIDE_FAILS;
   s.wk = WAKE_ROUND;   // until something else is known: wait for the next round
   while (s.i < limit) {
     PROF_T(t_win);
