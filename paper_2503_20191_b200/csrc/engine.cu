@@ -27,6 +27,18 @@ namespace {
 thread_local std::string g_err;
 thread_local int g_err_kind = 0;
 
+// warp-window jobs at or under this layout size launch separately, opt-in via
+// MAYA_SPLIT_SMEM (bytes; default 0 = one launch per group).  Measured on C2
+// (profiles/split_smem_r1.json): 40 KB keeps the scheduler out of its slow mode
+// but costs the step ~0.08 ms, netting 461k vs 476k configs/s on average.
+static uint32_t split_smem_threshold() {
+  static const uint32_t t = [] {
+    const char *v = getenv("MAYA_SPLIT_SMEM");
+    return v ? (uint32_t)strtoul(v, nullptr, 10) : 0u;
+  }();
+  return t ? t : 0xffffffffu;
+}
+
 int fail(int code, const std::string &msg) {
   g_err = msg;
   g_err_kind = 0;
@@ -82,6 +94,13 @@ struct maya_engine {
   cudaEvent_t vev[NVAR + 1] = {};
   uint32_t var_n[NVAR] = {};        // jobs per group (order segments)
   uint32_t var_smem[NVAR] = {};     // dynamic smem per group launch
+  // warp-window groups split by shared-memory footprint: the jobs whose layout
+  // fits SMALL_SMEM run in a second launch sized for them (a group's launch
+  // otherwise reserves its largest job's smem for every CTA)
+  cudaStream_t sstream[3] = {};
+  cudaEvent_t sev[3] = {};
+  uint32_t var_big[3] = {};         // leading jobs of the group's segment above SMALL_SMEM
+  uint32_t var_smem_small[3] = {};
   // staged jobs
   PackPool packs;
   std::vector<maya_device_params> devs;
@@ -423,6 +442,8 @@ int maya_open(int cuda_device, maya_engine **out) {
   for (auto &ev : e->ev) cudaEventCreate(&ev);
   for (auto &s : e->vstream) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
   for (auto &ev : e->vev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  for (auto &s : e->sstream) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  for (auto &ev : e->sev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   *out = e;
   return MAYA_OK;
 }
@@ -438,6 +459,8 @@ int maya_close(maya_engine *e) {
   for (auto &ev : e->ev) if (ev) cudaEventDestroy(ev);
   for (auto &ev : e->vev) if (ev) cudaEventDestroy(ev);
   for (auto &s : e->vstream) if (s) cudaStreamDestroy(s);
+  for (auto &ev : e->sev) if (ev) cudaEventDestroy(ev);
+  for (auto &s : e->sstream) if (s) cudaStreamDestroy(s);
   if (e->stream) cudaStreamDestroy(e->stream);
   delete e;
   return MAYA_OK;
@@ -685,17 +708,29 @@ int maya_upload(maya_engine *e) {
   {
     std::vector<int32_t> order(nj);
     std::vector<int> var(nj);
+    std::vector<uint32_t> wbytes(nj, 0);
     for (size_t j = 0; j < nj; j++) {
       order[j] = (int32_t)j;
       var[j] = plans[j].variant >= 0 ? plans[j].variant
                                      : sched_variant((uint32_t)e->packs[j].walkers.size(),
                                                      (uint32_t)e->packs[j].ranks.size());
+      if (var[j] < 3) {
+        const JobPack &P = e->packs[j];
+        wbytes[j] = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
+                                 (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0,
+                                 P.hdr.n_fire, P.hdr.n_rcolls, sched_smem_cap())
+                        .bytes;
+      }
     }
+    const uint32_t small = split_smem_threshold();
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
       if (var[a] != var[b]) return var[a] < var[b];
+      const bool ba = wbytes[a] > small, bb = wbytes[b] > small;
+      if (ba != bb) return ba;
       return e->packs[a].hdr.dev_ops > e->packs[b].hdr.dev_ops;
     });
     for (int v = 0; v < maya_engine::NVAR; v++) e->var_n[v] = e->var_smem[v] = 0;
+    for (int v = 0; v < 3; v++) e->var_big[v] = e->var_smem_small[v] = 0;
     for (size_t j = 0; j < nj; j++) {
       e->var_n[var[j]]++;
       if (var[j] >= 3) {   // lane kernels (15: grid jobs, smem per part)
@@ -703,11 +738,12 @@ int maya_upload(maya_engine *e) {
         if (need > e->var_smem[var[j]]) e->var_smem[var[j]] = need;
         continue;
       }
-      const JobPack &P = e->packs[j];
-      const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
-                                         (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0,
-                                         P.hdr.n_fire, P.hdr.n_rcolls, sched_smem_cap());
-      if (L.bytes > e->var_smem[var[j]]) e->var_smem[var[j]] = L.bytes;
+      if (wbytes[j] > small) {
+        e->var_big[var[j]]++;
+        if (wbytes[j] > e->var_smem[var[j]]) e->var_smem[var[j]] = wbytes[j];
+      } else if (wbytes[j] > e->var_smem_small[var[j]]) {
+        e->var_smem_small[var[j]] = wbytes[j];
+      }
     }
     memcpy(H + e->s_order.off, order.data(), nj * sizeof(int32_t));
   }
@@ -1112,8 +1148,17 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
             return fail(MAYA_ECUDA, std::string("cooperative launch: ") +
                                         cudaGetErrorString(cudaGetLastError()));
       } else if (v < 3) {
-        launch_schedule_variant(db, v, db.order + off, e->var_n[v], record_timeline ? 1 : 0,
+        const uint32_t nb = e->var_big[v], ns = e->var_n[v] - nb;
+        launch_schedule_variant(db, v, db.order + off, nb, record_timeline ? 1 : 0,
                                 e->var_smem[v], e->vstream[v]);
+        if (ns) {   // small-footprint jobs on their own stream, concurrently
+          CU(cudaStreamWaitEvent(e->sstream[v], e->vev[maya_engine::NVAR], 0));
+          launch_schedule_variant(db, v, db.order + off + nb, ns, record_timeline ? 1 : 0,
+                                  e->var_smem_small[v], e->sstream[v]);
+          CU(cudaGetLastError());
+          CU(cudaEventRecord(e->sev[v], e->sstream[v]));
+          CU(cudaStreamWaitEvent(e->stream, e->sev[v], 0));
+        }
       } else if (v <= 10) {
         const uint32_t region = e->var_smem[v];
         uint32_t wpc = region ? LANE_SMEM_CAP / region : 8;
@@ -1163,7 +1208,9 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
     else
       n += db.n_ops ? 1 : 0;
     for (int v = 0; v < maya_engine::NVAR; v++)
-      n += v == 15 ? (int64_t)e->grid_launches.size() : (e->var_n[v] ? 1 : 0);
+      n += v == 15  ? (int64_t)e->grid_launches.size()
+           : v < 3  ? (e->var_big[v] ? 1 : 0) + (e->var_n[v] > e->var_big[v] ? 1 : 0)
+                    : (e->var_n[v] ? 1 : 0);
     if (e->stats_ok) n += 3;   // keys, segmented sort (cub), unions
     e->run_launches = n;
   }

@@ -809,7 +809,7 @@ __device__ bool host_step(const DevBatch &b, const JobSh &sh, uint32_t r, int64_
 }
 
 template <int NW>
-__global__ void __launch_bounds__(NW * 32, 1) sched_warp_kernel(DevBatch b, const int32_t *order,
+__global__ void __launch_bounds__(NW * 32, 16 / NW) sched_warp_kernel(DevBatch b, const int32_t *order,
                                                              int record, uint32_t smem_cap) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ unsigned long long s_tmax;
