@@ -1578,12 +1578,21 @@ int maya_batch_add_generated(maya_engine *e, const maya_model *model, int32_t n,
   if (device < 0 || device >= 8) return fail(MAYA_EINVAL, "device index out of range");
   size_t base = e->packs.size();
   e->packs.resize(base + n);
+  // longest first (generation cost grows with stages x micro-batches x virtual
+  // stages, r = 0.8 over C2), so the workers' tail is short jobs
+  std::vector<int32_t> lpt(n);
+  for (int32_t i = 0; i < n; i++) lpt[i] = i;
+  auto cost = [&](int32_t i) {
+    return (int64_t)cfgs[i].pp * cfgs[i].micro_mult * std::max(1, cfgs[i].virtual_stages);
+  };
+  std::stable_sort(lpt.begin(), lpt.end(), [&](int32_t a, int32_t b) { return cost(a) > cost(b); });
   std::atomic<int> next(0);
   auto work = [&]() {
     thread_local GenJob g;
     for (;;) {
-      int i = next.fetch_add(1);
-      if (i >= n) break;
+      int q = next.fetch_add(1);
+      if (q >= n) break;
+      const int i = lpt[q];
       std::string err;
       JobPack &P = e->packs[base + i];
       const int32_t kr = key_ranks ? key_ranks[i] : i;
