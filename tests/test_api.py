@@ -182,3 +182,32 @@ def test_gen_pipeline_stream_matches_single_batches():
             assert np.array_equal(r1[f], r2[f]), f
         assert np.array_equal(np.asarray(t1), np.asarray(t2))
         assert np.array_equal(s1, s2)
+
+
+_SPLIT_SCRIPT = r"""
+import json, os, sys
+sys.path.insert(0, os.getcwd())
+from paper_2503_20191_b200 import workload as W
+from paper_2503_20191_b200.api import GpuPipelineEvaluator
+model = W.ModelSpec("gpt3-1.3b", 24, 2048, 2048, 51200)
+cluster = W.ClusterSpec(1, 8, 80 * 2 ** 30, W.load_device_preset("fast"))
+cfgs = W.enumerate_space(W.SearchSpace(global_batch=512), model, cluster)[:512]
+res = GpuPipelineEvaluator(model, cluster, dispatch_overhead_ns=5000).evaluate_many(cfgs)
+print(json.dumps([[r.time_ns, r.peak_mem_bytes, r.oom] for r in res]))
+"""
+
+
+@gpu
+@pytest.mark.parametrize("split", ["40960", "1"])
+def test_c2_with_split_warp_window_launches(split):
+    """The opt-in split of warp-window groups by shared-memory footprint
+    (MAYA_SPLIT_SMEM, read once per process) gives the golden C2 results."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _SPLIT_SCRIPT], cwd=root, check=True,
+                         capture_output=True, text=True,
+                         env=dict(os.environ, MAYA_SPLIT_SMEM=split)).stdout
+    got = json.loads(out.strip().splitlines()[-1])
+    gold = json.load(open(os.path.join(GOLDEN, "c2_results.json")))
+    assert got == [[g["total_ns"], g["peak_mem_bytes"], g["oom"]] for g in gold]
