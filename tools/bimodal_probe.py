@@ -12,7 +12,13 @@ for inst in range(2):
     eng.stage_generated(model, cfgs, cluster, dispatch_overhead_ns=5000, threads=16)
     eng.upload()
     ts = []
-    for _ in range(6):
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if os.environ.get("FLUSH") else None
+    for i in range(6):
+        if flush is not None:      # L2 flush on the engine stream, as bench.py does
+            with torch.cuda.stream(torch.cuda.ExternalStream(eng.stream_handle())):
+                flush.fill_(i & 0xff)
+                if os.environ.get("FLUSH") == "2":
+                    flush.max()        # then read it back: L2 left holding clean lines
         eng.run(); eng.results(); ts.append(eng.last_timings_ms()[2])
     print(inst, "sched ms", [round(t, 3) for t in ts[1:]], flush=True)
     keep.append(eng)   # keep alive so the next engine gets new addresses
