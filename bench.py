@@ -18,8 +18,10 @@ value  = configs/s with traces resident in HBM (CUDA events, L2 flushed
 e2e    = configs/s through the C ABI from the config list: native trace
          generation + SoA packing (host, C++ threads), H2D of the arena,
          kernels, D2H of results and the top-k.
-Reference arm: the CPU oracle port (oracle/: native generator + C++
-restatement of the reference's event-driven simulator) on all host threads.
+Reference arm: the UNMODIFIED reference (dltsim, copied to oracle/_ref by
+oracle/Makefile) on all host cores, one forked worker process per core:
+PipelineEvaluator.__call__ over a bounded, evenly spaced sample of the 512 C2
+configs per step (oracle/refbench.py); no module of the product is loaded.
 """
 
 from __future__ import annotations
@@ -50,13 +52,22 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--threads", type=int, default=0, help="host threads (0 = all)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=5.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 lattice sub-line")
     ap.add_argument("--c5", default="8x10000x4096",
                     help="C5 synthetic sweep point RANKSxOPSxCONFIGS for the HBM-roofline line "
                          "('' to skip)")
     return ap.parse_args()
+
+
+def bench_config(world: int) -> dict:
+    return {"workload": "C2: GPT-3 1.3B (24x2048, seq 2048, vocab 51200) on 1x8 'fast' 80 GiB; "
+                        "enumerate_space(SearchSpace(global_batch=512*2**rank))[:512]; 5 us gaps; "
+                        "RooflineEstimator",
+            "configs_per_gpu": N_CONFIGS, "ranks_per_config": 8, "topk": TOPK,
+            "l2": "flushed between timed steps (256 MiB write on the engine stream)",
+            "parallelism": f"config-sharded x{world}"}
 
 
 def host_threads() -> int:
@@ -177,9 +188,10 @@ def _gen_jobs(model, cluster, configs, threads):
                            configs))
 
 
-def cpu_baseline(model, cluster, configs, seconds: float, threads: int) -> dict:
-    """Oracle port (oracle/sim_oracle.cpp: C++ restatement of the reference's
-    event-driven simulate + annotate) on the host cores; pre-built jobs."""
+def port_baseline(model, cluster, configs, seconds: float, threads: int) -> dict:
+    """Secondary CPU figure: the oracle port (oracle/sim_oracle.cpp, a C++
+    restatement of the reference's event-driven simulate + annotate) on the
+    host cores, on jobs pre-built by the native generator."""
     from oracle import oracle
     from paper_2503_20191_b200._abi import Batch
     t0 = time.perf_counter()
@@ -197,58 +209,84 @@ def cpu_baseline(model, cluster, configs, seconds: float, threads: int) -> dict:
     n = len(jobs)
     rank_ops = sum(j.rank_ops() for j in jobs)
     return {"value": round(n / t_sim, 2), "unit": "configs/s", "cores": threads, "kind": "port",
-            "sample": f"all {n} C2 configs per pass, {reps} passes: oracle annotate+simulate "
-                      f"(C++ restatement of pkg/src/dltsim/sim.py + estimate.py) on pre-built "
-                      f"jobs, {threads} threads",
+            "sample": f"all {n} C2 configs per pass, {reps} passes, pre-built jobs",
             "trace_ops_per_s": round(rank_ops / t_sim, 1),
-            "e2e_equiv_configs_per_s": round(n / (t_sim + t_gen), 2),
-            "reference_python_survey": "2.8 configs/s e2e, 5.5 configs/s sim-only, 1 core "
-                                       "(BASELINE.md; the Python reference is not on the box)"}
+            "gen_plus_sim_configs_per_s": round(n / (t_sim + t_gen), 2)}
+
+
+REF_PER_WORKER = 4      # C2 configs per worker process per reference pass (~1-2 s)
+
+
+def reference_legs(cores: int, e2e_passes: int, warmup: int, extra: bool) -> dict:
+    """The unmodified reference (oracle/_ref/dltsim) on the host cores: e2e
+    PipelineEvaluator.__call__ with `cores` worker processes (the headline
+    leg), and, with `extra`, 1-core e2e and sim-only legs (oracle/refbench.py)."""
+    from oracle import refbench
+    out = {"e2e": refbench.measure("e2e", cores, REF_PER_WORKER, e2e_passes, warmup)}
+    if extra:
+        out["e2e_1core"] = refbench.measure("e2e", 1, 6, 1, 0)
+        out["sim_only"] = refbench.measure("sim", cores, REF_PER_WORKER, 2, 1)
+        out["sim_only_1core"] = refbench.measure("sim", 1, 6, 1, 0)
+    return out
+
+
+def _ref_sample_text(legs: dict, cores: int) -> str:
+    e = legs["e2e"]
+    return (f"{e['configs_per_pass']} of the 512 C2 configs (evenly spaced in enumeration "
+            f"order) per pass, {e['workers']} forked worker processes x {REF_PER_WORKER} "
+            f"configs, {e['passes']} timed passes: dltsim PipelineEvaluator.__call__ "
+            f"(generate -> collate -> annotate(RooflineEstimator) -> simulate -> compute_mfu, "
+            f"search.py:200-209), unmodified reference copied to oracle/_ref")
+
+
+def cpu_baseline(cores: int) -> dict:
+    """Our arm's cpu_baseline: the reference itself on the box's cores (bounded sample)."""
+    from oracle import refbench
+    why = refbench.available()
+    if why:
+        return {"value": None, "unit": "configs/s", "cores": cores, "kind": "reference",
+                "sample": why}
+    legs = reference_legs(cores, 2, 1, extra=True)
+    return {"value": legs["e2e"]["configs_per_s"], "unit": "configs/s", "cores": cores,
+            "kind": "reference", "sample": _ref_sample_text(legs, cores),
+            "e2e_1core_configs_per_s": legs["e2e_1core"]["configs_per_s"],
+            "sim_only_configs_per_s": legs["sim_only"]["configs_per_s"],
+            "sim_only_1core_configs_per_s": legs["sim_only_1core"]["configs_per_s"],
+            "parity_vs_golden": legs["e2e"]["parity"]}
 
 
 def bench_reference(args):
-    """--impl reference: the CPU port of the reference path, rank 0 only."""
-    import torch  # noqa: F401  (torchrun parity with our arm)
+    """--impl reference: the unmodified reference (dltsim, oracle/_ref) on the
+    host cores, rank 0 only.  No module of the product is imported here, so
+    libmaya_b200.so is never loaded in this process or its workers."""
     rank = int(os.environ.get("RANK", "0"))
-    n = args.gpus
     if rank != 0:
         return
-    from oracle import oracle
-    from paper_2503_20191_b200 import workload as W
-    from paper_2503_20191_b200._abi import Batch
-    threads = args.threads or host_threads()
-    model, cluster, configs = workload(0)
-
-    def step():
-        t0 = time.perf_counter()
-        jobs = _gen_jobs(model, cluster, configs, threads)
-        res = oracle.simulate_many(jobs, threads=threads, batch=Batch(jobs))
-        return time.perf_counter() - t0, res, jobs
-
-    for _ in range(max(0, args.warmup)):
-        step()
-    times = []
-    rank_ops = 0
-    for _ in range(args.steps):
-        dt, res, jobs = step()
-        times.append(dt)
-        rank_ops = int(res["rank_ops"].sum())
-    ms = 1000 * sum(times) / len(times)
-    val = N_CONFIGS / (ms / 1000)
+    from oracle import refbench
+    n = args.gpus
+    cores = args.threads or host_threads()
+    why = refbench.available()
+    if why:
+        print(json.dumps({"impl": "reference", "unavailable": why}), flush=True)
+        return
+    legs = reference_legs(cores, max(1, args.steps), max(0, args.warmup), extra=True)
+    e = legs["e2e"]
+    val = e["configs_per_s"]
     line = {
-        "impl": "reference", "metric": "simulated configs/sec", "value": round(val, 3),
+        "impl": "reference", "metric": "simulated configs/sec", "value": val,
         "unit": "configs/s", "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": "C2: GPT-3 1.3B, 512 configs x 8 ranks (rank 0's batch)"},
-        "trace_ops_per_s": round(rank_ops / (ms / 1000), 1),
-        "cpu_baseline": {"value": round(val, 3), "unit": "configs/s", "cores": threads,
-                         "kind": "port",
-                         "sample": "full 512-config C2 batch per step: native generator "
-                                   "+ oracle/sim_oracle.cpp annotate+simulate (C++ port of the "
-                                   f"reference's event-driven simulator), {threads} threads"},
-        "e2e": {"value": round(val, 3), "unit": "configs/s", "h2d_bytes_per_step": 0,
+        "ms_per_step": round(1000 * e["seconds_per_pass"], 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic: the reference's own trace generator (dltsim.workload)",
+        "config": bench_config(1),
+        "step": f"one pass over a bounded sample of the workload ({e['configs_per_pass']} "
+                f"configs); value = configs per second over the timed passes",
+        "cpu_baseline": {"value": val, "unit": "configs/s", "cores": cores, "kind": "reference",
+                         "sample": _ref_sample_text(legs, cores)},
+        "e2e": {"value": val, "unit": "configs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "legs": legs,
+        "full_batch_seconds_extrapolated": round(512 / val, 2),
     }
     print(json.dumps(line), flush=True)
 
@@ -547,13 +585,7 @@ def bench_ours(args):
             "vs_baseline": None, "dtype": "int64",
             "data": "synthetic: native restatement of the reference trace generator "
                     "(event-for-event identical, tests/test_gen.py)",
-            "config": {"workload": "C2: GPT-3 1.3B (24x2048, seq 2048, vocab 51200) on 1x8 "
-                                   "'fast' 80 GiB; enumerate_space(SearchSpace(global_batch="
-                                   "512*2**rank))[:512]; 5 us gaps; RooflineEstimator",
-                       "configs_per_gpu": N_CONFIGS, "ranks_per_config": 8,
-                       "rank_ops_per_gpu": rank_ops, "topk": TOPK,
-                       "l2": "flushed between timed steps (256 MiB write on the engine stream)",
-                       "parallelism": f"config-sharded x{world}"},
+            "config": dict(bench_config(world), rank_ops_per_gpu=rank_ops),
             "trace_ops_per_s": round(rank_ops * world / (ms_max / 1000), 1),
             "e2e": {"value": round(n_total / (e2e_ms_max / 1000), 2), "unit": "configs/s",
                     "ms_per_step": round(e2e_ms_max, 3),
@@ -586,8 +618,9 @@ def bench_ours(args):
         if world == 1 and not args.no_c3:
             line["c3"] = c3_lattice(local, threads)
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(model, cluster, configs, args.cpu_seconds,
-                                                host_threads())
+            line["cpu_baseline"] = cpu_baseline(host_threads())
+            line["cpu_baseline"]["port"] = port_baseline(model, cluster, configs,
+                                                         args.cpu_seconds, host_threads())
         print(json.dumps(line), flush=True)
     eng.close()
     if world > 1:
