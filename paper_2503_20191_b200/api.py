@@ -83,13 +83,14 @@ def _ref_types():
         from dltsim import sim as rs
         from dltsim import search as rsearch
         from dltsim import estimate as rest
+        from dltsim import workload as rwork
         return dict(SimReport=rs.SimReport, RankStats=rs.RankStats,
                     SimDeadlockError=rs.SimDeadlockError, EvalResult=rsearch.EvalResult,
-                    EstimationError=rest.EstimationError)
+                    EstimationError=rest.EstimationError, ConfigError=rwork.ConfigError)
     except Exception:
         return dict(SimReport=SimReport, RankStats=RankStats,
                     SimDeadlockError=SimDeadlockError, EvalResult=EvalResult,
-                    EstimationError=EstimationError)
+                    EstimationError=EstimationError, ConfigError=W.ConfigError)
 
 
 # --- engine singletons (one per CUDA device per process) -------------------------
@@ -100,17 +101,39 @@ def _engine(device: int = 0):
     return Engine(device)
 
 
-def _raise_for(status: int, what: str = "") -> None:
+def _raise_for(status: int, what: str = "", raw: RawJob | None = None, timeline=None) -> None:
+    """Raise the reference's exception for a failed job.  With the job (and,
+    for deadlocks, its timeline run) the text is the reference's own
+    (residue.py: sim.py:382-402, estimate.py:124-127 + 339-346)."""
+    from .residue import deadlock_message, estimation_message
     T = _ref_types()
     if status == ST_OK:
         return
     if status == ST_DEADLOCK:
+        if raw is not None and timeline is not None:
+            raise T["SimDeadlockError"](deadlock_message(raw, timeline))
         raise T["SimDeadlockError"](f"simulation deadlocked with blocked work{what}")
     if status == ST_ESTIMATION:
-        raise T["EstimationError"](f"estimator failed{what}")
+        msg = estimation_message(raw) if raw is not None else None
+        raise T["EstimationError"](msg or f"estimator failed{what}")
     if status == ST_INTERNAL:
         raise RuntimeError(f"internal error{what}")
     raise ValueError(f"engine status {STATUS_NAMES[status]}{what}")
+
+
+def _failure(status: int, raw: RawJob, device: int) -> Exception:
+    """The exception of a failed generated job: deadlocks are re-run alone with
+    a timeline (error path only) so the residue names the blocked objects."""
+    timeline = None
+    if status == ST_DEADLOCK:
+        res, eng = simulate_raw([raw], device, record_timeline=True)
+        if int(res[0]["status"]) == ST_DEADLOCK:
+            timeline = eng.timeline(0)
+    try:
+        _raise_for(status, "", raw, timeline)
+    except Exception as exc:  # noqa: BLE001 - returned to the caller
+        return exc
+    return RuntimeError("no failure")
 
 
 def _is_default_roofline(est) -> bool:
@@ -135,7 +158,8 @@ def simulate(annotated, cluster=None, record_timeline: bool = False, device: int
     raw = from_annotated(annotated, cluster)
     res, eng = simulate_raw([raw], device, record_timeline=True)
     r = res[0]
-    _raise_for(int(r["status"]))
+    st = int(r["status"])
+    _raise_for(st, "", raw, eng.timeline(0) if st == ST_DEADLOCK else None)
     T = _ref_types()
     # per-rank busy / exposed / idle / peak: segmented sort + union scans on the
     # device over the recorded timeline (stats.cu, _report sim.py:406-426)
@@ -233,7 +257,8 @@ class GpuPipelineEvaluator:
         return None, None
 
     def evaluate_many(self, configs: Sequence) -> list:
-        """EvalResult per config, or the exception its evaluation raised."""
+        """EvalResult per config, or the exception its evaluation raised (the
+        reference's class and text, as run_search records it, search.py:370-374)."""
         T = _ref_types()
         configs = list(configs)
         out: list = [None] * len(configs)
@@ -242,33 +267,41 @@ class GpuPipelineEvaluator:
             sched = self.schedule or W.default_schedule(c)
             errors = W.validate_config(self.model, c, self.cluster, sched)
             if errors:
-                out[i] = W.ConfigError("; ".join(errors))
+                out[i] = T["ConfigError"]("; ".join(errors))
             else:
                 todo.append(i)
         if not todo:
             return out
         eff, overhead = self._efficiency()
         eng = _engine(self.device)
-        sub = [configs[i] for i in todo]
+        raws = None
         if eff is not None:
-            st = eng.stage_generated(self.model, sub, self.cluster, schedule=self.schedule,
-                                     dispatch_overhead_ns=self.dispatch_overhead_ns,
-                                     efficiency=eff, overhead_ns=overhead, threads=self.threads)
+            sub = [configs[i] for i in todo]
+            eng.stage_generated(self.model, sub, self.cluster, schedule=self.schedule,
+                                dispatch_overhead_ns=self.dispatch_overhead_ns,
+                                efficiency=eff, overhead_ns=overhead, threads=self.threads)
             eng.upload()
-        else:  # user estimator: host annotations per unique feature (estimate.py:329-361)
-            raws = [self._annotated_raw(c) for c in sub]
+        else:  # user estimator: host annotations (estimate.py:329-361), per config
+            raws, keep = [], []
+            for i in todo:
+                try:
+                    raws.append(self._annotated_raw(configs[i]))
+                    keep.append(i)
+                except Exception as exc:  # noqa: BLE001 - per-config INVALID, as the reference
+                    out[i] = exc
+            todo = keep
+            if not todo:
+                return out
             eng.load(raws, threads=self.threads)
         eng.run()
         res = eng.results()
         flops = {}
+        failed = []
         for k, i in enumerate(todo):
             r = res[k]
             st_ = int(r["status"])
             if st_ != ST_OK:
-                try:
-                    _raise_for(st_, f" (config {configs[i].label()})")
-                except Exception as exc:  # noqa: BLE001 - surfaced to the caller
-                    out[i] = exc
+                failed.append((k, i, st_))
                 continue
             gb = configs[i].global_batch
             if gb not in flops:
@@ -277,9 +310,28 @@ class GpuPipelineEvaluator:
                        self.model.dtype)
             out[i] = T["EvalResult"](int(r["total_ns"]), mfu, int(r["peak_mem_bytes"]),
                                      bool(r["oom"]))
+        for k, i, st_ in failed:      # error path: rebuild the reference's exception text
+            raw = raws[k] if raws is not None else W.generate_job(
+                self.model, configs[i], self.cluster, self.schedule, self.dispatch_overhead_ns)
+            out[i] = _failure(st_, raw, self.device)
         return out
 
     def _annotated_raw(self, config) -> RawJob:
+        """Host-estimator path.  With the reference importable (a TableEstimator
+        or any dltsim estimator) the job comes from its own generate_representatives
+        -> collate -> annotate (workload.py:571-780, collate.py:256, estimate.py:329),
+        so KernelAttrs carry their dims and estimator errors their reference text;
+        the simulation then runs on the device.  Without it, the native generator's
+        features (no dims) feed annotate_raw."""
+        ref = _reference_frontend(self.model)
+        if ref is not None:
+            wl, col, est_mod = ref
+            sched = self.schedule or wl.default_schedule(config)
+            traces, expansion = wl.generate_representatives(
+                self.model, config, self.cluster, sched,
+                dispatch_overhead_ns=self.dispatch_overhead_ns)
+            job = col.collate(traces, expansion, self.cluster)
+            return from_annotated(est_mod.annotate(job, self.estimator))
         raw = W.generate_job(self.model, config, self.cluster, self.schedule,
                              self.dispatch_overhead_ns)
         return annotate_raw(raw, self.estimator, self.cluster.device)
@@ -295,6 +347,20 @@ class GpuPipelineEvaluator:
         if isinstance(r, Exception):
             raise r
         return r
+
+
+def _reference_frontend(model):
+    """(dltsim.workload, dltsim.collate, dltsim.estimate) when `model` is the
+    reference's own ModelSpec, else None."""
+    if not type(model).__module__.startswith("dltsim"):
+        return None
+    import importlib
+    try:   # submodules by name: the package re-exports functions of the same names
+        wl, col, est_mod = (importlib.import_module(f"dltsim.{m}")
+                            for m in ("workload", "collate", "estimate"))
+    except Exception:
+        return None
+    return wl, col, est_mod
 
 
 def annotate_raw(raw: RawJob, estimator, device) -> RawJob:

@@ -1103,6 +1103,9 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
     db.tl_end = (int64_t *)(X + e->scratch_bytes + align_up(e->n_tl * 8, 256));
     e->db.tl_start = db.tl_start;
     e->db.tl_end = db.tl_end;
+    // -1 = never completed: a deadlocked job's residue (sim.py:382-402) is read
+    // from the first unfinished op of every FIFO (api._deadlock_message)
+    if (e->n_tl) CU(cudaMemsetAsync(db.tl_end, 0xFF, e->n_tl * 8, e->stream));
   }
   char *X = (char *)e->d_scratch;
   // runs fold (fold_kernel) unless a per-op timeline is recorded

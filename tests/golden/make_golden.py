@@ -20,6 +20,9 @@ flattened job (rawtrace.RawJob) together with the reference's outputs:
 * workload.npz    — C1 (GPT-2 small, 2 ranks) and a spread of generated
                     Megatron-style configs (acceptance criterion-4 lattice and
                     GPT-3 1.3B / C2 samples) with RooflineEstimator.
+* deadlock.npz    — >= 60 deadlocking multi-rank jobs (crossed collective orders,
+                    events recorded behind stalled ops, host syncs on them,
+                    partial arrivals; 2-256 ranks) with SimDeadlockError's text.
 * estimators.json — estimate.py known answers (pkg/tests/test_estimate.py:27-117)
                     plus a seeded sweep of roofline/alpha-beta values.
 * c2_results.json — (--c2) reference results for all 512 C2 configs (BASELINE C2).
@@ -243,7 +246,8 @@ def syncfree_cases():
     return cases
 
 
-def random_multirank_job(rng: random.Random, n_ranks: int, n_steps: int, n_hosts: int = 1):
+def random_multirank_job(rng: random.Random, n_ranks: int, n_steps: int, n_hosts: int = 1,
+                         reorder=None):
     """Seeded random valid multi-rank job: collectives in a shared global order
     on random streams, cross-stream events, host syncs, memory, gaps."""
     from dltsim.cluster import ClusterSpec
@@ -278,6 +282,8 @@ def random_multirank_job(rng: random.Random, n_ranks: int, n_steps: int, n_hosts
         live = []
         na = 0
         prog = [p for p in program if r in comms[p[0]][1]]
+        if reorder is not None:
+            prog = reorder(r, prog)
         pi = 0
         nstreams = rng.randrange(1, 5)
         lrng = random.Random(rng.randrange(1 << 30))
@@ -353,6 +359,69 @@ def multirank_cases():
             {"gemm": rng.randrange(1, 9000), "gelu": 0}, default_ns=rng.randrange(0, 3000),
             coll_ns=rng.randrange(0, 40_000))
         cases.append(run_case(f"multirank_{i}", job, est))
+    return cases
+
+
+def _crossed(rng: random.Random, prog: list, swaps: int) -> list:
+    """Per-rank collective order with `swaps` random adjacent transpositions of
+    calls on DIFFERENT communicators (per-comm call_idx order stays valid, so
+    collate accepts the job; crossings between ranks deadlock it)."""
+    prog = list(prog)
+    for _ in range(swaps):
+        if len(prog) < 2:
+            break
+        i = rng.randrange(len(prog) - 1)
+        if prog[i][0] != prog[i + 1][0]:
+            prog[i], prog[i + 1] = prog[i + 1], prog[i]
+    return prog
+
+
+def random_deadlock_job(rng: random.Random, n_ranks: int, n_steps: int, n_hosts: int = 1):
+    """random_multirank_job with the even ranks' collective order locally
+    crossed (calls on different communicators swapped): the reference
+    deadlocks on most of them -- crossed collectives, streams waiting on
+    events recorded behind a stalled op, host syncs on such streams/events,
+    partial arrivals."""
+    seed = rng.randrange(1 << 30)
+    swaps = rng.randrange(1, 4)
+
+    def reorder(r, prog):
+        if r % 2:
+            return prog
+        return _crossed(random.Random(seed ^ (r * 7919)), prog, swaps)
+    return random_multirank_job(rng, n_ranks, n_steps, n_hosts, reorder=reorder)
+
+
+def deadlock_cases():
+    """>= 50 deadlocking multi-rank jobs (2-8 ranks) plus larger ones (160 and
+    256 ranks, hundreds of stream FIFOs: the lane scheduler runs them as grid
+    jobs), with the reference's SimDeadlockError text."""
+    from dltsim.estimate import RooflineEstimator
+    from builders import FixedEstimator
+    cases = []
+    rng = random.Random(0xDEAD10C)
+    tries = 0
+    while len(cases) < 60 and tries < 2000:
+        tries += 1
+        R = rng.choice([2, 3, 4, 6, 8])
+        nh = rng.choice([1, 2]) if R % 2 == 0 else 1
+        job, cluster = random_deadlock_job(rng, R, rng.randrange(10, 120), nh)
+        est = RooflineEstimator() if tries % 3 else FixedEstimator(
+            {"gemm": rng.randrange(1, 9000), "gelu": 0}, default_ns=rng.randrange(0, 3000),
+            coll_ns=rng.randrange(0, 40_000))
+        raw, exp = run_case(f"deadlock_{len(cases)}", job, est)
+        if exp["status"] == "deadlock":
+            cases.append((raw, exp))
+    big = 0
+    while big < 3 and tries < 4000:
+        tries += 1
+        R = (160, 256, 256)[big]
+        job, cluster = random_deadlock_job(rng, R, rng.randrange(30, 60), R // 8)
+        raw, exp = run_case(f"deadlock_big_{big}", job, RooflineEstimator(), timeline_limit=0)
+        if exp["status"] == "deadlock":
+            cases.append((raw, exp))
+            big += 1
+    print(f"  deadlock: {len(cases)} cases from {tries} tries")
     return cases
 
 
@@ -589,7 +658,7 @@ def main():
     setup(args.ref)
     only = set(args.only.split(",")) if args.only else None
     todo = [("unit", unit_cases), ("syncfree", syncfree_cases), ("multirank", multirank_cases),
-            ("workload", workload_cases), ("synth", synth_cases)]
+            ("workload", workload_cases), ("synth", synth_cases), ("deadlock", deadlock_cases)]
     for name, fn in todo:
         if only and name not in only:
             continue

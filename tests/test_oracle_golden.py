@@ -30,7 +30,7 @@ def check(job, exp):
         assert rows == exp["timeline"], exp["name"]
 
 
-@pytest.mark.parametrize("name", ["unit", "syncfree", "multirank", "workload", "synth"])
+@pytest.mark.parametrize("name", ["unit", "syncfree", "multirank", "workload", "synth", "deadlock"])
 def test_oracle_matches_reference(golden, name):
     jobs, exps = golden(name)
     for job, exp in zip(jobs, exps):
