@@ -370,55 +370,112 @@ def c5_sweep(spec: str, steps: int, dev_index: int) -> dict:
                                  "estimators + fold + schedulers"}}
 
 
-def c3_lattice(dev_index: int, threads: int) -> dict:
+def c3_lattice(dev_index: int, threads: int, rank: int = 0, world: int = 1) -> dict:
     """C3 (BASELINE configs[2]): GPT-3 18.4B, all 4,088 configs of the
-    64-1,024-rank lattices (act_recompute on, global batch 1,024 / 2,048), on one
-    GPU.  device: kernel time of each lattice batch with its trace resident (median
-    of 3 runs, summed); e2e: generation + packing + H2D + kernels + D2H + top-k per
-    batch on a warm engine (arenas already sized), summed."""
+    64-1,024-rank lattices (act_recompute on, global batch 1,024 / 2,048).
+    Each of the 10 lattice searches is sharded over the `world` GPUs (strong
+    scaling: LPT shards, local fused top-k, one NCCL all_gather of k x 24 B,
+    api.evaluate_sharded's merge); the overall best is merged across searches by
+    MFU (api.rank_by_mfu).  device: per search, the max over GPUs of its kernel
+    time (median of 3 runs, inputs resident), summed; e2e: per search, the max
+    over GPUs of generation + packing + H2D + kernels + D2H + top-k on a warm
+    engine, summed.  With world > 1, rank 0 re-runs every search alone and
+    checks the sharded top-k is identical."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
     from paper_2503_20191_b200 import workload as W
+    from paper_2503_20191_b200.api import (config_costs, gather_merge, key_ranks, merge_topk,
+                                           rank_by_mfu, shard_lpt)
     from paper_2503_20191_b200.engine import Engine
     model = W.ModelSpec("gpt3-18.4b", 40, 6144, 2048, 51200, "bf16")
     fast = W.load_device_preset("fast")
-    batches = []
+    searches = []
     for n in (64, 128, 256, 512, 1024):
         cl = W.ClusterSpec(n // 8, 8, 80 * 2 ** 30, fast)
         for gb in (1024, 2048):
-            batches.append((cl, W.enumerate_space(
-                W.SearchSpace(act_recompute=(True,), global_batch=gb), model, cl)))
+            cfgs = W.enumerate_space(W.SearchSpace(act_recompute=(True,), global_batch=gb),
+                                     model, cl)
+            kr = key_ranks(cfgs)
+            mine = shard_lpt(config_costs(cfgs), world)[rank]
+            searches.append((cl, cfgs, kr, mine))
     eng = Engine(dev_index)
+    dev = torch.device("cuda", dev_index)
 
-    def once(cl, cfgs):
-        eng.stage_generated(model, cfgs, cl, dispatch_overhead_ns=5000, threads=threads)
+    def rmax(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def once(cl, cfgs, kr, idx):
+        cand = np.full((TOPK, 3), -1, dtype=np.int64)
+        if not idx:
+            return None, cand
+        eng.stage_generated(model, [cfgs[i] for i in idx], cl, dispatch_overhead_ns=5000,
+                            key_ranks=kr[idx], threads=threads)
         eng.upload()
         eng.run()
         r = eng.results()
-        eng.topk(TOPK)
-        return r
-    for cl, cfgs in batches:          # warm: size the arenas once
-        once(cl, cfgs)
-    e2e_s, dev_ms, n_cfg, n_ok, rank_ops = 0.0, 0.0, 0, 0, 0
-    for cl, cfgs in batches:
+        for q, t in enumerate(eng.topk(TOPK)):
+            cand[q] = (int(t["time_ns"]), int(t["key_rank"]), idx[int(t["job"])])
+        return r, cand
+    for cl, cfgs, kr, mine in searches:          # warm: size the arenas once
+        once(cl, cfgs, kr, mine)
+    e2e_s, dev_ms, n_ok, rank_ops, class_ops = 0.0, 0.0, 0, 0, 0
+    merged_all = []
+    for q, (cl, cfgs, kr, mine) in enumerate(searches):
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        r = once(cl, cfgs)
-        e2e_s += time.perf_counter() - t0
+        r, cand = once(cl, cfgs, kr, mine)
+        merged = gather_merge(cand, TOPK) if world > 1 else merge_topk(cand, TOPK)
+        e2e_s += rmax(time.perf_counter() - t0)
         ks = []
         for _ in range(3):
-            eng.run()
-            eng.results()
-            ks.append(sum(eng.last_timings_ms()))
-        dev_ms += statistics.median(ks)
-        n_cfg += len(cfgs)
-        n_ok += int((r["status"] == 0).sum())
-        rank_ops += eng.batch_stats()["rank_ops"]
+            if mine:
+                eng.run()
+                eng.results()
+                ks.append(sum(eng.last_timings_ms()))
+            else:
+                ks.append(0.0)
+        dev_ms += rmax(statistics.median(ks))
+        if r is not None:
+            n_ok += int((r["status"] == 0).sum())
+            bs = eng.batch_stats()
+            rank_ops += bs["rank_ops"]
+            class_ops += bs["class_ops"]
+        merged_all.append(merged)
+    n_cfg = sum(len(c) for _, c, _, _ in searches)
+    rows = [(int(m[0]), q, int(m[2])) for q, mg in enumerate(merged_all) for m in mg if m[0] >= 0]
+    ranked = rank_by_mfu(rows, model,
+                         lambda row: (searches[row[1]][1][row[2]], searches[row[1]][0]))
+    best_row, best_mfu = ranked[0]
+    best_cfg = searches[best_row[1]][1][best_row[2]]
+    out = {"workload": "C3: GPT-3 18.4B (40 x 6144, seq 2048), 64-1,024 ranks (8 per host), "
+                       "SearchSpace(act_recompute=(True,), global_batch=1024|2048), 5 us gaps, "
+                       "RooflineEstimator; 10 lattice searches",
+           "configs": n_cfg, "gpus": world,
+           "sharding": "each search's configs LPT-sharded over the GPUs (strong scaling), local "
+                       "fused top-k, NCCL all_gather of k x 24 B, merge; best across searches "
+                       "by MFU (reference _rank order)",
+           "device_configs_per_s": round(n_cfg / (dev_ms / 1000), 1),
+           "e2e_configs_per_s": round(n_cfg / e2e_s, 1),
+           "best": {"key": list(best_cfg.key()), "ranks": searches[best_row[1]][0].num_devices,
+                    "time_ns": best_row[0], "mfu": best_mfu}}
+    if rank == 0:
+        out["ok_on_rank0"] = n_ok
+        out["rank_ops_per_s_device_rank0"] = round(rank_ops / (dev_ms / 1000), 1)
+        out["class_ops_per_s_device_rank0"] = round(class_ops / (dev_ms / 1000), 1)
+    if world > 1 and rank == 0:      # the sharded top-k equals one GPU's
+        same = True
+        for (cl, cfgs, kr, _), mg in zip(searches, merged_all):
+            _, cand = once(cl, cfgs, kr, list(range(len(cfgs))))
+            same &= bool(np.array_equal(merge_topk(cand, TOPK), mg))
+        out["sharded_topk_equals_single_gpu"] = same
     eng.close()
-    return {"workload": "C3: GPT-3 18.4B (40 x 6144, seq 2048), 64-1,024 ranks (8 per host), "
-                        "SearchSpace(act_recompute=(True,), global_batch=1024|2048), 5 us gaps, "
-                        "RooflineEstimator; 10 lattice batches",
-            "configs": n_cfg, "ok": n_ok,
-            "device_configs_per_s": round(n_cfg / (dev_ms / 1000), 1),
-            "e2e_configs_per_s": round(n_cfg / e2e_s, 1),
-            "rank_ops_per_s_device": round(rank_ops / (dev_ms / 1000), 1)}
+    return out
 
 
 def bench_ours(args):
@@ -489,14 +546,25 @@ def bench_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
 
-    # search reduction across GPUs: all_gather of k x 24 B candidates (NCCL), merge
-    from paper_2503_20191_b200.api import gather_merge, merge_topk
+    # search reduction across GPUs: all_gather of k x 24 B candidates (NCCL).
+    # Each GPU searched its own global batch (512 * 2**rank), so the merge ranks
+    # by MFU as the reference's _rank does (search.py:349-357; api.rank_by_mfu)
+    from paper_2503_20191_b200.api import rank_by_mfu
     cand = np.full((TOPK, 3), -1, dtype=np.int64)
     for q, e in enumerate(top):
-        cand[q] = (int(e["time_ns"]), (rank << 20) | int(e["key_rank"]), int(e["job"]))
-    merged = gather_merge(cand, TOPK) if world > 1 else merge_topk(cand, TOPK)
-    best = merged[0]
-    best_rank, best_kr = int(best[1]) >> 20, int(best[1]) & 0xfffff
+        cand[q] = (int(e["time_ns"]), rank, int(e["job"]))
+    if world > 1:
+        tc = torch.from_numpy(cand).to(dev)
+        parts = [torch.empty_like(tc) for _ in range(world)]
+        dist.all_gather(parts, tc)
+        allc = torch.cat(parts).cpu().numpy()
+    else:
+        allc = cand
+    by_rank = {r: workload(r)[2] for r in range(world)}
+    ranked = rank_by_mfu([tuple(int(x) for x in row) for row in allc if row[0] >= 0], model,
+                         lambda row: (by_rank[row[1]][row[2]], cluster))
+    best, best_mfu = ranked[0]
+    best_rank, best_cfg = best[1], by_rank[best[1]][best[2]]
 
     # --- the same batch on the full-rank path (no class collapse) -------------------
     full = None
@@ -524,6 +592,8 @@ def bench_ours(args):
         full = {"value": round(N_CONFIGS / (statistics.mean(fms) / 1000), 2), "unit": "configs/s",
                 "ms_per_step": round(statistics.mean(fms), 4),
                 "trace_ops_per_s": round(stats["rank_ops"] / (statistics.mean(fms) / 1000), 1),
+                "class_ops_per_s": round(eng.batch_stats()["class_ops"]
+                                         / (statistics.mean(fms) / 1000), 1),
                 "identical_results_to_collapsed": same}
         eng.set_collapse(True)
         eng.stage_generated(model, configs, cluster, dispatch_overhead_ns=5000, key_ranks=kr,
@@ -565,6 +635,8 @@ def bench_ours(args):
         dist.barrier()
     e2e_ms_max = float(e.item())
 
+    c3 = None if args.no_c3 else c3_lattice(local, threads, rank, world)
+
     if rank == 0:
         n_total = N_CONFIGS * world
         value = n_total / (ms_max / 1000)
@@ -587,6 +659,10 @@ def bench_ours(args):
                     "(event-for-event identical, tests/test_gen.py)",
             "config": dict(bench_config(world), rank_ops_per_gpu=rank_ops),
             "trace_ops_per_s": round(rank_ops * world / (ms_max / 1000), 1),
+            "class_ops_per_s": round(stats["class_ops"] * world / (ms_max / 1000), 1),
+            "ops_note": "trace_ops_per_s: rank-ops (sum over ALL ranks of the rep trace length, "
+                        "the reference's work unit); class_ops_per_s: the ops the engine "
+                        "executed (rank classes of collapsed jobs, SURVEY 7.8)",
             "e2e": {"value": round(n_total / (e2e_ms_max / 1000), 2), "unit": "configs/s",
                     "ms_per_step": round(e2e_ms_max, 3),
                     "h2d_bytes_per_step": int(stats["arena_bytes"]),
@@ -606,7 +682,8 @@ def bench_ours(args):
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "rounds": {"max": int(res["rounds"].max()), "median": float(np.median(res["rounds"]))},
-            "best": {"rank": best_rank, "key_rank": best_kr, "time_ns": int(best[0])},
+            "best": {"rank": best_rank, "key": list(best_cfg.key()), "time_ns": int(best[0]),
+                     "mfu": best_mfu},
             "class_collapse": {"collapsed_configs": int(n_collapsed), "simulated_ranks":
                                stats["ranks"], "note": "exact rank-class collapse (SURVEY 7.8), "
                                "verified per config; value/e2e use it"},
@@ -615,8 +692,8 @@ def bench_ours(args):
         }
         if world == 1 and args.c5:
             line["c5"] = c5_sweep(args.c5, args.steps, local)
-        if world == 1 and not args.no_c3:
-            line["c3"] = c3_lattice(local, threads)
+        if c3 is not None:
+            line["c3"] = c3
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(host_threads())
             line["cpu_baseline"]["port"] = port_baseline(model, cluster, configs,

@@ -188,7 +188,8 @@ int64_t maya_arena_bytes(maya_engine *eng);
  * [6] rank-ops, [7] arena bytes, [8] ranks, [9] reps, [10] kernels launched by
  * the last maya_run, [11] kernels launched by the last maya_topk, [12] kernel
  * blocks, [13] block feature ids, [14] wire features (unique call records),
- * [15] reserved. */
+ * [15] executed class-ops: sum over SIMULATED ranks (rank classes of collapsed
+ * jobs) of their rep trace length (rank-ops [6] counts every rank). */
 int maya_batch_stats(maya_engine *eng, int64_t *out16);
 
 /* Scheduler phase counters of instrumented builds (-DMAYA_PROFILE); returns

@@ -578,31 +578,67 @@ def shard_lpt(costs: Sequence[int], n: int) -> list:
     return [sorted(x) for x in out]
 
 
+def config_costs(configs) -> list:
+    """LPT cost proxy of a config's simulation: pipeline steps per rank times
+    stages (microbatches x virtual stages x pp)."""
+    return [c.micro_mult * c.pp * c.pp * c.virtual_stages for c in configs]
+
+
+def evaluate_sharded(model, configs, cluster, k: int = 8, engine=None, rank: int = 0,
+                     world: int = 1, dispatch_overhead_ns: int = 0, schedule=None,
+                     threads: int = 8, key_order=None):
+    """ONE search's config list sharded over `world` processes (one per GPU):
+    LPT on config_costs, the local fused device top-k, one all_gather of
+    k x 24 B candidates (NCCL; gloo on CPU), and the same merge on every rank.
+    Within one search (one cluster, one global batch) MFU is a decreasing
+    function of time_ns, so the (time_ns, key rank) order of the merge is the
+    reference ranking (search.py:349-357).
+    -> (merged (k, 3) rows: time_ns, key rank, GLOBAL config index; my indices)"""
+    kr = key_ranks(configs) if key_order is None else np.asarray(key_order, dtype=np.int32)
+    mine = shard_lpt(config_costs(configs), world)[rank]
+    eng = engine if engine is not None else _engine(0)
+    cand = np.full((k, 3), -1, dtype=np.int64)
+    if mine:
+        sub = [configs[i] for i in mine]
+        eng.stage_generated(model, sub, cluster, schedule=schedule,
+                            dispatch_overhead_ns=dispatch_overhead_ns, key_ranks=kr[mine],
+                            threads=threads)
+        eng.upload()
+        eng.run()
+        for q, t in enumerate(eng.topk(k)):
+            cand[q] = (int(t["time_ns"]), int(t["key_rank"]), mine[int(t["job"])])
+    merged = gather_merge(cand, k) if world > 1 else merge_topk(cand, k)
+    return merged, mine
+
+
 def evaluate_space_distributed(space, model, cluster, k: int = 8, dispatch_overhead_ns: int = 0,
-                               schedule=None, threads: int = 8):
-    """One process per GPU (torch.distributed): configs sharded by LPT on a
-    cost proxy, local fused top-k, one all_gather of k x 24 B per GPU, merge."""
+                               schedule=None, threads: int = 8, engine=None):
+    """One process per GPU (torch.distributed): every valid config of `space`,
+    sharded by evaluate_sharded.  -> (merged top-k rows, configs)"""
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(), dist.get_world_size()
     configs = W.enumerate_space(space, model, cluster)
-    kr = key_ranks(configs)
-    costs = [c.micro_mult * c.pp * c.virtual_stages for c in configs]
-    mine = shard_lpt(costs, world)[rank]
-    dev = torch.cuda.current_device() if torch.cuda.is_available() else 0
-    eng = _engine(dev)
-    sub = [configs[i] for i in mine]
-    eng.stage_generated(model, sub, cluster, schedule=schedule,
-                        dispatch_overhead_ns=dispatch_overhead_ns, key_ranks=kr[mine],
-                        threads=threads)
-    eng.upload()
-    eng.run()
-    eng.results()
-    top = eng.topk(k)
-    cand = np.full((k, 3), -1, dtype=np.int64)
-    for q, t in enumerate(top):
-        cand[q] = (int(t["time_ns"]), int(t["key_rank"]), mine[int(t["job"])])
-    return gather_merge(cand, k), configs
+    if engine is None:
+        engine = _engine(torch.cuda.current_device() if torch.cuda.is_available() else 0)
+    merged, _ = evaluate_sharded(model, configs, cluster, k, engine, rank, world,
+                                 dispatch_overhead_ns, schedule, threads)
+    return merged, configs
+
+
+def rank_by_mfu(rows, model, configs_of) -> list:
+    """Merge candidates of DIFFERENT searches (global batches / clusters) the
+    reference's way: (-mfu, time_ns, config.key()) (search.py:349-357), MFU by
+    compute_mfu's arithmetic (sim.py:488-497).  rows: (time_ns, ..., cfg handle);
+    configs_of(row) -> (config, cluster)."""
+    out = []
+    for row in rows:
+        cfg, cl = configs_of(row)
+        t = int(row[0])
+        mfu = _mfu(t, False, iteration_flops(model, cfg.global_batch), cl, model.dtype)
+        out.append((-mfu, t, cfg.key(), row))
+    out.sort(key=lambda x: x[:3])
+    return [(r, -m) for m, _, _, r in out]
 
 
 def gather_merge(cand: np.ndarray, k: int) -> np.ndarray:

@@ -1295,6 +1295,7 @@ int maya_batch_stats(maya_engine *e, int64_t *o) {
     o[12] += (int64_t)P.blocks.size();
     o[13] += (int64_t)P.blk_fids.size();
     o[14] += (int64_t)P.wfeats.size();
+    for (const RankRec &rr : P.ranks) o[15] += P.reps[rr.rep].n_events;   // class-ops
   }
   o[7] = (int64_t)e->arena_bytes;
   return MAYA_OK;

@@ -249,7 +249,7 @@ class Engine:
         _check(lib().maya_batch_stats(self._h, o))
         keys = ("jobs", "rep_events", "rank_comms", "features", "slots", "device_ops",
                 "rank_ops", "arena_bytes", "ranks", "reps", "run_launches", "topk_launches",
-                "kernel_blocks", "block_fids", "wire_features")
+                "kernel_blocks", "block_fids", "wire_features", "class_ops")
         return {k: int(v) for k, v in zip(keys, o)}
 
     def arena_bytes(self) -> int:
