@@ -146,6 +146,19 @@ def parity(res: dict) -> dict:
     return {"checked": len(res), "mismatches": bad}
 
 
+def _sample_weight(idx: list):
+    """Mean rank-ops of the sampled configs over the mean of all 512 (from the
+    committed reference goldens): > 1 means the sample is heavier than the batch."""
+    path = os.path.join(os.path.dirname(HERE), "tests", "golden", "c2_results.json")
+    try:
+        with open(path) as f:
+            gold = json.load(f)
+    except OSError:
+        return None
+    mean_all = sum(r["rank_ops"] for r in gold) / len(gold)
+    return round(sum(gold[i]["rank_ops"] for i in idx) / len(idx) / mean_all, 4)
+
+
 def measure(mode: str, n_workers: int, per_worker: int, passes: int, warmup: int = 1) -> dict:
     """Throughput of one leg: `passes` timed passes of n_workers x per_worker
     configs (after `warmup` untimed passes)."""
@@ -162,5 +175,6 @@ def measure(mode: str, n_workers: int, per_worker: int, passes: int, warmup: int
         pool.close()
     t = sum(times) / len(times)
     return {"configs_per_s": round(len(idx) / t, 3), "seconds_per_pass": round(t, 4),
+            "sample_rank_ops_vs_all_512": _sample_weight(idx),
             "configs_per_pass": len(idx), "workers": pool.n, "passes": passes,
             "times": [round(x, 4) for x in times], "parity": parity(res)}

@@ -595,6 +595,23 @@ int maya_upload(maya_engine *e) {
       if (plans[j].variant >= 0 && plans[j].variant != 15)
         n_perm += (size_t)plans[j].per_lane * plans[j].threads;
     }
+    // a grid job runs only if all its parts are co-resident under the batch's
+    // grid launch shape (the largest part layout); otherwise it is scheduled
+    // by the warp-window kernel (2,048-rank full-rank jobs with many streams)
+    for (;;) {
+      uint32_t smax = 0;
+      for (size_t j = 0; j < nj; j++)
+        if (plans[j].variant == 15) smax = std::max(smax, (plans[j].smem + 127u) & ~127u);
+      if (!smax) break;
+      const size_t cap = (size_t)std::max(1, grid_max_ctas(smax));
+      bool demoted = false;
+      for (size_t j = 0; j < nj; j++)
+        if (plans[j].variant == 15 && plans[j].parts.size() > cap) {
+          plans[j] = LanePlan();
+          demoted = true;
+        }
+      if (!demoted) break;
+    }
   }
   if (n_reps > 0xffffffffull) return fail(MAYA_EINVAL, "too many representatives in batch");
   if (n_feats >= 0xffffffffull) return fail(MAYA_EINVAL, "too many kernel features in batch");
