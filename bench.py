@@ -347,27 +347,60 @@ def c5_sweep(spec: str, steps: int, dev_index: int) -> dict:
     alg = (16 * st["rep_events"] + 4 * st["rank_comms"] + 16 * (st["features"] + st["slots"])
            + 24 * st["jobs"])
     peak, peak_kind = measured_peak_hbm()
-    achieved = alg / (ms / 1000) / 1e9
     step_ms = est_ms + fold_ms + ms
+    achieved = alg / (step_ms / 1000) / 1e9
     eng.close()
     del flush
+    traffic = c5_ncu_traffic(R, n, B)
     return {"workload": f"C5 synthetic: {R} ranks x {n} events/rank, {B} configs per batch "
                         f"({distinct} distinct seeds tiled; every config has its own arena copy)",
             "configs_per_s": round(B / (step_ms / 1000), 1),
             "rank_ops_per_s": round(st["rank_ops"] / (step_ms / 1000), 1),
-            "ok": ok, "configs": B, "sched_ms": round(ms, 4),
+            "class_ops_per_s": round(st["class_ops"] / (step_ms / 1000), 1),
+            "ok": ok, "configs": B,
             "step_ms": {"estimators": round(est_ms, 4), "memscan+fold+resolve": round(fold_ms, 4),
-                        "schedulers": round(ms, 4)},
-            "step_achieved_gbs": round(alg / (step_ms / 1000) / 1e9, 1),
-            "step_frac": round(alg / (step_ms / 1000) / 1e9 / peak, 4),
-            "roofline": {"bound": "hbm", "kernel": "sched_lane_warp_kernel",
+                        "schedulers": round(ms, 4), "total": round(step_ms, 4)},
+            "roofline": {"bound": "hbm",
+                         "kernels": "the whole step: estimate_features + fold_count + fold_write "
+                                    "+ sched_lane_warp (+ small tables), i.e. every kernel that "
+                                    "reads the algorithmic bytes",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_source": peak_kind,
-                         "algorithmic_bytes_per_launch": alg,
-                         "note": "16 B x rep events + tables (DESIGN.md roofline) over the "
-                                 "scheduler kernels' time; kernel runs were folded by the "
-                                 "resolve pass (fold_count/fold_write), see step_frac for "
-                                 "estimators + fold + schedulers"}}
+                         "algorithmic_bytes_per_step": alg,
+                         "traffic": traffic.get("step_dram_bytes"),
+                         "traffic_over_algorithmic": (round(traffic["step_dram_bytes"] / alg, 3)
+                                                      if traffic.get("step_dram_bytes") else None),
+                         "per_kernel": traffic.get("per_kernel"),
+                         "traffic_source": traffic.get("source"),
+                         "note": "algorithmic bytes = 16 B x rep events + tables (DESIGN.md "
+                                 "roofline) over the step's device time; per_kernel: ncu "
+                                 "dram__bytes and time of one cold launch each (committed "
+                                 "profile of the same workload)"},
+            "scheduler_only": {"ms": round(ms, 4),
+                               "input_frac": round(alg / (ms / 1000) / 1e9 / peak, 4),
+                               "note": "algorithmic bytes over the scheduler kernel alone -- NOT "
+                                       "a roofline of that kernel: the estimator and fold "
+                                       "kernels stream those bytes; the scheduler reads the "
+                                       "folded ops (per_kernel)"}}
+
+
+def c5_ncu_traffic(R: int, n: int, B: int) -> dict:
+    """Per-kernel DRAM bytes of the C5 step from the committed ncu launch list
+    (profiles/c5_step_kernels_r2.json, tools/ncu_summary.py), when it was
+    captured on this workload shape."""
+    path = os.path.join(REPO, "profiles", "c5_step_kernels_r2.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return {}
+    if d.get("workload") not in (None, f"{R}x{n}x{B}"):
+        return {}
+    per = {k: {"ms": round(v["mean_ms"], 4),
+               "dram_bytes": int(v["dram_read_bytes"] + v["dram_write_bytes"])}
+           for k, v in d["kernels"].items()}
+    return {"step_dram_bytes": sum(v["dram_bytes"] for v in per.values()), "per_kernel": per,
+            "source": "profiles/c5_step_kernels_r2.json (" + str(d.get("source")) + ")"}
 
 
 def c3_lattice(dev_index: int, threads: int, rank: int = 0, world: int = 1) -> dict:

@@ -13,10 +13,16 @@ import numpy as np
 from paper_2503_20191_b200.engine import Engine
 from paper_2503_20191_b200.synth import c5_job
 
-GRID = [(8, 1000, 8192, 64), (8, 10000, 4096, 64), (8, 100000, 296, 32), (8, 1000000, 32, 8),
-        (64, 1000, 2048, 64), (64, 10000, 296, 32), (64, 100000, 32, 8),
-        (512, 1000, 296, 16), (512, 10000, 32, 8), (512, 100000, 4, 2),
-        (2048, 1000, 74, 4), (2048, 10000, 8, 2)]
+# (ranks, events/rank, max configs, distinct seeds).  The batch holds
+# min(max configs, what fits BUDGET_GB of device arena) configurations: a long-
+# trace point runs as many configs as HBM holds (one job per warp / CTA / grid).
+GRID = [(8, 1000, 8192, 64), (8, 10000, 4096, 64), (8, 100000, 2368, 16), (8, 1000000, 296, 4),
+        (64, 1000, 2048, 64), (64, 10000, 592, 32), (64, 100000, 148, 8), (64, 1000000, 16, 2),
+        (512, 1000, 296, 16), (512, 10000, 64, 8), (512, 100000, 8, 2), (512, 1000000, 1, 1),
+        (2048, 1000, 74, 4), (2048, 10000, 16, 2), (2048, 100000, 2, 1), (2048, 1000000, 1, 1)]
+BUDGET_GB = float(os.environ.get("C5_BUDGET_GB", "60"))
+BYTES_PER_EVENT = 40      # device arena + scratch per trace event (measured: arena_bytes)
+
 
 def _peak():
     try:
@@ -37,6 +43,7 @@ def main():
     for R, n, B, distinct in GRID:
         if only and f"{R}x{n}" not in only:
             continue
+        B = max(1, min(B, int(BUDGET_GB * 1e9 / (BYTES_PER_EVENT * R * n))))
         t0 = time.time()
         base = [c5_job(R, n, cfg=c) for c in range(min(B, distinct))]
         jobs = [base[c % len(base)] for c in range(B)]
@@ -59,12 +66,13 @@ def main():
                "sched_gbs": round(alg / sched / 1e6, 1),
                "sched_frac": round(alg / sched / 1e6 / PEAK, 4),
                "step_frac": round(alg / step / 1e6 / PEAK, 4),
-               "ok": int((r["status"] == 0).sum()), "gen_s": round(tg, 1)}
+               "ok": int((r["status"] == 0).sum()), "gen_s": round(tg, 1),
+               "arena_gb": round(st["arena_bytes"] / 1e9, 2)}
         rows.append(row)
         print(json.dumps(row), flush=True)
         del jobs, base
     out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out",
-                       "c5_sweep_r1.json")
+                       "c5_sweep_r2.json")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     with open(out, "w") as f:
         json.dump(rows, f, indent=1)
