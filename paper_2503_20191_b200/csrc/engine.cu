@@ -323,8 +323,12 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
   uint32_t fc = 0;
   while ((1u << fc) < 8 * R && fc < 12) fc++;
   struct Try { uint32_t lgd, flags; };
+  // deep rings before on-chip tables once the tables do not fit: a long FIFO
+  // (1e5-1e6 events per rank) stalls on refills with 2 slots, while its record
+  // and collective tables are read through the tagged cache / L1 anyway
   const Try tries[] = {{3, LANE_FIRE_SMEM | LANE_RCX_SMEM}, {2, LANE_FIRE_SMEM | LANE_RCX_SMEM},
-                       {1, LANE_FIRE_SMEM | LANE_RCX_SMEM},
+                       {1, LANE_FIRE_SMEM | LANE_RCX_SMEM}, {3, LANE_FIRE_SMEM}, {3, 0},
+                       {2, LANE_FIRE_SMEM}, {2, 0},
                        {1, LANE_FIRE_SMEM}, {1, 0}, {0xff, LANE_FIRE_SMEM}, {0xff, 0}};
   for (int pass = 0; pass < 2; pass++) {
     const uint32_t cap = pass == 0 ? budget : LANE_SMEM_CAP;
@@ -1062,13 +1066,23 @@ int maya_upload(maya_engine *e) {
     t.eff_den[i] = e->eff_den[i];
   }
   t.overhead_ns = e->overhead_ns;
+  // floor(2^64 / y) for y >= 2 (fits: <= 2^63); 0 stands for y == 1 (and for y <= 0,
+  // which the kernel never divides by on this path)
+  auto magic = [](int64_t y) -> uint64_t {
+    if (y <= 1) return 0;
+    return (uint64_t)(((unsigned __int128)1 << 64) / (unsigned __int128)(uint64_t)y);
+  };
   for (int d = 0; d < t.n_devs && d < 8; d++) {
-    for (int q = 0; q < MAYA_MAX_DTYPES; q++)
+    for (int q = 0; q < MAYA_MAX_DTYPES; q++) {
       t.inv_peak[d][q] = t.devs[d].peak_flops[q] > 0 ? 1.0 / (double)t.devs[d].peak_flops[q] : 0.0;
+      t.mag_peak[d][q] = magic(t.devs[d].peak_flops[q]);
+    }
     t.inv_hbm[d] = t.devs[d].hbm_bytes_per_s > 0 ? 1.0 / (double)t.devs[d].hbm_bytes_per_s : 0.0;
+    t.mag_hbm[d] = magic(t.devs[d].hbm_bytes_per_s);
   }
   for (int q = 0; q < t.n_op_kinds && q < 64; q++) {
     t.inv_num[q] = t.eff_num[q] > 0 ? 1.0 / (double)t.eff_num[q] : 0.0;
+    t.mag_num[q] = magic(t.eff_num[q]);
     const unsigned __int128 scale = (unsigned __int128)1000000000ull * (uint64_t)t.eff_den[q];
     t.max_flops[q] = (t.eff_den[q] > 0 && (scale >> 64) == 0) ? UINT64_MAX / (uint64_t)scale : 0;
     t.max_peak[q] = t.eff_num[q] > 0 ? UINT64_MAX / (uint64_t)t.eff_num[q] : 0;

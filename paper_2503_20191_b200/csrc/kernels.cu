@@ -95,15 +95,26 @@ __device__ __forceinline__ bool ceil_div_inv(uint64_t x, uint64_t y, double inv,
   return ceil_div_i64((u128)x, (u128)y, out);
 }
 
+// ceil(x / y) for y >= 1 with the host-made magic M = floor(2^64 / y) (M == 0:
+// y == 1).  q0 = floor(x * M / 2^64) satisfies x/y - 1 < q0 <= x/y (M > 2^64/y - 1
+// and x < 2^64), so q0 is floor(x / y) or one less and one conditional
+// subtraction fixes it; branch-free, ~12 instructions.
+__device__ __forceinline__ uint64_t ceil_div_magic(uint64_t x, uint64_t y, uint64_t M) {
+  if (M == 0) return x;
+  uint64_t q = __umul64hi(x, M);
+  uint64_t r = x - q * y;
+  const bool c = r >= y;
+  q += c ? 1u : 0u;
+  r -= c ? y : 0u;
+  return q + (r != 0 ? 1u : 0u);
+}
+
 // ---------------------------------------------------------------------------
 // estimators
 
-__global__ void estimate_features_kernel(DevBatch b, DevTables t) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= b.n_feats) return;
-  const longlong2 fv = __ldg(reinterpret_cast<const longlong2 *>(b.feats) + i);
-  const uint32_t meta = __ldg(b.feat_meta + i);
-  if (meta & FMETA_FIXED) { b.feat_ns[i] = fv.x; return; }
+// one feature's roofline duration (-1 on EstimationError / overflow)
+__device__ __forceinline__ int64_t estimate_one(const DevTables &t, longlong2 fv, uint32_t meta) {
+  if (meta & FMETA_FIXED) return fv.x;
   struct { int64_t flops, bytes; int32_t op_kind, dtype, device; } f{
       fv.x, fv.y, fmeta_op(meta), fmeta_dtype(meta), fmeta_device(meta)};
   const maya_device_params &dev = t.devs[f.device];
@@ -113,11 +124,14 @@ __global__ void estimate_features_kernel(DevBatch b, DevTables t) {
     int64_t peak = (f.dtype >= 0 && f.dtype < MAYA_MAX_DTYPES) ? dev.peak_flops[f.dtype] : 0;
     if (peak <= 0 || f.op_kind < 0 || f.op_kind >= t.n_op_kinds) {
       ok = false;  // EstimationError: no peak rate for dtype (estimate.py:124-127)
-    } else if ((uint64_t)f.flops <= t.max_flops[f.op_kind] && (uint64_t)peak <= t.max_peak[f.op_kind]) {
-      // 64-bit fast path: flops * 1e9 * den and peak * num both fit (host bounds)
-      ok = ceil_div_inv((uint64_t)f.flops * (1000000000ull * (uint64_t)t.eff_den[f.op_kind]),
-                        (uint64_t)peak * (uint64_t)t.eff_num[f.op_kind],
-                        t.inv_peak[f.device][f.dtype] * t.inv_num[f.op_kind], &compute);
+    } else if ((uint64_t)f.flops <= t.max_flops[f.op_kind] && t.eff_num[f.op_kind] > 0) {
+      // 64-bit fast path: X = flops * 1e9 * den fits (host bound);
+      // ceil(X / (peak * num)) = ceil(ceil(X / peak) / num), both by invariant divisors
+      const uint64_t X = (uint64_t)f.flops * (1000000000ull * (uint64_t)t.eff_den[f.op_kind]);
+      const uint64_t q1 = ceil_div_magic(X, (uint64_t)peak, t.mag_peak[f.device][f.dtype]);
+      const uint64_t q = ceil_div_magic(q1, (uint64_t)t.eff_num[f.op_kind], t.mag_num[f.op_kind]);
+      ok = q <= (uint64_t)INT64_MAX;
+      compute = (int64_t)q;
     } else {
       u128 num, den;
       ok = mul_u128_u64((u128)(uint64_t)f.flops * 1000000000ull, (uint64_t)t.eff_den[f.op_kind],
@@ -132,18 +146,46 @@ __global__ void estimate_features_kernel(DevBatch b, DevTables t) {
   }
   if (ok && f.bytes > 0) {
     const u128 mb = (u128)(uint64_t)f.bytes * 1000000000ull;
-    ok = (mb >> 64) == 0
-             ? ceil_div_inv((uint64_t)mb, (uint64_t)dev.hbm_bytes_per_s, t.inv_hbm[f.device], &memory)
-             : ceil_div_i64(mb, (u128)(uint64_t)dev.hbm_bytes_per_s, &memory);
+    if ((mb >> 64) == 0 && dev.hbm_bytes_per_s > 0) {
+      const uint64_t q = ceil_div_magic((uint64_t)mb, (uint64_t)dev.hbm_bytes_per_s,
+                                        t.mag_hbm[f.device]);
+      ok = q <= (uint64_t)INT64_MAX;
+      memory = (int64_t)q;
+    } else {
+      ok = ceil_div_i64(mb, (u128)(uint64_t)dev.hbm_bytes_per_s, &memory);
+    }
   }
   int64_t m = compute > memory ? compute : memory;
   if (ok && m > INT64_MAX - t.overhead_ns) ok = false;
-  if (!ok) {
-    b.feat_ns[i] = -1;
-    atomicOr(b.err_flag, 1);
-    return;
+  return ok ? m + t.overhead_ns : -1;
+}
+
+// EST_PER features per thread, all loads issued before the arithmetic (memory-
+// level parallelism: the kernel streams 20 B in and 8 B out per feature)
+static constexpr uint32_t EST_PER = 4;
+__global__ void __launch_bounds__(256) estimate_features_kernel(DevBatch b, DevTables t) {
+  const uint32_t base = blockIdx.x * (256 * EST_PER) + threadIdx.x;
+  longlong2 fv[EST_PER];
+  uint32_t meta[EST_PER];
+#pragma unroll
+  for (uint32_t k = 0; k < EST_PER; k++) {
+    const uint32_t i = base + k * 256;
+    if (i < b.n_feats) {
+      fv[k] = __ldg(reinterpret_cast<const longlong2 *>(b.feats) + i);
+      meta[k] = __ldg(b.feat_meta + i);
+    }
   }
-  b.feat_ns[i] = m + t.overhead_ns;
+  bool bad = false;
+#pragma unroll
+  for (uint32_t k = 0; k < EST_PER; k++) {
+    const uint32_t i = base + k * 256;
+    if (i < b.n_feats) {
+      const int64_t v = estimate_one(t, fv[k], meta[k]);
+      b.feat_ns[i] = v;
+      bad |= v < 0;
+    }
+  }
+  if (bad) atomicOr(b.err_flag, 1);
 }
 
 __global__ void estimate_wire_kernel(DevBatch b, DevTables t) {
@@ -171,7 +213,8 @@ __global__ void estimate_wire_kernel(DevBatch b, DevTables t) {
 }
 
 void launch_estimate(const DevBatch &b, const DevTables &t, cudaStream_t s) {
-  if (b.n_feats) estimate_features_kernel<<<(b.n_feats + 255) / 256, 256, 0, s>>>(b, t);
+  if (b.n_feats)
+    estimate_features_kernel<<<(b.n_feats + 256 * EST_PER - 1) / (256 * EST_PER), 256, 0, s>>>(b, t);
   if (b.n_wfeats) estimate_wire_kernel<<<(b.n_wfeats + 255) / 256, 256, 0, s>>>(b, t);
 }
 

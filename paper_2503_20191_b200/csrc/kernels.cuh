@@ -81,6 +81,10 @@ struct DevTables {
   double inv_peak[8][MAYA_MAX_DTYPES];
   double inv_num[64];
   double inv_hbm[8];
+  // exact division by these invariant divisors: M = floor(2^64 / y) (0: y == 1)
+  uint64_t mag_peak[8][MAYA_MAX_DTYPES];
+  uint64_t mag_num[64];
+  uint64_t mag_hbm[8];
   // 64-bit fast-path bounds per op kind: flops * 1e9 * eff_den and
   // peak * eff_num stay below 2^64
   uint64_t max_flops[64];
