@@ -281,15 +281,62 @@ def _strategy_kind(strategy) -> str:
     return getattr(strategy, "name", type(strategy).__name__)
 
 
+class BulkEvaluator:
+    """Evaluator wrapper for the reference's own ``run_search``: the first call
+    evaluates the whole enumerated space as ONE engine batch (speculatively --
+    the evaluator is pure, so pruned or never-reached configs only cost device
+    work), later calls are served from the memo.  Failures are re-raised per
+    config, so the reference records them as INVALID with their text
+    (search.py:370-374)."""
+
+    def __init__(self, evaluator, configs):
+        self.outcomes = _Outcomes(evaluator)
+        self.configs = list(configs)
+        self.primed = False
+
+    def __call__(self, config):
+        if not self.primed:
+            self.outcomes.prepare(self.configs)
+            self.primed = True
+        r = self.outcomes(config)
+        if isinstance(r, Exception):
+            raise r
+        return r
+
+
+def _reference_search(strategy, stop):
+    """dltsim.search when the caller uses the reference's own strategy (and stop
+    rule) objects, else None."""
+    if not type(strategy).__module__.startswith("dltsim"):
+        return None
+    if stop is not None and not type(stop).__module__.startswith("dltsim"):
+        return None
+    try:
+        import importlib
+        return importlib.import_module("dltsim.search")
+    except Exception:
+        return None
+
+
 def run_search(space, evaluator, strategy, model, cluster, jobs: int = 1,
                use_tactics: bool = True, stop: StopRule | None = None,
                max_trials: int | None = None, deterministic: bool = False) -> SearchResult:
     """dltsim.search.run_search with bulk speculative evaluation (module docstring).
 
-    ``jobs`` only sets the batch size, as in the reference (each batch's tactic
-    verdicts are taken against the history before its results); evaluation
-    itself is the engine's, not a process pool's."""
+    With the reference's own strategy objects (and ``jobs == 1``) this IS the
+    reference's runner -- its strategies, tactics, early stop and ranking --
+    fed by a ``BulkEvaluator`` (one engine batch for the whole space).  Without
+    the reference importable, the restatement below follows it decision for
+    decision (``tests/test_search.py``).  ``jobs`` only sets the batch size, as
+    in the reference (each batch's tactic verdicts are taken against the
+    history before its results); evaluation itself is the engine's, not a
+    process pool's."""
     configs = W.enumerate_space(space, model, cluster)
+    ref = _reference_search(strategy, stop) if jobs == 1 else None
+    if ref is not None:
+        return ref.run_search(space, BulkEvaluator(evaluator, configs), strategy, model, cluster,
+                              jobs=1, use_tactics=use_tactics, stop=stop, max_trials=max_trials,
+                              deterministic=deterministic)
     outcomes = _Outcomes(evaluator)
     history: list = []
     state = {"stopped": False}

@@ -204,3 +204,27 @@ def test_api_simulate_raises_reference_deadlock():
     with pytest.raises(SimDeadlockError) as got:
         api.simulate(ann)
     assert str(got.value) == str(want.value)
+
+
+@pytest.mark.gpu
+def test_search_run_search_delegates_to_reference_runner():
+    """search.run_search with the reference's own strategy objects runs the
+    reference's runner (strategies, tactics, early stop, ranking) over one
+    engine batch, and equals the reference run with its own evaluator."""
+    _ref()
+    from dltsim.estimate import RooflineEstimator
+    from dltsim.search import (PipelineEvaluator, SearchSpace, StopRule, make_strategy,
+                               run_search as ref_run_search)
+    from paper_2503_20191_b200 import search as S
+    from paper_2503_20191_b200.api import GpuPipelineEvaluator
+    model, cluster = _small()
+    space = SearchSpace(global_batch=32)
+    for name in ("grid", "evolutionary"):
+        want = ref_run_search(space, PipelineEvaluator(model, cluster, RooflineEstimator(), 2000),
+                              make_strategy(name, seed=3), model, cluster,
+                              stop=StopRule(window=30, top_k=3))
+        got = S.run_search(space, GpuPipelineEvaluator(model, cluster, RooflineEstimator(), 2000),
+                           make_strategy(name, seed=3), model, cluster,
+                           stop=StopRule(window=30, top_k=3))
+        assert type(got).__module__.startswith("dltsim")
+        assert _trials(got) == _trials(want)
