@@ -141,6 +141,9 @@ int maya_batch_num_jobs(maya_engine *eng);
 #define MAYA_OPT_NO_BLOCKS 16 /* generated jobs: one op per kernel launch instead of interned
                                  kernel blocks (runs of launches of one stream, folded on the
                                  device); required to record a timeline of generated jobs */
+#define MAYA_OPT_NO_CHAIN 32  /* never use the chain kernel (latency-bound jobs resident in one
+                                 warp's shared memory); default: every job that fits it, unless
+                                 MAYA_OPT_WARP_SCHED / MAYA_OPT_LANE_SCHED force a kernel */
 int maya_set_options(maya_engine *eng, int32_t options);
 /* Per staged job: 1 if it is simulated as rank classes. */
 int maya_batch_collapsed(maya_engine *eng, uint8_t *out);

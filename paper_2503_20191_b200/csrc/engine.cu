@@ -89,7 +89,10 @@ struct maya_engine {
   // scheduler launch groups: 0-2 warp-window kernel (4/8/16 warps), 3-10 lane
   // kernel warp jobs (by shared-memory region class), 11-14 lane kernel CTA
   // jobs (2/4/8/16 warps); each group runs on its own stream (fork/join)
-  static const int NVAR = 16;   // 15: grid jobs (cooperative launch over their parts)
+  // 15: grid jobs (cooperative launch over their parts); 16..: chain kernel
+  // jobs by shared-memory region class (CHAIN_REGION), one-warp CTAs then
+  // two-warp CTAs
+  static const int NVAR = 16 + 2 * (int)CHAIN_CLASSES;
   cudaStream_t vstream[NVAR] = {};
   cudaEvent_t vev[NVAR + 1] = {};
   uint32_t var_n[NVAR] = {};        // jobs per group (order segments)
@@ -121,7 +124,7 @@ struct maya_engine {
   // segments
   Seg s_fmeta;
   Seg s_jobs, s_ranks, s_rank_comm, s_comms, s_wfeats, s_walkers, s_reps, s_ops, s_streams,
-      s_coll_lc, s_coll_idx, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
+      s_coll_lc, s_coll_idx, s_coll_wf, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
       s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks, s_grid_parts, s_comm_part, s_blocks,
       s_blk_fids;
   Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst, x_gsync;
@@ -247,6 +250,34 @@ bool plan_grid(const JobPack &P, LanePlan &pl) {
   return true;
 }
 
+// Chain-kernel plan (sched_chain.cu): the whole job resident in one warp's
+// shared-memory region -- every FIFO's folded ops, record times, collective
+// rings and rank collective table -- with at most two FIFOs per lane.  Only
+// for jobs whose collectives rendezvous in rings (JOB_RING).  n_slots carries
+// the job's folded op count (the region's op area).
+LanePlan plan_chain(const JobPack &P) {
+  LanePlan pl;
+  const uint32_t W = (uint32_t)P.walkers.size(), R = (uint32_t)P.ranks.size();
+  const uint32_t nc = (uint32_t)P.comms.size();
+  if (P.hdr.status != MAYA_ST_OK || W == 0 || W > CHAIN_MAX_FIFOS) return pl;
+  if (!(P.hdr.flags & JOB_RING) || nc > RING_MAX_COMMS) return pl;
+  uint64_t n_ops = 0;
+  for (uint32_t w = 0; w < W; w++) {
+    const Walker wk = P.walkers[w];
+    n_ops += P.streams[P.reps[P.ranks[wk.rank].rep].streams + wk.stream].folded;
+  }
+  const ChainLayout L = chain_layout(W, R, nc, P.hdr.n_fire, P.hdr.n_rcolls, n_ops);
+  if (L.bytes > CHAIN_REGION[CHAIN_CLASSES - 1]) return pl;
+  uint32_t c = 0;
+  while (CHAIN_REGION[c] < L.bytes) c++;
+  pl.threads = W <= 32 ? 32 : 64;
+  pl.variant = 16 + (int)c + (pl.threads == 64 ? (int)CHAIN_CLASSES : 0);
+  pl.smem = L.bytes;
+  pl.n_slots = (uint32_t)n_ops;
+  pl.per_lane = 1;
+  return pl;
+}
+
 LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
   LanePlan pl;
   if (P.hdr.status != MAYA_ST_OK) { pl.variant = 3; return pl; }
@@ -343,7 +374,7 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
       const LaneLayout L =
           lane_layout(W, R, nc, fl, (uint32_t)slots, P.hdr.n_fire, P.hdr.n_rcolls, fc);
       if (L.bytes > cap) continue;
-      pl.flags = fl;
+      pl.flags = fl | (getenv("MAYA_LANE_CHASE") ? LANE_CHASE : 0u);
       pl.n_slots = (uint32_t)slots;
       pl.smem = L.bytes;
       pl.lgd_max = t.lgd;
@@ -411,7 +442,7 @@ bool vec_eq(const std::vector<T> &a, const std::vector<T> &b) {
 bool pack_eq(const JobPack &a, const JobPack &b) {
   return memcmp(&a.hdr, &b.hdr, sizeof(JobHdr)) == 0 && vec_eq(a.reps, b.reps) &&
          vec_eq(a.ops, b.ops) && vec_eq(a.op_seq, b.op_seq) && vec_eq(a.streams, b.streams) &&
-         vec_eq(a.coll_lc, b.coll_lc) && vec_eq(a.coll_idx, b.coll_idx) &&
+         vec_eq(a.coll_lc, b.coll_lc) && vec_eq(a.coll_idx, b.coll_idx) && vec_eq(a.coll_wf, b.coll_wf) &&
          vec_eq(a.syncs, b.syncs) && vec_eq(a.counts, b.counts) && vec_eq(a.mems, b.mems) &&
          vec_eq(a.feats, b.feats) && vec_eq(a.feat_meta, b.feat_meta) && vec_eq(a.comms, b.comms) && vec_eq(a.slots, b.slots) &&
          vec_eq(a.ranks, b.ranks) && vec_eq(a.rank_comm, b.rank_comm) &&
@@ -594,11 +625,21 @@ int maya_upload(maya_engine *e) {
     if (budget < LANE_REGION[0]) budget = LANE_REGION[0];
     if (budget > LANE_SMEM_CAP) budget = LANE_SMEM_CAP;
     for (size_t j = 0; j < nj; j++) {
-      if (!(e->options & MAYA_OPT_WARP_SCHED))
+      const bool forced = (e->options & (MAYA_OPT_WARP_SCHED | MAYA_OPT_LANE_SCHED)) != 0;
+      if (!forced && !(e->options & MAYA_OPT_NO_CHAIN)) plans[j] = plan_chain(e->packs[j]);
+      if (plans[j].variant < 0 && !(e->options & MAYA_OPT_WARP_SCHED))
         plans[j] = plan_lane(e->packs[j], (uint32_t)budget, (e->options & MAYA_OPT_LANE_SCHED) != 0);
       if (plans[j].variant >= 0 && plans[j].variant != 15)
         n_perm += (size_t)plans[j].per_lane * plans[j].threads;
     }
+    if (getenv("MAYA_DEBUG_PLAN"))
+      for (size_t j = 0; j < nj; j++) {
+        const JobPack &P = e->packs[j];
+        fprintf(stderr, "plan job %zu: variant %d smem %u per_lane %u W %zu R %zu comms %zu ring %d rcolls %u fire %u\n",
+                j, plans[j].variant, plans[j].smem, plans[j].per_lane, P.walkers.size(),
+                P.ranks.size(), P.comms.size(), (P.hdr.flags & JOB_RING) ? 1 : 0, P.hdr.n_rcolls,
+                P.hdr.n_fire);
+      }
     // a grid job runs only if all its parts are co-resident under the batch's
     // grid launch shape (the largest part layout); otherwise it is scheduled
     // by the warp-window kernel (2,048-rank full-rank jobs with many streams)
@@ -643,6 +684,7 @@ int maya_upload(maya_engine *e) {
   seg(e->s_streams, n_streams * sizeof(StreamRange));
   seg(e->s_coll_lc, n_colls * sizeof(uint32_t));
   seg(e->s_coll_idx, n_colls * sizeof(uint32_t));
+  seg(e->s_coll_wf, n_colls * sizeof(uint32_t));
   seg(e->s_syncs, n_syncs * sizeof(SyncRec));
   seg(e->s_counts, n_counts * sizeof(uint32_t));
   seg(e->s_mems, n_mems * sizeof(MemRec));
@@ -938,6 +980,11 @@ int maya_upload(maya_engine *e) {
         }
         const Walker wk = P.walkers[w];
         const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
+        if (pl.variant >= 16) {   // chain job: the FIFO's first op in the region's op area
+          ws[w] = slot;
+          slot += P.streams[h.streams + wk.stream].folded;
+          continue;
+        }
         const uint32_t n = pl.variant >= 3 ? lane_slots_of(P.streams[h.streams + wk.stream].folded,
                                                            lgd_max)
                                            : 0;
@@ -980,6 +1027,11 @@ int maya_upload(maya_engine *e) {
     CPY(s_streams, streams, B.streams)
     CPY(s_coll_lc, coll_lc, B.colls)
     CPY(s_coll_idx, coll_idx, B.colls)
+    {  // foldable collectives: batch-global wire feature
+      uint32_t *dst = (uint32_t *)(H + e->s_coll_wf.off) + B.colls;
+      for (size_t q = 0; q < P.coll_wf.size(); q++)
+        dst[q] = P.coll_wf[q] == NO_WF ? NO_WF : (uint32_t)(B.wfeats + P.coll_wf[q]);
+    }
     CPY(s_syncs, syncs, B.syncs)
     CPY(s_counts, counts, B.counts)
     CPY(s_mems, mems, B.mems)
@@ -1026,6 +1078,7 @@ int maya_upload(maya_engine *e) {
   db.streams = (const StreamRange *)(D + e->s_streams.off);
   db.coll_lc = (const uint32_t *)(D + e->s_coll_lc.off);
   db.coll_idx = (const uint32_t *)(D + e->s_coll_idx.off);
+  db.coll_wf = (const uint32_t *)(D + e->s_coll_wf.off);
   db.syncs = (const SyncRec *)(D + e->s_syncs.off);
   db.counts = (const uint32_t *)(D + e->s_counts.off);
   db.mems = (const MemRec *)(D + e->s_mems.off);
@@ -1193,6 +1246,10 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
           CU(cudaEventRecord(e->sev[v], e->sstream[v]));
           CU(cudaStreamWaitEvent(e->stream, e->sev[v], 0));
         }
+      } else if (v >= 16) {
+        launch_schedule_chain(db, db.order + off, e->var_n[v],
+                              v >= 16 + (int)CHAIN_CLASSES ? 64u : 32u, record_timeline ? 1 : 0,
+                              e->var_smem[v], e->vstream[v]);
       } else if (v <= 10) {
         const uint32_t region = e->var_smem[v];
         uint32_t wpc = region ? LANE_SMEM_CAP / region : 8;
@@ -1298,6 +1355,7 @@ int maya_results(maya_engine *e, maya_job_result *out) {
 int maya_prof_read(unsigned long long *out16, int reset) {
   const int a = prof_read(out16, reset);
   lane_prof_read(out16 + 8, reset);
+  if (getenv("MAYA_PROF_CHAIN")) chain_prof_read(out16 + 8, reset);   // chain counters instead
   return a;
 }
 

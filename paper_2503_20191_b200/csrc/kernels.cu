@@ -1155,8 +1155,12 @@ __device__ __forceinline__ int64_t sat_add(int64_t x, int64_t y) {   // x, y in 
 // Both passes give each lane 32 consecutive ops of the 1,024-op chunk and walk
 // them sequentially (a few instructions per op, not a warp scan per 32 ops);
 // the warp combines the 32 lane results once per chunk.
-__device__ __forceinline__ bool op_foldable(const Op &o) {
-  return op_tag(o.meta) == TAG_KERN && o.disp < ((int64_t)1 << 61);
+// Collectives enter runs too when their rep's coll_wf entry names a wire
+// feature (pack.cpp: every simulated rank meets them alone): done = ready + wire
+// is the kernel map with d = wire.  cw: the rep's coll_wf entries.
+__device__ __forceinline__ bool op_foldable(const Op &o, const uint32_t *cw) {
+  const uint32_t tg = op_tag(o.meta);
+  return o.disp < ((int64_t)1 << 61) && (tg == TAG_KERN || (tg == TAG_COLL && cw[o.arg] != NO_WF));
 }
 
 // Kernel blocks (soa.h KBLOCK): the composite of a block's n kernels, kernel k
@@ -1241,6 +1245,7 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) fold_count_kernel(DevBatch b)
   const RepHdr &h = b.reps[fc.rep];
   const StreamRange sr = b.streams[h.streams + fc.st];
   const Op *in = b.ops + h.ops + sr.begin;
+  const uint32_t *cw = b.coll_wf + h.colls;
   const uint32_t lo = fc.chunk * FOLD_CHUNK, hi = min(sr.len, lo + FOLD_CHUNK);
   fold_stage(in, lo, hi, sm, lane);
   const uint32_t k0 = lo + lane * 32u, k1 = min(hi, k0 + 32u);
@@ -1251,11 +1256,11 @@ __global__ void __launch_bounds__(FOLD_WARPS * 32) fold_count_kernel(DevBatch b)
     if (k0 > lo) {
       const Op &p = fold_at(sm, k0 - 1 - lo);
       pseg = op_seg(p.meta);
-      pfold = op_foldable(p);
+      pfold = op_foldable(p, cw);
     }
     for (uint32_t i = k0; i < k1; i++) {
       const Op &o = fold_at(sm, i - lo);
-      const bool f = op_foldable(o);
+      const bool f = op_foldable(o, cw);
       const uint32_t sg = op_seg(o.meta);
       cnt += (i == lo || !f || !pfold || sg != pseg) ? 1u : 0u;
       pseg = sg;
@@ -1282,6 +1287,7 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
   const uint32_t ns = h.n_streams, nsync = h.n_syncs;
   const StreamRange sr = b.streams[h.streams + fc.st];
   const Op *in = b.ops + h.ops + sr.begin;
+  const uint32_t *cw = b.coll_wf + h.colls;
   ExecOp *out = b.exec + h.ops + sr.begin;
   uint32_t *cc = b.ccounts + h.counts + fc.st;
   const uint32_t n = sr.len;
@@ -1304,10 +1310,13 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
       v[t] = j0 + t < hi;
       o[t] = v[t] ? in[j0 + t] : Op{0, 0, 0};
       sg[t] = op_seg(o[t].meta);
-      f[t] = v[t] && op_foldable(o[t]);
+      f[t] = v[t] && op_foldable(o[t], cw);
       d[t] = 0;
       bx[t] = -1;
-      if (v[t] && op_tag(o[t].meta) == TAG_KERN) {
+      if (f[t] && op_tag(o[t].meta) == TAG_COLL) {
+        d[t] = b.wire[cw[o[t].arg]];   // < 0: failed estimate, saturates (host sets ESTIMATION)
+        if (d[t] < 0) d[t] = FOLD_SAT;
+      } else if (v[t] && op_tag(o[t].meta) == TAG_KERN) {
         if (BLOCKS && (o[t].arg & KBLOCK)) {
           const longlong2 ab =
               *reinterpret_cast<const longlong2 *>(b.blk_ab + 2 * (size_t)(o[t].arg & ~KBLOCK));
@@ -1444,7 +1453,7 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
     bool next_start = true;
     if (more) {
       const Op on = in[base + 128];
-      next_start = !op_foldable(on) || !lfold || op_seg(on.meta) != lseg;
+      next_start = !op_foldable(on, cw) || !lfold || op_seg(on.meta) != lseg;
     }
     if (lfold && lane == 0) {
       if (!more || next_start) {

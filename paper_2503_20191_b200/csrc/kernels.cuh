@@ -28,6 +28,7 @@ struct DevBatch {
   const StreamRange *streams;
   const uint32_t *coll_lc;
   const uint32_t *coll_idx;
+  const uint32_t *coll_wf;    // per rep collective: batch-global wire feature if it folds (NO_WF)
   const SyncRec *syncs;
   const uint32_t *counts;
   const MemRec *mems;
@@ -106,9 +107,13 @@ void launch_schedule_lane(const DevBatch &b, const int32_t *order, uint32_t n, u
 // grid jobs: parts [p0, p1) of b.grid_parts in one cooperative launch
 int launch_schedule_grid(const DevBatch &b, uint32_t p0, uint32_t p1, int record, uint32_t smem,
                          cudaStream_t s);
+// chain jobs (sched_chain.cu): one warp-sized CTA per job, whole job on chip
+void launch_schedule_chain(const DevBatch &b, const int32_t *order, uint32_t n, uint32_t threads,
+                           int record, uint32_t smem, cudaStream_t s);
 int grid_max_ctas(uint32_t smem);   // co-resident CTAs of the grid kernel at this smem
 int prof_read(unsigned long long *out8, int reset);   // MAYA_PROFILE builds only
 int lane_prof_read(unsigned long long *out8, int reset);
+int chain_prof_read(unsigned long long *out8, int reset);
 void launch_topk(const DevBatch &b, int k, maya_topk_entry *out, int32_t *n_out, void *scratch,
                  cudaStream_t s);
 size_t topk_scratch_bytes(uint32_t n_jobs, int k);

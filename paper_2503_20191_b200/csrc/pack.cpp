@@ -127,6 +127,26 @@ struct FeatState {
   }
 };
 
+// Ops of a FIFO after the device folds its affine runs (kernels.cu
+// fold_count_kernel: the same rule): kernels, and collectives whose coll_wf
+// entry names a wire feature, whose gap prefix is below 2^61, join the run of
+// the op before them within one host-sync segment; runs are cut every
+// FOLD_CHUNK ops.  coll_wf: the rep's per-collective entries (null: none).
+uint32_t folded_len(const Op *v, uint32_t n, const uint32_t *coll_wf) {
+  uint32_t folded = 0, ps = 0;
+  bool pf = false;
+  for (uint32_t i = 0; i < n; i++) {
+    const uint32_t tg = op_tag(v[i].meta);
+    const bool f = v[i].disp < ((int64_t)1 << 61) &&
+                   (tg == TAG_KERN || (tg == TAG_COLL && coll_wf && coll_wf[v[i].arg] != NO_WF));
+    const uint32_t sg = op_seg(v[i].meta);
+    folded += (i % FOLD_CHUNK == 0 || !f || !pf || sg != ps) ? 1u : 0u;
+    pf = f;
+    ps = sg;
+  }
+  return folded;
+}
+
 // Per-event half of the packer for ONE representative trace, in trace order.
 // pack_job drives it from raw event arrays (ordinals precomputed by a first
 // pass, so a wait may precede its record); the fused generator drives it
@@ -469,19 +489,7 @@ struct RepPacker {
     for (size_t s = 0; s < RB.size(); s++) {
       // ops the scheduler sees after the device folds kernel runs (kernels.cu
       // fold_count_kernel: same rule), for sizing its staging rings
-      uint32_t folded = 0;
-      {
-        bool pf = false;
-        uint32_t ps = 0;
-        const auto &v = RB.sops[s];
-        for (size_t i = 0; i < v.size(); i++) {
-          const bool f = op_tag(v[i].meta) == TAG_KERN && v[i].disp < ((int64_t)1 << 61);
-          const uint32_t sg = op_seg(v[i].meta);
-          folded += (i % FOLD_CHUNK == 0 || !f || !pf || sg != ps) ? 1u : 0u;
-          pf = f;
-          ps = sg;
-        }
-      }
+      const uint32_t folded = folded_len(RB.sops[s].data(), (uint32_t)RB.sops[s].size(), nullptr);
       P->streams.push_back(StreamRange{pos, (uint32_t)RB.sops[s].size(), RB.raw_of[s], folded});
       P->stream_events.push_back(RB.sev[s]);
       P->ops.insert(P->ops.end(), RB.sops[s].begin(), RB.sops[s].end());
@@ -894,6 +902,41 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
       P.rcolls.push_back(((uint64_t)nr << 48) | ((uint64_t)g << 32) | idx);
     }
     if (P.rcolls.size() > 0xffffffffull) throw Fail{MAYA_ST_BAD_INPUT, "too many collectives"};
+  }
+  // Collectives every simulated rank of a rep meets alone (the communicator is
+  // one member class: done = ready + wire, no rendezvous, sim.py:326-343 with
+  // one arrival) and with the same wire feature are affine maps of the stream
+  // clock, exactly like kernels: the fold pass composes them into kernel runs
+  // (kernels.cu fold_*), so a tensor-parallel layer body of a collapsed job is
+  // one op.  Folded FIFO lengths (ring sizing) follow the same rule.
+  {
+    P.coll_wf.assign(P.coll_lc.size(), NO_WF);
+    std::vector<uint8_t> seen(P.reps.size(), 0);
+    for (size_t sr = 0; sr < P.ranks.size(); sr++) {
+      const RankRec &rr = P.ranks[sr];
+      const RepHdr &h = P.reps[rr.rep];
+      for (uint32_t c2 = 0; c2 < h.n_colls; c2++) {
+        const RankColl ent = P.rcolls[rr.rslot + c2];
+        const uint32_t g = (uint32_t)(ent >> 32) & 0xffffu, idx = (uint32_t)ent;
+        const uint32_t wf = (ent >> 48) == 1 ? P.slot_wf[P.comms[g].call_base + idx] : NO_WF - 1;
+        uint32_t &cw = P.coll_wf[h.colls + c2];
+        if (!seen[rr.rep]) cw = wf;
+        else if (cw != wf) cw = NO_WF - 1;
+      }
+      seen[rr.rep] = 1;
+    }
+    bool any = false;
+    for (uint32_t &cw : P.coll_wf) {
+      if (cw == NO_WF - 1) cw = NO_WF;
+      any |= cw != NO_WF;
+    }
+    if (any)
+      for (const RepHdr &h : P.reps)
+        for (uint32_t s = 0; s < h.n_streams; s++) {
+          StreamRange &st = P.streams[h.streams + s];
+          st.folded = folded_len(P.ops.data() + h.ops + st.begin, st.len,
+                                 P.coll_wf.data() + h.colls);
+        }
   }
   // walkers rank-major: a scheduler warp owns whole ranks
   P.wids.resize(P.walkers.size());

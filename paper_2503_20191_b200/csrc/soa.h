@@ -31,6 +31,7 @@ enum OpTag : uint32_t { TAG_KERN = 0, TAG_COLL = 1, TAG_REC = 2, TAG_WAIT = 3 };
 enum SyncType : uint32_t { SYNC_ESYNC = 0, SYNC_SSYNC = 1, SYNC_DSYNC = 2 };
 
 static const uint32_t NO_REC = 0xFFFFFFFFu;
+static const uint32_t NO_WF = 0xFFFFFFFFu;   // coll_wf: the collective does not fold
 // Op.arg flag of a KERN op that stands for a kernel BLOCK: n consecutive
 // kernel launches of one stream, each after a host gap of `gap` ns, with no
 // other event in between (the generator's layer bodies).  Blocks are interned
@@ -119,6 +120,7 @@ enum LaneFlags : uint32_t {
   LANE_RCX_SMEM = 4,    // per-rank collective table in shared memory
   LANE_CTX_SMEM = 8,    // FIFO contexts in shared memory (lanes own several FIFOs)
   LANE_ST_GLOBAL = 16,  // FIFO states in global memory (jobs with thousands of FIFOs)
+  LANE_CHASE = 32,      // a lane retires every ready op of its FIFO per step (latency-bound jobs)
 };
 struct LaneJob {
   uint32_t flags;       // LaneFlags
@@ -146,6 +148,46 @@ struct GridSync {
   unsigned long long tmax;
   long long peak, oom_t;
 };
+
+// ---- chain scheduler (sched_chain.cu) ---------------------------------------
+// Latency-bound jobs (few FIFOs, frequent hand-offs: pipeline stages) run with
+// one warp per job and EVERYTHING resident in shared memory: the folded op
+// stream of every FIFO, record times, collective rings and the rank
+// collective table.  Per-walker word (lane_wslot): the FIFO's first op in the
+// region's op area.  Region classes by footprint.
+static const uint32_t CHAIN_MAX_FIFOS = 64;   // one FIFO per thread, 1 or 2 warps
+static const uint32_t CHAIN_CLASSES = 10;
+static const uint32_t CHAIN_REGION[CHAIN_CLASSES] = {8u << 10,  12u << 10, 16u << 10, 24u << 10,
+                                                     32u << 10, 48u << 10, 64u << 10, 96u << 10,
+                                                     144u << 10, 220u << 10};
+struct ChainLayout {
+  uint32_t bar, ring, hostk, fst_i, fst_x, fire, rcx, ops, bytes;
+};
+__host__ __device__ inline ChainLayout chain_layout(uint32_t W, uint32_t R, uint32_t n_comms,
+                                                    uint32_t n_fire, uint32_t n_rcolls,
+                                                    uint64_t n_ops) {
+  ChainLayout L{};
+  uint64_t off = 0;
+  L.bar = 0;
+  off = 16;
+  L.ring = (uint32_t)off;
+  off += 32ull * n_comms;                 // 2 CollSlot per communicator
+  L.hostk = (uint32_t)off;
+  off = (off + 4ull * R + 15) & ~15ull;
+  L.fst_i = (uint32_t)off;
+  off = (off + 4ull * W + 15) & ~15ull;
+  L.fst_x = (uint32_t)off;
+  off += 8ull * W;
+  off = (off + 15) & ~15ull;
+  L.fire = (uint32_t)off;
+  off = (off + 8ull * n_fire + 15) & ~15ull;
+  L.rcx = (uint32_t)off;
+  off += 16ull * n_rcolls;
+  L.ops = (uint32_t)off;
+  off += 16ull * n_ops;
+  L.bytes = off > 0xffffffffull ? 0xffffffffu : (uint32_t)off;
+  return L;
+}
 
 // per-walker ring word: first slot (job-local, 28 bits) | log2(slots) << 28
 // (0xF << 28: the FIFO reads global memory directly)

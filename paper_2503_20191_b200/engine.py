@@ -36,6 +36,9 @@ EXPORTED = (
 )
 
 
+SCHEDS = ("auto", "nochain", "lane", "warp")
+
+
 class EngineError(RuntimeError):
     pass
 
@@ -109,8 +112,8 @@ class Engine:
         L = lib()
         self._h = C.c_void_p()
         _check(L.maya_open(int(device), C.byref(self._h)))
-        if sched not in ("auto", "lane", "warp"):
-            raise ValueError(f"sched must be 'auto', 'lane' or 'warp', not {sched!r}")
+        if sched not in SCHEDS:
+            raise ValueError(f"sched must be one of {SCHEDS}, not {sched!r}")
         self._collapse = bool(collapse)
         self._sched = sched
         self._fold = bool(fold)
@@ -126,10 +129,12 @@ class Engine:
         self._apply_options()
 
     def set_sched(self, sched: str) -> None:
-        """Scheduler kernel: 'auto' (per job, default), 'lane' (lane-parallel
+        """Scheduler kernel: 'auto' (per job, default: the chain kernel where the
+        job fits it, else lane-parallel or warp-window by the shape of its
+        FIFOs), 'nochain' (auto without the chain kernel), 'lane' (lane-parallel
         wherever it fits) or 'warp' (warp-window for every job)."""
-        if sched not in ("auto", "lane", "warp"):
-            raise ValueError(f"sched must be 'auto', 'lane' or 'warp', not {sched!r}")
+        if sched not in SCHEDS:
+            raise ValueError(f"sched must be one of {SCHEDS}, not {sched!r}")
         self._sched = sched
         self._apply_options()
 
@@ -143,7 +148,8 @@ class Engine:
     def _apply_options(self) -> None:
         opts = ((1 if self._collapse else 0) | (2 if self._sched == "warp" else 0)
                 | (4 if self._sched == "lane" else 0) | (0 if self._fold else 8)
-                | (16 if not (self._blocks and self._fold) else 0))
+                | (16 if not (self._blocks and self._fold) else 0)
+                | (32 if self._sched == "nochain" else 0))
         _check(lib().maya_set_options(self._h, opts))
 
     def collapsed(self) -> np.ndarray:

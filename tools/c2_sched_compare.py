@@ -15,7 +15,7 @@ cluster = W.ClusterSpec(1, 8, 80 * 2 ** 30, W.load_device_preset("fast"))
 cfgs = W.enumerate_space(W.SearchSpace(global_batch=512), model, cluster)[:512]
 out = {}
 ref = None
-for sched in ("auto", "lane", "warp"):
+for sched in ("auto", "nochain", "lane", "warp"):
     eng = Engine(0, collapse=True, sched=sched)
     eng.stage_generated(model, cfgs, cluster, dispatch_overhead_ns=5000, threads=16)
     eng.upload()
