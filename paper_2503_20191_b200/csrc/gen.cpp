@@ -351,19 +351,64 @@ struct Builder {
   std::vector<std::vector<std::pair<int8_t, int64_t>>> calls;  // per local comm
   std::vector<int64_t> next_version, last_version;   // by event id (small)
   int64_t next_alloc = 0;
-  // kernel blocks (sinks that take them): the open run of kernel launches
+  // kernel blocks (sinks that take them): the open run of kernel launches, as
+  // segments of the trace's kernel lists (run-length coded).  A run whose
+  // segments repeat an earlier run of this trace (a layer body of the next
+  // microbatch) is emitted by its block id, without building or hashing its
+  // launch list; the packer interns the list itself the first time.
   bool blocks = false;
   int32_t run_stream = 0;
-  std::vector<KSpec> run;
+  struct Seg {
+    const KSpec *p;
+    uint32_t n, rep;
+    bool operator==(const Seg &o) const { return p == o.p && n == o.n && rep == o.rep; }
+  };
+  std::vector<Seg> rsegs;
+  size_t run_n = 0;
+  bool run_owned = false;          // a segment points at a temporary: never memoised
+  std::vector<KSpec> run;          // materialised launch list (first occurrence)
+  std::vector<KSpec> singles;      // copies of single launches passed by value
+  struct Memo {
+    uint64_t h;
+    uint32_t seg0, nseg, id;
+  };
+  std::vector<Memo> memo;
+  std::vector<Seg> memo_segs;
 
   void flush() {
-    if (run.empty()) return;
-    sink->kernel_block(run_stream, run.data(), run.size(), overhead > 0 ? overhead : 0, dtype);
+    if (rsegs.empty()) return;
+    const int64_t gap = overhead > 0 ? overhead : 0;
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    for (const Seg &g : rsegs)
+      h = (h ^ ((uint64_t)(uintptr_t)g.p + ((uint64_t)g.n << 40) + ((uint64_t)g.rep << 52))) *
+          0xff51afd7ed558ccdull;
+    if (!run_owned)
+      for (const Memo &m : memo)
+        if (m.h == h && m.nseg == rsegs.size() &&
+            std::equal(rsegs.begin(), rsegs.end(), memo_segs.begin() + m.seg0)) {
+          if (sink->kernel_block_id(run_stream, m.id, run_n, gap)) {
+            rsegs.clear();
+            run_n = 0;
+            return;
+          }
+          break;
+        }
     run.clear();
+    for (const Seg &g : rsegs)
+      for (uint32_t r = 0; r < g.rep; r++) run.insert(run.end(), g.p, g.p + g.n);
+    const uint32_t id = sink->kernel_block(run_stream, run.data(), run.size(), gap, dtype);
+    if (id != ~0u && !run_owned) {
+      memo.push_back(Memo{h, (uint32_t)memo_segs.size(), (uint32_t)rsegs.size(), id});
+      memo_segs.insert(memo_segs.end(), rsegs.begin(), rsegs.end());
+    }
+    rsegs.clear();
+    run_n = 0;
+    run_owned = false;
+    singles.clear();
   }
   void ev(uint8_t k, int32_t s, int64_t a, int64_t b = 0, int64_t c = 0, int64_t d = 0) {
     if (sink) {
-      if (!run.empty()) flush();
+      if (!rsegs.empty()) flush();
       sink->ev(k, s, a, b, c, d);
       return;
     }
@@ -380,25 +425,35 @@ struct Builder {
   void gap() {
     if (overhead > 0) ev(MAYA_EV_HOSTGAP, 0, overhead);
   }
-  void kernel(int32_t s, const KSpec &k) {
-    if (blocks) {   // [HostGap, KernelLaunch] joins the open run of stream s
-      if (!run.empty() && run_stream != s) flush();
-      run_stream = s;
-      run.push_back(k);
+  // a launch of a kernel list that lives for the whole trace
+  void kernel(int32_t s, const KSpec &k) { kernels(s, &k, 1); }
+  // a launch passed by value (a temporary): copied, its run never memoised
+  void kernel_tmp(int32_t s, const KSpec &k) {
+    if (blocks) {
+      if (!rsegs.empty() && run_stream != s) flush();
+      singles.reserve(16);
+      if (singles.size() == singles.capacity()) flush();   // keep earlier segment pointers valid
+      singles.push_back(k);
+      run_owned = true;
+      kernels(s, &singles.back(), 1);
       return;
     }
-    gap();
-    ev(MAYA_EV_KERNEL, s, k.op, dtype, k.flops, k.bytes);
+    kernels(s, &k, 1);
   }
-  // n consecutive launches on stream s (one append to the open run in block mode)
+  // n consecutive launches on stream s (one segment of the open run in block mode)
   void kernels(int32_t s, const KSpec *k, size_t n) {
     if (blocks) {
-      if (!run.empty() && run_stream != s) flush();
+      if (!rsegs.empty() && run_stream != s) flush();
       run_stream = s;
-      run.insert(run.end(), k, k + n);
+      if (!rsegs.empty() && rsegs.back().p == k && rsegs.back().n == n) rsegs.back().rep++;
+      else rsegs.push_back(Seg{k, (uint32_t)n, 1});
+      run_n += n;
       return;
     }
-    for (size_t i = 0; i < n; i++) kernel(s, k[i]);
+    for (size_t i = 0; i < n; i++) {
+      gap();
+      ev(MAYA_EV_KERNEL, s, k[i].op, dtype, k[i].flops, k[i].bytes);
+    }
   }
   void memcpy_h2d(int32_t s, int64_t n) {
     gap();
@@ -634,7 +689,7 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
     B.record(STREAM_GRAD_COMM, eid[{E_DP_DONE, -1}]);
     B.wait_last(STREAM_COMPUTE, eid[{E_DP_DONE, -1}]);
   }
-  B.kernel(STREAM_COMPUTE, KSpec{OK_OPTIMIZER, chk((i128)6 * params), chk((i128)16 * params)});
+  B.kernel_tmp(STREAM_COMPUTE, KSpec{OK_OPTIMIZER, chk((i128)6 * params), chk((i128)16 * params)});
   if (d > 1 && cfg.dist_optimizer) {
     const int dp_lc = lc_of(C_DP, i, stage, 0);
     B.record(STREAM_COMPUTE, eid[{E_OPT_DONE, -1}]);

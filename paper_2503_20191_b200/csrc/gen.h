@@ -60,7 +60,13 @@ struct EventSink {
   // launches on one stream (with nothing else in between) as ONE call: the
   // events [HostGap(gap) if gap > 0, KernelLaunch(ks[i], dtype)] for i < n.
   virtual bool takes_blocks() const { return false; }
-  virtual void kernel_block(int32_t, const KSpec *, size_t, int64_t, int32_t) {}
+  // Returns the block's id (interned per job), or ~0u if the run went through
+  // the per-event path.
+  virtual uint32_t kernel_block(int32_t, const KSpec *, size_t, int64_t, int32_t) { return ~0u; }
+  // The same run again (its launch list interned as `id` by an earlier
+  // kernel_block of this trace): emit it by id.  False: not possible here (the
+  // caller then sends the launch list).
+  virtual bool kernel_block_id(int32_t, uint32_t, size_t, int64_t) { return false; }
 };
 
 // Returns 0 or a negative code with *err set (invalid configuration).  With a

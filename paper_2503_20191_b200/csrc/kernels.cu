@@ -1155,12 +1155,11 @@ __device__ __forceinline__ int64_t sat_add(int64_t x, int64_t y) {   // x, y in 
 // Both passes give each lane 32 consecutive ops of the 1,024-op chunk and walk
 // them sequentially (a few instructions per op, not a warp scan per 32 ops);
 // the warp combines the 32 lane results once per chunk.
-// Collectives enter runs too when their rep's coll_wf entry names a wire
-// feature (pack.cpp: every simulated rank meets them alone): done = ready + wire
-// is the kernel map with d = wire.  cw: the rep's coll_wf entries.
-__device__ __forceinline__ bool op_foldable(const Op &o, const uint32_t *cw) {
-  const uint32_t tg = op_tag(o.meta);
-  return o.disp < ((int64_t)1 << 61) && (tg == TAG_KERN || (tg == TAG_COLL && cw[o.arg] != NO_WF));
+// Collectives enter runs too when the packer marked them OP_FOLDC (their rep's
+// coll_wf entry names a wire feature: every simulated rank meets them alone):
+// done = ready + wire is the kernel map with d = wire.
+__device__ __forceinline__ bool op_foldable(const Op &o, const uint32_t *) {
+  return o.disp < ((int64_t)1 << 61) && (op_tag(o.meta) == TAG_KERN || (o.meta & OP_FOLDC));
 }
 
 // Kernel blocks (soa.h KBLOCK): the composite of a block's n kernels, kernel k

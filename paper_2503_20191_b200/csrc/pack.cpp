@@ -249,7 +249,7 @@ struct RepPacker {
 
   void emit(int32_t stream, uint32_t tag, uint32_t arg) {
     int ls = RB.local_stream(stream, true);
-    if (seg >= (1u << 30)) throw Fail{MAYA_ST_BAD_INPUT, "too many host syncs"};
+    if (seg >= (1u << 29)) throw Fail{MAYA_ST_BAD_INPUT, "too many host syncs"};
     RB.sops[ls].push_back(Op{gpre, arg, tag | (seg << 2)});
     if (keep_seq) RB.sseq[ls].push_back(seq);
     RB.sev[ls]++;
@@ -294,9 +294,27 @@ struct RepPacker {
   // whose disp is the first kernel's, the block interned per job.  Single
   // kernels, and runs reaching the fold limit of the gap prefix (2^61), go
   // through the per-event path (kernels.cu op_foldable).
-  void kernel_block(int32_t stream, const KSpec *ks, size_t n, int64_t gap, int32_t dtype) {
-    const bool fits = gap >= 0 && n >= 2 && n < (1u << 24) &&
-                      (gap == 0 || (int64_t)n <= (((int64_t)1 << 61) - 1 - gpre) / gap);
+  bool block_fits(size_t n, int64_t gap) const {
+    return gap >= 0 && n >= 2 && n < (1u << 24) &&
+           (gap == 0 || (int64_t)n <= (((int64_t)1 << 61) - 1 - gpre) / gap);
+  }
+  // emit interned block `id` (n launches, host gap `gap` before each)
+  void emit_block(int32_t stream, uint32_t id, size_t n, int64_t gap) {
+    gpre += gap;                     // the first kernel's gap
+    seq += gap > 0 ? 1 : 0;
+    emit(stream, TAG_KERN, KBLOCK | id);
+    gpre += (int64_t)(n - 1) * gap;
+    seq += (uint32_t)((n - 1) * (gap > 0 ? 2 : 1) + 1);
+    n_devev += (uint32_t)(n - 1);
+    RB.sev[RB.local_stream(stream, false)] += (uint32_t)(n - 1);
+  }
+  bool kernel_block_id(int32_t stream, uint32_t id, size_t n, int64_t gap) {
+    if (!block_fits(n, gap)) return false;
+    emit_block(stream, id, n, gap);
+    return true;
+  }
+  uint32_t kernel_block(int32_t stream, const KSpec *ks, size_t n, int64_t gap, int32_t dtype) {
+    const bool fits = block_fits(n, gap);
     if (!fits) {
       for (size_t i = 0; i < n; i++) {
         if (gap > 0) {
@@ -306,7 +324,7 @@ struct RepPacker {
         const int64_t f[4] = {ks[i].op, dtype, ks[i].flops, ks[i].bytes};
         event(MAYA_EV_KERNEL, stream, f, -1, false);
       }
-      return;
+      return ~0u;
     }
     // intern by the launch list itself: a repeated layer body costs a hash
     // and a compare, no per-kernel feature lookups
@@ -347,13 +365,8 @@ struct RepPacker {
       if (F->blk_map.emplace(hsh, id).second) ce = FeatState::BlkCacheEnt{hsh, id};
       // (a colliding hash keeps its first block interned; later ones stay unshared)
     }
-    gpre += gap;                     // the first kernel's gap
-    seq += gap > 0 ? 1 : 0;
-    emit(stream, TAG_KERN, KBLOCK | id);
-    gpre += (int64_t)(n - 1) * gap;
-    seq += (uint32_t)((n - 1) * (gap > 0 ? 2 : 1) + 1);
-    n_devev += (uint32_t)(n - 1);
-    RB.sev[RB.local_stream(stream, false)] += (uint32_t)(n - 1);
+    emit_block(stream, id, n, gap);
+    return id;
   }
 
   // one event (trace.py:71-151 as rawtrace.py arrays); host_ns >= 0: a
@@ -931,12 +944,17 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
       any |= cw != NO_WF;
     }
     if (any)
-      for (const RepHdr &h : P.reps)
+      for (const RepHdr &h : P.reps) {
+        for (uint32_t q = 0; q < h.n_ops; q++) {
+          Op &o = P.ops[h.ops + q];
+          if (op_tag(o.meta) == TAG_COLL && P.coll_wf[h.colls + o.arg] != NO_WF) o.meta |= OP_FOLDC;
+        }
         for (uint32_t s = 0; s < h.n_streams; s++) {
           StreamRange &st = P.streams[h.streams + s];
           st.folded = folded_len(P.ops.data() + h.ops + st.begin, st.len,
                                  P.coll_wf.data() + h.colls);
         }
+      }
   }
   // walkers rank-major: a scheduler warp owns whole ranks
   P.wids.resize(P.walkers.size());
@@ -992,8 +1010,11 @@ struct PackSink final : EventSink {
   std::vector<uint32_t> *rep_comms;
   bool blocks = false;
   bool takes_blocks() const override { return blocks; }
-  void kernel_block(int32_t s, const KSpec *ks, size_t n, int64_t gap, int32_t dtype) override {
-    RP->kernel_block(s, ks, n, gap, dtype);
+  uint32_t kernel_block(int32_t s, const KSpec *ks, size_t n, int64_t gap, int32_t dtype) override {
+    return RP->kernel_block(s, ks, n, gap, dtype);
+  }
+  bool kernel_block_id(int32_t s, uint32_t id, size_t n, int64_t gap) override {
+    return RP->kernel_block_id(s, id, n, gap);
   }
   void rep_begin(size_t est_events) override {
     RP->begin(*P, *F, device, true, est_events / 2 + 16);

@@ -242,8 +242,12 @@ struct alignas(16) Op {
   uint32_t meta;   // tag (2 bits) | sync segment << 2
 };
 
+// meta bit 31 (OP_FOLDC): a collective that folds into kernel runs (pack.cpp
+// coll_wf: every simulated rank of the rep meets it alone), so the fold pass's
+// eligibility test reads the op only; segments stay below 2^29.
+static const uint32_t OP_FOLDC = 0x80000000u;
 __host__ __device__ inline uint32_t op_tag(uint32_t meta) { return meta & 3u; }
-__host__ __device__ inline uint32_t op_seg(uint32_t meta) { return meta >> 2; }
+__host__ __device__ inline uint32_t op_seg(uint32_t meta) { return (meta >> 2) & 0x1FFFFFFFu; }
 
 struct StreamRange {
   uint32_t begin;  // rep-local op index
