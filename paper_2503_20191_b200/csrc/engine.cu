@@ -255,6 +255,8 @@ bool plan_grid(const JobPack &P, LanePlan &pl) {
 // rings and rank collective table -- with at most two FIFOs per lane.  Only
 // for jobs whose collectives rendezvous in rings (JOB_RING).  n_slots carries
 // the job's folded op count (the region's op area).
+static const uint64_t CHAIN_WAVE_BYTES = 148ull * 200 * 1024;   // ~one wave of chain CTAs
+
 LanePlan plan_chain(const JobPack &P) {
   LanePlan pl;
   const uint32_t W = (uint32_t)P.walkers.size(), R = (uint32_t)P.ranks.size();
@@ -624,9 +626,21 @@ int maya_upload(maya_engine *e) {
     if (const char *ev = getenv("MAYA_LANE_BUDGET")) budget = strtoull(ev, nullptr, 10);
     if (budget < LANE_REGION[0]) budget = LANE_REGION[0];
     if (budget > LANE_SMEM_CAP) budget = LANE_SMEM_CAP;
+    // chain kernel (whole job on chip, latency-optimised) when the batch's
+    // chain jobs fit the GPU in one wave: a batch of many large jobs (C5's
+    // thousands of per-rank-distinct traces) is throughput-bound and keeps
+    // the lane kernel's resident rings
+    const bool forced = (e->options & (MAYA_OPT_WARP_SCHED | MAYA_OPT_LANE_SCHED)) != 0;
+    if (!forced && !(e->options & MAYA_OPT_NO_CHAIN)) {
+      uint64_t total = 0;
+      for (size_t j = 0; j < nj; j++) {
+        plans[j] = plan_chain(e->packs[j]);
+        if (plans[j].variant >= 0) total += (plans[j].smem + 1023u) & ~1023u;
+      }
+      if (total > CHAIN_WAVE_BYTES)
+        for (size_t j = 0; j < nj; j++) plans[j] = LanePlan();
+    }
     for (size_t j = 0; j < nj; j++) {
-      const bool forced = (e->options & (MAYA_OPT_WARP_SCHED | MAYA_OPT_LANE_SCHED)) != 0;
-      if (!forced && !(e->options & MAYA_OPT_NO_CHAIN)) plans[j] = plan_chain(e->packs[j]);
       if (plans[j].variant < 0 && !(e->options & MAYA_OPT_WARP_SCHED))
         plans[j] = plan_lane(e->packs[j], (uint32_t)budget, (e->options & MAYA_OPT_LANE_SCHED) != 0);
       if (plans[j].variant >= 0 && plans[j].variant != 15)

@@ -673,9 +673,76 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
     act_ids.erase(it);
   };
 
+  // Phase templates (kernel-block sinks): every forward / backward of one
+  // chunk emits the same events up to counters, so the packer captures the
+  // first occurrence and stamps the later ones; the builder replays its own
+  // side -- call lists and call numbers, event versions, allocation handles
+  // (pack.cpp RepPacker::phase_*).
+  struct BTpl {
+    int id = -2;                                   // -2: not captured, -1: not replayable
+    int tries = 0;                                 // captures attempted (the first occurrence
+                                                   // of a phase often opens communicators)
+    std::vector<std::pair<int, std::pair<int8_t, int64_t>>> calls;   // (lc, (kind, bytes))
+    std::vector<std::pair<int64_t, int64_t>> vers; // (event id, records)
+    int64_t allocs = 0;
+  };
+  // (kernel-block mode always cuts runs at phase boundaries, replay or not, so
+  // both pack the same kernel blocks)
+  const bool tpl_on = B.blocks;
+  const bool replay = tpl_on && sink->replays();
+  std::vector<BTpl> btpl(tpl_on ? 2 * chunks.size() : 0);
+  std::vector<size_t> calls0;
+  std::vector<int64_t> vers0;
   for (const Step &st : pipeline_order(schedule, p, m, v, stage)) {
+    if (!tpl_on) {
+      if (st.phase == FWD) emit_forward(st.mb, st.chunk);
+      else emit_backward(st.mb, st.chunk);
+      continue;
+    }
+    BTpl &bt = btpl[2 * st.chunk + (st.phase == FWD ? 0 : 1)];
+    B.flush();   // phases start and end outside a kernel run
+    if (replay && bt.id >= 0 && sink->phase_replay(bt.id, B.next_alloc)) {
+      if (st.phase == FWD) act_ids[{st.chunk, st.mb}] = B.next_alloc;   // its one allocation
+      else act_ids.erase({st.chunk, st.mb});
+      B.next_alloc += bt.allocs;
+      for (const auto &c : bt.calls) {
+        B.call_idx[c.first]++;
+        B.calls[c.first].push_back(c.second);
+      }
+      for (const auto &e : bt.vers) {
+        B.next_version[e.first] += e.second;
+        B.last_version[e.first] = B.next_version[e.first] - 1;
+      }
+      continue;
+    }
+    const bool capture = replay && bt.id < 0 && bt.tries < 3;
+    if (capture) {
+      sink->phase_begin(B.next_alloc);
+      calls0.resize(B.calls.size());
+      for (size_t lc = 0; lc < B.calls.size(); lc++) calls0[lc] = B.calls[lc].size();
+      vers0 = B.next_version;
+    }
+    const int64_t aid0 = B.next_alloc;
     if (st.phase == FWD) emit_forward(st.mb, st.chunk);
     else emit_backward(st.mb, st.chunk);
+    B.flush();
+    if (capture) {
+      bt.tries++;
+      bt.calls.clear();
+      bt.vers.clear();
+      bt.id = sink->phase_end();
+      bt.allocs = B.next_alloc - aid0;
+      if (st.phase == FWD && bt.allocs != 1) bt.id = -1;   // replay assumes one activation alloc
+      // call lists in issue order across communicators are not needed: each
+      // communicator's list is appended in its own order
+      for (size_t lc = 0; lc < B.calls.size(); lc++)
+        for (size_t q = calls0[lc]; q < B.calls[lc].size(); q++)
+          bt.calls.push_back({(int)lc, B.calls[lc][q]});
+      for (size_t e = 0; e < B.next_version.size(); e++) {
+        const int64_t before = e < vers0.size() ? vers0[e] : 0;
+        if (B.next_version[e] != before) bt.vers.push_back({(int64_t)e, B.next_version[e] - before});
+      }
+    }
   }
 
   // gradient reduction and optimizer step (:757-777)

@@ -67,6 +67,15 @@ struct EventSink {
   // kernel_block of this trace): emit it by id.  False: not possible here (the
   // caller then sends the launch list).
   virtual bool kernel_block_id(int32_t, uint32_t, size_t, int64_t) { return false; }
+  // Phase templates (kernel-block sinks): the generator brackets each
+  // microbatch phase with phase_begin / phase_end (which returns a template id,
+  // or -1 if the phase cannot be replayed) and later asks phase_replay(id) to
+  // stamp an identical phase (false: emit it event by event).  aid_base: the
+  // first allocation handle the phase uses.
+  virtual bool replays() const { return false; }
+  virtual void phase_begin(int64_t) {}
+  virtual int phase_end() { return -1; }
+  virtual bool phase_replay(int, int64_t) { return false; }
 };
 
 // Returns 0 or a negative code with *err set (invalid configuration).  With a

@@ -180,7 +180,155 @@ struct RepPacker {
     return ((uint64_t)ev << 32) | (uint64_t)ver;
   }
 
+  // ---- phase templates (fused generator, kernel-block mode) ----------------
+  // A microbatch phase of the synthetic frontend (forward or backward of one
+  // model chunk, workload.py:571-756) emits the same events every time up to
+  // counters: gap prefix, event seq, record ordinals, collective indices and
+  // call numbers, allocation handles.  The first occurrence is packed event by
+  // event and captured as a template of relative records; later occurrences
+  // are stamped from it (no per-event work).  A phase that changes packer
+  // state a template cannot carry (a new stream, a sync, a first use of a
+  // communicator, an out-of-order collective, a wait on an earlier phase's
+  // record) is never replayed.
+  struct PhaseTpl {
+    bool ok = false;
+    uint32_t seg = 0;
+    std::vector<std::vector<Op>> ops;        // per local stream, relative fields
+    std::vector<uint32_t> sev;               // per local stream: device events added
+    std::vector<uint32_t> coll_lc, coll_rel; // new collective entries (call_idx - comm_next)
+    std::vector<std::pair<uint32_t, uint32_t>> lc_adv;   // (lc, calls issued)
+    std::vector<MemRec> mems;                // gpre / seq relative
+    std::vector<std::pair<int64_t, int64_t>> allocs;     // (handle - aid base, size)
+    int64_t dgpre = 0;
+    uint32_t dseq = 0, ddevev = 0, drecs = 0;
+  };
+  std::vector<PhaseTpl> tpls;
+  bool cap = false;
+  int64_t cap_aid = 0;
+  struct Snap {
+    int64_t gpre;
+    uint32_t seq, devev, recs, seg;
+    size_t colls, mems, nst;
+    bool ring_ok;
+  } snap0{};
+  std::vector<size_t> cap_size;
+  std::vector<uint32_t> cap_sev;
+  std::vector<int64_t> cap_next;
+  std::vector<int32_t> cap_cstream;
+  std::vector<std::pair<int64_t, int64_t>> cap_allocs;
+
+  void phase_begin(int64_t aid_base) {
+    cap = true;
+    cap_aid = aid_base;
+    snap0 = Snap{gpre, seq, n_devev, n_recs, seg, P->coll_lc.size(), P->mems.size(), RB.size(),
+                 ring_ok};
+    cap_size.resize(RB.size());
+    cap_sev.resize(RB.size());
+    for (size_t q = 0; q < RB.size(); q++) {
+      cap_size[q] = RB.sops[q].size();
+      cap_sev[q] = RB.sev[q];
+    }
+    cap_next = comm_next;
+    cap_cstream = comm_stream;
+    cap_allocs.clear();
+  }
+  int phase_end() {
+    cap = false;
+    PhaseTpl t;
+    t.ok = RB.size() == snap0.nst && seg == snap0.seg && coll_seen.empty() &&
+           ring_ok == snap0.ring_ok && comm_stream == cap_cstream && gpre >= snap0.gpre &&
+           !keep_seq;
+    if (!t.ok) return -1;
+    const uint32_t c0 = (uint32_t)(snap0.colls - coll0);
+    t.seg = seg;
+    t.ops.resize(RB.size());
+    t.sev.resize(RB.size());
+    for (size_t q = 0; q < RB.size(); q++) {
+      t.sev[q] = RB.sev[q] - cap_sev[q];
+      for (size_t k = cap_size[q]; k < RB.sops[q].size(); k++) {
+        Op o = RB.sops[q][k];
+        o.disp -= snap0.gpre;
+        const uint32_t tg = op_tag(o.meta);
+        if (tg == TAG_REC || tg == TAG_WAIT) {
+          if (o.arg == NO_REC || o.arg < snap0.recs) return -1;   // an earlier phase's record
+          o.arg -= snap0.recs;
+        } else if (tg == TAG_COLL) {
+          o.arg -= c0;
+        }
+        t.ops[q].push_back(o);
+      }
+    }
+    for (size_t k = snap0.colls; k < P->coll_lc.size(); k++) {
+      const uint32_t lc = P->coll_lc[k];
+      t.coll_lc.push_back(lc);
+      t.coll_rel.push_back((uint32_t)(P->coll_idx[k] - cap_next[lc]));
+    }
+    for (uint32_t lc = 0; lc < comm_next.size(); lc++)
+      if (comm_next[lc] != cap_next[lc])
+        t.lc_adv.push_back({lc, (uint32_t)(comm_next[lc] - cap_next[lc])});
+    for (size_t k = snap0.mems; k < P->mems.size(); k++) {
+      MemRec m = P->mems[k];
+      m.gpre -= snap0.gpre;
+      m.seq -= snap0.seq;
+      t.mems.push_back(m);
+    }
+    t.allocs = cap_allocs;
+    t.dgpre = gpre - snap0.gpre;
+    t.dseq = seq - snap0.seq;
+    t.ddevev = n_devev - snap0.devev;
+    t.drecs = n_recs - snap0.recs;
+    tpls.push_back(std::move(t));
+    return (int)tpls.size() - 1;
+  }
+  // stamp template `id` at the current state; false: not here (the caller
+  // emits the phase event by event)
+  bool phase_replay(int id, int64_t aid_base) {
+    const PhaseTpl &t = tpls[id];
+    if (seg != t.seg || t.ops.size() > RB.size()) return false;
+    // the run-folding limit and block fits (kernel_block) assume gap prefixes
+    // well below 2^61: replay only far from it
+    if (gpre > ((int64_t)1 << 59) - t.dgpre) return false;
+    const uint32_t cb = (uint32_t)(P->coll_lc.size() - coll0);
+    for (size_t q = 0; q < t.ops.size(); q++) {
+      std::vector<Op> &dst = RB.sops[q];
+      for (Op o : t.ops[q]) {
+        o.disp += gpre;
+        const uint32_t tg = op_tag(o.meta);
+        if (tg == TAG_REC || tg == TAG_WAIT) o.arg += n_recs;
+        else if (tg == TAG_COLL) o.arg += cb;
+        dst.push_back(o);
+      }
+      RB.sev[q] += t.sev[q];
+    }
+    for (size_t k = 0; k < t.coll_lc.size(); k++) {
+      P->coll_lc.push_back(t.coll_lc[k]);
+      P->coll_idx.push_back((uint32_t)(t.coll_rel[k] + comm_next[t.coll_lc[k]]));
+    }
+    for (const auto &a : t.lc_adv) comm_next[a.first] += a.second;
+    for (MemRec m : t.mems) {
+      m.gpre += gpre;
+      m.seq += seq;
+      P->mems.push_back(m);
+    }
+    for (const auto &a : t.allocs) {
+      const int64_t h = aid_base + a.first;
+      if (h >= 0 && h < (1 << 20)) {
+        if ((size_t)h >= alloc_small.size()) alloc_small.resize(h + 64, INT64_MIN);
+        alloc_small[h] = a.second;
+      } else {
+        alloc_big[h] = a.second;
+      }
+    }
+    gpre += t.dgpre;
+    seq += t.dseq;
+    n_devev += t.ddevev;
+    n_recs += t.drecs;
+    return true;
+  }
+
   void begin(JobPack &pk, FeatState &fs, int32_t dev, bool on_the_fly, size_t reserve_hint) {
+    tpls.clear();
+    cap = false;
     keep_seq = true;
     P = &pk;
     F = &fs;
@@ -404,6 +552,7 @@ struct RepPacker {
         break;
       }
       case MAYA_EV_MEMALLOC:
+        if (cap) cap_allocs.push_back({f[0] - cap_aid, f[1]});
         if (f[0] >= 0 && f[0] < (1 << 20)) {
           if ((size_t)f[0] >= alloc_small.size()) alloc_small.resize(f[0] + 64, INT64_MIN);
           alloc_small[f[0]] = f[1];
@@ -500,10 +649,8 @@ struct RepPacker {
     h.n_streams = (uint32_t)RB.size();
     uint32_t pos = 0;
     for (size_t s = 0; s < RB.size(); s++) {
-      // ops the scheduler sees after the device folds kernel runs (kernels.cu
-      // fold_count_kernel: same rule), for sizing its staging rings
-      const uint32_t folded = folded_len(RB.sops[s].data(), (uint32_t)RB.sops[s].size(), nullptr);
-      P->streams.push_back(StreamRange{pos, (uint32_t)RB.sops[s].size(), RB.raw_of[s], folded});
+      // (folded: set by pack_tail once the foldable collectives are known)
+      P->streams.push_back(StreamRange{pos, (uint32_t)RB.sops[s].size(), RB.raw_of[s], 0});
       P->stream_events.push_back(RB.sev[s]);
       P->ops.insert(P->ops.end(), RB.sops[s].begin(), RB.sops[s].end());
       if (keep_seq) P->op_seq.insert(P->op_seq.end(), RB.sseq[s].begin(), RB.sseq[s].end());
@@ -943,18 +1090,20 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
       if (cw == NO_WF - 1) cw = NO_WF;
       any |= cw != NO_WF;
     }
-    if (any)
-      for (const RepHdr &h : P.reps) {
+    for (const RepHdr &h : P.reps) {
+      if (any)
         for (uint32_t q = 0; q < h.n_ops; q++) {
           Op &o = P.ops[h.ops + q];
           if (op_tag(o.meta) == TAG_COLL && P.coll_wf[h.colls + o.arg] != NO_WF) o.meta |= OP_FOLDC;
         }
-        for (uint32_t s = 0; s < h.n_streams; s++) {
-          StreamRange &st = P.streams[h.streams + s];
-          st.folded = folded_len(P.ops.data() + h.ops + st.begin, st.len,
-                                 P.coll_wf.data() + h.colls);
-        }
+      // ops each FIFO keeps after the device folds its runs (kernels.cu
+      // fold_count_kernel: same rule), for sizing the schedulers' staging
+      for (uint32_t s = 0; s < h.n_streams; s++) {
+        StreamRange &st = P.streams[h.streams + s];
+        st.folded = folded_len(P.ops.data() + h.ops + st.begin, st.len,
+                               any ? P.coll_wf.data() + h.colls : nullptr);
       }
+    }
   }
   // walkers rank-major: a scheduler warp owns whole ranks
   P.wids.resize(P.walkers.size());
@@ -1016,6 +1165,11 @@ struct PackSink final : EventSink {
   bool kernel_block_id(int32_t s, uint32_t id, size_t n, int64_t gap) override {
     return RP->kernel_block_id(s, id, n, gap);
   }
+  bool replays() const override { return blocks && replay; }
+  void phase_begin(int64_t aid_base) override { RP->phase_begin(aid_base); }
+  int phase_end() override { return RP->phase_end(); }
+  bool phase_replay(int id, int64_t aid_base) override { return RP->phase_replay(id, aid_base); }
+  bool replay = true;
   void rep_begin(size_t est_events) override {
     RP->begin(*P, *F, device, true, est_events / 2 + 16);
     RP->keep_seq = !blocks;   // block batches never record a timeline (engine.cu)
@@ -1032,6 +1186,8 @@ struct PackSink final : EventSink {
 };
 
 }  // namespace
+
+bool g_phase_replay = true;
 
 void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P, bool collapse) {
   pack_header(job, key_rank, P);
@@ -1066,6 +1222,7 @@ int pack_generated(const maya_model &model, const maya_config &cfg, const maya_c
   sink.device = device;
   sink.rep_comms = &rep_comms;
   sink.blocks = blocks;
+  sink.replay = g_phase_replay;
   int rc;
   try {
     rc = generate_job(model, cfg, cl, schedule, overhead, G, err, &sink);

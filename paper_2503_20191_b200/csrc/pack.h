@@ -68,6 +68,10 @@ void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &out, bool coll
 // Returns generate_job's code (invalid configuration: <0 with *err set).
 // With blocks, runs of kernel launches become interned kernel blocks (one
 // KBLOCK op each): the batch must then be run folded (no timeline).
+// Phase templates in pack_generated's kernel-block mode (default on; tests
+// compare against the event-by-event packing).
+extern bool g_phase_replay;
+
 int pack_generated(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
                    int32_t schedule, int64_t overhead, int32_t device, int32_t key_rank,
                    bool collapse, GenJob &scratch, JobPack &out, std::string *err,
