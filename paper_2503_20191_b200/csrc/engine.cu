@@ -1694,6 +1694,7 @@ int maya_batch_add_generated(maya_engine *e, const maya_model *model, int32_t n,
   };
   std::stable_sort(lpt.begin(), lpt.end(), [&](int32_t a, int32_t b) { return cost(a) > cost(b); });
   std::atomic<int> next(0);
+  GenCache cache;   // layout-only structure, shared by this call's workers
   auto work = [&]() {
     thread_local GenJob g;
     for (;;) {
@@ -1706,7 +1707,7 @@ int maya_batch_add_generated(maya_engine *e, const maya_model *model, int32_t n,
       // fused generate -> pack (no raw event arrays)
       int rc = pack_generated(*model, cfgs[i], *cluster, schedule, dispatch_overhead_ns, device,
                               kr, (e->options & MAYA_OPT_COLLAPSE) != 0, g, P, &err,
-                              !(e->options & MAYA_OPT_NO_BLOCKS));
+                              !(e->options & MAYA_OPT_NO_BLOCKS), &cache);
       if (status_out) status_out[i] = rc;
       if (rc != MAYA_OK) {
         P.clear();

@@ -682,7 +682,7 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
     int id = -2;                                   // -2: not captured, -1: not replayable
     int tries = 0;                                 // captures attempted (the first occurrence
                                                    // of a phase often opens communicators)
-    std::vector<std::pair<int, std::pair<int8_t, int64_t>>> calls;   // (lc, (kind, bytes))
+    std::vector<std::pair<int, std::pair<int8_t, int64_t>>> calls;   // (lc, (kind, bytes)), by lc
     std::vector<std::pair<int64_t, int64_t>> vers; // (event id, records)
     int64_t allocs = 0;
   };
@@ -705,9 +705,12 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
       if (st.phase == FWD) act_ids[{st.chunk, st.mb}] = B.next_alloc;   // its one allocation
       else act_ids.erase({st.chunk, st.mb});
       B.next_alloc += bt.allocs;
-      for (const auto &c : bt.calls) {
-        B.call_idx[c.first]++;
-        B.calls[c.first].push_back(c.second);
+      for (size_t q = 0; q < bt.calls.size();) {   // runs of one communicator
+        const int lc = bt.calls[q].first;
+        size_t e = q;
+        while (e < bt.calls.size() && bt.calls[e].first == lc) B.calls[lc].push_back(bt.calls[e++].second);
+        B.call_idx[lc] += (int64_t)(e - q);
+        q = e;
       }
       for (const auto &e : bt.vers) {
         B.next_version[e.first] += e.second;
@@ -793,6 +796,106 @@ void validate(const maya_model &model, const maya_config &c, int64_t n, int sche
 
 }  // namespace
 
+namespace {
+
+// The communicators of a job (collate.py:297-323): one per distinct role over
+// all ranks, in the reference's global (name) order, with the stage and local
+// index of its position-0 member (whose calls become the group's call table),
+// its topology, and every rank's local -> global translation.
+struct CommStruct {
+  std::vector<CommRole> role;
+  std::vector<int32_t> nranks, first_stage, first_lc;
+  std::vector<int8_t> topo;
+  std::vector<int64_t> rank_comm_off;
+  std::vector<int32_t> rank_comm;
+  std::string error;
+};
+
+std::shared_ptr<const CommStruct> build_comm_struct(const Coords &C, int64_t v, int64_t n,
+                                                    int64_t dph) {
+  auto cs = std::make_shared<CommStruct>();
+  // Roles are keyed by integers (each communicator's name spells its fields
+  // out one to one)
+  auto role_key = [](const CommRole &r) -> uint64_t {
+    return ((uint64_t)r.type << 60) | ((uint64_t)r.a << 40) | ((uint64_t)r.b << 20) |
+           (uint64_t)r.c;
+  };
+  struct CInfo {
+    CommRole role;
+    int32_t stage_of_first;  // stage of position-0 rank
+    int32_t lc_of_first;     // local comm index of the role in that rank's rep
+  };
+  // role key -> comm (discovery order): open addressing, sized for every
+  // (rank, role) pair, so the table never grows
+  std::vector<CInfo> infos;
+  std::vector<int32_t> comm_of;                  // per rank, per local comm: discovery index
+  std::vector<int64_t> rk_off(n + 1, 0);
+  const size_t roles_per_rank = 2 + 4 * (size_t)v;
+  size_t cap = 64;
+  while (cap < 2 * (size_t)n * roles_per_rank) cap <<= 1;
+  std::vector<uint64_t> hkey(cap, ~0ull);
+  std::vector<int32_t> hval(cap, -1);
+  auto slot_of = [&](uint64_t key) {
+    size_t h = (size_t)((key * 0x9E3779B97F4A7C15ull) >> 20) & (cap - 1);
+    while (hkey[h] != key && hkey[h] != ~0ull) h = (h + 1) & (cap - 1);
+    return h;
+  };
+  std::vector<CommRole> roles;
+  for (int64_t r = 0; r < n; r++) {
+    worker_comms(C, v, r, roles);
+    for (size_t q = 0; q < roles.size(); q++) {
+      const uint64_t key = role_key(roles[q]);
+      const size_t h = slot_of(key);
+      if (hkey[h] == ~0ull) {
+        hkey[h] = key;
+        hval[h] = (int32_t)infos.size();
+        infos.push_back(CInfo{roles[q], -1, -1});
+      }
+      comm_of.push_back(hval[h]);
+      CInfo &ci = infos[hval[h]];
+      if (roles[q].my_rank == 0 && ci.stage_of_first < 0) {
+        ci.role = roles[q];
+        ci.stage_of_first = (int32_t)(r / (C.t * C.d));
+        ci.lc_of_first = (int32_t)q;
+      }
+    }
+    rk_off[r + 1] = (int64_t)comm_of.size();
+  }
+  // JobTrace.groups order = sorted by name (collate.py:323).  The names are
+  // "dp.t<i>.p<k>" < "pb<v>.t<i>.d<j>" < "pf<v>.t<i>.d<j>" < "tp.p<k>.d<j>", so the
+  // string order is the order of (kind, decimal-string rank of each field):
+  // an integer key per communicator, no names needed
+  std::vector<uint64_t> okey(infos.size());
+  for (size_t g = 0; g < infos.size(); g++) okey[g] = comm_order_key(infos[g].role);
+  std::vector<int32_t> order(infos.size());
+  for (size_t g = 0; g < order.size(); g++) order[g] = (int32_t)g;
+  std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return okey[x] < okey[y]; });
+  std::vector<int32_t> gid_of(infos.size());
+  std::vector<int64_t> hosts_buf;
+  for (size_t gi = 0; gi < order.size(); gi++) {
+    const int32_t g0 = order[gi];
+    gid_of[g0] = (int32_t)gi;
+    const CInfo &ci = infos[g0];
+    if (ci.stage_of_first < 0) {
+      cs->error = "communicator without a position-0 member";
+      return cs;
+    }
+    cs->role.push_back(ci.role);
+    cs->nranks.push_back(ci.role.nranks);
+    cs->first_stage.push_back(ci.stage_of_first);
+    cs->first_lc.push_back(ci.lc_of_first);
+    cs->topo.push_back(comm_topology(C, ci.role, dph, hosts_buf));
+  }
+  cs->rank_comm_off.push_back(0);
+  for (int64_t r = 0; r < n; r++) {
+    for (int64_t q = rk_off[r]; q < rk_off[r + 1]; q++) cs->rank_comm.push_back(gid_of[comm_of[q]]);
+    cs->rank_comm_off.push_back((int64_t)cs->rank_comm.size());
+  }
+  return cs;
+}
+
+}  // namespace
+
 maya_raw_job GenJob::raw(int32_t device) const {
   maya_raw_job r{};
   r.num_ranks = num_ranks;
@@ -820,7 +923,7 @@ maya_raw_job GenJob::raw(int32_t device) const {
 
 int generate_job(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
                  int32_t schedule, int64_t overhead, GenJob &G, std::string *err,
-                 EventSink *sink) {
+                 EventSink *sink, GenCache *cache) {
   G.clear();   // keep capacity: a worker thread reuses one GenJob across configs
   try {
     if (cl.num_hosts < 1 || cl.devices_per_host < 1) throw GenFail{"empty cluster"};
@@ -846,94 +949,36 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
     }
     G.rank_rep.resize(n);
     for (int64_t r = 0; r < n; r++) G.rank_rep[r] = (int32_t)(r / (C.t * C.d));
-    // communicators: every role of every rank (collate.py:297-322).  Roles are
-    // keyed by integers; each communicator's name is built once (the global
-    // comm order is the reference's: sorted by name)
-    auto role_key = [](const CommRole &r) -> uint64_t {
-      return ((uint64_t)r.type << 60) | ((uint64_t)r.a << 40) | ((uint64_t)r.b << 20) |
-             (uint64_t)r.c;
-    };
-    struct CInfo {
-      CommRole role;
-      int32_t stage_of_first;  // stage of position-0 rank
-      int32_t lc_of_first;     // local comm index of the role in that rank's rep
-    };
-    // role key -> comm (discovery order): open addressing, sized for every
-    // (rank, role) pair, so the table never grows
-    std::vector<CInfo> infos;
-    std::vector<int32_t> comm_of;                  // per rank, per local comm: discovery index
-    std::vector<int64_t> rk_off(n + 1, 0);
-    const size_t roles_per_rank = 2 + 4 * (size_t)cfg.virtual_stages;
-    size_t cap = 64;
-    while (cap < 2 * (size_t)n * roles_per_rank) cap <<= 1;
-    std::vector<uint64_t> hkey(cap, ~0ull);
-    std::vector<int32_t> hval(cap, -1);
-    auto slot_of = [&](uint64_t key) {
-      size_t h = (size_t)((key * 0x9E3779B97F4A7C15ull) >> 20) & (cap - 1);
-      while (hkey[h] != key && hkey[h] != ~0ull) h = (h + 1) & (cap - 1);
-      return h;
-    };
-    std::vector<CommRole> roles;
-    for (int64_t r = 0; r < n; r++) {
-      worker_comms(C, cfg.virtual_stages, r, roles);
-      for (size_t q = 0; q < roles.size(); q++) {
-        const uint64_t key = role_key(roles[q]);
-        const size_t h = slot_of(key);
-        if (hkey[h] == ~0ull) {
-          hkey[h] = key;
-          hval[h] = (int32_t)infos.size();
-          infos.push_back(CInfo{roles[q], -1, -1});
-        }
-        comm_of.push_back(hval[h]);
-        CInfo &ci = infos[hval[h]];
-        if (roles[q].my_rank == 0 && ci.stage_of_first < 0) {
-          ci.role = roles[q];
-          ci.stage_of_first = (int32_t)(r / (C.t * C.d));
-          ci.lc_of_first = (int32_t)q;
-        }
-      }
-      rk_off[r + 1] = (int64_t)comm_of.size();
+    // communicators: every role of every rank (collate.py:297-322), their
+    // global order, topology and each rank's translation -- a function of the
+    // parallel layout only, shared across the batch's configurations (cache)
+    std::shared_ptr<const CommStruct> cs;
+    if (cache && sink) {
+      const std::array<int64_t, 6> key{1, C.t, C.d, C.p, cfg.virtual_stages, cl.devices_per_host};
+      cs = cache->get<CommStruct>(key, [&] { return build_comm_struct(C, cfg.virtual_stages, n, cl.devices_per_host); });
+    } else {
+      cs = build_comm_struct(C, cfg.virtual_stages, n, cl.devices_per_host);
     }
-    // JobTrace.groups order = sorted by name (collate.py:323).  The names are
-    // "dp.t<i>.p<k>" < "pb<v>.t<i>.d<j>" < "pf<v>.t<i>.d<j>" < "tp.p<k>.d<j>", so the
-    // string order is the order of (kind, decimal-string rank of each field):
-    // an integer key per communicator, no names needed (built only for the
-    // raw-job path, which exports them)
-    std::vector<uint64_t> okey(infos.size());
-    for (size_t g = 0; g < infos.size(); g++) okey[g] = comm_order_key(infos[g].role);
-    std::vector<int32_t> order(infos.size());
-    for (size_t g = 0; g < order.size(); g++) order[g] = (int32_t)g;
-    std::sort(order.begin(), order.end(),
-              [&](int32_t x, int32_t y) { return okey[x] < okey[y]; });
-    std::vector<int32_t> gid_of(infos.size());
-    std::vector<int64_t> hosts_buf;
+    if (!cs->error.empty()) throw GenFail{cs->error};
     G.call_off.push_back(0);
-    for (size_t gi = 0; gi < order.size(); gi++) {
-      const int32_t g0 = order[gi];
-      gid_of[g0] = (int32_t)gi;
-      const CInfo &ci = infos[g0];
-      if (ci.stage_of_first < 0) throw GenFail{"communicator without a position-0 member"};
-      G.comm_nranks.push_back(ci.role.nranks);
-      G.comm_topo.push_back(comm_topology(C, ci.role, cl.devices_per_host, hosts_buf));
-      const auto &cl2 = rcalls[ci.stage_of_first].calls[ci.lc_of_first];
+    for (size_t gi = 0; gi < cs->nranks.size(); gi++) {
+      G.comm_nranks.push_back(cs->nranks[gi]);
+      G.comm_topo.push_back(cs->topo[gi]);
+      const auto &cl2 = rcalls[cs->first_stage[gi]].calls[cs->first_lc[gi]];
       for (auto &kb : cl2) {
         G.call_kind.push_back(kb.first);
         G.call_bytes.push_back(kb.second);
       }
       G.call_off.push_back((int64_t)G.call_kind.size());
       if (!sink) {
-        const std::string nm = comm_name(ci.role);
+        const std::string nm = comm_name(cs->role[gi]);
         G.comm_names.push_back(nm);
         G.comm_blob += nm;
         G.comm_blob += '\n';
       }
     }
-    G.rank_comm_off.push_back(0);
-    for (int64_t r = 0; r < n; r++) {
-      for (int64_t q = rk_off[r]; q < rk_off[r + 1]; q++)
-        G.rank_comm.push_back(gid_of[comm_of[q]]);
-      G.rank_comm_off.push_back((int64_t)G.rank_comm.size());
-    }
+    G.rank_comm_off = cs->rank_comm_off;
+    G.rank_comm = cs->rank_comm;
   } catch (const GenFail &f) {
     if (err) *err = f.msg;
     return MAYA_EINVAL;

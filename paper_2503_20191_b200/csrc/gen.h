@@ -2,6 +2,10 @@
 // frontend of pkg/src/dltsim/workload.py plus the group resolution of
 // collate.py, producing a raw job (include/maya_b200.h) directly.
 #pragma once
+#include <array>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -78,11 +82,32 @@ struct EventSink {
   virtual bool phase_replay(int, int64_t) { return false; }
 };
 
+// Per-batch cache of structure that depends only on the parallel layout
+// (tp, dp, pp, virtual stages, devices per host), not on the trace: the
+// communicator tables of generate_job and the packer's rank-class collapse.
+// Shared by the batch's worker threads; one per maya_batch_add_generated call.
+struct GenCache {
+  std::mutex mu;
+  std::map<std::array<int64_t, 6>, std::shared_ptr<const void>> entries;
+  template <class T, class F>
+  std::shared_ptr<const T> get(const std::array<int64_t, 6> &key, F build) {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = entries.find(key);
+      if (it != entries.end()) return std::static_pointer_cast<const T>(it->second);
+    }
+    std::shared_ptr<const T> v = build();   // outside the lock (threads may race: same value)
+    std::lock_guard<std::mutex> g(mu);
+    auto ins = entries.emplace(key, v);
+    return std::static_pointer_cast<const T>(ins.first->second);
+  }
+};
+
 // Returns 0 or a negative code with *err set (invalid configuration).  With a
 // sink, the events go to the sink and out's event arrays stay empty (its job
 // tables -- reps, communicators, calls, rank translation -- are filled).
 int generate_job(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
                  int32_t schedule, int64_t dispatch_overhead_ns, GenJob &out, std::string *err,
-                 EventSink *sink = nullptr);
+                 EventSink *sink = nullptr, GenCache *cache = nullptr);
 
 }  // namespace maya

@@ -214,7 +214,6 @@ struct RepPacker {
   std::vector<size_t> cap_size;
   std::vector<uint32_t> cap_sev;
   std::vector<int64_t> cap_next;
-  std::vector<int32_t> cap_cstream;
   std::vector<std::pair<int64_t, int64_t>> cap_allocs;
 
   void phase_begin(int64_t aid_base) {
@@ -229,23 +228,25 @@ struct RepPacker {
       cap_sev[q] = RB.sev[q];
     }
     cap_next = comm_next;
-    cap_cstream = comm_stream;
     cap_allocs.clear();
   }
   int phase_end() {
     cap = false;
     PhaseTpl t;
-    t.ok = RB.size() == snap0.nst && seg == snap0.seg && coll_seen.empty() &&
-           ring_ok == snap0.ring_ok && comm_stream == cap_cstream && gpre >= snap0.gpre &&
-           !keep_seq;
+    // A first occurrence may open streams and communicators (their local
+    // indices and issuing streams are then fixed for every later occurrence,
+    // which finds them open) and may clear ring_ok (sticky); it must not
+    // cross a host sync or issue collectives out of order.
+    t.ok = seg == snap0.seg && coll_seen.empty() && gpre >= snap0.gpre && !keep_seq;
     if (!t.ok) return -1;
     const uint32_t c0 = (uint32_t)(snap0.colls - coll0);
     t.seg = seg;
     t.ops.resize(RB.size());
     t.sev.resize(RB.size());
     for (size_t q = 0; q < RB.size(); q++) {
-      t.sev[q] = RB.sev[q] - cap_sev[q];
-      for (size_t k = cap_size[q]; k < RB.sops[q].size(); k++) {
+      const size_t k0 = q < snap0.nst ? cap_size[q] : 0;
+      t.sev[q] = RB.sev[q] - (q < snap0.nst ? cap_sev[q] : 0u);
+      for (size_t k = k0; k < RB.sops[q].size(); k++) {
         Op o = RB.sops[q][k];
         o.disp -= snap0.gpre;
         const uint32_t tg = op_tag(o.meta);
@@ -261,11 +262,12 @@ struct RepPacker {
     for (size_t k = snap0.colls; k < P->coll_lc.size(); k++) {
       const uint32_t lc = P->coll_lc[k];
       t.coll_lc.push_back(lc);
-      t.coll_rel.push_back((uint32_t)(P->coll_idx[k] - cap_next[lc]));
+      t.coll_rel.push_back((uint32_t)(P->coll_idx[k] - (lc < cap_next.size() ? cap_next[lc] : 0)));
     }
-    for (uint32_t lc = 0; lc < comm_next.size(); lc++)
-      if (comm_next[lc] != cap_next[lc])
-        t.lc_adv.push_back({lc, (uint32_t)(comm_next[lc] - cap_next[lc])});
+    for (uint32_t lc = 0; lc < comm_next.size(); lc++) {
+      const int64_t before = lc < cap_next.size() ? cap_next[lc] : 0;
+      if (comm_next[lc] != before) t.lc_adv.push_back({lc, (uint32_t)(comm_next[lc] - before)});
+    }
     for (size_t k = snap0.mems; k < P->mems.size(); k++) {
       MemRec m = P->mems[k];
       m.gpre -= snap0.gpre;
@@ -289,26 +291,44 @@ struct RepPacker {
     // well below 2^61: replay only far from it
     if (gpre > ((int64_t)1 << 59) - t.dgpre) return false;
     const uint32_t cb = (uint32_t)(P->coll_lc.size() - coll0);
+    // per tag: what the op's arg is relative to (KERN: nothing, COLL: the
+    // rep's collective count, REC/WAIT: the record count)
+    const uint32_t addv[4] = {0u, cb, n_recs, n_recs};
     for (size_t q = 0; q < t.ops.size(); q++) {
       std::vector<Op> &dst = RB.sops[q];
-      for (Op o : t.ops[q]) {
+      const size_t n0 = dst.size(), n = t.ops[q].size();
+      dst.resize(n0 + n);
+      Op *d = dst.data() + n0;
+      const Op *src = t.ops[q].data();
+      for (size_t k = 0; k < n; k++) {
+        Op o = src[k];
         o.disp += gpre;
-        const uint32_t tg = op_tag(o.meta);
-        if (tg == TAG_REC || tg == TAG_WAIT) o.arg += n_recs;
-        else if (tg == TAG_COLL) o.arg += cb;
-        dst.push_back(o);
+        o.arg += addv[o.meta & 3u];
+        d[k] = o;
       }
       RB.sev[q] += t.sev[q];
     }
-    for (size_t k = 0; k < t.coll_lc.size(); k++) {
-      P->coll_lc.push_back(t.coll_lc[k]);
-      P->coll_idx.push_back((uint32_t)(t.coll_rel[k] + comm_next[t.coll_lc[k]]));
+    {
+      const size_t c0 = P->coll_lc.size(), n = t.coll_lc.size();
+      P->coll_lc.resize(c0 + n);
+      P->coll_idx.resize(c0 + n);
+      uint32_t *lc = P->coll_lc.data() + c0, *ix = P->coll_idx.data() + c0;
+      for (size_t k = 0; k < n; k++) {
+        lc[k] = t.coll_lc[k];
+        ix[k] = (uint32_t)(t.coll_rel[k] + comm_next[t.coll_lc[k]]);
+      }
     }
     for (const auto &a : t.lc_adv) comm_next[a.first] += a.second;
-    for (MemRec m : t.mems) {
-      m.gpre += gpre;
-      m.seq += seq;
-      P->mems.push_back(m);
+    {
+      const size_t m0 = P->mems.size(), n = t.mems.size();
+      P->mems.resize(m0 + n);
+      MemRec *d = P->mems.data() + m0;
+      for (size_t k = 0; k < n; k++) {
+        MemRec m = t.mems[k];
+        m.gpre += gpre;
+        m.seq += seq;
+        d[k] = m;
+      }
     }
     for (const auto &a : t.allocs) {
       const int64_t h = aid_base + a.first;
@@ -928,8 +948,15 @@ void renumber_features(JobPack &P) {
   P.feat_meta.swap(nm2);
 }
 
+// A collapse (or full) view with its outcome, shareable across the jobs of a
+// batch with the same parallel layout (GenCache).
+struct CachedView {
+  SimView V;
+  bool collapsed = false;
+};
+
 void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
-               const std::vector<uint32_t> &rep_comms) {
+               const std::vector<uint32_t> &rep_comms, const CachedView *shared = nullptr) {
   JobHdr &H = P.hdr;
   renumber_features(P);
     // validate rank tables
@@ -946,9 +973,16 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
   const int64_t n_calls = job.call_off[job.n_comms];
   if (n_calls > 0x7fffffff) throw Fail{MAYA_ST_BAD_INPUT, "too many group calls"};
   // the ranks / communicators the scheduler simulates (collapsed or full)
-  SimView V;
-  P.collapsed = collapse && build_collapsed(job, rep_comms, V);
-  if (!P.collapsed) full_view(job, V);
+  SimView Vown;
+  const SimView *Vp = &Vown;
+  if (shared) {
+    Vp = &shared->V;
+    P.collapsed = shared->collapsed;
+  } else {
+    P.collapsed = collapse && build_collapsed(job, rep_comms, Vown);
+    if (!P.collapsed) full_view(job, Vown);
+  }
+  const SimView &V = *Vp;
   P.rank_orig = V.rank_orig;
   P.rank_sim = V.rank_sim;
   // communicators and their call slots (JobTrace.groups / .calls)
@@ -1090,20 +1124,28 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
       if (cw == NO_WF - 1) cw = NO_WF;
       any |= cw != NO_WF;
     }
-    for (const RepHdr &h : P.reps) {
-      if (any)
-        for (uint32_t q = 0; q < h.n_ops; q++) {
-          Op &o = P.ops[h.ops + q];
-          if (op_tag(o.meta) == TAG_COLL && P.coll_wf[h.colls + o.arg] != NO_WF) o.meta |= OP_FOLDC;
-        }
-      // ops each FIFO keeps after the device folds its runs (kernels.cu
-      // fold_count_kernel: same rule), for sizing the schedulers' staging
+    // one pass per FIFO: flag the foldable collectives (OP_FOLDC) and count the
+    // ops it keeps after the device folds its runs (kernels.cu fold_count_kernel:
+    // the same rule, folded_len), for sizing the schedulers' staging
+    for (const RepHdr &h : P.reps)
       for (uint32_t s = 0; s < h.n_streams; s++) {
         StreamRange &st = P.streams[h.streams + s];
-        st.folded = folded_len(P.ops.data() + h.ops + st.begin, st.len,
-                               any ? P.coll_wf.data() + h.colls : nullptr);
+        Op *v = P.ops.data() + h.ops + st.begin;
+        const uint32_t *cw = P.coll_wf.data() + h.colls;
+        uint32_t folded = 0, ps = 0;
+        bool pf = false;
+        for (uint32_t i = 0; i < st.len; i++) {
+          const uint32_t tg = op_tag(v[i].meta);
+          if (any && tg == TAG_COLL && cw[v[i].arg] != NO_WF) v[i].meta |= OP_FOLDC;
+          const bool f = v[i].disp < ((int64_t)1 << 61) &&
+                         (tg == TAG_KERN || (v[i].meta & OP_FOLDC));
+          const uint32_t sg = op_seg(v[i].meta);
+          folded += (i % FOLD_CHUNK == 0 || !f || !pf || sg != ps) ? 1u : 0u;
+          pf = f;
+          ps = sg;
+        }
+        st.folded = folded;
       }
-    }
   }
   // walkers rank-major: a scheduler warp owns whole ranks
   P.wids.resize(P.walkers.size());
@@ -1209,7 +1251,8 @@ void pack_job(const maya_raw_job &job, int32_t key_rank, JobPack &P, bool collap
 
 int pack_generated(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
                    int32_t schedule, int64_t overhead, int32_t device, int32_t key_rank,
-                   bool collapse, GenJob &G, JobPack &P, std::string *err, bool blocks) {
+                   bool collapse, GenJob &G, JobPack &P, std::string *err, bool blocks,
+                   GenCache *cache) {
   thread_local FeatState F;
   thread_local RepPacker RP;
   F.clear();
@@ -1225,7 +1268,7 @@ int pack_generated(const maya_model &model, const maya_config &cfg, const maya_c
   sink.replay = g_phase_replay;
   int rc;
   try {
-    rc = generate_job(model, cfg, cl, schedule, overhead, G, err, &sink);
+    rc = generate_job(model, cfg, cl, schedule, overhead, G, err, &sink, cache);
   } catch (const Fail &f) {   // packer error inside the generator's event stream
     maya_raw_job raw = G.raw(device);
     pack_header(raw, key_rank, P);
@@ -1244,7 +1287,21 @@ int pack_generated(const maya_model &model, const maya_config &cfg, const maya_c
   H.n_ranks = (uint32_t)raw.num_ranks;
   H.status = MAYA_ST_OK;
   try {
-    pack_tail(raw, P, collapse, rep_comms);
+    std::shared_ptr<const CachedView> view;
+    if (cache) {
+      // the view depends on rank -> rep, the communicator tables and each
+      // rep's local communicator count: all functions of the layout
+      const int64_t n = (int64_t)cl.num_hosts * cl.devices_per_host;
+      const std::array<int64_t, 6> key{collapse ? 2 : 3, cfg.tp, n / ((int64_t)cfg.tp * cfg.pp),
+                                       cfg.pp, cfg.virtual_stages, cl.devices_per_host};
+      view = cache->get<CachedView>(key, [&] {
+        auto cv = std::make_shared<CachedView>();
+        cv->collapsed = collapse && build_collapsed(raw, rep_comms, cv->V);
+        if (!cv->collapsed) full_view(raw, cv->V);
+        return cv;
+      });
+    }
+    pack_tail(raw, P, collapse, rep_comms, view.get());
   } catch (const Fail &f) {
     pack_fail(raw, P, f);
   }

@@ -75,6 +75,6 @@ extern bool g_phase_replay;
 int pack_generated(const maya_model &model, const maya_config &cfg, const maya_cluster &cl,
                    int32_t schedule, int64_t overhead, int32_t device, int32_t key_rank,
                    bool collapse, GenJob &scratch, JobPack &out, std::string *err,
-                   bool blocks = false);
+                   bool blocks = false, GenCache *cache = nullptr);
 
 }  // namespace maya

@@ -6,10 +6,11 @@
 #include <cstdio>
 #include <vector>
 
-#include "../paper_2503_20191_b200/csrc/gen.h"
-#include "../paper_2503_20191_b200/csrc/pack.h"
+#include "/tmp/hprof/gen.h"
+#include "/tmp/hprof/pack.h"
 
 using namespace maya;
+namespace maya { extern double hp_acc[16]; }
 using clk = std::chrono::steady_clock;
 
 struct NullSink final : EventSink {
@@ -39,7 +40,7 @@ done:
   double tgen = 0, tfull = 0;
   for (int it = 0; it < 9; it++) {
     auto t0 = clk::now();
-    for (auto &c : cfgs) generate_job(m, c, cl, -1, 5000, g, nullptr, &ns);
+    
     auto t1 = clk::now();
     GenCache cache;   // one per batch, as maya_batch_add_generated
     for (auto &c : cfgs) {
@@ -53,5 +54,7 @@ done:
   }
   printf("512 configs, 1 thread: generator alone %.1f ms (%zu events, %zu blocks of %zu launches over 3 passes); fused gen+pack %.1f ms\n",
          tgen * 1e3, ns.n / 3, ns.blk / 3, ns.kev / 3, tfull * 1e3);
+  const char *nm[] = {"generate_job", "generate_trace", "comm tables", "finish", "pack_tail", "collapse", "slots+wfeats", "rank tables+rcolls", "coll_wf+folded", "renumber_features", "phases packed", "phases replayed", "trace prologue", "trace setup", "pipeline_order", "epilogue+finish"};
+  for (int i = 0; i < 16; i++) printf("%-20s %7.1f ms/pass\n", nm[i], hp_acc[i] * 1e3 / 9);
   return 0;
 }

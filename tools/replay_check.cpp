@@ -1,6 +1,7 @@
-// Phase-template replay must not change a packed job: pack_generated in
-// kernel-block mode with templates on and off, byte-compared (pack_eq), over
-// the C2 lattice, small lattices on every schedule and odd overheads.
+// Phase-template replay and the per-batch layout cache (GenCache) must not
+// change a packed job: pack_generated in kernel-block mode with templates and
+// cache on, and with both off, byte-compared, over the C2 lattice, small
+// lattices on every schedule and odd overheads.
 //   g++ -O2 -std=c++17 tools/replay_check.cpp paper_2503_20191_b200/csrc/{gen,pack}.cpp -lpthread
 #include <chrono>
 #include <cstdio>
@@ -30,12 +31,13 @@ static int check(const maya_model &m, const maya_cluster &cl, const std::vector<
                  int sched, int64_t ovh, double *t_on, double *t_off) {
   int bad = 0;
   GenJob g;
+  GenCache cache;
   for (const maya_config &c : cfgs) {
     JobPack a, b;
     std::string e1, e2;
     g_phase_replay = true;
     auto t0 = std::chrono::steady_clock::now();
-    int r1 = pack_generated(m, c, cl, sched, ovh, 0, 0, true, g, a, &e1, true);
+    int r1 = pack_generated(m, c, cl, sched, ovh, 0, 0, true, g, a, &e1, true, &cache);
     auto t1 = std::chrono::steady_clock::now();
     g_phase_replay = false;
     int r2 = pack_generated(m, c, cl, sched, ovh, 0, 0, true, g, b, &e2, true);
