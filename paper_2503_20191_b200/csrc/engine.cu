@@ -1,6 +1,7 @@
 // C ABI of the engine (include/maya_b200.h): batch assembly, upload, run,
 // results, search reduction, timeline.
 #include <cuda_runtime.h>
+#include <chrono>
 
 #include <algorithm>
 #include <cstdlib>
@@ -566,6 +567,14 @@ int maya_batch_collapsed(maya_engine *e, uint8_t *out) {
 }
 
 int maya_upload(maya_engine *e) {
+  static const bool dbg_t = getenv("MAYA_DEBUG_UPLOAD") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t_up0 = now();
+  auto lap = [&](const char *what) {
+    if (dbg_t)
+      fprintf(stderr, "upload %-10s %.3f ms\n", what,
+              std::chrono::duration<double>(now() - t_up0).count() * 1e3);
+  };
   CU(cudaSetDevice(e->device));
   const size_t nj = e->packs.size();
   // totals
@@ -615,6 +624,7 @@ int maya_upload(maya_engine *e) {
     }
   }
   e->rank_seg.push_back(n_tl);
+  lap("totals");
   // scheduler plans (lane kernel unless disabled or the job does not fit it)
   std::vector<LanePlan> plans(nj);
   size_t n_perm = 0;
@@ -780,6 +790,7 @@ int maya_upload(maya_engine *e) {
     e->d_scratch_cap = cap;
   }
   char *H = (char *)e->h_arena;
+  lap("plans");
   // job order: grouped by scheduler variant, largest work first in each group
   // (LPT over the CTA scheduler)
   {
@@ -911,6 +922,7 @@ int maya_upload(maya_engine *e) {
     if (!e->grid_parts.empty())
       memcpy(H + e->s_grid_parts.off, e->grid_parts.data(), e->grid_parts.size() * sizeof(GridPart));
   }
+  lap("layout");
   auto copy_job = [&](size_t j) {
     const JobPack &P = e->packs[j];
     const Base &B = bases[j];
@@ -1066,7 +1078,9 @@ int maya_upload(maya_engine *e) {
     };
     WorkerPool::get().run(nt, work);
   }
+  lap("copy");
   CU(cudaMemcpyAsync(e->d_arena, e->h_arena, e->arena_bytes, cudaMemcpyHostToDevice, e->stream));
+  lap("h2d");
   // device view
   char *D = (char *)e->d_arena;
   char *X = (char *)e->d_scratch;

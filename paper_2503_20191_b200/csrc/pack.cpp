@@ -194,6 +194,7 @@ struct RepPacker {
     bool ok = false;
     uint32_t seg = 0;
     std::vector<std::vector<Op>> ops;        // per local stream, relative fields
+    size_t nst = 0;                          // local streams the template covers
     std::vector<uint32_t> sev;               // per local stream: device events added
     std::vector<uint32_t> coll_lc, coll_rel; // new collective entries (call_idx - comm_next)
     std::vector<std::pair<uint32_t, uint32_t>> lc_adv;   // (lc, calls issued)
@@ -202,7 +203,8 @@ struct RepPacker {
     int64_t dgpre = 0;
     uint32_t dseq = 0, ddevev = 0, drecs = 0;
   };
-  std::vector<PhaseTpl> tpls;
+  std::vector<PhaseTpl> tpls;   // the first ntpl are this rep's (objects reused: no
+  size_t ntpl = 0;              // allocation per rep)
   bool cap = false;
   int64_t cap_aid = 0;
   struct Snap {
@@ -232,7 +234,16 @@ struct RepPacker {
   }
   int phase_end() {
     cap = false;
-    PhaseTpl t;
+    if (ntpl == tpls.size()) tpls.emplace_back();
+    PhaseTpl &t = tpls[ntpl];
+    t.ok = false;
+    for (auto &v : t.ops) v.clear();
+    t.sev.clear();
+    t.coll_lc.clear();
+    t.coll_rel.clear();
+    t.lc_adv.clear();
+    t.mems.clear();
+    t.allocs.clear();
     // A first occurrence may open streams and communicators (their local
     // indices and issuing streams are then fixed for every later occurrence,
     // which finds them open) and may clear ring_ok (sticky); it must not
@@ -241,7 +252,8 @@ struct RepPacker {
     if (!t.ok) return -1;
     const uint32_t c0 = (uint32_t)(snap0.colls - coll0);
     t.seg = seg;
-    t.ops.resize(RB.size());
+    if (t.ops.size() < RB.size()) t.ops.resize(RB.size());
+    t.nst = RB.size();
     t.sev.resize(RB.size());
     for (size_t q = 0; q < RB.size(); q++) {
       const size_t k0 = q < snap0.nst ? cap_size[q] : 0;
@@ -279,14 +291,13 @@ struct RepPacker {
     t.dseq = seq - snap0.seq;
     t.ddevev = n_devev - snap0.devev;
     t.drecs = n_recs - snap0.recs;
-    tpls.push_back(std::move(t));
-    return (int)tpls.size() - 1;
+    return (int)ntpl++;
   }
   // stamp template `id` at the current state; false: not here (the caller
   // emits the phase event by event)
   bool phase_replay(int id, int64_t aid_base) {
     const PhaseTpl &t = tpls[id];
-    if (seg != t.seg || t.ops.size() > RB.size()) return false;
+    if (seg != t.seg || t.nst > RB.size()) return false;
     // the run-folding limit and block fits (kernel_block) assume gap prefixes
     // well below 2^61: replay only far from it
     if (gpre > ((int64_t)1 << 59) - t.dgpre) return false;
@@ -294,7 +305,7 @@ struct RepPacker {
     // per tag: what the op's arg is relative to (KERN: nothing, COLL: the
     // rep's collective count, REC/WAIT: the record count)
     const uint32_t addv[4] = {0u, cb, n_recs, n_recs};
-    for (size_t q = 0; q < t.ops.size(); q++) {
+    for (size_t q = 0; q < t.nst; q++) {
       std::vector<Op> &dst = RB.sops[q];
       const size_t n0 = dst.size(), n = t.ops[q].size();
       dst.resize(n0 + n);
@@ -347,7 +358,7 @@ struct RepPacker {
   }
 
   void begin(JobPack &pk, FeatState &fs, int32_t dev, bool on_the_fly, size_t reserve_hint) {
-    tpls.clear();
+    ntpl = 0;
     cap = false;
     keep_seq = true;
     P = &pk;
@@ -358,7 +369,7 @@ struct RepPacker {
     RB.reset(reserve_hint);
     fly = on_the_fly;
     rec.clear();
-    rec_small.clear();
+    for (auto &v : rec_small) v.clear();   // keep the per-event capacity
     n_recs = 0;
     n_local_comms = 0;
     snap.clear();
