@@ -768,24 +768,26 @@ int maya_upload(maya_engine *e) {
   seg(e->x_tl_end, 0);
   e->scratch_bytes = off;
 
+  // pinned host / device arenas grow geometrically (x2): pinning GBs costs
+  // ~1 s, so a search whose batches grow re-pins a few times, not per batch
   if (e->arena_bytes > e->h_arena_cap) {
     if (e->h_arena) cudaFreeHost(e->h_arena);
     e->h_arena = nullptr;
-    size_t cap = align_up(e->arena_bytes + e->arena_bytes / 4, 1 << 20);
+    size_t cap = align_up(std::max(e->arena_bytes + e->arena_bytes / 4, 2 * e->h_arena_cap), 1 << 20);
     CU(cudaMallocHost(&e->h_arena, cap));
     e->h_arena_cap = cap;
   }
   if (e->arena_bytes > e->d_arena_cap) {
     if (e->d_arena) cudaFree(e->d_arena);
     e->d_arena = nullptr;
-    size_t cap = align_up(e->arena_bytes + e->arena_bytes / 4, 1 << 20);
+    size_t cap = align_up(std::max(e->arena_bytes + e->arena_bytes / 4, 2 * e->d_arena_cap), 1 << 20);
     CU(cudaMalloc(&e->d_arena, cap));
     e->d_arena_cap = cap;
   }
   if (e->scratch_bytes > e->d_scratch_cap) {
     if (e->d_scratch) cudaFree(e->d_scratch);
     e->d_scratch = nullptr;
-    size_t cap = align_up(e->scratch_bytes + e->scratch_bytes / 4, 1 << 20);
+    size_t cap = align_up(std::max(e->scratch_bytes + e->scratch_bytes / 4, 2 * e->d_scratch_cap), 1 << 20);
     CU(cudaMalloc(&e->d_scratch, cap));
     e->d_scratch_cap = cap;
   }

@@ -960,6 +960,21 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
       cs = build_comm_struct(C, cfg.virtual_stages, n, cl.devices_per_host);
     }
     if (!cs->error.empty()) throw GenFail{cs->error};
+    if (cache && sink) {   // lazy call tables (GenJob::comm_calls)
+      G.lazy_calls = true;
+      G.comm_nranks = cs->nranks;
+      G.comm_topo = cs->topo;
+      G.comm_first_stage = cs->first_stage;
+      G.comm_first_lc = cs->first_lc;
+      G.rep_calls.resize(rcalls.size());
+      for (size_t k = 0; k < rcalls.size(); k++) G.rep_calls[k] = std::move(rcalls[k].calls);
+      int64_t nc = 0;
+      for (size_t gi = 0; gi < cs->nranks.size(); gi++) nc += (int64_t)G.comm_calls(gi).size();
+      G.n_calls_total = nc;
+      G.rank_comm_off = cs->rank_comm_off;
+      G.rank_comm = cs->rank_comm;
+      return MAYA_OK;
+    }
     G.call_off.push_back(0);
     for (size_t gi = 0; gi < cs->nranks.size(); gi++) {
       G.comm_nranks.push_back(cs->nranks[gi]);

@@ -35,6 +35,31 @@ struct GenJob {
   std::vector<int64_t> rank_comm_off;
   std::vector<int32_t> rank_comm;
   std::string comm_blob;  // comm names joined by '\n'
+  // Lazy call tables (fused path with a GenCache): every communicator's call
+  // table is the call list of its position-0 member's representative at that
+  // member's local communicator index (collate.py:323-340), so the per-comm
+  // tables (thousands of communicators at 2,048 ranks) are not materialised:
+  // call_off / call_kind / call_bytes stay empty and readers go through
+  // rep_calls[comm_first_stage[g]][comm_first_lc[g]] (materialize_calls()
+  // builds the arrays when a reader needs them).
+  bool lazy_calls = false;
+  std::vector<std::vector<std::vector<std::pair<int8_t, int64_t>>>> rep_calls;
+  std::vector<int32_t> comm_first_stage, comm_first_lc;
+  int64_t n_calls_total = 0;
+  const std::vector<std::pair<int8_t, int64_t>> &comm_calls(size_t g) const {
+    return rep_calls[comm_first_stage[g]][comm_first_lc[g]];
+  }
+  void materialize_calls() {
+    if (!lazy_calls || !call_off.empty()) return;
+    call_off.push_back(0);
+    for (size_t g = 0; g < comm_first_stage.size(); g++) {
+      for (const auto &kb : comm_calls(g)) {
+        call_kind.push_back(kb.first);
+        call_bytes.push_back(kb.second);
+      }
+      call_off.push_back((int64_t)call_kind.size());
+    }
+  }
 
   maya_raw_job raw(int32_t device) const;
   void clear() {
@@ -43,6 +68,8 @@ struct GenJob {
     rep_ranks.clear(); rank_rep.clear(); ev_off.clear(); ev_kind.clear(); ev_stream.clear();
     ev_f.clear(); comm_names.clear(); comm_nranks.clear(); comm_topo.clear(); call_off.clear();
     call_kind.clear(); call_bytes.clear(); rank_comm_off.clear(); rank_comm.clear();
+    lazy_calls = false; rep_calls.clear(); comm_first_stage.clear(); comm_first_lc.clear();
+    n_calls_total = 0;
     comm_blob.clear();
   }
 };

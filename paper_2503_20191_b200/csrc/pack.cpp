@@ -766,8 +766,13 @@ uint64_t mix64(uint64_t h, uint64_t v) {
   return h * 0xff51afd7ed558ccdull;
 }
 
+// lazy: the job's call tables live in the generator (GenJob lazy_calls); then
+// *structural reports whether every identified pair of communicators takes its
+// calls from the same (representative, local index) -- equal for every
+// configuration of the layout, so the view is shareable (GenCache).
 bool build_collapsed(const maya_raw_job &job, const std::vector<uint32_t> &rep_comms,
-                     SimView &V) {
+                     SimView &V, const GenJob *lazy = nullptr, bool *structural = nullptr) {
+  if (structural) *structural = true;
   const int R = job.num_ranks, G = job.n_comms;
   if (R <= 1) return false;
   std::vector<std::vector<int32_t>> members(G);
@@ -884,13 +889,21 @@ bool build_collapsed(const maya_raw_job &job, const std::vector<uint32_t> &rep_c
     const int32_t sg = it->second, g0 = V.comm_real[sg];
     if (job.comm_topo[g] != job.comm_topo[g0] || job.comm_nranks[g] != job.comm_nranks[g0])
       return false;
-    const int64_t n0 = job.call_off[g0 + 1] - job.call_off[g0];
-    if (job.call_off[g + 1] - job.call_off[g] != n0) return false;
-    for (int64_t i = 0; i < n0; i++) {
-      const int64_t a = job.call_off[g] + i, b = job.call_off[g0] + i;
-      if (job.call_kind[a] != job.call_kind[b] || job.call_bytes[a] != job.call_bytes[b])
-        return false;
-      if (job.wire_ns && job.wire_ns[a] != job.wire_ns[b]) return false;
+    if (lazy) {
+      if (lazy->comm_first_stage[g] != lazy->comm_first_stage[g0] ||
+          lazy->comm_first_lc[g] != lazy->comm_first_lc[g0]) {
+        if (structural) *structural = false;
+        if (lazy->comm_calls(g) != lazy->comm_calls(g0)) return false;
+      }
+    } else {
+      const int64_t n0 = job.call_off[g0 + 1] - job.call_off[g0];
+      if (job.call_off[g + 1] - job.call_off[g] != n0) return false;
+      for (int64_t i = 0; i < n0; i++) {
+        const int64_t a = job.call_off[g] + i, b = job.call_off[g0] + i;
+        if (job.call_kind[a] != job.call_kind[b] || job.call_bytes[a] != job.call_bytes[b])
+          return false;
+        if (job.wire_ns && job.wire_ns[a] != job.wire_ns[b]) return false;
+      }
     }
     for (int32_t m : members[g]) cls_of[sg].push_back(color[m]);
   }
@@ -964,10 +977,12 @@ void renumber_features(JobPack &P) {
 struct CachedView {
   SimView V;
   bool collapsed = false;
+  bool shareable = true;   // false: each job of the layout computes its own view
 };
 
 void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
-               const std::vector<uint32_t> &rep_comms, const CachedView *shared = nullptr) {
+               const std::vector<uint32_t> &rep_comms, const CachedView *shared = nullptr,
+               const GenJob *lazy = nullptr) {
   JobHdr &H = P.hdr;
   renumber_features(P);
     // validate rank tables
@@ -981,7 +996,7 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
       if (job.rank_comm[q] < 0 || job.rank_comm[q] >= job.n_comms)
         throw Fail{MAYA_ST_BAD_INPUT, "rank_comm out of range"};
   }
-  const int64_t n_calls = job.call_off[job.n_comms];
+  const int64_t n_calls = lazy ? lazy->n_calls_total : job.call_off[job.n_comms];
   if (n_calls > 0x7fffffff) throw Fail{MAYA_ST_BAD_INPUT, "too many group calls"};
   // the ranks / communicators the scheduler simulates (collapsed or full)
   SimView Vown;
@@ -990,7 +1005,7 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
     Vp = &shared->V;
     P.collapsed = shared->collapsed;
   } else {
-    P.collapsed = collapse && build_collapsed(job, rep_comms, Vown);
+    P.collapsed = collapse && build_collapsed(job, rep_comms, Vown, lazy);
     if (!P.collapsed) full_view(job, Vown);
   }
   const SimView &V = *Vp;
@@ -999,6 +1014,19 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
   // communicators and their call slots (JobTrace.groups / .calls)
   for (size_t sg = 0; sg < V.comm_real.size(); sg++) {
     const int g = V.comm_real[sg];
+    if (lazy) {   // the generator's call list of the comm (no wire_ns on this path)
+      const auto &calls = lazy->comm_calls(g);
+      CommRec cr{job.comm_nranks[g], job.comm_topo[g], (uint32_t)P.slots.size(),
+                 (uint32_t)calls.size()};
+      if (cr.topo < 0 || cr.topo > 2) throw Fail{MAYA_ST_BAD_INPUT, "topology class"};
+      P.comms.push_back(cr);
+      P.comm_rdv.push_back(V.comm_rdv[sg]);
+      for (const auto &kb : calls) {
+        if (kb.first > 4) throw Fail{MAYA_ST_BAD_INPUT, "collective kind"};
+        P.slots.push_back(SlotRec{kb.second, -1, kb.first, cr.nranks, cr.topo, job.device});
+      }
+      continue;
+    }
     CommRec cr{job.comm_nranks[g], job.comm_topo[g], (uint32_t)P.slots.size(),
                (uint32_t)(job.call_off[g + 1] - job.call_off[g])};
     if (cr.topo < 0 || cr.topo > 2) throw Fail{MAYA_ST_BAD_INPUT, "topology class"};
@@ -1299,20 +1327,28 @@ int pack_generated(const maya_model &model, const maya_config &cfg, const maya_c
   H.status = MAYA_ST_OK;
   try {
     std::shared_ptr<const CachedView> view;
-    if (cache) {
-      // the view depends on rank -> rep, the communicator tables and each
-      // rep's local communicator count: all functions of the layout
+    const GenJob *lazy = G.lazy_calls ? &G : nullptr;
+    if (cache && lazy) {
+      // The view depends on rank -> rep, the communicator tables, each rep's
+      // local communicator count -- functions of the layout -- and on the
+      // identified communicators having equal call tables, which holds for
+      // every configuration of the layout when each identified pair takes its
+      // calls from the same (representative, local index); otherwise each job
+      // builds its own (shareable = false).
       const int64_t n = (int64_t)cl.num_hosts * cl.devices_per_host;
       const std::array<int64_t, 6> key{collapse ? 2 : 3, cfg.tp, n / ((int64_t)cfg.tp * cfg.pp),
                                        cfg.pp, cfg.virtual_stages, cl.devices_per_host};
       view = cache->get<CachedView>(key, [&] {
         auto cv = std::make_shared<CachedView>();
-        cv->collapsed = collapse && build_collapsed(raw, rep_comms, cv->V);
+        bool structural = true;
+        cv->collapsed = collapse && build_collapsed(raw, rep_comms, cv->V, lazy, &structural);
         if (!cv->collapsed) full_view(raw, cv->V);
+        cv->shareable = structural;
         return cv;
       });
+      if (!view->shareable) view.reset();
     }
-    pack_tail(raw, P, collapse, rep_comms, view.get());
+    pack_tail(raw, P, collapse, rep_comms, view.get(), lazy);
   } catch (const Fail &f) {
     pack_fail(raw, P, f);
   }

@@ -79,4 +79,4 @@ p=rep(p,"""  // walkers rank-major: a scheduler warp owns whole ranks""","""  ma
   // walkers rank-major: a scheduler warp owns whole ranks""")
 open('/tmp/hprof/pack.cpp','w').write(p)
 EOF
-g++ -O2 -std=c++17 -I/root/repo/include /root/repo/tools/hostprof/hpp.cpp /tmp/hprof/gen.cpp /tmp/hprof/pack.cpp -lpthread -o /tmp/hpp && /tmp/hpp
+g++ -O2 -std=c++17 -I/root/repo/include /root/repo/tools/hostprof/${HPP:-hpp}.cpp /tmp/hprof/gen.cpp /tmp/hprof/pack.cpp -lpthread -o /tmp/hpp && /tmp/hpp

@@ -81,6 +81,26 @@ int main() {
         n += (int)cfgs.size();
       }
   }
+  {  // C3 / C4 shapes at 64-2,048 ranks (a sample of each lattice)
+    maya_model c3{40, 6144, 2048, 51200, 0, 0}, c4{80, 8192, 8192, 128256, 0, 0};
+    for (int ranks : {64, 256, 1024, 2048}) {
+      maya_cluster cl{ranks / 8, 8, 80ll << 30};
+      for (int which = 0; which < 2; which++) {
+        const maya_model &m = which ? c4 : c3;
+        std::vector<maya_config> cfgs;
+        int k = 0;
+        for (int tp : {1, 2, 4, 8}) for (int pp : {1, 2, 4, 8, 16}) for (int mm : {1, 3, 8})
+          for (int vs : {1, 2, 4, 5, 10}) for (int rc : {0, 1}) for (int dz : {0, 1}) {
+            if ((k++ % 7) != 0) continue;
+            maya_config c{tp, pp, mm, vs, rc, which ? 1 : rc, dz, 0, which ? 4096 : 2048};
+            GenJob g;
+            if (generate_job(m, c, cl, -1, 5000, g, nullptr) == 0) cfgs.push_back(c);
+          }
+        bad += check(m, cl, cfgs, -1, 5000, &on, &off);
+        n += (int)cfgs.size();
+      }
+    }
+  }
   printf("%d packs compared, %d mismatches; replay %.1f ms, event-by-event %.1f ms\n", n, bad,
          on * 1e3, off * 1e3);
   return bad != 0;
