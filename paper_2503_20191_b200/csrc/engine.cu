@@ -128,7 +128,8 @@ struct maya_engine {
       s_coll_lc, s_coll_idx, s_coll_wf, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
       s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks, s_grid_parts, s_comm_part, s_blocks,
       s_blk_fids;
-  Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst, x_gsync;
+  Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst, x_gsync, x_macros;
+  uint32_t chain_first = 0, chain_jobs = 0;   // chain jobs: the tail of the job order
   std::vector<GridPart> grid_parts;        // host copy (launch grouping)
   std::vector<std::pair<uint32_t, uint32_t>> grid_launches;   // part ranges per launch
   uint32_t grid_smem = 0;
@@ -251,11 +252,12 @@ bool plan_grid(const JobPack &P, LanePlan &pl) {
   return true;
 }
 
-// Chain-kernel plan (sched_chain.cu): the whole job resident in one warp's
-// shared-memory region -- every FIFO's folded ops, record times, collective
-// rings and rank collective table -- with at most two FIFOs per lane.  Only
-// for jobs whose collectives rendezvous in rings (JOB_RING).  n_slots carries
-// the job's folded op count (the region's op area).
+// Chain-kernel plan (sched_chain.cu): the whole job resident in one CTA's
+// shared-memory region -- every FIFO's macro ops (its folded ops fused into
+// [WAIT]? [KERN | COLL]? [REC]? groups), record times, collective rings and
+// rank collective table -- one FIFO per thread.  Only for jobs whose
+// collectives rendezvous in rings (JOB_RING).  n_slots carries the job's
+// macro op count (the region's op area).
 static const uint64_t CHAIN_WAVE_BYTES = 148ull * 200 * 1024;   // ~one wave of chain CTAs
 
 LanePlan plan_chain(const JobPack &P) {
@@ -264,10 +266,10 @@ LanePlan plan_chain(const JobPack &P) {
   const uint32_t nc = (uint32_t)P.comms.size();
   if (P.hdr.status != MAYA_ST_OK || W == 0 || W > CHAIN_MAX_FIFOS) return pl;
   if (!(P.hdr.flags & JOB_RING) || nc > RING_MAX_COMMS) return pl;
-  uint64_t n_ops = 0;
+  uint64_t n_ops = 0;   // macro ops (soa.h ChainMacro) of the job's FIFOs
   for (uint32_t w = 0; w < W; w++) {
     const Walker wk = P.walkers[w];
-    n_ops += P.streams[P.reps[P.ranks[wk.rank].rep].streams + wk.stream].folded;
+    n_ops += P.stream_macros[P.reps[P.ranks[wk.rank].rep].streams + wk.stream];
   }
   const ChainLayout L = chain_layout(W, R, nc, P.hdr.n_fire, P.hdr.n_rcolls, n_ops);
   if (L.bytes > CHAIN_REGION[CHAIN_CLASSES - 1]) return pl;
@@ -627,7 +629,7 @@ int maya_upload(maya_engine *e) {
   lap("totals");
   // scheduler plans (lane kernel unless disabled or the job does not fit it)
   std::vector<LanePlan> plans(nj);
-  size_t n_perm = 0;
+  size_t n_perm = 0, n_macros = 0;
   {
     // per-job shared-memory budget: the whole CTA budget for small batches,
     // else enough to keep the batch resident (148 SMs x 228 KB)
@@ -655,6 +657,7 @@ int maya_upload(maya_engine *e) {
         plans[j] = plan_lane(e->packs[j], (uint32_t)budget, (e->options & MAYA_OPT_LANE_SCHED) != 0);
       if (plans[j].variant >= 0 && plans[j].variant != 15)
         n_perm += (size_t)plans[j].per_lane * plans[j].threads;
+      if (plans[j].variant >= 16) n_macros += plans[j].n_slots;
     }
     if (getenv("MAYA_DEBUG_PLAN"))
       for (size_t j = 0; j < nj; j++) {
@@ -748,6 +751,7 @@ int maya_upload(maya_engine *e) {
   seg(e->x_chunk_cnt, n_chunks * sizeof(uint32_t));
   seg(e->x_lctx, n_walkers * 64);
   seg(e->x_lst, n_walkers * 48);
+  seg(e->x_macros, n_macros * sizeof(ChainMacro));
   seg(e->x_gsync, nj * sizeof(GridSync));
   seg(e->x_ccounts, n_counts * sizeof(uint32_t));
   seg(e->x_rcw, n_rcolls * sizeof(RCX));
@@ -836,11 +840,15 @@ int maya_upload(maya_engine *e) {
       }
     }
     memcpy(H + e->s_order.off, order.data(), nj * sizeof(int32_t));
+    // chain jobs (variants 16..) close the order: their macro pass takes that tail
+    e->chain_jobs = 0;
+    for (size_t j = 0; j < nj; j++) e->chain_jobs += var[j] >= 16 ? 1u : 0u;
+    e->chain_first = (uint32_t)(nj - e->chain_jobs);
   }
   // per-job bases (serial prefix), then parallel copy
   struct Base {
     size_t ranks, rank_comm, comms, slots, walkers, reps, ops, streams, colls, syncs, counts,
-        mems, feats, fire, delay, wstate, rcolls, perm, blocks, blk_fids, wfeats;
+        mems, feats, fire, delay, wstate, rcolls, perm, blocks, blk_fids, wfeats, macros;
   };
   std::vector<Base> bases(nj);
   {
@@ -869,6 +877,7 @@ int maya_upload(maya_engine *e) {
       b.rcolls += P.rcolls.size();
       if (plans[j].variant >= 0 && plans[j].variant != 15)
         b.perm += (size_t)plans[j].per_lane * plans[j].threads;
+      if (plans[j].variant >= 16) b.macros += plans[j].n_slots;
       const SchedLayout L = sched_layout((uint32_t)P.walkers.size(), (uint32_t)P.ranks.size(),
                                          (uint32_t)P.comms.size(), (P.hdr.flags & JOB_RING) != 0,
                                          P.hdr.n_fire, P.hdr.n_rcolls, sched_smem_cap());
@@ -992,7 +1001,7 @@ int maya_upload(maya_engine *e) {
     CPY(s_rcolls, rcolls, B.rcolls)
     {  // lane-scheduler plan and per-walker ring words
       const LanePlan &pl = plans[j];
-      LaneJob lj{pl.flags, pl.n_slots, B.walkers, B.perm, pl.per_lane, pl.fc_log2};
+      LaneJob lj{B.macros, pl.flags, pl.n_slots, B.walkers, B.perm, pl.per_lane, pl.fc_log2};
       memcpy(H + e->s_lane_jobs.off + j * sizeof(LaneJob), &lj, sizeof lj);
       if (pl.variant >= 0 && pl.variant != 15 && P.hdr.status == MAYA_ST_OK)
         lane_perm_fill(P, pl, (uint32_t *)(H + e->s_lane_perm.off) + B.perm);
@@ -1008,9 +1017,9 @@ int maya_upload(maya_engine *e) {
         }
         const Walker wk = P.walkers[w];
         const RepHdr &h = P.reps[P.ranks[wk.rank].rep];
-        if (pl.variant >= 16) {   // chain job: the FIFO's first op in the region's op area
+        if (pl.variant >= 16) {   // chain job: the FIFO's first macro op in the job's area
           ws[w] = slot;
-          slot += P.streams[h.streams + wk.stream].folded;
+          slot += P.stream_macros[h.streams + wk.stream];
           continue;
         }
         const uint32_t n = pl.variant >= 3 ? lane_slots_of(P.streams[h.streams + wk.stream].folded,
@@ -1228,6 +1237,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   db.blk_ab = (int64_t *)(X + e->x_blk_ab.off);
   db.lane_gctx = (uint8_t *)(X + e->x_lctx.off);
   db.lane_gst = (uint8_t *)(X + e->x_lst.off);
+  db.macros = (ChainMacro *)(X + e->x_macros.off);
   db.gsync = (GridSync *)(X + e->x_gsync.off);
   db.chunk_cnt = (uint32_t *)(X + e->x_chunk_cnt.off);
   db.ccounts = fold ? (uint32_t *)(X + e->x_ccounts.off) : nullptr;
@@ -1243,6 +1253,10 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   CU(cudaGetLastError());
   launch_resolve(db, e->stream);
   CU(cudaGetLastError());
+  if (fold && e->chain_jobs) {   // chain jobs: macro ops of their folded FIFOs
+    launch_chain_macros(db, db.order + e->chain_first, e->chain_jobs, e->stream);
+    CU(cudaGetLastError());
+  }
   CU(cudaEventRecord(e->ev[2], e->stream));
   {
     // variants run concurrently on their own streams (fork/join)
@@ -1325,7 +1339,8 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
     int64_t n = (db.n_feats ? 1 : 0) + (db.n_wfeats ? 1 : 0) + (db.n_reps ? 1 : 0) +
                 (db.n_rcolls ? 1 : 0);
     if (fold)
-      n += (db.n_blocks ? 1 : 0) + (db.n_chunks ? 2 : 0) + (db.n_reps ? 1 : 0);
+      n += (db.n_blocks ? 1 : 0) + (db.n_chunks ? 2 : 0) + (db.n_reps ? 1 : 0) +
+           (e->chain_jobs ? 1 : 0);
     else
       n += db.n_ops ? 1 : 0;
     for (int v = 0; v < maya_engine::NVAR; v++)

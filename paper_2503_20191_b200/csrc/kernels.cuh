@@ -61,6 +61,7 @@ struct DevBatch {
   const uint32_t *comm_part;  // per comm: the grid part holding all its members, else ~0
   uint8_t *lane_gctx;         // per walker: 64 B FIFO context when not in shared memory
   uint8_t *lane_gst;          // per walker: 48 B FIFO state when LANE_ST_GLOBAL
+  ChainMacro *macros;         // chain jobs, folded runs: each FIFO's macro ops (chain_macro_kernel)
   const FoldChunk *chunks;    // fold work items (one per 1,024 ops of a FIFO)
   uint32_t *chunk_cnt;        // folded ops per chunk
   uint32_t n_chunks;
@@ -107,7 +108,9 @@ void launch_schedule_lane(const DevBatch &b, const int32_t *order, uint32_t n, u
 // grid jobs: parts [p0, p1) of b.grid_parts in one cooperative launch
 int launch_schedule_grid(const DevBatch &b, uint32_t p0, uint32_t p1, int record, uint32_t smem,
                          cudaStream_t s);
-// chain jobs (sched_chain.cu): one warp-sized CTA per job, whole job on chip
+// chain jobs (sched_chain.cu): the macro ops of every FIFO of the n jobs
+// order[0..n) (folded runs), then one CTA per job, whole job on chip
+void launch_chain_macros(const DevBatch &b, const int32_t *order, uint32_t n, cudaStream_t s);
 void launch_schedule_chain(const DevBatch &b, const int32_t *order, uint32_t n, uint32_t threads,
                            int record, uint32_t smem, cudaStream_t s);
 int grid_max_ctas(uint32_t smem);   // co-resident CTAs of the grid kernel at this smem

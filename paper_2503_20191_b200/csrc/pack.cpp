@@ -1163,6 +1163,7 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
       if (cw == NO_WF - 1) cw = NO_WF;
       any |= cw != NO_WF;
     }
+    P.stream_macros.assign(P.streams.size(), 0);
     // one pass per FIFO: flag the foldable collectives (OP_FOLDC) and count the
     // ops it keeps after the device folds its runs (kernels.cu fold_count_kernel:
     // the same rule, folded_len), for sizing the schedulers' staging
@@ -1171,19 +1172,27 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
         StreamRange &st = P.streams[h.streams + s];
         Op *v = P.ops.data() + h.ops + st.begin;
         const uint32_t *cw = P.coll_wf.data() + h.colls;
-        uint32_t folded = 0, ps = 0;
+        uint32_t folded = 0, ps = 0, macros = 0;
         bool pf = false;
+        MacroFuse mf;
         for (uint32_t i = 0; i < st.len; i++) {
           const uint32_t tg = op_tag(v[i].meta);
           if (any && tg == TAG_COLL && cw[v[i].arg] != NO_WF) v[i].meta |= OP_FOLDC;
           const bool f = v[i].disp < ((int64_t)1 << 61) &&
                          (tg == TAG_KERN || (v[i].meta & OP_FOLDC));
           const uint32_t sg = op_seg(v[i].meta);
-          folded += (i % FOLD_CHUNK == 0 || !f || !pf || sg != ps) ? 1u : 0u;
+          if (i % FOLD_CHUNK == 0 || !f || !pf || sg != ps) {   // a folded op starts here
+            folded++;
+            // its class for the chain kernel's macro fusion (kernel: a folded run)
+            const uint32_t cls = f ? 0u : tg == TAG_KERN ? 0u : tg == TAG_COLL ? 1u
+                                 : tg == TAG_REC ? 2u : 3u;
+            macros += mf.push(cls, sg) ? 1u : 0u;
+          }
           pf = f;
           ps = sg;
         }
         st.folded = folded;
+        P.stream_macros[h.streams + s] = macros;
       }
   }
   // walkers rank-major: a scheduler warp owns whole ranks

@@ -181,7 +181,6 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
   }
   const LaneJob LJ = b.lane_jobs[j];
   const uint32_t W = J.n_walkers, R = J.n_ranks;
-  constexpr bool resident = RES;
   const ChainLayout L = chain_layout(W, R, J.n_comms, J.n_fire, J.n_rcolls, LJ.n_slots);
   ChainSh sh;
   sh.J = &J;
@@ -193,7 +192,6 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
   sh.rcx = (const RCX *)(dsm + L.rcx);
   sh.delay = b.delay + J.delay;
   uint64_t *bar = (uint64_t *)(dsm + L.bar);
-  ExecOp *sops = (ExecOp *)(dsm + L.ops);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_u32(bar)), "r"(nt) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -202,18 +200,21 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
   // this thread's FIFO: loop invariants and walker state in registers
   const uint32_t w = b.lane_perm[LJ.perm + tid];
   const bool valid = w != 0xffffffffu;
-  const ExecOp *ops = nullptr;
+  const ExecOp *ops = nullptr;       // global ExecOps (the FIFO's ops, folded when RES)
   const uint32_t *cnt = nullptr;
   uint64_t tl = 0;
   uint32_t len = 0, rank = 0, ns = 0, nsync = 0, fb = 0, rcb = 0, dlb = 0;
-  const ExecOp *src = nullptr;
+  uint32_t nops = 0;                 // the FIFO's (folded) ops
+  uint32_t mac_sm = 0;               // RES: its macro area (shared memory)
+  const ChainMacro *mac_g = nullptr; // RES: its macro ops (global)
+  int err = 0;
   if (valid) {
     const Walker wk = b.walkers[J.walkers + w];
     const RankRec rr = b.ranks[J.ranks + wk.rank];
     const RepHdr &h = b.reps[rr.rep];
     const StreamRange sr = b.streams[h.streams + wk.stream];
-    len = resident ? b.clen[h.streams + wk.stream] : sr.len;
-    cnt = (resident ? b.ccounts : b.counts) + h.counts + wk.stream;
+    nops = RES ? b.clen[h.streams + wk.stream] : sr.len;
+    cnt = (RES ? b.ccounts : b.counts) + h.counts + wk.stream;
     tl = J.timeline + rr.tl + sr.begin;
     rank = wk.rank;
     ns = h.n_streams;
@@ -221,13 +222,21 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
     fb = rr.fire;
     rcb = rr.rslot;
     dlb = rr.delay;
-    src = b.exec + h.ops + sr.begin;
-    ops = resident ? sops + b.lane_wslot[J.walkers + w] : src;
+    ops = b.exec + h.ops + sr.begin;
+    len = nops;
+    if (RES) {   // the FIFO's macro ops (chain_macro_kernel), host-planned count
+      const uint32_t m0 = b.lane_wslot[J.walkers + w];
+      const uint32_t m1 = w + 1 < W ? b.lane_wslot[J.walkers + w + 1] : LJ.n_slots;
+      len = m1 - m0;
+      mac_sm = sm_u32(dsm + L.ops) + m0 * (uint32_t)sizeof(ChainMacro);
+      mac_g = b.macros + LJ.mbase + m0;
+      if (len == 0 && nops > 0) err = MAYA_ST_INTERNAL;   // plan and fold disagree
+    }
   }
-  const uint32_t ops_sm = RES && valid ? sm_u32(ops) : 0u;
   // op streams (each thread its FIFO) and the collective table (thread 0),
   // all bulk copies in flight at once
-  const uint32_t bytes = (resident && valid ? len * 16u : 0u) + (tid == 0 ? J.n_rcolls * 16u : 0u);
+  const uint32_t bytes = (RES && valid ? len * (uint32_t)sizeof(ChainMacro) : 0u) +
+                         (tid == 0 ? J.n_rcolls * 16u : 0u);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_u32(bar)),
                "r"(bytes)
                : "memory");
@@ -237,11 +246,11 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
             "r"(sm_u32(dsm + L.rcx)),
         "l"(b.rcx + J.rcolls), "r"(J.n_rcolls * 16u), "r"(sm_u32(bar))
         : "memory");
-  if (resident && valid && len)
+  if (RES && valid && len)
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(sm_u32(ops)),
-        "l"(src), "r"(len * 16u), "r"(sm_u32(bar))
+            "r"(mac_sm),
+        "l"(mac_g), "r"(len * (uint32_t)sizeof(ChainMacro)), "r"(sm_u32(bar))
         : "memory");
   // tables: record times unfired, rings empty, no host sync resolved
   for (uint32_t q = tid; q < J.n_fire; q += nt) sh.fire[q] = -1;
@@ -265,28 +274,67 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
           : "r"(sm_u32(bar))
           : "memory");
   }
+#ifdef MAYA_PROFILE
+  const long long t_copied = clock64();
+  if (tid == 0) atomicAdd(&g_cprof[6], (unsigned long long)(t_copied - t_start));
+#endif
+  if (RES && valid && len && !err) {   // the macro pass flags a FIFO it could not fuse
+    uint32_t k0;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(k0) : "r"(mac_sm + 40u) : "memory");
+    if (k0 == CM_FAIL) err = MAYA_ST_INTERNAL;
+  }
   group_sync<NW>();
 #ifdef MAYA_PROFILE
   if (tid == 0) atomicAdd(&g_cprof[5], (unsigned long long)(clock64() - t_start));
+  if (tid == 0) atomicAdd(&g_cprof[7], (unsigned long long)(clock64() - t_copied));
   unsigned long long n_it = 0, c_it = 0, n_ops = 0;
 #endif
 
   int64_t x = 0, cdel = 0;
-  uint32_t i = 0, seg = 0, bound = valid ? (nsync ? cnt[0] : len) : 0, lim = 0;
+  uint32_t i = 0, iops = 0, seg = 0, bound = valid ? (nsync ? cnt[0] : nops) : 0, lim = 0;
   bool posted = false;
-  // the op at the head of the FIFO, prefetched when its predecessor retires
-  auto load_op = [&](uint32_t q) -> ExecOp {
+  // the unit at the head of the FIFO (a macro op; without folding, one op),
+  // prefetched when its predecessor retires
+  auto load_unit = [&](uint32_t q) -> ChainMacro {
+    ChainMacro c;
     if (RES) {
-      uint64_t a, c;
-      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(c) : "r"(ops_sm + q * 16u));
-      return ExecOp{(int64_t)a, c};
+      const uint32_t a = mac_sm + q * (uint32_t)sizeof(ChainMacro);
+      uint64_t r1, dk, rr, wr;
+      uint32_t cidx, end, kind, pad;
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r1), "=l"(dk) : "r"(a) : "memory");
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(rr), "=l"(wr) : "r"(a + 16u) : "memory");
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(cidx), "=r"(end), "=r"(kind), "=r"(pad) : "r"(a + 32u) : "memory");
+      c = ChainMacro{(int64_t)r1, (int64_t)dk, (int64_t)rr, (uint32_t)wr, (uint32_t)(wr >> 32),
+                     cidx, end, kind, 0};
+      return c;
     }
     const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(ops + q));
-    return ExecOp{v.x, (uint64_t)v.y};
+    const uint64_t wv = (uint64_t)v.y;
+    const uint32_t tag = (uint32_t)(wv & 3u);
+    const uint64_t pay = wv >> 2;
+    c = ChainMacro{CNEG, 0, CNEG, 0, 0, 0, q + 1, 0, 0};
+    if (tag == TAG_REC) {
+      c.kind = CM_REC;
+      c.rr = v.x;
+      c.ridx = (uint32_t)pay;
+    } else {
+      c.r1 = v.x;
+      if (tag == TAG_KERN) {
+        c.kind = CM_KERN | (wv == EXEC_BAD ? CM_BAD : 0u) | (wv == EXEC_OVF ? CM_OVF : 0u);
+        c.dk = (int64_t)pay;
+      } else if (tag == TAG_COLL) {
+        c.kind = CM_COLL;
+        c.cidx = (uint32_t)pay;
+      } else {
+        c.kind = CM_WAIT | (pay == (EXEC_NONE >> 2) ? CM_NEVER : 0u);
+        c.widx = (uint32_t)pay;
+      }
+    }
+    return c;
   };
-  ExecOp nxt{0, 0};
-  if (valid && len) nxt = load_op(0);
-  int err = 0;
+  ChainMacro cm{};
+  if (valid && len && !err) cm = load_unit(0);
   int64_t rounds = 0;
   const uint32_t fire_sm = sm_u32(sh.fire + fb), rcx_sm = sm_u32(sh.rcx + rcb);
   for (;;) {
@@ -295,40 +343,39 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
     group_sync<NW>();
     if (valid) {
       const uint32_t hk = sh.hostk[rank];
-      lim = hk < nsync ? cnt[hk * ns] : len;
+      lim = hk < nsync ? cnt[hk * ns] : nops;   // in (folded) ops
     }
-    if (err) lim = i;   // a failed FIFO stops (the job's status is the error)
+    if (err) lim = iops;   // a failed FIFO stops (the job's status is the error)
     for (;;) {
 #ifdef MAYA_PROFILE
       const long long t0 = clock64();
 #endif
       bool prog = false;
-      if (i < lim) {
-        if (i >= bound) {   // next host-sync segment (rare)
-          while (i >= bound && seg < nsync) {
+      if (i < len && iops < lim) {
+        if (iops >= bound) {   // next host-sync segment (rare)
+          while (iops >= bound && seg < nsync) {
             seg++;
             cdel = sh.delay[dlb + seg];
-            bound = seg < nsync ? cnt[seg * ns] : len;
+            bound = seg < nsync ? cnt[seg * ns] : nops;
           }
         }
-        // one predicated evaluation for every op kind
-        const uint32_t tag = (uint32_t)(nxt.w & 3u);
-        const uint32_t pay32 = (uint32_t)(nxt.w >> 2);    // REC/WAIT/COLL index
-        const int64_t rdisp = nxt.disp + cdel;
-        const int64_t ready = x > rdisp ? x : rdisp;
-        const bool isK = tag == TAG_KERN, isR = tag == TAG_REC, isW = tag == TAG_WAIT,
-                   isC = tag == TAG_COLL;
-        int64_t fv = -1;   // WAIT: the record time (never-recorded: stays -1, blocks forever)
-        if (isW && (nxt.w >> 2) != (EXEC_NONE >> 2))
-          asm volatile("ld.volatile.shared.s64 %0, [%1];" : "=l"(fv) : "r"(fire_sm + pay32 * 8u) : "memory");
+        // one predicated evaluation of the unit [WAIT]? [KERN | COLL]? [REC]?
+        const uint32_t kind = cm.kind;
+        const int64_t r1 = cm.r1 + cdel;
+        const int64_t ready0 = x > r1 ? x : r1;
+        int64_t fv = -1;   // WAIT: the record time (never recorded: stays -1, blocks forever)
+        if ((kind & (CM_WAIT | CM_NEVER)) == CM_WAIT)
+          asm volatile("ld.volatile.shared.s64 %0, [%1];" : "=l"(fv) : "r"(fire_sm + cm.widx * 8u) : "memory");
+        const bool wait_ok = !(kind & CM_WAIT) || fv >= 0;
+        const int64_t ready = ready0 > fv ? ready0 : fv;
         uint64_t ent = 1ull << 48;
         int64_t wire = 0;
-        if (isC)
-          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(ent), "=l"(wire) : "r"(rcx_sm + pay32 * 16u));
+        if (kind & CM_COLL)
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(ent), "=l"(wire) : "r"(rcx_sm + cm.cidx * 16u));
         const uint32_t nr = (uint32_t)(ent >> 48);
-        bool ok = isK || isR || fv >= 0 || (isC && nr == 1);
-        int64_t base = ready > fv ? ready : fv;
-        if (isC && nr != 1) {                      // collective rendezvous (sim.py:326-343)
+        bool ok = wait_ok;
+        int64_t base = ready;
+        if ((kind & CM_COLL) && nr != 1 && wait_ok) {   // collective rendezvous (sim.py:326-343)
           const uint32_t g = (uint32_t)(ent >> 32) & 0xffffu, idx = (uint32_t)ent;
           CollSlot *cs = sh.ring + 2 * g + (idx & 1u);
           const uint32_t target = ((idx >> 1) + 1u) * nr;
@@ -350,9 +397,9 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
           }
           ok = done_c && !err;
         }
-        const int64_t add = isK ? (int64_t)(nxt.w >> 2) : wire;   // (wire = 0 unless COLL)
-        if (isK && nxt.w >= EXEC_OVF) {            // EXEC_OVF / EXEC_BAD (cold)
-          err = nxt.w == EXEC_BAD ? MAYA_ST_ESTIMATION : MAYA_ST_OVERFLOW;
+        const int64_t add = (kind & CM_KERN) ? cm.dk : wire;   // (wire = 0 unless COLL)
+        if (kind & (CM_BAD | CM_OVF)) {            // a failed estimate / overflowed run (cold)
+          err = (kind & CM_BAD) ? MAYA_ST_ESTIMATION : MAYA_ST_OVERFLOW;
           ok = false;
         }
         if (ok && (base >= CLIM || add >= CLIM) && add > INT64_MAX - base) {
@@ -360,23 +407,26 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
           ok = false;
         }
         if (ok) {
-          const int64_t done = base + add;
-          if (isR)
-            asm volatile("st.volatile.shared.s64 [%0], %1;" ::"r"(fire_sm + pay32 * 8u), "l"(ready) : "memory");
-          if (REC) {
-            b.tl_start[tl + i] = ready;
+          const int64_t v = base + add;
+          const int64_t rr = cm.rr + cdel;
+          const int64_t done = (kind & CM_REC) && rr > v ? rr : v;
+          if (kind & CM_REC)
+            asm volatile("st.volatile.shared.s64 [%0], %1;" ::"r"(fire_sm + cm.ridx * 8u), "l"(done) : "memory");
+          if (REC) {   // (timeline runs: one op per unit)
+            b.tl_start[tl + i] = kind == CM_REC ? done : ready0;
             b.tl_end[tl + i] = done;
           }
           x = done;
           posted = false;
+          iops = cm.end;
           i++;
-          if (i < len) nxt = load_op(i);
+          if (i < len) cm = load_unit(i);
           prog = true;
 #ifdef MAYA_PROFILE
           n_ops++;
 #endif
         }
-        if (err) lim = i;
+        if (err) lim = iops;
       }
       const bool anyp = group_any<NW>(prog);
 #ifdef MAYA_PROFILE
@@ -387,7 +437,7 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
       progress = true;
     }
     if (valid) {
-      sh.fst_i[w] = i;
+      sh.fst_i[w] = iops;
       sh.fst_x[w] = x;
     }
     rounds++;
@@ -419,7 +469,7 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
     s_oom_t = INT64_MAX;
   }
   group_sync<NW>();
-  bool incomplete = valid && i < len;
+  bool incomplete = valid && i < len;   // (units: macro ops or ops)
   int64_t oom_t = INT64_MAX, peak = 0;
   int32_t oom_rank = INT32_MAX;
   for (uint32_t r = tid; r < R; r += nt) {
@@ -467,6 +517,120 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
     r.rounds = rounds;
     *res = r;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Macro pass: the folded ops of every FIFO of a chain job grouped into macro
+// ops (soa.h MacroFuse), written to DevBatch.macros for the chain kernel to
+// bulk-copy.  One CTA per chain job, a warp per FIFO in turn (8 warps).  The
+// rule is local -- an op joins the macro of the op before it (same segment)
+// iff it is a body after a WAIT or a REC after a WAIT or a body, so a macro
+// has at most 3 members -- hence chunks of 32 ops: lanes 0-29 lead macros
+// whose members all lie in the chunk, and the next chunk starts at the first
+// op no written macro covers.
+static constexpr uint32_t MACRO_WARPS = 8;
+
+__global__ void __launch_bounds__(MACRO_WARPS * 32) chain_macro_kernel(DevBatch b,
+                                                                       const int32_t *order) {
+  const uint32_t j = (uint32_t)order[blockIdx.x];
+  const JobHdr &J = b.jobs[j];
+  if (J.status != MAYA_ST_OK) return;
+  const LaneJob LJ = b.lane_jobs[j];
+  const uint32_t lane = threadIdx.x & 31u, wp = threadIdx.x >> 5, W = J.n_walkers;
+  for (uint32_t w = wp; w < W; w += MACRO_WARPS) {
+    const Walker wk = b.walkers[J.walkers + w];
+    const RankRec rr = b.ranks[J.ranks + wk.rank];
+    const RepHdr &h = b.reps[rr.rep];
+    const StreamRange sr = b.streams[h.streams + wk.stream];
+    const uint32_t nops = b.clen[h.streams + wk.stream];
+    const ExecOp *ops = b.exec + h.ops + sr.begin;
+    const uint32_t *cnt = b.ccounts + h.counts + wk.stream;
+    const uint32_t ns = h.n_streams, nsync = h.n_syncs;
+    const uint32_t m0 = b.lane_wslot[J.walkers + w];
+    const uint32_t len = (w + 1 < W ? b.lane_wslot[J.walkers + w + 1] : LJ.n_slots) - m0;
+    ChainMacro *out = b.macros + LJ.mbase + m0;
+    // the first four sync boundaries (a segment: the syncs whose count <= q)
+    const uint32_t bnd = lane < nsync && lane < 4u ? cnt[lane * ns] : 0xffffffffu;
+    const uint32_t fb0 = __shfl_sync(FULL, bnd, 0), fb1 = __shfl_sync(FULL, bnd, 1),
+                   fb2 = __shfl_sync(FULL, bnd, 2), fb3 = __shfl_sync(FULL, bnd, 3);
+    uint32_t m_base = 0, p_cls = 4, p_seg = 0;   // macros written, op before the chunk
+    bool fail = false;
+    for (uint32_t q0 = 0; q0 < nops && !fail;) {
+      const uint32_t q = q0 + lane;
+      const bool have = q < nops;
+      longlong2 v = make_longlong2(0, 0);
+      if (have) v = __ldg(reinterpret_cast<const longlong2 *>(ops + q));
+      const uint64_t dsp = (uint64_t)v.x, wv = (uint64_t)v.y;
+      uint32_t sg = (q >= fb0) + (q >= fb1) + (q >= fb2) + (q >= fb3);
+      if (have && nsync > 4) {   // many host syncs: binary search
+        uint32_t lo = 0, hi = nsync;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (cnt[mid * ns] <= q) lo = mid + 1; else hi = mid;
+        }
+        sg = lo;
+      }
+      const uint32_t tag = (uint32_t)(wv & 3u);
+      const uint32_t cls = !have ? 5u : tag == TAG_KERN ? 0u : tag == TAG_COLL ? 1u
+                         : tag == TAG_REC ? 2u : 3u;
+      uint32_t pc = __shfl_up_sync(FULL, cls, 1), ps = __shfl_up_sync(FULL, sg, 1);
+      if (lane == 0) { pc = p_cls; ps = p_seg; }
+      const bool body = cls <= 1u;
+      const bool joins = have && pc < 4u && ps == sg &&
+                         ((body && pc == 3u) || (cls == 2u && (pc == 3u || pc <= 1u)));
+      const bool lead = have && lane < 30u && !joins;
+      const uint32_t j1 = __shfl_down_sync(FULL, joins ? 1u : 0u, 1);
+      const uint32_t j2 = __shfl_down_sync(FULL, joins ? 1u : 0u, 2);
+      const uint64_t d1 = __shfl_down_sync(FULL, dsp, 1), w1 = __shfl_down_sync(FULL, wv, 1);
+      const uint64_t d2 = __shfl_down_sync(FULL, dsp, 2), w2 = __shfl_down_sync(FULL, wv, 2);
+      const uint32_t nmem = 1u + ((lane < 31u && j1) ? 1u + ((lane < 30u && j2) ? 1u : 0u) : 0u);
+      const unsigned lm = __ballot_sync(FULL, lead);
+      const uint32_t midx = m_base + __popc(lm & ((1u << lane) - 1u));
+      if (lead && midx < len) {
+        ChainMacro c{CNEG, 0, CNEG, 0, 0, 0, q + nmem, 0, 0};
+#pragma unroll
+        for (uint32_t k = 0; k < 3; k++) {
+          if (k >= nmem) break;
+          const uint64_t dk = k == 0 ? dsp : k == 1 ? d1 : d2;
+          const uint64_t wk2 = k == 0 ? wv : k == 1 ? w1 : w2;
+          const uint32_t tk = (uint32_t)(wk2 & 3u);
+          const uint64_t pay = wk2 >> 2;
+          if (tk == TAG_REC) {
+            c.kind |= CM_REC;
+            c.rr = (int64_t)dk;
+            c.ridx = (uint32_t)pay;
+          } else {
+            if ((int64_t)dk > c.r1) c.r1 = (int64_t)dk;
+            if (tk == TAG_KERN) {
+              c.kind |= CM_KERN | (wk2 == EXEC_BAD ? CM_BAD : 0u) | (wk2 == EXEC_OVF ? CM_OVF : 0u);
+              c.dk = (int64_t)pay;
+            } else if (tk == TAG_COLL) {
+              c.kind |= CM_COLL;
+              c.cidx = (uint32_t)pay;
+            } else {
+              c.kind |= CM_WAIT | (pay == (EXEC_NONE >> 2) ? CM_NEVER : 0u);
+              c.widx = (uint32_t)pay;
+            }
+          }
+        }
+        longlong2 *o = reinterpret_cast<longlong2 *>(out + midx);
+        o[0] = make_longlong2(c.r1, c.dk);
+        o[1] = make_longlong2(c.rr, (long long)(((uint64_t)c.ridx << 32) | c.widx));
+        o[2] = make_longlong2((long long)(((uint64_t)c.end << 32) | c.cidx), (long long)c.kind);
+      }
+      m_base += __popc(lm);
+      fail = m_base > len;
+      const uint32_t cov = __reduce_max_sync(FULL, lead ? lane + nmem : 0u);
+      p_cls = __shfl_sync(FULL, cls, cov - 1);
+      p_seg = __shfl_sync(FULL, sg, cov - 1);
+      q0 += cov;
+    }
+    if ((fail || m_base != len) && len && lane == 0) out[0].kind = CM_FAIL;
+  }
+}
+
+void launch_chain_macros(const DevBatch &b, const int32_t *order, uint32_t n, cudaStream_t s) {
+  if (n) chain_macro_kernel<<<n, MACRO_WARPS * 32, 0, s>>>(b, order);
 }
 
 int chain_prof_read(unsigned long long *out8, int reset) {

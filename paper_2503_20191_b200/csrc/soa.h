@@ -123,6 +123,7 @@ enum LaneFlags : uint32_t {
   LANE_CHASE = 32,      // a lane retires every ready op of its FIFO per step (latency-bound jobs)
 };
 struct LaneJob {
+  uint64_t mbase;       // chain jobs: batch index of the job's first macro op (DevBatch.macros)
   uint32_t flags;       // LaneFlags
   uint32_t n_slots;     // ring slots of the job (sum over FIFOs)
   uint64_t wslot;       // batch index of the job's first per-walker ring word
@@ -147,6 +148,47 @@ struct GridSync {
   int oom_rank, rounds;
   unsigned long long tmax;
   long long peak, oom_t;
+};
+
+// Chain-kernel macro ops: the folded FIFO grouped greedily into
+// [WAIT]? [KERN | COLL]? [REC]? within one host-sync segment (sched_chain.cu
+// chain_macro_kernel builds them; the host counts them with the same rule to
+// size the shared-memory region).  One macro op is one lockstep iteration:
+//   ready = max(x, r1 + delay, fire[widx]);  body: + dk | rendezvous + wire;
+//   out = max(body, rr + delay);  fire[ridx] = out.
+struct alignas(16) ChainMacro {
+  int64_t r1;        // max dispatch (gap prefix) of the WAIT and body ops (INT64_MIN/4: none)
+  int64_t dk;        // KERN duration (folded run)
+  int64_t rr;        // REC dispatch (INT64_MIN/4: none)
+  uint32_t widx;     // WAIT: rep-local record ordinal
+  uint32_t ridx;     // REC: rep-local record ordinal
+  uint32_t cidx;     // COLL: rep-local collective index
+  uint32_t end;      // folded ops of the FIFO up to and including this macro
+  uint32_t kind;     // CM_* bits
+  uint32_t pad;
+};
+static_assert(sizeof(ChainMacro) == 48, "ChainMacro");
+enum : uint32_t {
+  CM_WAIT = 1, CM_REC = 2, CM_KERN = 4, CM_COLL = 8,
+  CM_NEVER = 16,     // the WAIT's event is never recorded: blocks forever
+  CM_BAD = 32,       // the kernel's estimate failed (EXEC_BAD)
+  CM_OVF = 64,       // the folded run's composite overflowed (EXEC_OVF)
+  CM_FAIL = 0xffffffffu,   // (first macro's kind) the macro pass disagreed with the plan
+};
+// op classes of the fusion rule: 0 kernel (incl. folded runs), 1 collective,
+// 2 record, 3 wait.  Greedy state machine (one per FIFO, reset per segment).
+struct MacroFuse {
+  int state = 0;             // 0 closed, 1 open after a WAIT, 2 open after a body
+  uint32_t seg = 0xffffffffu;
+  // true: op of class `cls` in segment `sg` starts a new macro
+  __host__ __device__ bool push(uint32_t cls, uint32_t sg) {
+    if (sg != seg) { seg = sg; state = 0; }
+    const bool body = cls <= 1;
+    if (state == 1 && (body || cls == 2)) { state = body ? 2 : 0; return false; }
+    if (state == 2 && cls == 2) { state = 0; return false; }
+    state = cls == 3 ? 1 : body ? 2 : 0;
+    return true;
+  }
 };
 
 // ---- chain scheduler (sched_chain.cu) ---------------------------------------
@@ -184,7 +226,7 @@ __host__ __device__ inline ChainLayout chain_layout(uint32_t W, uint32_t R, uint
   L.rcx = (uint32_t)off;
   off += 16ull * n_rcolls;
   L.ops = (uint32_t)off;
-  off += 16ull * n_ops;
+  off += sizeof(ChainMacro) * n_ops;   // n_ops: the job's macro ops (folded runs: resident)
   L.bytes = off > 0xffffffffull ? 0xffffffffu : (uint32_t)off;
   return L;
 }

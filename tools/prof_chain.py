@@ -8,7 +8,7 @@ from paper_2503_20191_b200 import workload as W
 L = E.lib()
 L.maya_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 eng = E.Engine(0)
-names = ["kernel_cyc", "steps", "step_cyc", "ops", "rounds", "setup_cyc", "max_lane_ops", "-"]  # steps = lockstep iterations
+names = ["kernel_cyc", "steps", "step_cyc", "ops", "rounds", "setup_cyc", "copied_cyc", "fuse_cyc"]  # steps = lockstep iterations
 model = W.ModelSpec("gpt3-1.3b", 24, 2048, 2048, 51200)
 cluster = W.ClusterSpec(1, 8, 80 * 2 ** 30, W.load_device_preset("fast"))
 cfgs = W.enumerate_space(W.SearchSpace(global_batch=512), model, cluster)[:512]
@@ -22,4 +22,4 @@ for lab in sys.argv[1:]:
     d = dict(zip(names, list(buf)[8:]))
     st = max(d["steps"], 1)
     print(lab, "sched ms", round(eng.last_timings_ms()[2], 3), d, "cyc/step", d["step_cyc"] // st,
-          "ops/step", round(d["ops"] / st, 2), "maxlane/step", round(d["max_lane_ops"] / st, 2), flush=True)
+          "ops/step", round(d["ops"] / st, 2), flush=True)
