@@ -147,6 +147,9 @@ int maya_batch_num_jobs(maya_engine *eng);
 int maya_set_options(maya_engine *eng, int32_t options);
 /* Per staged job: 1 if it is simulated as rank classes. */
 int maya_batch_collapsed(maya_engine *eng, uint8_t *out);
+/* After maya_upload, per staged job: the scheduler kernel chosen for it --
+   0 warp-window, 1 lane-parallel (warp or CTA job), 2 grid job, 3 chain. */
+int maya_batch_kernels(maya_engine *eng, int32_t *out);
 
 /* Upload the staged batch to HBM (the H2D leg). */
 int maya_upload(maya_engine *eng);

@@ -130,6 +130,7 @@ struct maya_engine {
       s_blk_fids;
   Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst, x_gsync, x_macros;
   uint32_t chain_first = 0, chain_jobs = 0;   // chain jobs: the tail of the job order
+  std::vector<int32_t> job_kernel;            // per job: 0 warp-window, 1 lane, 2 grid, 3 chain
   std::vector<GridPart> grid_parts;        // host copy (launch grouping)
   std::vector<std::pair<uint32_t, uint32_t>> grid_launches;   // part ranges per launch
   uint32_t grid_smem = 0;
@@ -255,9 +256,9 @@ bool plan_grid(const JobPack &P, LanePlan &pl) {
 // Chain-kernel plan (sched_chain.cu): the whole job resident in one CTA's
 // shared-memory region -- every FIFO's macro ops (its folded ops fused into
 // [WAIT]? [KERN | COLL]? [REC]? groups), record times, collective rings and
-// rank collective table -- one FIFO per thread.  Only for jobs whose
-// collectives rendezvous in rings (JOB_RING).  n_slots carries the job's
-// macro op count (the region's op area).
+// rank collective table -- one FIFO per thread (collectives rendezvous in
+// shared-memory rings when the job allows them, JOB_RING, else in global
+// slots).  n_slots carries the job's macro op count (the region's op area).
 static const uint64_t CHAIN_WAVE_BYTES = 148ull * 200 * 1024;   // ~one wave of chain CTAs
 
 LanePlan plan_chain(const JobPack &P) {
@@ -265,7 +266,6 @@ LanePlan plan_chain(const JobPack &P) {
   const uint32_t W = (uint32_t)P.walkers.size(), R = (uint32_t)P.ranks.size();
   const uint32_t nc = (uint32_t)P.comms.size();
   if (P.hdr.status != MAYA_ST_OK || W == 0 || W > CHAIN_MAX_FIFOS) return pl;
-  if (!(P.hdr.flags & JOB_RING) || nc > RING_MAX_COMMS) return pl;
   uint64_t n_ops = 0;   // macro ops (soa.h ChainMacro) of the job's FIFOs
   for (uint32_t w = 0; w < W; w++) {
     const Walker wk = P.walkers[w];
@@ -563,6 +563,12 @@ int maya_set_options(maya_engine *e, int32_t options) {
   return MAYA_OK;
 }
 
+int maya_batch_kernels(maya_engine *e, int32_t *out) {
+  if (!e->uploaded) return fail(MAYA_ESTATE, "maya_batch_kernels before maya_upload");
+  for (size_t j = 0; j < e->packs.size(); j++) out[j] = e->job_kernel[j];
+  return MAYA_OK;
+}
+
 int maya_batch_collapsed(maya_engine *e, uint8_t *out) {
   for (size_t j = 0; j < e->packs.size(); j++) out[j] = e->packs[j].collapsed ? 1 : 0;
   return MAYA_OK;
@@ -840,6 +846,9 @@ int maya_upload(maya_engine *e) {
       }
     }
     memcpy(H + e->s_order.off, order.data(), nj * sizeof(int32_t));
+    e->job_kernel.resize(nj);
+    for (size_t j = 0; j < nj; j++)
+      e->job_kernel[j] = var[j] >= 16 ? 3 : var[j] == 15 ? 2 : var[j] >= 3 ? 1 : 0;
     // chain jobs (variants 16..) close the order: their macro pass takes that tail
     e->chain_jobs = 0;
     for (size_t j = 0; j < nj; j++) e->chain_jobs += var[j] >= 16 ? 1u : 0u;

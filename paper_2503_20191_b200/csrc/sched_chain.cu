@@ -254,7 +254,8 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
         : "memory");
   // tables: record times unfired, rings empty, no host sync resolved
   for (uint32_t q = tid; q < J.n_fire; q += nt) sh.fire[q] = -1;
-  for (uint32_t q = tid; q < 2 * J.n_comms; q += nt) sh.ring[q] = CollSlot{0, 0, 0};
+  if (J.n_comms <= RING_MAX_COMMS)
+    for (uint32_t q = tid; q < 2 * J.n_comms; q += nt) sh.ring[q] = CollSlot{0, 0, 0};
   for (uint32_t r = tid; r < R; r += nt) {
     sh.hostk[r] = 0;
     sh.delay[b.ranks[J.ranks + r].delay] = 0;
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
   if (valid && len && !err) cm = load_unit(0);
   int64_t rounds = 0;
   const uint32_t fire_sm = sm_u32(sh.fire + fb), rcx_sm = sm_u32(sh.rcx + rcb);
+  const bool ring = (J.flags & JOB_RING) && J.n_comms <= RING_MAX_COMMS;
   for (;;) {
     bool progress = false;
     for (uint32_t r = tid; r < R; r += nt) progress |= chain_host_step(b, sh, r);
@@ -377,8 +379,18 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
         int64_t base = ready;
         if ((kind & CM_COLL) && nr != 1 && wait_ok) {   // collective rendezvous (sim.py:326-343)
           const uint32_t g = (uint32_t)(ent >> 32) & 0xffffu, idx = (uint32_t)ent;
-          CollSlot *cs = sh.ring + 2 * g + (idx & 1u);
-          const uint32_t target = ((idx >> 1) + 1u) * nr;
+          // shared-memory rings (2 slots per communicator, cumulative counts)
+          // when every rank issues a communicator's calls in order from one
+          // stream (JOB_RING); else one global slot per call
+          CollSlot *cs;
+          uint32_t target;
+          if (ring) {
+            cs = sh.ring + 2 * g + (idx & 1u);
+            target = ((idx >> 1) + 1u) * nr;
+          } else {
+            cs = b.cslots + J.slots + b.comms[J.comms + g].call_base + idx;
+            target = nr;
+          }
           bool done_c;
           if (!posted) {
             atomicMax(&cs->maxarr, (unsigned long long)ready);
@@ -389,11 +401,11 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
             if (old + 1 > target) err = MAYA_ST_INTERNAL;
             done_c = old + 1 == target;
           } else {
-            done_c = lds_vol_u32(&cs->count) >= target;
+            done_c = *(volatile const uint32_t *)&cs->count >= target;
           }
           if (done_c) {
             __threadfence_block();
-            base = (int64_t)lds_vol_s64(&cs->maxarr);
+            base = (int64_t)*(volatile const unsigned long long *)&cs->maxarr;
           }
           ok = done_c && !err;
         }

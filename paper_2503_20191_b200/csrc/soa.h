@@ -213,7 +213,7 @@ __host__ __device__ inline ChainLayout chain_layout(uint32_t W, uint32_t R, uint
   L.bar = 0;
   off = 16;
   L.ring = (uint32_t)off;
-  off += 32ull * n_comms;                 // 2 CollSlot per communicator
+  off += 32ull * (n_comms <= RING_MAX_COMMS ? n_comms : 0);   // 2 CollSlot per communicator
   L.hostk = (uint32_t)off;
   off = (off + 4ull * R + 15) & ~15ull;
   L.fst_i = (uint32_t)off;

@@ -29,7 +29,8 @@ EXPORTED = (
     "maya_topk", "maya_timeline_size", "maya_timeline", "maya_last_timings",
     "maya_get_stream", "maya_arena_bytes", "maya_gen_job", "maya_gen_view_of", "maya_gen_free",
     "maya_gen_op_kind_name", "maya_gen_dtype_name", "maya_batch_add_generated",
-    "maya_batch_stats", "maya_set_options", "maya_batch_collapsed", "maya_prof_read",
+    "maya_batch_stats", "maya_set_options", "maya_batch_collapsed", "maya_batch_kernels",
+    "maya_prof_read",
     "maya_debug_pack_compare", "maya_rank_stats", "maya_last_error_kind", "maya_trace_parse",
     "maya_trace_info", "maya_trace_serialize", "maya_trace_free", "maya_job_load",
     "maya_job_save", "maya_gen_names", "maya_topk_async",
@@ -77,6 +78,7 @@ def lib():
     L.maya_batch_stats.argtypes = [vp, P(C.c_int64)]
     L.maya_set_options.argtypes = [vp, C.c_int32]
     L.maya_batch_collapsed.argtypes = [vp, P(C.c_uint8)]
+    L.maya_batch_kernels.argtypes = [vp, P(C.c_int32)]
     L.maya_rank_stats.argtypes = [vp, C.c_int32, C.c_int32, P(C.c_int64)]
     L.maya_topk_async.argtypes = [vp, C.c_int32]
     _lib = L
@@ -151,6 +153,16 @@ class Engine:
                 | (16 if not (self._blocks and self._fold) else 0)
                 | (32 if self._sched == "nochain" else 0))
         _check(lib().maya_set_options(self._h, opts))
+
+    KERNELS = ("warp", "lane", "grid", "chain")
+
+    def kernels(self) -> list:
+        """Scheduler kernel of each staged job (after upload): 'warp'
+        (warp-window), 'lane' (lane-parallel), 'grid' (multi-CTA lane job) or
+        'chain' (latency-bound job resident in one CTA's shared memory)."""
+        out = np.zeros(max(self.n_jobs, 1), dtype=np.int32)
+        _check(lib().maya_batch_kernels(self._h, out.ctypes.data_as(C.POINTER(C.c_int32))))
+        return [self.KERNELS[int(v)] for v in out[:self.n_jobs]]
 
     def collapsed(self) -> np.ndarray:
         out = np.zeros(max(self.n_jobs, 1), dtype=np.uint8)
