@@ -491,10 +491,23 @@ struct RepCalls {
   std::vector<std::vector<std::pair<int8_t, int64_t>>> calls;  // per local comm
 };
 
+// The builder side of a phase template (generate_trace): the template id in
+// the packer, and the calls, event versions and allocations a replay adds.
+struct BTpl {
+  int id = -2;                                   // -2: not captured, -1: not replayable
+  int tries = 0;                                 // captures attempted (the first occurrence
+                                                 // of a phase often opens communicators)
+  std::vector<std::pair<int, std::pair<int8_t, int64_t>>> calls;   // (lc, (kind, bytes)), by lc
+  std::vector<std::pair<int64_t, int64_t>> vers; // (event id, records)
+  int64_t allocs = 0;
+};
+typedef std::array<int64_t, 20> TplKey;
+typedef std::map<TplKey, BTpl> JobTpls;        // per job, shared by its reps
+
 // workload.py:571-780 for one representative rank; appends events.
 void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int schedule,
                     int64_t rank, int64_t overhead, int32_t dtype, GenJob &G, RepCalls &rc,
-                    EventSink *sink) {
+                    EventSink *sink, JobTpls *jtpl) {
   const int64_t t = C.t, d = C.d;
   const int64_t i = rank % t, j = (rank / t) % d, stage = rank / (t * d);
   const int64_t p = cfg.pp, v = cfg.virtual_stages, total_vs = p * v;
@@ -677,20 +690,35 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   // chunk emits the same events up to counters, so the packer captures the
   // first occurrence and stamps the later ones; the builder replays its own
   // side -- call lists and call numbers, event versions, allocation handles
-  // (pack.cpp RepPacker::phase_*).
-  struct BTpl {
-    int id = -2;                                   // -2: not captured, -1: not replayable
-    int tries = 0;                                 // captures attempted (the first occurrence
-                                                   // of a phase often opens communicators)
-    std::vector<std::pair<int, std::pair<int8_t, int64_t>>> calls;   // (lc, (kind, bytes)), by lc
-    std::vector<std::pair<int64_t, int64_t>> vers; // (event id, records)
-    int64_t allocs = 0;
-  };
+  // (pack.cpp RepPacker::phase_*).  Templates are shared by the job's reps:
+  // a phase's events are fixed by its chunk's shape and the local indices it
+  // touches (streams, event ids, communicators) -- the key -- and the
+  // config-wide kernel lists and sizes, so isomorphic pipeline stages (every
+  // middle stage) pack each phase once per job.
   // (kernel-block mode always cuts runs at phase boundaries, replay or not, so
   // both pack the same kernel blocks)
-  const bool tpl_on = B.blocks;
+  const bool tpl_on = B.blocks && jtpl;
   const bool replay = tpl_on && sink->replays();
-  std::vector<BTpl> btpl(tpl_on ? 2 * chunks.size() : 0);
+  std::vector<BTpl *> btpl(tpl_on ? 2 * chunks.size() : 0);
+  if (tpl_on)
+    for (size_t c = 0; c < chunks.size(); c++) {
+      const Chunk &ch = chunks[c];
+      const int64_t vs = ch.vs;
+      const bool in = vs > 0, out = vs < total_vs - 1;
+      for (int ph = 0; ph < 2; ph++) {
+        const TplKey key{ph, ch.layers, ch.has_embed ? 1 : 0, ch.has_head ? 1 : 0, in, out,
+                         in ? p2p_stream[{vs - 1, R_FIN}] : -1,
+                         in ? p2p_stream[{vs - 1, R_BOUT}] : -1,
+                         out ? p2p_stream[{vs, R_FOUT}] : -1,
+                         out ? p2p_stream[{vs, R_BIN}] : -1,
+                         in ? eid[{E_FIN, vs - 1}] : -1, in ? eid[{E_BOUT, vs - 1}] : -1,
+                         out ? eid[{E_FOUT, vs}] : -1, out ? eid[{E_BIN, vs}] : -1,
+                         in ? lc_of(C_PF, vs - 1, i, j) : -1, in ? lc_of(C_PB, vs - 1, i, j) : -1,
+                         out ? lc_of(C_PF, vs, i, j) : -1, out ? lc_of(C_PB, vs, i, j) : -1,
+                         tp_lc, chunk_stash_bytes(M, cfg, b, ch)};
+        btpl[2 * c + (ph == 0 ? 0 : 1)] = &(*jtpl)[key];
+      }
+    }
   std::vector<size_t> calls0;
   std::vector<int64_t> vers0;
   for (const Step &st : pipeline_order(schedule, p, m, v, stage)) {
@@ -699,7 +727,7 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
       else emit_backward(st.mb, st.chunk);
       continue;
     }
-    BTpl &bt = btpl[2 * st.chunk + (st.phase == FWD ? 0 : 1)];
+    BTpl &bt = *btpl[2 * st.chunk + (st.phase == FWD ? 0 : 1)];
     B.flush();   // phases start and end outside a kernel run
     if (replay && bt.id >= 0 && sink->phase_replay(bt.id, B.next_alloc)) {
       if (st.phase == FWD) act_ids[{st.chunk, st.mb}] = B.next_alloc;   // its one allocation
@@ -940,11 +968,12 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
     G.capacity = cl.device_memory_bytes;
     // representatives: one per stage (unique_workers, :281-298)
     std::vector<RepCalls> rcalls(cfg.pp);
+    JobTpls jtpl;   // phase templates of the job
     G.ev_off.push_back(0);
     for (int k = 0; k < cfg.pp; k++) {
       int64_t rep = rank_of(C, 0, 0, k);
       G.rep_ranks.push_back(rep);
-      generate_trace(M, cfg, C, schedule, rep, overhead, model.dtype, G, rcalls[k], sink);
+      generate_trace(M, cfg, C, schedule, rep, overhead, model.dtype, G, rcalls[k], sink, &jtpl);
       G.ev_off.push_back((int64_t)G.ev_kind.size());
     }
     G.rank_rep.resize(n);

@@ -193,9 +193,12 @@ struct RepPacker {
   struct PhaseTpl {
     bool ok = false;
     uint32_t seg = 0;
-    std::vector<std::vector<Op>> ops;        // per local stream, relative fields
-    size_t nst = 0;                          // local streams the template covers
-    std::vector<uint32_t> sev;               // per local stream: device events added
+    std::vector<std::vector<Op>> ops;        // per stream, relative fields
+    size_t nst = 0;                          // streams the template covers
+    std::vector<int32_t> raw;                // their trace stream handles (templates are
+                                             // shared by the reps of a job, whose local
+                                             // stream numbering may differ)
+    std::vector<uint32_t> sev;               // per stream: device events added
     std::vector<uint32_t> coll_lc, coll_rel; // new collective entries (call_idx - comm_next)
     std::vector<std::pair<uint32_t, uint32_t>> lc_adv;   // (lc, calls issued)
     std::vector<MemRec> mems;                // gpre / seq relative
@@ -203,8 +206,9 @@ struct RepPacker {
     int64_t dgpre = 0;
     uint32_t dseq = 0, ddevev = 0, drecs = 0;
   };
-  std::vector<PhaseTpl> tpls;   // the first ntpl are this rep's (objects reused: no
-  size_t ntpl = 0;              // allocation per rep)
+  std::vector<PhaseTpl> tpls;   // the first ntpl are this job's (objects reused: no
+  size_t ntpl = 0;              // allocation per job); job_begin() resets
+  std::vector<int> rmap;        // replay: template stream -> local stream
   bool cap = false;
   int64_t cap_aid = 0;
   struct Snap {
@@ -239,6 +243,7 @@ struct RepPacker {
     t.ok = false;
     for (auto &v : t.ops) v.clear();
     t.sev.clear();
+    t.raw.clear();
     t.coll_lc.clear();
     t.coll_rel.clear();
     t.lc_adv.clear();
@@ -255,6 +260,7 @@ struct RepPacker {
     if (t.ops.size() < RB.size()) t.ops.resize(RB.size());
     t.nst = RB.size();
     t.sev.resize(RB.size());
+    t.raw.assign(RB.raw_of.begin(), RB.raw_of.begin() + RB.size());
     for (size_t q = 0; q < RB.size(); q++) {
       const size_t k0 = q < snap0.nst ? cap_size[q] : 0;
       t.sev[q] = RB.sev[q] - (q < snap0.nst ? cap_sev[q] : 0u);
@@ -297,16 +303,27 @@ struct RepPacker {
   // emits the phase event by event)
   bool phase_replay(int id, int64_t aid_base) {
     const PhaseTpl &t = tpls[id];
-    if (seg != t.seg || t.nst > RB.size()) return false;
+    if (seg != t.seg) return false;
     // the run-folding limit and block fits (kernel_block) assume gap prefixes
     // well below 2^61: replay only far from it
     if (gpre > ((int64_t)1 << 59) - t.dgpre) return false;
+    // the streams and communicators the template touches must be open here
+    rmap.resize(t.nst);
+    for (size_t q = 0; q < t.nst; q++) {
+      rmap[q] = -1;
+      if (t.ops[q].empty() && t.sev[q] == 0) continue;
+      rmap[q] = RB.local_stream(t.raw[q], false);
+      if (rmap[q] < 0) return false;
+    }
+    for (const auto &a : t.lc_adv)
+      if (a.first >= comm_next.size()) return false;
     const uint32_t cb = (uint32_t)(P->coll_lc.size() - coll0);
     // per tag: what the op's arg is relative to (KERN: nothing, COLL: the
     // rep's collective count, REC/WAIT: the record count)
     const uint32_t addv[4] = {0u, cb, n_recs, n_recs};
     for (size_t q = 0; q < t.nst; q++) {
-      std::vector<Op> &dst = RB.sops[q];
+      if (rmap[q] < 0) continue;
+      std::vector<Op> &dst = RB.sops[rmap[q]];
       const size_t n0 = dst.size(), n = t.ops[q].size();
       dst.resize(n0 + n);
       Op *d = dst.data() + n0;
@@ -317,7 +334,7 @@ struct RepPacker {
         o.arg += addv[o.meta & 3u];
         d[k] = o;
       }
-      RB.sev[q] += t.sev[q];
+      RB.sev[rmap[q]] += t.sev[q];
     }
     {
       const size_t c0 = P->coll_lc.size(), n = t.coll_lc.size();
@@ -357,8 +374,8 @@ struct RepPacker {
     return true;
   }
 
+  void job_begin() { ntpl = 0; }
   void begin(JobPack &pk, FeatState &fs, int32_t dev, bool on_the_fly, size_t reserve_hint) {
-    ntpl = 0;
     cap = false;
     keep_seq = true;
     P = &pk;
@@ -1314,6 +1331,7 @@ int pack_generated(const maya_model &model, const maya_config &cfg, const maya_c
   sink.rep_comms = &rep_comms;
   sink.blocks = blocks;
   sink.replay = g_phase_replay;
+  RP.job_begin();   // phase templates are shared by the job's reps
   int rc;
   try {
     rc = generate_job(model, cfg, cl, schedule, overhead, G, err, &sink, cache);
