@@ -382,32 +382,49 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
           // shared-memory rings (2 slots per communicator, cumulative counts)
           // when every rank issues a communicator's calls in order from one
           // stream (JOB_RING); else one global slot per call
-          CollSlot *cs;
-          uint32_t target;
+          // (explicit address spaces: a generic pointer would make every
+          // atomic and volatile load generic, system scope)
+          uint32_t target, old = 0, cnt = 0;
+          uint64_t mx = 0;
           if (ring) {
-            cs = sh.ring + 2 * g + (idx & 1u);
+            const uint32_t cs = sm_u32(sh.ring + 2 * g + (idx & 1u));
             target = ((idx >> 1) + 1u) * nr;
+            if (!posted) {
+              asm volatile("atom.shared.max.u64 %0, [%1], %2;" : "=l"(mx) : "r"(cs), "l"((uint64_t)ready) : "memory");
+              asm volatile("fence.acq_rel.cta;" ::: "memory");
+              asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(cs + 8u) : "memory");
+              cnt = old + 1;
+            } else {
+              asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(cnt) : "r"(cs + 8u) : "memory");
+            }
+            if (cnt >= target) {
+              asm volatile("fence.acq_rel.cta;" ::: "memory");
+              asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(mx) : "r"(cs) : "memory");
+            }
           } else {
-            cs = b.cslots + J.slots + b.comms[J.comms + g].call_base + idx;
+            CollSlot *cs = b.cslots + J.slots + b.comms[J.comms + g].call_base + idx;
             target = nr;
+            if (!posted) {
+              asm volatile("atom.global.max.u64 %0, [%1], %2;" : "=l"(mx) : "l"(&cs->maxarr), "l"((uint64_t)ready) : "memory");
+              asm volatile("fence.acq_rel.cta;" ::: "memory");
+              asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&cs->count) : "memory");
+              cnt = old + 1;
+            } else {
+              asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(cnt) : "l"(&cs->count) : "memory");
+            }
+            if (cnt >= target) {
+              asm volatile("fence.acq_rel.cta;" ::: "memory");
+              asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(mx) : "l"(&cs->maxarr) : "memory");
+            }
           }
-          bool done_c;
           if (!posted) {
-            atomicMax(&cs->maxarr, (unsigned long long)ready);
-            __threadfence_block();
-            const uint32_t old = atomicAdd(&cs->count, 1u);
             posted = true;
             prog = true;
-            if (old + 1 > target) err = MAYA_ST_INTERNAL;
-            done_c = old + 1 == target;
-          } else {
-            done_c = *(volatile const uint32_t *)&cs->count >= target;
+            if (cnt > target) err = MAYA_ST_INTERNAL;
           }
-          if (done_c) {
-            __threadfence_block();
-            base = (int64_t)*(volatile const unsigned long long *)&cs->maxarr;
-          }
-          ok = done_c && !err;
+          const bool done_c = cnt >= target && !err;
+          if (done_c) base = (int64_t)mx;
+          ok = done_c;
         }
         const int64_t add = (kind & CM_KERN) ? cm.dk : wire;   // (wire = 0 unless COLL)
         if (kind & (CM_BAD | CM_OVF)) {            // a failed estimate / overflowed run (cold)
@@ -539,17 +556,20 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
 // iff it is a body after a WAIT or a REC after a WAIT or a body, so a macro
 // has at most 3 members -- hence chunks of 32 ops: lanes 0-29 lead macros
 // whose members all lie in the chunk, and the next chunk starts at the first
-// op no written macro covers.
+// op no written macro covers.  Grid: CHAIN_MAX_FIFOS / 8 CTAs of 8 warps per
+// chain job, one warp per FIFO, so every FIFO of the batch is fused at once.
 static constexpr uint32_t MACRO_WARPS = 8;
 
 __global__ void __launch_bounds__(MACRO_WARPS * 32) chain_macro_kernel(DevBatch b,
                                                                        const int32_t *order) {
-  const uint32_t j = (uint32_t)order[blockIdx.x];
+  constexpr uint32_t PARTS = CHAIN_MAX_FIFOS / MACRO_WARPS;
+  const uint32_t j = (uint32_t)order[blockIdx.x / PARTS];
   const JobHdr &J = b.jobs[j];
-  if (J.status != MAYA_ST_OK) return;
+  const uint32_t lane = threadIdx.x & 31u, W = J.n_walkers;
+  const uint32_t w = (blockIdx.x % PARTS) * MACRO_WARPS + (threadIdx.x >> 5);
+  if (J.status != MAYA_ST_OK || w >= W) return;
   const LaneJob LJ = b.lane_jobs[j];
-  const uint32_t lane = threadIdx.x & 31u, wp = threadIdx.x >> 5, W = J.n_walkers;
-  for (uint32_t w = wp; w < W; w += MACRO_WARPS) {
+  {
     const Walker wk = b.walkers[J.walkers + w];
     const RankRec rr = b.ranks[J.ranks + wk.rank];
     const RepHdr &h = b.reps[rr.rep];
@@ -642,7 +662,7 @@ __global__ void __launch_bounds__(MACRO_WARPS * 32) chain_macro_kernel(DevBatch 
 }
 
 void launch_chain_macros(const DevBatch &b, const int32_t *order, uint32_t n, cudaStream_t s) {
-  if (n) chain_macro_kernel<<<n, MACRO_WARPS * 32, 0, s>>>(b, order);
+  if (n) chain_macro_kernel<<<n * (CHAIN_MAX_FIFOS / MACRO_WARPS), MACRO_WARPS * 32, 0, s>>>(b, order);
 }
 
 int chain_prof_read(unsigned long long *out8, int reset) {
