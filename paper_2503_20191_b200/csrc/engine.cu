@@ -131,6 +131,9 @@ struct maya_engine {
   Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst, x_gsync, x_macros;
   uint32_t chain_first = 0, chain_jobs = 0;   // chain jobs: the tail of the job order
   std::vector<int32_t> job_kernel;            // per job: 0 warp-window, 1 lane, 2 grid, 3 chain
+  cudaGraphExec_t graph_exec = nullptr;       // the run's device work, captured (maya_run)
+  bool graph_fold = false;
+  uint32_t runs_since_upload = 0;
   std::vector<GridPart> grid_parts;        // host copy (launch grouping)
   std::vector<std::pair<uint32_t, uint32_t>> grid_launches;   // part ranges per launch
   uint32_t grid_smem = 0;
@@ -496,6 +499,7 @@ int maya_close(maya_engine *e) {
   if (e->d_scratch) cudaFree(e->d_scratch);
   if (e->d_stats) cudaFree(e->d_stats);
   if (e->h_topk) cudaFreeHost(e->h_topk);
+  if (e->graph_exec) cudaGraphExecDestroy(e->graph_exec);
   for (auto &ev : e->ev) if (ev) cudaEventDestroy(ev);
   for (auto &ev : e->vev) if (ev) cudaEventDestroy(ev);
   for (auto &s : e->vstream) if (s) cudaStreamDestroy(s);
@@ -1194,6 +1198,12 @@ int maya_upload(maya_engine *e) {
       return fail(MAYA_EINVAL, "job references a device class that was not set");
   }
   e->uploaded = true;
+  // a new batch: the captured run (kernel arguments, grid sizes) is stale
+  if (e->graph_exec) {
+    cudaGraphExecDestroy(e->graph_exec);
+    e->graph_exec = nullptr;
+  }
+  e->runs_since_upload = 0;
   e->ran = false;
   return MAYA_OK;
 }
@@ -1214,6 +1224,10 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
       CU(cudaStreamSynchronize(e->stream));
       CU(cudaMalloc(&p, need));
       cudaFree(e->d_scratch);
+      if (e->graph_exec) {   // its kernels point into the old scratch
+        cudaGraphExecDestroy(e->graph_exec);
+        e->graph_exec = nullptr;
+      }
       e->d_scratch = p;
       e->d_scratch_cap = need;
       char *X = (char *)p;
@@ -1250,75 +1264,121 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   db.gsync = (GridSync *)(X + e->x_gsync.off);
   db.chunk_cnt = (uint32_t *)(X + e->x_chunk_cnt.off);
   db.ccounts = fold ? (uint32_t *)(X + e->x_ccounts.off) : nullptr;
-  CU(cudaEventRecord(e->ev[0], e->stream));
-  CU(cudaMemsetAsync(X + e->x_err.off, 0, 16, e->stream));
-  launch_estimate(db, e->tables, e->stream);
-  CU(cudaGetLastError());
-  CU(cudaEventRecord(e->ev[1], e->stream));
-  CU(cudaMemsetAsync(X + e->x_fire.off, 0xff, e->x_fire.bytes, e->stream));
-  CU(cudaMemsetAsync(X + e->x_cslots.off, 0, e->x_cslots.bytes, e->stream));
-  if (!e->grid_parts.empty()) CU(cudaMemsetAsync(X + e->x_gsync.off, 0, e->x_gsync.bytes, e->stream));
-  launch_memscan(db, e->stream);
-  CU(cudaGetLastError());
-  launch_resolve(db, e->stream);
-  CU(cudaGetLastError());
-  if (fold && e->chain_jobs) {   // chain jobs: macro ops of their folded FIFOs
-    launch_chain_macros(db, db.order + e->chain_first, e->chain_jobs, e->stream);
+  // The run's device work (estimators, memory scan, fold / resolve, macro
+  // pass, the scheduler groups on their streams, joined back).  Runs without a
+  // timeline replay it as ONE CUDA graph from the second run of a batch on
+  // (captured once per upload): ~25 launches and their fork/join events cost
+  // one graph launch.  The phase-timing events become external event-record
+  // nodes, so maya_last_timings keeps its three phases.
+  auto enqueue = [&](bool captured) -> int {
+    auto rec = [&](cudaEvent_t ev) {
+      return captured ? cudaEventRecordWithFlags(ev, e->stream, cudaEventRecordExternal)
+                      : cudaEventRecord(ev, e->stream);
+    };
+    CU(rec(e->ev[0]));
+    CU(cudaMemsetAsync(X + e->x_err.off, 0, 16, e->stream));
+    launch_estimate(db, e->tables, e->stream);
     CU(cudaGetLastError());
-  }
-  CU(cudaEventRecord(e->ev[2], e->stream));
-  {
-    // variants run concurrently on their own streams (fork/join)
-    CU(cudaEventRecord(e->vev[maya_engine::NVAR], e->stream));
-    uint32_t var_off[maya_engine::NVAR];
-    for (int v = 0, o = 0; v < maya_engine::NVAR; v++) { var_off[v] = (uint32_t)o; o += (int)e->var_n[v]; }
-    // groups of larger jobs first (grid jobs, CTA lane jobs, then warp-window
-    // jobs from 16 down to 4 warps): the longest dependency chains get their
-    // SMs before the short jobs fill the machine (measured: C2's step stays at
-    // its fast mode in 5 of 6 processes instead of 2 of 5)
-    for (int vi = 0; vi < maya_engine::NVAR; vi++) {
-      const int v = maya_engine::NVAR - 1 - vi;
-      const uint32_t off = var_off[v];
-      if (!e->var_n[v]) continue;
-      CU(cudaStreamWaitEvent(e->vstream[v], e->vev[maya_engine::NVAR], 0));
-      if (v == 15) {   // grid jobs: one cooperative launch per group of co-resident parts
-        for (auto &pr : e->grid_launches)
-          if (launch_schedule_grid(db, pr.first, pr.second, record_timeline ? 1 : 0,
-                                   e->grid_smem, e->vstream[v]) != 0)
-            return fail(MAYA_ECUDA, std::string("cooperative launch: ") +
-                                        cudaGetErrorString(cudaGetLastError()));
-      } else if (v < 3) {
-        const uint32_t nb = e->var_big[v], ns = e->var_n[v] - nb;
-        launch_schedule_variant(db, v, db.order + off, nb, record_timeline ? 1 : 0,
-                                e->var_smem[v], e->vstream[v]);
-        if (ns) {   // small-footprint jobs on their own stream, concurrently
-          CU(cudaStreamWaitEvent(e->sstream[v], e->vev[maya_engine::NVAR], 0));
-          launch_schedule_variant(db, v, db.order + off + nb, ns, record_timeline ? 1 : 0,
-                                  e->var_smem_small[v], e->sstream[v]);
-          CU(cudaGetLastError());
-          CU(cudaEventRecord(e->sev[v], e->sstream[v]));
-          CU(cudaStreamWaitEvent(e->stream, e->sev[v], 0));
-        }
-      } else if (v >= 16) {
-        launch_schedule_chain(db, db.order + off, e->var_n[v],
-                              v >= 16 + (int)CHAIN_CLASSES ? 64u : 32u, record_timeline ? 1 : 0,
-                              e->var_smem[v], e->vstream[v]);
-      } else if (v <= 10) {
-        const uint32_t region = e->var_smem[v];
-        uint32_t wpc = region ? LANE_SMEM_CAP / region : 8;
-        wpc = wpc < 1 ? 1 : wpc > 8 ? 8 : wpc;
-        launch_schedule_lane_warp(db, db.order + off, e->var_n[v], wpc, region,
-                                  record_timeline ? 1 : 0, e->vstream[v]);
-      } else {
-        launch_schedule_lane(db, db.order + off, e->var_n[v], 64u << (v - 11),
-                             record_timeline ? 1 : 0, e->var_smem[v], e->vstream[v]);
-      }
+    CU(rec(e->ev[1]));
+    CU(cudaMemsetAsync(X + e->x_fire.off, 0xff, e->x_fire.bytes, e->stream));
+    CU(cudaMemsetAsync(X + e->x_cslots.off, 0, e->x_cslots.bytes, e->stream));
+    if (!e->grid_parts.empty()) CU(cudaMemsetAsync(X + e->x_gsync.off, 0, e->x_gsync.bytes, e->stream));
+    launch_memscan(db, e->stream);
+    CU(cudaGetLastError());
+    launch_resolve(db, e->stream);
+    CU(cudaGetLastError());
+    if (fold && e->chain_jobs) {   // chain jobs: macro ops of their folded FIFOs
+      launch_chain_macros(db, db.order + e->chain_first, e->chain_jobs, e->stream);
       CU(cudaGetLastError());
-      CU(cudaEventRecord(e->vev[v], e->vstream[v]));
-      CU(cudaStreamWaitEvent(e->stream, e->vev[v], 0));
     }
+    CU(rec(e->ev[2]));
+    {
+      // variants run concurrently on their own streams (fork/join)
+      CU(cudaEventRecord(e->vev[maya_engine::NVAR], e->stream));
+      uint32_t var_off[maya_engine::NVAR];
+      for (int v = 0, o = 0; v < maya_engine::NVAR; v++) { var_off[v] = (uint32_t)o; o += (int)e->var_n[v]; }
+      // groups of larger jobs first (grid jobs, CTA lane jobs, then warp-window
+      // jobs from 16 down to 4 warps): the longest dependency chains get their
+      // SMs before the short jobs fill the machine (measured: C2's step stays at
+      // its fast mode in 5 of 6 processes instead of 2 of 5)
+      for (int vi = 0; vi < maya_engine::NVAR; vi++) {
+        const int v = maya_engine::NVAR - 1 - vi;
+        const uint32_t off = var_off[v];
+        if (!e->var_n[v]) continue;
+        CU(cudaStreamWaitEvent(e->vstream[v], e->vev[maya_engine::NVAR], 0));
+        if (v == 15) {   // grid jobs: one cooperative launch per group of co-resident parts
+          for (auto &pr : e->grid_launches)
+            if (launch_schedule_grid(db, pr.first, pr.second, record_timeline ? 1 : 0,
+                                     e->grid_smem, e->vstream[v]) != 0)
+              return fail(MAYA_ECUDA, std::string("cooperative launch: ") +
+                                          cudaGetErrorString(cudaGetLastError()));
+        } else if (v < 3) {
+          const uint32_t nb = e->var_big[v], ns = e->var_n[v] - nb;
+          launch_schedule_variant(db, v, db.order + off, nb, record_timeline ? 1 : 0,
+                                  e->var_smem[v], e->vstream[v]);
+          if (ns) {   // small-footprint jobs on their own stream, concurrently
+            CU(cudaStreamWaitEvent(e->sstream[v], e->vev[maya_engine::NVAR], 0));
+            launch_schedule_variant(db, v, db.order + off + nb, ns, record_timeline ? 1 : 0,
+                                    e->var_smem_small[v], e->sstream[v]);
+            CU(cudaGetLastError());
+            CU(cudaEventRecord(e->sev[v], e->sstream[v]));
+            CU(cudaStreamWaitEvent(e->stream, e->sev[v], 0));
+          }
+        } else if (v >= 16) {
+          launch_schedule_chain(db, db.order + off, e->var_n[v],
+                                v >= 16 + (int)CHAIN_CLASSES ? 64u : 32u, record_timeline ? 1 : 0,
+                                e->var_smem[v], e->vstream[v]);
+        } else if (v <= 10) {
+          const uint32_t region = e->var_smem[v];
+          uint32_t wpc = region ? LANE_SMEM_CAP / region : 8;
+          wpc = wpc < 1 ? 1 : wpc > 8 ? 8 : wpc;
+          launch_schedule_lane_warp(db, db.order + off, e->var_n[v], wpc, region,
+                                    record_timeline ? 1 : 0, e->vstream[v]);
+        } else {
+          launch_schedule_lane(db, db.order + off, e->var_n[v], 64u << (v - 11),
+                               record_timeline ? 1 : 0, e->var_smem[v], e->vstream[v]);
+        }
+        CU(cudaGetLastError());
+        CU(cudaEventRecord(e->vev[v], e->vstream[v]));
+        CU(cudaStreamWaitEvent(e->stream, e->vev[v], 0));
+      }
+    }
+    CU(rec(e->ev[3]));
+    return MAYA_OK;
+  };
+  const bool graph_ok = !record_timeline && e->grid_launches.empty() && !getenv("MAYA_NO_GRAPH");
+  if (graph_ok && e->graph_exec && e->graph_fold == fold) {
+    CU(cudaGraphLaunch(e->graph_exec, e->stream));
+  } else if (graph_ok && e->runs_since_upload > 0) {
+    if (e->graph_exec) {
+      cudaGraphExecDestroy(e->graph_exec);
+      e->graph_exec = nullptr;
+    }
+    CU(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = enqueue(true);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
+    bool launched = false;
+    if (rc == MAYA_OK && ce == cudaSuccess && g) {
+      if (cudaGraphInstantiate(&e->graph_exec, g, 0) == cudaSuccess) {
+        e->graph_fold = fold;
+        CU(cudaGraphLaunch(e->graph_exec, e->stream));
+        launched = true;
+      } else {
+        e->graph_exec = nullptr;
+      }
+    }
+    if (g) cudaGraphDestroy(g);
+    if (!launched) {   // capture not possible here: run eagerly
+      cudaGetLastError();
+      const int rc2 = enqueue(false);
+      if (rc2 != MAYA_OK) return rc2;
+    }
+  } else {
+    const int rc = enqueue(false);
+    if (rc != MAYA_OK) return rc;
   }
-  CU(cudaEventRecord(e->ev[3], e->stream));
+  e->runs_since_upload++;
   e->stats_ok = false;
   if (record_timeline) {
     // per-rank busy statistics (_report, sim.py:406-426) from the recorded timeline
