@@ -301,7 +301,7 @@ def measured_peak_hbm():
 
 def ncu_traffic():
     """dram bytes per launch of the scheduler from the committed ncu summary."""
-    path = os.path.join(REPO, "profiles", "schedule_kernel_ncu.json")
+    path = os.path.join(REPO, "profiles", "schedule_kernel_ncu_r2.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -361,7 +361,7 @@ def c5_sweep(spec: str, steps: int, dev_index: int) -> dict:
             "step_ms": {"estimators": round(est_ms, 4), "memscan+fold+resolve": round(fold_ms, 4),
                         "schedulers": round(ms, 4), "total": round(step_ms, 4)},
             "roofline": {"bound": "hbm",
-                         "kernels": "the whole step: estimate_features + fold_count + fold_write "
+                         "kernels": "the whole step: estimate_features + fold_write (one pass) "
                                     "+ sched_lane_warp (+ small tables), i.e. every kernel that "
                                     "reads the algorithmic bytes",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -705,13 +705,15 @@ def bench_ours(args):
                             "top-k; step k+1's host work overlaps step k's device work",
                     "identical_results_to_device_step": e2e_same,
                     "best": list(e2e_best) if e2e_best else None},
-            "roofline": {"bound": "hbm", "kernel": "sched_warp_kernel",
+            "roofline": {"bound": "hbm", "kernel": "sched_chain_kernel",
                          "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 5), "traffic": ncu_traffic(),
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "kernel_ms": round(sched, 4), "peak_source": peak_kind,
-                         "note": "C2 is latency-bound (dedup and kernel blocks make the "
-                                 "compulsory bytes << work)"},
+                         "note": "C2 is latency-bound: the step is the slowest job's chain of "
+                                 "stage hand-offs (~800 lockstep iterations of the chain "
+                                 "kernel for pp8 x 64 microbatches); dedup, kernel blocks and "
+                                 "folding make the compulsory bytes << work"},
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "rounds": {"max": int(res["rounds"].max()), "median": float(np.median(res["rounds"]))},

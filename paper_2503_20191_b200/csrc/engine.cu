@@ -128,7 +128,7 @@ struct maya_engine {
       s_coll_lc, s_coll_idx, s_coll_wf, s_syncs, s_counts, s_mems, s_feats, s_order, s_rcolls, s_wids, s_rcslot,
       s_lane_jobs, s_lane_wslot, s_lane_perm, s_chunks, s_grid_parts, s_comm_part, s_blocks,
       s_blk_fids;
-  Seg x_clen, x_ccounts, x_chunk_cnt, x_lctx, x_lst, x_gsync, x_macros;
+  Seg x_clen, x_ccounts, x_lctx, x_lst, x_gsync, x_macros;
   uint32_t chain_first = 0, chain_jobs = 0;   // chain jobs: the tail of the job order
   std::vector<int32_t> job_kernel;            // per job: 0 warp-window, 1 lane, 2 grid, 3 chain
   cudaGraphExec_t graph_exec = nullptr;       // the run's device work, captured (maya_run)
@@ -758,7 +758,6 @@ int maya_upload(maya_engine *e) {
   off = 0;
   seg(e->x_exec, n_ops * sizeof(ExecOp));
   seg(e->x_clen, n_streams * sizeof(uint32_t));
-  seg(e->x_chunk_cnt, n_chunks * sizeof(uint32_t));
   seg(e->x_lctx, n_walkers * 64);
   seg(e->x_lst, n_walkers * 48);
   seg(e->x_macros, n_macros * sizeof(ChainMacro));
@@ -897,18 +896,19 @@ int maya_upload(maya_engine *e) {
       if (!L.on_chip) b.wstate += spill_bytes(P.walkers.size(), P.ranks.size());
     }
   }
-  {  // run-folding work items: one per 1,024 ops of every FIFO
+  {  // run-folding work items: one per 1,024 ops of every FIFO, with the folded
+     // ops before each (host-counted in pack_tail: no counting pass on the device)
     FoldChunk *fcs = (FoldChunk *)(H + e->s_chunks.off);
     size_t q = 0;
     for (size_t j = 0; j < nj; j++) {
       const JobPack &P = e->packs[j];
+      size_t k = 0;
       for (size_t r = 0; r < P.reps.size(); r++) {
         const RepHdr &h = P.reps[r];
         for (uint32_t st = 0; st < h.n_streams; st++) {
           const uint32_t len = P.streams[h.streams + st].len;
-          const uint32_t first = (uint32_t)q;
           for (uint32_t c = 0; c * FOLD_CHUNK < len; c++)
-            fcs[q++] = FoldChunk{(uint32_t)(bases[j].reps + r), st, c, first};
+            fcs[q++] = FoldChunk{(uint32_t)(bases[j].reps + r), st, c, P.fold_base[k++]};
         }
       }
     }
@@ -1262,7 +1262,6 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
   db.lane_gst = (uint8_t *)(X + e->x_lst.off);
   db.macros = (ChainMacro *)(X + e->x_macros.off);
   db.gsync = (GridSync *)(X + e->x_gsync.off);
-  db.chunk_cnt = (uint32_t *)(X + e->x_chunk_cnt.off);
   db.ccounts = fold ? (uint32_t *)(X + e->x_ccounts.off) : nullptr;
   // The run's device work (estimators, memory scan, fold / resolve, macro
   // pass, the scheduler groups on their streams, joined back).  Runs without a
@@ -1408,7 +1407,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
     int64_t n = (db.n_feats ? 1 : 0) + (db.n_wfeats ? 1 : 0) + (db.n_reps ? 1 : 0) +
                 (db.n_rcolls ? 1 : 0);
     if (fold)
-      n += (db.n_blocks ? 1 : 0) + (db.n_chunks ? 2 : 0) + (db.n_reps ? 1 : 0) +
+      n += (db.n_blocks ? 1 : 0) + (db.n_chunks ? 1 : 0) + (db.n_reps ? 1 : 0) +
            (e->chain_jobs ? 1 : 0);
     else
       n += db.n_ops ? 1 : 0;

@@ -1215,62 +1215,8 @@ __global__ void block_compose_kernel(DevBatch b) {
   }
 }
 
-// pass 1: folded ops per chunk
-static constexpr uint32_t FOLD_WARPS = 2;             // warps (chunks) per CTA
-static constexpr uint32_t FOLD_PAD = FOLD_CHUNK + FOLD_CHUNK / 32;   // one pad op per 32
-
-// Coalesced copy of a chunk into shared memory, padded so that lane L's 32
-// consecutive ops (L*33 + t) spread over the banks.
-__device__ __forceinline__ void fold_stage(const Op *in, uint32_t lo, uint32_t hi, Op *sm,
-                                           uint32_t lane) {
-  // every load in flight at once (LDGSTS), then one wait
-  for (uint32_t j = lane; lo + j < hi; j += 32) {
-    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm[j + (j >> 5)]);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(in + lo + j)
-                 : "memory");
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
-}
-__device__ __forceinline__ const Op &fold_at(const Op *sm, uint32_t j) { return sm[j + (j >> 5)]; }
-
-__global__ void __launch_bounds__(FOLD_WARPS * 32) fold_count_kernel(DevBatch b) {
-  __shared__ Op sm_all[FOLD_WARPS][FOLD_PAD];
-  const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const uint32_t c = blockIdx.x * FOLD_WARPS + wp;
-  if (c >= b.n_chunks) return;
-  Op *sm = sm_all[wp];
-  const FoldChunk fc = b.chunks[c];
-  const RepHdr &h = b.reps[fc.rep];
-  const StreamRange sr = b.streams[h.streams + fc.st];
-  const Op *in = b.ops + h.ops + sr.begin;
-  const uint32_t *cw = b.coll_wf + h.colls;
-  const uint32_t lo = fc.chunk * FOLD_CHUNK, hi = min(sr.len, lo + FOLD_CHUNK);
-  fold_stage(in, lo, hi, sm, lane);
-  const uint32_t k0 = lo + lane * 32u, k1 = min(hi, k0 + 32u);
-  uint32_t cnt = 0;
-  if (k0 < hi) {
-    uint32_t pseg = 0;
-    bool pfold = false;
-    if (k0 > lo) {
-      const Op &p = fold_at(sm, k0 - 1 - lo);
-      pseg = op_seg(p.meta);
-      pfold = op_foldable(p, cw);
-    }
-    for (uint32_t i = k0; i < k1; i++) {
-      const Op &o = fold_at(sm, i - lo);
-      const bool f = op_foldable(o, cw);
-      const uint32_t sg = op_seg(o.meta);
-      cnt += (i == lo || !f || !pfold || sg != pseg) ? 1u : 0u;
-      pseg = sg;
-      pfold = f;
-    }
-  }
-  cnt = __reduce_add_sync(FULL, cnt);
-  if (lane == 0) b.chunk_cnt[c] = cnt;
-}
-
-// pass 2: fold and write each chunk at its offset; sync counts; lengths.
+// One pass: fold and write each chunk at its offset (FoldChunk.out, counted by
+// the host packer with the same rule, pack.cpp); sync counts; lengths.
 // 128-op windows, 4 consecutive ops per lane: a lane composes its 4 maps
 // sequentially (branch-free), the warp scans the 32 lane composites once, and
 // each lane writes the runs that end among its ops.
@@ -1291,9 +1237,7 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
   uint32_t *cc = b.ccounts + h.counts + fc.st;
   const uint32_t n = sr.len;
   const uint32_t lo = fc.chunk * FOLD_CHUNK, hi = min(n, lo + FOLD_CHUNK);
-  uint32_t outpos = 0;   // folded ops of the FIFO before this window
-  for (uint32_t q = fc.first + lane; q < c; q += 32) outpos += b.chunk_cnt[q];
-  outpos = __reduce_add_sync(FULL, outpos);
+  uint32_t outpos = fc.out;   // folded ops of the FIFO before this window (host-counted)
   // carry from the previous window: last op's segment / foldability, open run
   uint32_t cseg = lo > 0 ? op_seg(in[lo - 1].meta) : 0;
   bool cfold = false;            // the chunk's first op always starts a run
@@ -1493,8 +1437,6 @@ void launch_resolve(const DevBatch &b, cudaStream_t s) {
     if (b.n_blocks)
       block_compose_kernel<<<(unsigned)((b.n_blocks * 32ull + 255) / 256), 256, 0, s>>>(b);
     if (b.n_chunks) {
-      const unsigned g = (b.n_chunks + FOLD_WARPS - 1) / FOLD_WARPS;
-      fold_count_kernel<<<g, FOLD_WARPS * 32, 0, s>>>(b);
       const unsigned gw = (unsigned)((b.n_chunks * 32ull + 127) / 128);
       if (b.n_blocks) fold_write_kernel<true><<<gw, 128, 0, s>>>(b);
       else fold_write_kernel<false><<<gw, 128, 0, s>>>(b);

@@ -63,7 +63,6 @@ struct DevBatch {
   uint8_t *lane_gst;          // per walker: 48 B FIFO state when LANE_ST_GLOBAL
   ChainMacro *macros;         // chain jobs, folded runs: each FIFO's macro ops (chain_macro_kernel)
   const FoldChunk *chunks;    // fold work items (one per 1,024 ops of a FIFO)
-  uint32_t *chunk_cnt;        // folded ops per chunk
   uint32_t n_chunks;
   uint32_t *clen;             // folded FIFO lengths (fold_kernel) or null: unfolded ops
   uint32_t *ccounts;          // host-sync dispatch counts in folded indices (with clen)

@@ -128,7 +128,7 @@ struct FeatState {
 };
 
 // Ops of a FIFO after the device folds its affine runs (kernels.cu
-// fold_count_kernel: the same rule): kernels, and collectives whose coll_wf
+// fold_write_kernel: the same rule): kernels, and collectives whose coll_wf
 // entry names a wire feature, whose gap prefix is below 2^61, join the run of
 // the op before them within one host-sync segment; runs are cut every
 // FOLD_CHUNK ops.  coll_wf: the rep's per-collective entries (null: none).
@@ -1181,8 +1181,9 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
       any |= cw != NO_WF;
     }
     P.stream_macros.assign(P.streams.size(), 0);
+    P.fold_base.clear();
     // one pass per FIFO: flag the foldable collectives (OP_FOLDC) and count the
-    // ops it keeps after the device folds its runs (kernels.cu fold_count_kernel:
+    // ops it keeps after the device folds its runs (kernels.cu fold_write_kernel:
     // the same rule, folded_len), for sizing the schedulers' staging
     for (const RepHdr &h : P.reps)
       for (uint32_t s = 0; s < h.n_streams; s++) {
@@ -1198,6 +1199,7 @@ void pack_tail(const maya_raw_job &job, JobPack &P, bool collapse,
           const bool f = v[i].disp < ((int64_t)1 << 61) &&
                          (tg == TAG_KERN || (v[i].meta & OP_FOLDC));
           const uint32_t sg = op_seg(v[i].meta);
+          if (i % FOLD_CHUNK == 0) P.fold_base.push_back(folded);   // the fold pass's chunk
           if (i % FOLD_CHUNK == 0 || !f || !pf || sg != ps) {   // a folded op starts here
             folded++;
             // its class for the chain kernel's macro fusion (kernel: a folded run)

@@ -18,6 +18,7 @@ struct JobPack {
   std::vector<StreamRange> streams;
   std::vector<uint32_t> stream_events; // host only: device events per stream (blocks expanded)
   std::vector<uint32_t> stream_macros; // host only: chain-kernel macro ops per stream (soa.h)
+  std::vector<uint32_t> fold_base;     // per stream, per 1,024-op chunk: folded ops before it
   std::vector<uint32_t> coll_lc, coll_idx;
   std::vector<uint32_t> coll_wf;       // per rep collective: job-local wire feature when every
                                        // simulated rank of the rep meets it alone (one member
@@ -49,7 +50,7 @@ struct JobPack {
 
   void clear() {   // keeps capacity (see engine.cu PackPool)
     hdr = JobHdr{};
-    reps.clear(); ops.clear(); op_seq.clear(); streams.clear(); stream_events.clear(); stream_macros.clear(); coll_lc.clear();
+    reps.clear(); ops.clear(); op_seq.clear(); streams.clear(); stream_events.clear(); stream_macros.clear(); fold_base.clear(); coll_lc.clear();
     coll_idx.clear(); coll_wf.clear(); syncs.clear(); counts.clear(); mems.clear(); feats.clear(); feat_meta.clear(); comms.clear();
     blocks.clear(); blk_fids.clear();
     slots.clear(); wfeats.clear(); slot_wf.clear(); ranks.clear(); rank_comm.clear(); walkers.clear(); wids.clear();

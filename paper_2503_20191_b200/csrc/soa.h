@@ -273,7 +273,7 @@ struct FoldChunk {
   uint32_t rep;        // batch rep index
   uint32_t st;         // local stream
   uint32_t chunk;      // chunk index within the FIFO
-  uint32_t first;      // batch chunk id of the FIFO's chunk 0
+  uint32_t out;        // folded ops of the FIFO before this chunk (host-counted, pack.cpp)
 };
 
 // 16-byte device op record.
