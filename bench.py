@@ -702,7 +702,7 @@ def bench_ours(args):
                     "d2h_bytes_per_step": int(N_CONFIGS * 64 + TOPK * 16),
                     "path": "api.GenPipeline.evaluate_stream: per step, config list -> fused "
                             "native gen+pack (C++ threads) -> H2D -> kernels -> D2H results + "
-                            "top-k; step k+1's host work overlaps step k's device work",
+                            "top-k; step k+1's generation overlaps step k's arena assembly + upload (helper thread) and device work",
                     "identical_results_to_device_step": e2e_same,
                     "best": list(e2e_best) if e2e_best else None},
             "roofline": {"bound": "hbm", "kernel": "sched_chain_kernel",

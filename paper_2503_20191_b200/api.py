@@ -519,10 +519,11 @@ class GenPipeline:
         """Evaluate a stream of config batches (a search's successive
         populations), yielding (results, top-k rows, status) per batch in
         order.  Batch q+1 is generated and packed on the host threads while
-        batch q's H2D, kernels and D2H run on the device (the two engines
-        alternate), so a long search runs at the speed of the slower side
-        instead of the sum.  Every batch still goes through generation, H2D,
-        the kernels, the D2H of its results and the top-k."""
+        batch q's arena is assembled and uploaded (a helper thread) and its
+        kernels and D2H run on the device (the two engines alternate), so a
+        long search runs at the speed of the slowest stage instead of the sum.
+        Every batch still goes through generation, H2D, the kernels, the D2H
+        of its results and the top-k."""
         from ._abi import RESULT_DTYPE
 
         def collect(item):
@@ -533,26 +534,40 @@ class GenPipeline:
                                        for t in e.topk(k)], dtype=np.int64).reshape(-1, 3), k)
             return res, top, st
 
-        pending = None
-        for q, configs in enumerate(batches):
-            e = self.engines[q % 2]
-            kr = (key_ranks(configs) if key_orders is None or key_orders[q] is None
-                  else np.asarray(key_orders[q]))
-            st = e.stage_generated(model, configs, cluster, schedule=schedule,
-                                   dispatch_overhead_ns=dispatch_overhead_ns,
-                                   efficiency=efficiency, overhead_ns=overhead_ns,
-                                   key_ranks=kr, threads=threads)
-            # the previous batch's D2H before this batch's H2D: a pageable D2H
-            # queued behind the 26 MB upload would wait for it (measured 0.54 ms)
-            done = collect(pending) if pending is not None else None
+        # Three stages overlap: the main thread generates + packs batch q (pool 0
+        # of the native workers) while a helper thread assembles batch q-1's
+        # arena (pool 1), uploads it and enqueues its run; the device runs
+        # batch q-1 meanwhile.  An engine is restaged only after its previous
+        # batch's results were read.
+        from concurrent.futures import ThreadPoolExecutor
+
+        def launch(e):
             e.upload()
             e.run()
             e.topk_async(k)                    # behind the run on its stream: no wait
-            if done is not None:
-                yield done
-            pending = (e, len(configs), st)
-        if pending is not None:
-            yield collect(pending)
+
+        inflight = [None, None]                # per engine: (batch, future, n configs, status)
+        with ThreadPoolExecutor(max_workers=1) as pool:
+            for q, configs in enumerate(batches):
+                e = self.engines[q % 2]
+                if inflight[q % 2] is not None:   # batch q-2 on this engine: read it first
+                    _, fut, n, st = inflight[q % 2]
+                    fut.result()
+                    inflight[q % 2] = None
+                    yield collect((e, n, st))
+                kr = (key_ranks(configs) if key_orders is None or key_orders[q] is None
+                      else np.asarray(key_orders[q]))
+                st = e.stage_generated(model, configs, cluster, schedule=schedule,
+                                       dispatch_overhead_ns=dispatch_overhead_ns,
+                                       efficiency=efficiency, overhead_ns=overhead_ns,
+                                       key_ranks=kr, threads=threads)
+                inflight[q % 2] = (q, pool.submit(launch, e), len(configs), st)
+            for slot in sorted((0, 1), key=lambda x: inflight[x][0] if inflight[x] else -1):
+                if inflight[slot] is not None:     # the last batches, in order
+                    _, fut, n, st = inflight[slot]
+                    fut.result()
+                    inflight[slot] = None
+                    yield collect((self.engines[slot], n, st))
 
 
 def merge_topk(candidates: np.ndarray, k: int) -> np.ndarray:

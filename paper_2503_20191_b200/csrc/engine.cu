@@ -1100,7 +1100,7 @@ int maya_upload(maya_engine *e) {
         copy_job(j);
       }
     };
-    WorkerPool::get().run(nt, work);
+    WorkerPool::get(1).run(nt, work);
   }
   lap("copy");
   CU(cudaMemcpyAsync(e->d_arena, e->h_arena, e->arena_bytes, cudaMemcpyHostToDevice, e->stream));

@@ -13,9 +13,12 @@ namespace maya {
 
 class WorkerPool {
  public:
-  static WorkerPool &get() {
-    static WorkerPool p;
-    return p;
+  // Pool 0 stages batches (generation + packing), pool 1 assembles arenas, so
+  // a pipeline can assemble batch q while it generates batch q+1 (api.py
+  // GenPipeline).  Each pool runs one parallel region at a time.
+  static WorkerPool &get(int id = 0) {
+    static WorkerPool p[2];
+    return p[id & 1];
   }
   // Run `work` on nt threads (the caller is one of them) and wait for all.
   void run(int nt, const std::function<void()> &work) {
