@@ -587,7 +587,9 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   const int64_t tp_coll_bytes = chk(b * s * h * esz);
   const int64_t loss_reduce_bytes = chk(b * s * 8);
   const int tp_lc = t > 1 ? lc_of(C_TP, stage, j, 0) : -1;
-  std::map<std::pair<int, int64_t>, int64_t> act_ids;
+  // activation allocation handle of each (chunk, micro-batch), -1: none
+  std::vector<int64_t> act_ids(chunks.size() * (size_t)m, -1);
+  auto act = [&](int c, int64_t mb) -> int64_t & { return act_ids[(size_t)c * (size_t)m + (size_t)mb]; };
 
   const std::vector<KSpec> lks = layer_fwd(M, b, t, sp);
   const std::vector<KSpec> hks = head_fwd(M, b, t, sp);
@@ -638,7 +640,7 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   auto emit_forward = [&](int64_t mb, int chunk_id) {
     const Chunk &ch = chunks[chunk_id];
     const int64_t vs = ch.vs;
-    act_ids[{chunk_id, mb}] = B.alloc(chunk_stash_bytes(M, cfg, b, ch));
+    act(chunk_id, mb) = B.alloc(chunk_stash_bytes(M, cfg, b, ch));
     if (vs > 0) {
       int32_t fin = p2p_stream[{vs - 1, R_FIN}];
       B.collective(fin, lc_of(C_PF, vs - 1, i, j), K_SENDRECV, p2p_payload);
@@ -681,9 +683,9 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
       B.wait_last(bout, eid[{E_BOUT, vs - 1}]);
       B.collective(bout, lc_of(C_PB, vs - 1, i, j), K_SENDRECV, p2p_payload);
     }
-    auto it = act_ids.find({chunk_id, mb});
-    B.free_(it->second);
-    act_ids.erase(it);
+    int64_t &h = act(chunk_id, mb);
+    B.free_(h);
+    h = -1;
   };
 
   // Phase templates (kernel-block sinks): every forward / backward of one
@@ -730,8 +732,7 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
     BTpl &bt = *btpl[2 * st.chunk + (st.phase == FWD ? 0 : 1)];
     B.flush();   // phases start and end outside a kernel run
     if (replay && bt.id >= 0 && sink->phase_replay(bt.id, B.next_alloc)) {
-      if (st.phase == FWD) act_ids[{st.chunk, st.mb}] = B.next_alloc;   // its one allocation
-      else act_ids.erase({st.chunk, st.mb});
+      act(st.chunk, st.mb) = st.phase == FWD ? B.next_alloc : -1;   // its one allocation
       B.next_alloc += bt.allocs;
       for (size_t q = 0; q < bt.calls.size();) {   // runs of one communicator
         const int lc = bt.calls[q].first;
@@ -836,6 +837,9 @@ struct CommStruct {
   std::vector<int8_t> topo;
   std::vector<int64_t> rank_comm_off;
   std::vector<int32_t> rank_comm;
+  // distinct (first stage, first local index) pairs and how many comms take
+  // their calls from each (total call count = sum of mult x calls of the pair)
+  std::vector<int32_t> pair_stage, pair_lc, pair_mult;
   std::string error;
 };
 
@@ -919,6 +923,15 @@ std::shared_ptr<const CommStruct> build_comm_struct(const Coords &C, int64_t v, 
     for (int64_t q = rk_off[r]; q < rk_off[r + 1]; q++) cs->rank_comm.push_back(gid_of[comm_of[q]]);
     cs->rank_comm_off.push_back((int64_t)cs->rank_comm.size());
   }
+  {
+    std::map<std::pair<int32_t, int32_t>, int32_t> mult;
+    for (size_t g = 0; g < cs->first_stage.size(); g++) mult[{cs->first_stage[g], cs->first_lc[g]}]++;
+    for (const auto &kv : mult) {
+      cs->pair_stage.push_back(kv.first.first);
+      cs->pair_lc.push_back(kv.first.second);
+      cs->pair_mult.push_back(kv.second);
+    }
+  }
   return cs;
 }
 
@@ -998,7 +1011,8 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
       G.rep_calls.resize(rcalls.size());
       for (size_t k = 0; k < rcalls.size(); k++) G.rep_calls[k] = std::move(rcalls[k].calls);
       int64_t nc = 0;
-      for (size_t gi = 0; gi < cs->nranks.size(); gi++) nc += (int64_t)G.comm_calls(gi).size();
+      for (size_t q = 0; q < cs->pair_stage.size(); q++)
+        nc += (int64_t)cs->pair_mult[q] * (int64_t)G.rep_calls[cs->pair_stage[q]][cs->pair_lc[q]].size();
       G.n_calls_total = nc;
       G.rank_comm_off = cs->rank_comm_off;
       G.rank_comm = cs->rank_comm;

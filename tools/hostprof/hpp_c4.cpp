@@ -30,14 +30,17 @@ int main(int argc, char **argv) {
   maya_cluster cl{ranks / 8, 8, 80ll << 30};
   std::vector<maya_config> cfgs;
   int tps[] = {1, 2, 4, 8}, pps[] = {2, 4, 8, 16}, vss[] = {2, 4, 5, 10};
-  for (int tp : tps) for (int pp : pps) for (int mm = 1; mm <= 16; mm += 3) for (int vs : vss)
+  const bool big = argc > 3;   // the largest configs only (pp x virtual stages >= 40, micro_mult >= 8)
+  for (int tp : tps) for (int pp : pps) for (int mm = big ? 8 : 1; mm <= 16; mm += big ? 4 : 3) for (int vs : vss)
     for (int rc = 1; rc >= 0; rc--) for (int dz = 1; dz >= 0; dz--) {
+      if (big && pp * vs < 40) continue;
       maya_config c{tp, pp, mm, vs, rc, 1, dz, 0, gbs};
       GenJob g;
       if (generate_job(m, c, cl, -1, 5000, g, nullptr) == 0) cfgs.push_back(c);
       if (cfgs.size() == 64) goto done;
     }
 done:
+  for (int q = 0; q < 16; q++) hp_acc[q] = 0;   // only the timed passes
   GenJob g;
   NullSink ns;
   double tgen = 0, tfull = 0;

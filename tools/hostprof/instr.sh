@@ -20,8 +20,8 @@ g=rep(g,"""  G.clear();   // keep capacity: a worker thread reuses one GenJob ac
 g=rep(g,"""    G.rank_rep.resize(n);""","""    HP(2);
     G.rank_rep.resize(n);""")
 g=rep(g,"""                    int64_t rank, int64_t overhead, int32_t dtype, GenJob &G, RepCalls &rc,
-                    EventSink *sink) {""","""                    int64_t rank, int64_t overhead, int32_t dtype, GenJob &G, RepCalls &rc,
-                    EventSink *sink) {
+                    EventSink *sink, JobTpls *jtpl) {""","""                    int64_t rank, int64_t overhead, int32_t dtype, GenJob &G, RepCalls &rc,
+                    EventSink *sink, JobTpls *jtpl) {
   HP(1);""")
 g=rep(g,"""    if (replay && bt.id >= 0 && sink->phase_replay(bt.id, B.next_alloc)) {""","""    auto tph = std::chrono::steady_clock::now();
     if (replay && bt.id >= 0 && sink->phase_replay(bt.id, B.next_alloc)) {""")
@@ -55,8 +55,8 @@ g=rep(g,"""  for (const Step &st : pipeline_order(schedule, p, m, v, stage)) {
 g=rep(g,"""  // gradient reduction and optimizer step (:757-777)""","""  auto tepi = std::chrono::steady_clock::now();
   struct EpiT { std::chrono::steady_clock::time_point t; ~EpiT(){ maya::hp_acc[15]+=std::chrono::duration<double>(std::chrono::steady_clock::now()-t).count(); } } epit{tepi};
   // gradient reduction and optimizer step (:757-777)""")
-g=rep(g,"""  const bool tpl_on = B.blocks;""","""  maya::hp_acc[12]+=std::chrono::duration<double>(std::chrono::steady_clock::now()-tpro).count();
-  const bool tpl_on = B.blocks;""")
+g=rep(g,"""  const bool tpl_on = B.blocks && jtpl;""","""  maya::hp_acc[12]+=std::chrono::duration<double>(std::chrono::steady_clock::now()-tpro).count();
+  const bool tpl_on = B.blocks && jtpl;""")
 open('/tmp/hprof/gen.cpp','w').write(g)
 p=open('/tmp/hprof/pack.cpp').read()
 p=rep(p,'#include "pack.h"','#include "pack.h"\n'+hdr+'namespace maya { double hp_acc[16]; }\n')
@@ -79,4 +79,4 @@ p=rep(p,"""  // walkers rank-major: a scheduler warp owns whole ranks""","""  ma
   // walkers rank-major: a scheduler warp owns whole ranks""")
 open('/tmp/hprof/pack.cpp','w').write(p)
 EOF
-g++ -O2 -std=c++17 -I/root/repo/include /root/repo/tools/hostprof/${HPP:-hpp}.cpp /tmp/hprof/gen.cpp /tmp/hprof/pack.cpp -lpthread -o /tmp/hpp && /tmp/hpp
+g++ -O2 -std=c++17 -I/root/repo/include /root/repo/tools/hostprof/${HPP:-hpp}.cpp /tmp/hprof/gen.cpp /tmp/hprof/pack.cpp -lpthread -o /tmp/hpp && /tmp/hpp $HPP_ARGS
