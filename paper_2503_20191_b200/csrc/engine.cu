@@ -91,9 +91,9 @@ struct maya_engine {
   // kernel warp jobs (by shared-memory region class), 11-14 lane kernel CTA
   // jobs (2/4/8/16 warps); each group runs on its own stream (fork/join)
   // 15: grid jobs (cooperative launch over their parts); 16..: chain kernel
-  // jobs by shared-memory region class (CHAIN_REGION), one-warp CTAs then
-  // two-warp CTAs
-  static const int NVAR = 16 + 2 * (int)CHAIN_CLASSES;
+  // jobs by shared-memory region class (CHAIN_REGION) and CTA size (1, 2, 4,
+  // 8 warps: CHAIN_CLASSES variants each)
+  static const int NVAR = 16 + 4 * (int)CHAIN_CLASSES;
   cudaStream_t vstream[NVAR] = {};
   cudaEvent_t vev[NVAR + 1] = {};
   uint32_t var_n[NVAR] = {};        // jobs per group (order segments)
@@ -130,6 +130,7 @@ struct maya_engine {
       s_blk_fids;
   Seg x_clen, x_ccounts, x_lctx, x_lst, x_gsync, x_macros;
   uint32_t chain_first = 0, chain_jobs = 0;   // chain jobs: the tail of the job order
+  uint32_t chain_maxw = 0;                    // their largest FIFO count
   std::vector<int32_t> job_kernel;            // per job: 0 warp-window, 1 lane, 2 grid, 3 chain
   cudaGraphExec_t graph_exec = nullptr;       // the run's device work, captured (maya_run)
   bool graph_fold = false;
@@ -262,8 +263,6 @@ bool plan_grid(const JobPack &P, LanePlan &pl) {
 // rank collective table -- one FIFO per thread (collectives rendezvous in
 // shared-memory rings when the job allows them, JOB_RING, else in global
 // slots).  n_slots carries the job's macro op count (the region's op area).
-static const uint64_t CHAIN_WAVE_BYTES = 148ull * 200 * 1024;   // ~one wave of chain CTAs
-
 LanePlan plan_chain(const JobPack &P) {
   LanePlan pl;
   const uint32_t W = (uint32_t)P.walkers.size(), R = (uint32_t)P.ranks.size();
@@ -278,8 +277,9 @@ LanePlan plan_chain(const JobPack &P) {
   if (L.bytes > CHAIN_REGION[CHAIN_CLASSES - 1]) return pl;
   uint32_t c = 0;
   while (CHAIN_REGION[c] < L.bytes) c++;
-  pl.threads = W <= 32 ? 32 : 64;
-  pl.variant = 16 + (int)c + (pl.threads == 64 ? (int)CHAIN_CLASSES : 0);
+  const int lw = W <= 32 ? 0 : W <= 64 ? 1 : W <= 128 ? 2 : 3;   // log2 warps
+  pl.threads = 32u << lw;
+  pl.variant = 16 + (int)c + lw * (int)CHAIN_CLASSES;
   pl.smem = L.bytes;
   pl.n_slots = (uint32_t)n_ops;
   pl.per_lane = 1;
@@ -648,23 +648,18 @@ int maya_upload(maya_engine *e) {
     if (const char *ev = getenv("MAYA_LANE_BUDGET")) budget = strtoull(ev, nullptr, 10);
     if (budget < LANE_REGION[0]) budget = LANE_REGION[0];
     if (budget > LANE_SMEM_CAP) budget = LANE_SMEM_CAP;
-    // chain kernel (whole job on chip, latency-optimised) when the batch's
-    // chain jobs fit the GPU in one wave: a batch of many large jobs (C5's
-    // thousands of per-rank-distinct traces) is throughput-bound and keeps
-    // the lane kernel's resident rings
+    // Jobs whose FIFOs suit lockstep lanes (many balanced FIFOs that block
+    // often: C5's per-rank-distinct traces) are throughput-bound and take the
+    // lane kernel's resident rings.  The others -- chains of hand-offs between
+    // few FIFOs (pipelines) -- take the chain kernel when the job fits one
+    // CTA's shared memory (latency-optimised: ~1 k cycles per hand-off against
+    // ~10 k for the warp-window kernel, which keeps the rest).
     const bool forced = (e->options & (MAYA_OPT_WARP_SCHED | MAYA_OPT_LANE_SCHED)) != 0;
-    if (!forced && !(e->options & MAYA_OPT_NO_CHAIN)) {
-      uint64_t total = 0;
-      for (size_t j = 0; j < nj; j++) {
-        plans[j] = plan_chain(e->packs[j]);
-        if (plans[j].variant >= 0) total += (plans[j].smem + 1023u) & ~1023u;
-      }
-      if (total > CHAIN_WAVE_BYTES)
-        for (size_t j = 0; j < nj; j++) plans[j] = LanePlan();
-    }
     for (size_t j = 0; j < nj; j++) {
-      if (plans[j].variant < 0 && !(e->options & MAYA_OPT_WARP_SCHED))
+      if (!(e->options & MAYA_OPT_WARP_SCHED))
         plans[j] = plan_lane(e->packs[j], (uint32_t)budget, (e->options & MAYA_OPT_LANE_SCHED) != 0);
+      if (plans[j].variant < 0 && !forced && !(e->options & MAYA_OPT_NO_CHAIN))
+        plans[j] = plan_chain(e->packs[j]);
       if (plans[j].variant >= 0 && plans[j].variant != 15)
         n_perm += (size_t)plans[j].per_lane * plans[j].threads;
       if (plans[j].variant >= 16) n_macros += plans[j].n_slots;
@@ -854,7 +849,12 @@ int maya_upload(maya_engine *e) {
       e->job_kernel[j] = var[j] >= 16 ? 3 : var[j] == 15 ? 2 : var[j] >= 3 ? 1 : 0;
     // chain jobs (variants 16..) close the order: their macro pass takes that tail
     e->chain_jobs = 0;
-    for (size_t j = 0; j < nj; j++) e->chain_jobs += var[j] >= 16 ? 1u : 0u;
+    e->chain_maxw = 0;
+    for (size_t j = 0; j < nj; j++)
+      if (var[j] >= 16) {
+        e->chain_jobs++;
+        e->chain_maxw = std::max(e->chain_maxw, (uint32_t)e->packs[j].walkers.size());
+      }
     e->chain_first = (uint32_t)(nj - e->chain_jobs);
   }
   // per-job bases (serial prefix), then parallel copy
@@ -1287,7 +1287,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
     launch_resolve(db, e->stream);
     CU(cudaGetLastError());
     if (fold && e->chain_jobs) {   // chain jobs: macro ops of their folded FIFOs
-      launch_chain_macros(db, db.order + e->chain_first, e->chain_jobs, e->stream);
+      launch_chain_macros(db, db.order + e->chain_first, e->chain_jobs, e->chain_maxw, e->stream);
       CU(cudaGetLastError());
     }
     CU(rec(e->ev[2]));
@@ -1325,7 +1325,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
           }
         } else if (v >= 16) {
           launch_schedule_chain(db, db.order + off, e->var_n[v],
-                                v >= 16 + (int)CHAIN_CLASSES ? 64u : 32u, record_timeline ? 1 : 0,
+                                32u << ((v - 16) / (int)CHAIN_CLASSES), record_timeline ? 1 : 0,
                                 e->var_smem[v], e->vstream[v]);
         } else if (v <= 10) {
           const uint32_t region = e->var_smem[v];

@@ -109,7 +109,8 @@ int launch_schedule_grid(const DevBatch &b, uint32_t p0, uint32_t p1, int record
                          cudaStream_t s);
 // chain jobs (sched_chain.cu): the macro ops of every FIFO of the n jobs
 // order[0..n) (folded runs), then one CTA per job, whole job on chip
-void launch_chain_macros(const DevBatch &b, const int32_t *order, uint32_t n, cudaStream_t s);
+void launch_chain_macros(const DevBatch &b, const int32_t *order, uint32_t n, uint32_t max_fifos,
+                         cudaStream_t s);
 void launch_schedule_chain(const DevBatch &b, const int32_t *order, uint32_t n, uint32_t threads,
                            int record, uint32_t smem, cudaStream_t s);
 int grid_max_ctas(uint32_t smem);   // co-resident CTAs of the grid kernel at this smem

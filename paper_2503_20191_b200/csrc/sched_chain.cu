@@ -556,13 +556,15 @@ __global__ void __launch_bounds__(NW * 32) sched_chain_kernel(DevBatch b, const 
 // iff it is a body after a WAIT or a REC after a WAIT or a body, so a macro
 // has at most 3 members -- hence chunks of 32 ops: lanes 0-29 lead macros
 // whose members all lie in the chunk, and the next chunk starts at the first
-// op no written macro covers.  Grid: CHAIN_MAX_FIFOS / 8 CTAs of 8 warps per
-// chain job, one warp per FIFO, so every FIFO of the batch is fused at once.
+// op no written macro covers.  Grid: `parts` CTAs of 8 warps per chain job
+// (enough for its largest FIFO count), one warp per FIFO, so every FIFO of the
+// batch is fused at once.
 static constexpr uint32_t MACRO_WARPS = 8;
 
 __global__ void __launch_bounds__(MACRO_WARPS * 32) chain_macro_kernel(DevBatch b,
-                                                                       const int32_t *order) {
-  constexpr uint32_t PARTS = CHAIN_MAX_FIFOS / MACRO_WARPS;
+                                                                       const int32_t *order,
+                                                                       uint32_t parts) {
+  const uint32_t PARTS = parts;
   const uint32_t j = (uint32_t)order[blockIdx.x / PARTS];
   const JobHdr &J = b.jobs[j];
   const uint32_t lane = threadIdx.x & 31u, W = J.n_walkers;
@@ -661,8 +663,10 @@ __global__ void __launch_bounds__(MACRO_WARPS * 32) chain_macro_kernel(DevBatch 
   }
 }
 
-void launch_chain_macros(const DevBatch &b, const int32_t *order, uint32_t n, cudaStream_t s) {
-  if (n) chain_macro_kernel<<<n * (CHAIN_MAX_FIFOS / MACRO_WARPS), MACRO_WARPS * 32, 0, s>>>(b, order);
+void launch_chain_macros(const DevBatch &b, const int32_t *order, uint32_t n, uint32_t max_fifos,
+                         cudaStream_t s) {
+  const uint32_t parts = (max_fifos + MACRO_WARPS - 1) / MACRO_WARPS;
+  if (n && parts) chain_macro_kernel<<<n * parts, MACRO_WARPS * 32, 0, s>>>(b, order, parts);
 }
 
 int chain_prof_read(unsigned long long *out8, int reset) {
@@ -687,24 +691,26 @@ void launch_schedule_chain(const DevBatch &b, const int32_t *order, uint32_t n, 
   static bool attr = false;
   if (!attr) {
     const int cap = (int)CHAIN_REGION[CHAIN_CLASSES - 1];
-    cudaFuncSetAttribute(sched_chain_kernel<1, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
-    cudaFuncSetAttribute(sched_chain_kernel<2, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
-    cudaFuncSetAttribute(sched_chain_kernel<1, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
-    cudaFuncSetAttribute(sched_chain_kernel<2, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
-    cudaFuncSetAttribute(sched_chain_kernel<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
-    cudaFuncSetAttribute(sched_chain_kernel<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+#define CHAIN_ATTR(NW)                                                                                  \
+  cudaFuncSetAttribute(sched_chain_kernel<NW, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap); \
+  cudaFuncSetAttribute(sched_chain_kernel<NW, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap); \
+  cudaFuncSetAttribute(sched_chain_kernel<NW, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    CHAIN_ATTR(1) CHAIN_ATTR(2) CHAIN_ATTR(4) CHAIN_ATTR(8)
+#undef CHAIN_ATTR
     attr = true;
   }
   const bool res = b.clen != nullptr;   // folded runs (never with a timeline)
-  if (threads <= 32) {
-    if (record) sched_chain_kernel<1, false, true><<<n, 32, smem, s>>>(b, order);
-    else if (res) sched_chain_kernel<1, true, false><<<n, 32, smem, s>>>(b, order);
-    else sched_chain_kernel<1, false, false><<<n, 32, smem, s>>>(b, order);
-  } else {
-    if (record) sched_chain_kernel<2, false, true><<<n, 64, smem, s>>>(b, order);
-    else if (res) sched_chain_kernel<2, true, false><<<n, 64, smem, s>>>(b, order);
-    else sched_chain_kernel<2, false, false><<<n, 64, smem, s>>>(b, order);
-  }
+#define CHAIN_LAUNCH(NW)                                                                     \
+  do {                                                                                       \
+    if (record) sched_chain_kernel<NW, false, true><<<n, NW * 32, smem, s>>>(b, order);      \
+    else if (res) sched_chain_kernel<NW, true, false><<<n, NW * 32, smem, s>>>(b, order);    \
+    else sched_chain_kernel<NW, false, false><<<n, NW * 32, smem, s>>>(b, order);            \
+  } while (0)
+  if (threads <= 32) CHAIN_LAUNCH(1);
+  else if (threads <= 64) CHAIN_LAUNCH(2);
+  else if (threads <= 128) CHAIN_LAUNCH(4);
+  else CHAIN_LAUNCH(8);
+#undef CHAIN_LAUNCH
 }
 
 }  // namespace maya

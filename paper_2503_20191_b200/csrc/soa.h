@@ -197,7 +197,7 @@ struct MacroFuse {
 // stream of every FIFO, record times, collective rings and the rank
 // collective table.  Per-walker word (lane_wslot): the FIFO's first op in the
 // region's op area.  Region classes by footprint.
-static const uint32_t CHAIN_MAX_FIFOS = 64;   // one FIFO per thread, 1 or 2 warps
+static const uint32_t CHAIN_MAX_FIFOS = 256;  // one FIFO per thread, 1, 2, 4 or 8 warps
 static const uint32_t CHAIN_CLASSES = 10;
 static const uint32_t CHAIN_REGION[CHAIN_CLASSES] = {8u << 10,  12u << 10, 16u << 10, 24u << 10,
                                                      32u << 10, 48u << 10, 64u << 10, 96u << 10,

@@ -6,7 +6,8 @@ macro ops ([WAIT]? [KERN|COLL]? [REC]?, built by chain_macro_kernel); with a
 timeline it evaluates one op per step.  The engine picks it per batch
 ('auto'); these tests check that it is really chosen where expected and that
 its results equal the reference's (golden fixtures from pkg/src/dltsim) on
-every golden family, folded and with a timeline, deadlocks included.
+every golden family, folded and with a timeline, deadlocks included, and on
+C4-shaped pipelines of up to 256 FIFOs (8 warps).
 """
 import json
 import os
@@ -73,7 +74,7 @@ def test_chain_deadlocks_folded(golden):
 
 
 def test_chain_runs_c2_and_matches_reference():
-    """All 512 C2 configs fit the chain kernel in one wave and give the
+    """All 512 C2 configs (pipelines: chain-shaped) run on the chain kernel and give the
     reference's results (c2_results.json made by the reference itself)."""
     from paper_2503_20191_b200 import workload as W
     from paper_2503_20191_b200.engine import Engine
@@ -102,30 +103,55 @@ def test_chain_runs_c2_and_matches_reference():
                 (g["total_ns"], g["peak_mem_bytes"], g["oom"]), sched
 
 
-def test_chain_declined_for_throughput_batches():
-    """A batch whose chain footprint exceeds one wave (many 8-rank x 10k-event
-    per-rank-distinct traces, C5-shaped) keeps the lane kernel's rings; the
-    CPU oracle agrees on the results."""
+def test_chain_declined_for_throughput_jobs():
+    """Jobs shaped for lockstep lanes (many balanced FIFOs that block often:
+    8-rank x 10k-event per-rank-distinct traces, C5) keep the lane kernel's
+    rings, in a large batch or alone; the CPU oracle agrees on the results."""
     from oracle import oracle
     from paper_2503_20191_b200.engine import Engine
     from paper_2503_20191_b200.synth import c5_job
     base = [c5_job(8, 10000, cfg=c) for c in range(4)]
-    jobs = [base[q % 4] for q in range(256)]
-    e = Engine(0, sched="auto")
-    try:
-        res = e.simulate(jobs)
-        kinds = e.kernels()
-    finally:
-        e.close()
-    assert "chain" not in kinds
-    for q in range(4):
-        o = oracle.simulate(base[q])
-        assert int(res[q]["total_ns"]) == o["total_ns"]
-        assert int(res[q]["peak_mem_bytes"]) == o["peak_mem_bytes"]
-    small = Engine(0, sched="auto")
-    try:
-        r2 = small.simulate(base[:2])
-        assert small.kernels() == ["chain", "chain"]
-    finally:
-        small.close()
-    assert np.array_equal(r2["total_ns"], res["total_ns"][:2])
+    for jobs in ([base[q % 4] for q in range(256)], base[:2]):
+        e = Engine(0, sched="auto")
+        try:
+            res = e.simulate(jobs)
+            kinds = e.kernels()
+        finally:
+            e.close()
+        assert set(kinds) == {"lane"}
+        for q in range(min(4, len(jobs))):
+            o = oracle.simulate(base[q])
+            assert int(res[q]["total_ns"]) == o["total_ns"]
+            assert int(res[q]["peak_mem_bytes"]) == o["peak_mem_bytes"]
+
+
+def test_chain_c4_pipelines_match_reference():
+    """C4 lattice configs (Llama-70B shape, 256-2,048 ranks, up to 16 stages x
+    10 virtual stages) pinned to the reference (scale_big_results.json /
+    scale_results.json, made by pkg/src/dltsim): the ones that fit run on the
+    chain kernel with 1-8 warps and give the reference's totals."""
+    import json
+    from paper_2503_20191_b200 import workload as W
+    from paper_2503_20191_b200.engine import Engine
+    rows = []
+    for name in ("scale_results.json", "scale_big_results.json"):
+        path = os.path.join(GOLDEN, name)
+        if os.path.exists(path):
+            rows += json.load(open(path))
+    used = 0
+    for r in rows:
+        m = W.ModelSpec(*r["model"])
+        cl = W.ClusterSpec(r["ranks"] // 8, 8, 80 * 2 ** 30, W.load_device_preset("fast"))
+        e = Engine(0, sched="auto")
+        try:
+            e.stage_generated(m, [W.ConfigPoint(*r["key"])], cl, dispatch_overhead_ns=5000, threads=4)
+            e.upload()
+            kind = e.kernels()[0]
+            e.run()
+            res = e.results()[0]
+        finally:
+            e.close()
+        used += kind == "chain"
+        assert int(res["total_ns"]) == r["total_ns"], (r["key"], kind)
+        assert int(res["peak_mem_bytes"]) == r["peak_mem_bytes"], (r["key"], kind)
+    assert used >= 10
