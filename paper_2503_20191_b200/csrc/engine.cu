@@ -117,6 +117,8 @@ struct maya_engine {
   size_t d_arena_cap = 0;
   size_t arena_bytes = 0;
   void *d_scratch = nullptr;
+  void *d_est = nullptr;    // DevTables copy + EstClass table (estimator)
+  size_t d_est_cap = 0;
   size_t d_scratch_cap = 0;
   size_t scratch_bytes = 0;
   bool uploaded = false, ran = false, recorded = false;
@@ -140,7 +142,7 @@ struct maya_engine {
   uint32_t grid_smem = 0;
   Seg x_blk_ab;
   bool has_blocks = false;             // staged jobs carry kernel blocks (must run folded)
-  Seg x_exec, x_rcw, x_feat_ns, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
+  Seg x_exec, x_rcw, x_feat_ns, x_feat_d32, x_wire, x_fire, x_delay, x_wstate, x_cslots, x_repout, x_tl_start, x_tl_end,
       x_results, x_err, x_topk, x_topk_out, x_topk_n;
   uint64_t n_tl = 0;
   std::vector<uint64_t> job_tl;      // per job timeline base
@@ -497,6 +499,7 @@ int maya_close(maya_engine *e) {
   if (e->h_arena) cudaFreeHost(e->h_arena);
   if (e->d_arena) cudaFree(e->d_arena);
   if (e->d_scratch) cudaFree(e->d_scratch);
+  if (e->d_est) cudaFree(e->d_est);
   if (e->d_stats) cudaFree(e->d_stats);
   if (e->h_topk) cudaFreeHost(e->h_topk);
   if (e->graph_exec) cudaGraphExecDestroy(e->graph_exec);
@@ -760,6 +763,7 @@ int maya_upload(maya_engine *e) {
   seg(e->x_ccounts, n_counts * sizeof(uint32_t));
   seg(e->x_rcw, n_rcolls * sizeof(RCX));
   seg(e->x_feat_ns, n_feats * 8);
+  seg(e->x_feat_d32, n_feats * 4);
   seg(e->x_blk_ab, n_blocks * 16);
   seg(e->x_wire, n_wfeats * 8);
   seg(e->x_fire, n_fire * 8);
@@ -1146,6 +1150,7 @@ int maya_upload(maya_engine *e) {
   db.exec = (ExecOp *)(X + e->x_exec.off);
   db.n_ops = n_ops;
   db.feat_ns = (int64_t *)(X + e->x_feat_ns.off);
+  db.feat_d32 = (uint32_t *)(X + e->x_feat_d32.off);
   db.wire = (int64_t *)(X + e->x_wire.off);
   db.fire = (int64_t *)(X + e->x_fire.off);
   db.delay = (int64_t *)(X + e->x_delay.off);
@@ -1192,6 +1197,47 @@ int maya_upload(maya_engine *e) {
     t.max_flops[q] = (t.eff_den[q] > 0 && (scale >> 64) == 0) ? UINT64_MAX / (uint64_t)scale : 0;
     t.max_peak[q] = t.eff_num[q] > 0 ? UINT64_MAX / (uint64_t)t.eff_num[q] : 0;
   }
+  {  // per (device, dtype, op kind) constants of the estimator's fast path
+    const int nd = std::min(t.n_devs, 8), no = std::max(t.n_op_kinds, 1);
+    std::vector<EstClass> cls((size_t)std::max(nd, 1) * MAYA_MAX_DTYPES * no);
+    auto magic_nb = [](uint64_t y) -> uint64_t {   // floor(2^64 / y), ~0 for y == 1
+      return y == 1 ? ~0ull : (uint64_t)(((unsigned __int128)1 << 64) / y);
+    };
+    for (int dv = 0; dv < nd; dv++)
+      for (int dt = 0; dt < MAYA_MAX_DTYPES; dt++)
+        for (int op = 0; op < t.n_op_kinds; op++) {
+          EstClass &c = cls[(size_t)(dv * MAYA_MAX_DTYPES + dt) * no + op];
+          c = EstClass{0, 0, 0, 0, 0, 0};
+          const int64_t peak = t.devs[dv].peak_flops[dt], num = t.eff_num[op], den = t.eff_den[op];
+          const unsigned __int128 K = (unsigned __int128)1000000000ull * (uint64_t)(den > 0 ? den : 0);
+          const unsigned __int128 D = (unsigned __int128)(uint64_t)(peak > 0 ? peak : 0) *
+                                      (uint64_t)(num > 0 ? num : 0);
+          if (peak > 0 && num > 0 && den > 0 && (K >> 64) == 0 && (D >> 64) == 0) {
+            c.K = (uint64_t)K;
+            c.D = (uint64_t)D;
+            c.MD = magic_nb(c.D);
+            c.maxf = UINT64_MAX / c.K;
+          }
+          const int64_t hbm = t.devs[dv].hbm_bytes_per_s;
+          if (hbm > 0) {
+            c.H = (uint64_t)hbm;
+            c.MH = magic_nb(c.H);
+          }
+        }
+    const size_t need = cls.size() * sizeof(EstClass) + sizeof(DevTables);
+    if (need > e->d_est_cap) {
+      if (e->d_est) cudaFree(e->d_est);
+      e->d_est = nullptr;
+      CU(cudaMalloc(&e->d_est, need));
+      e->d_est_cap = need;
+    }
+    char *E = (char *)e->d_est;
+    t.gtab = (const DevTables *)E;
+    t.cls = (const EstClass *)(E + sizeof(DevTables));
+    CU(cudaMemcpy(E, &t, sizeof(DevTables), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(E + sizeof(DevTables), cls.data(), cls.size() * sizeof(EstClass),
+                  cudaMemcpyHostToDevice));
+  }
   for (size_t j = 0; j < nj; j++) {
     const JobPack &P = e->packs[j];
     if (P.hdr.status == MAYA_ST_OK && (int)P.hdr.device >= t.n_devs && !P.feats.empty())
@@ -1234,6 +1280,7 @@ int maya_run(maya_engine *e, int32_t record_timeline) {
       db.exec = (ExecOp *)(X + e->x_exec.off);
       db.rcx = (RCX *)(X + e->x_rcw.off);
       db.feat_ns = (int64_t *)(X + e->x_feat_ns.off);
+      db.feat_d32 = (uint32_t *)(X + e->x_feat_d32.off);
       db.wire = (int64_t *)(X + e->x_wire.off);
       db.fire = (int64_t *)(X + e->x_fire.off);
       db.delay = (int64_t *)(X + e->x_delay.off);
@@ -1441,17 +1488,18 @@ int maya_results(maya_engine *e, maya_job_result *out) {
   cudaEventElapsedTime(&e->last_ms[0], e->ev[0], e->ev[1]);
   cudaEventElapsedTime(&e->last_ms[1], e->ev[1], e->ev[2]);
   cudaEventElapsedTime(&e->last_ms[2], e->ev[2], e->ev[3]);
-  if (err_flag) {
+  if (err_flag & 3) {
     // Estimation errors are raised by annotate() for ANY event, before the
     // simulation (estimate.py:344-347): attribute failed features to jobs.
-    std::vector<int64_t> fns(e->db.n_feats), wns(e->db.n_wfeats);
-    CU(cudaMemcpy(fns.data(), e->db.feat_ns, fns.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> fns(e->db.n_feats);
+    std::vector<int64_t> wns(e->db.n_wfeats);
+    CU(cudaMemcpy(fns.data(), e->db.feat_d32, fns.size() * 4, cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(wns.data(), e->db.wire, wns.size() * 8, cudaMemcpyDeviceToHost));
     size_t fb = 0, sb = 0;
     for (size_t j = 0; j < nj; j++) {
       const JobPack &P = e->packs[j];
       bool bad = false;
-      for (size_t f = 0; f < P.feats.size(); f++) bad |= fns[fb + f] < 0;
+      for (size_t f = 0; f < P.feats.size(); f++) bad |= fns[fb + f] == DUR32_FAIL;
       for (size_t s = 0; s < P.wfeats.size(); s++) bad |= wns[sb + s] < 0;
       // annotate() raises before simulate() runs (estimate.py:344-347): any
       // failed estimate of the job decides its status, whatever the schedule did

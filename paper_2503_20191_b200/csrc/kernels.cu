@@ -108,12 +108,29 @@ __device__ __forceinline__ uint64_t ceil_div_magic(uint64_t x, uint64_t y, uint6
   r -= c ? y : 0u;
   return q + (r != 0 ? 1u : 0u);
 }
+// The same with M = ~0 standing for y == 1 (EstClass): then q0 = x - 1 for x >= 1
+// (x * (2^64 - 1) / 2^64 = x - x / 2^64), still within one, so no branch.
+__device__ __forceinline__ uint64_t ceil_div_magic_nb(uint64_t x, uint64_t y, uint64_t M) {
+  uint64_t q = __umul64hi(x, M);
+  uint64_t r = x - q * y;
+  const bool c = r >= y;
+  q += c ? 1u : 0u;
+  r -= c ? y : 0u;
+  return q + (r != 0 ? 1u : 0u);
+}
 
 // ---------------------------------------------------------------------------
 // estimators
 
+// a feature's duration as written by estimate_features_kernel (-1: failed)
+__device__ __forceinline__ int64_t feat_dur(const DevBatch &b, uint32_t i) {
+  const uint32_t w = b.feat_d32[i];
+  if (w < DUR32_WIDE) return (int64_t)w;
+  return w == DUR32_FAIL ? -1 : b.feat_ns[i];
+}
+
 // one feature's roofline duration (-1 on EstimationError / overflow)
-__device__ __forceinline__ int64_t estimate_one(const DevTables &t, longlong2 fv, uint32_t meta) {
+__device__ __noinline__ int64_t estimate_one(const DevTables &t, longlong2 fv, uint32_t meta) {
   if (meta & FMETA_FIXED) return fv.x;
   struct { int64_t flops, bytes; int32_t op_kind, dtype, device; } f{
       fv.x, fv.y, fmeta_op(meta), fmeta_dtype(meta), fmeta_device(meta)};
@@ -160,6 +177,30 @@ __device__ __forceinline__ int64_t estimate_one(const DevTables &t, longlong2 fv
   return ok ? m + t.overhead_ns : -1;
 }
 
+// Straight-line fast path: one invariant division per term through the class
+// table (EstClass); every other case (bad ids, no rate, wide products) takes
+// the general routine above, so the results are the same.
+__device__ __forceinline__ int64_t estimate_fast(const DevTables &t, longlong2 fv, uint32_t meta) {
+  if (meta & FMETA_FIXED) return fv.x;
+  const int32_t op = fmeta_op(meta), dt = fmeta_dtype(meta), dv = fmeta_device(meta);
+  if (op < t.n_op_kinds && dt < MAYA_MAX_DTYPES && dv < t.n_devs) {
+    const EstClass *c = t.cls + ((size_t)(dv * MAYA_MAX_DTYPES + dt) * t.n_op_kinds + op);
+    const ulonglong2 kd = __ldg(reinterpret_cast<const ulonglong2 *>(c));
+    const ulonglong2 mm = __ldg(reinterpret_cast<const ulonglong2 *>(c) + 1);
+    const ulonglong2 hh = __ldg(reinterpret_cast<const ulonglong2 *>(c) + 2);
+    const bool fok = fv.x <= 0 || (kd.y != 0 && (uint64_t)fv.x <= mm.y);
+    const bool bok = fv.y <= 0 || (hh.x != 0 && (uint64_t)fv.y <= 18446744073ull);
+    if (fok && bok) {
+      const uint64_t comp = fv.x > 0 ? ceil_div_magic_nb((uint64_t)fv.x * kd.x, kd.y, mm.x) : 0;
+      const uint64_t mem = fv.y > 0 ? ceil_div_magic_nb((uint64_t)fv.y * 1000000000ull, hh.x, hh.y) : 0;
+      if (comp > (uint64_t)INT64_MAX || mem > (uint64_t)INT64_MAX) return -1;
+      const int64_t m = (int64_t)(comp > mem ? comp : mem);
+      return m > INT64_MAX - t.overhead_ns ? -1 : m + t.overhead_ns;
+    }
+  }
+  return estimate_one(*t.gtab, fv, meta);
+}
+
 // EST_PER features per thread, all loads issued before the arithmetic (memory-
 // level parallelism: the kernel streams 20 B in and 8 B out per feature)
 static constexpr uint32_t EST_PER = 4;
@@ -175,17 +216,26 @@ __global__ void __launch_bounds__(256) estimate_features_kernel(DevBatch b, DevT
       meta[k] = __ldg(b.feat_meta + i);
     }
   }
-  bool bad = false;
+  bool bad = false, wide = false;
 #pragma unroll
   for (uint32_t k = 0; k < EST_PER; k++) {
     const uint32_t i = base + k * 256;
     if (i < b.n_feats) {
-      const int64_t v = estimate_one(t, fv[k], meta[k]);
-      b.feat_ns[i] = v;
-      bad |= v < 0;
+      const int64_t v = estimate_fast(t, fv[k], meta[k]);
+      // 4 B per duration (DUR32_*): the fold / resolve passes read them back
+      uint32_t w = (uint32_t)v;
+      if (v < 0) {
+        w = DUR32_FAIL;
+        bad = true;
+      } else if (v >= (int64_t)DUR32_WIDE) {
+        w = DUR32_WIDE;
+        b.feat_ns[i] = v;
+        wide = true;
+      }
+      b.feat_d32[i] = w;
     }
   }
-  if (bad) atomicOr(b.err_flag, 1);
+  if (bad || wide) atomicOr(b.err_flag, (bad ? 1 : 0) | (wide ? ERR_WIDE_DUR : 0));
 }
 
 __global__ void estimate_wire_kernel(DevBatch b, DevTables t) {
@@ -271,7 +321,7 @@ __global__ void resolve_kernel(DevBatch b) {
   const uint32_t tag = op_tag(op.meta);
   uint64_t pay;
   if (tag == TAG_KERN) {
-    const int64_t d = b.feat_ns[op.arg];   // batch-global feature id
+    const int64_t d = feat_dur(b, op.arg);   // batch-global feature id
     pay = (d < 0 || d >= (int64_t)(EXEC_BAD >> 2)) ? (EXEC_BAD >> 2) : (uint64_t)d;
   } else {
     pay = (op.arg == NO_REC) ? (EXEC_NONE >> 2) : (uint64_t)op.arg;
@@ -1179,7 +1229,7 @@ __global__ void block_compose_kernel(DevBatch b) {
   int64_t A = 0, B = 0;
   bool any = false;
   for (uint32_t k = k0; k < k1; k++) {
-    const int64_t d = b.feat_ns[fp[k]];
+    const int64_t d = feat_dur(b, fp[k]);
     const int64_t de = (d < 0 || d > FOLD_SAT) ? FOLD_SAT : d;
     const int64_t bk = sat_add((int64_t)k * kb.gap, de);   // k * gap < 2^61 (packer)
     if (!any) {
@@ -1238,6 +1288,9 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
   const uint32_t n = sr.len;
   const uint32_t lo = fc.chunk * FOLD_CHUNK, hi = min(n, lo + FOLD_CHUNK);
   uint32_t outpos = fc.out;   // folded ops of the FIFO before this window (host-counted)
+  // no failed or wide duration in the batch (estimate_features_kernel's flags):
+  // every feature's duration is its 4-byte word
+  const bool plain = (*(volatile const int32_t *)b.err_flag & (1 | ERR_WIDE_DUR)) == 0;
   // carry from the previous window: last op's segment / foldability, open run
   uint32_t cseg = lo > 0 ? op_seg(in[lo - 1].meta) : 0;
   bool cfold = false;            // the chunk's first op always starts a run
@@ -1266,7 +1319,7 @@ __global__ void __launch_bounds__(128) fold_write_kernel(DevBatch b) {
           d[t] = ab.x;
           bx[t] = ab.y;
         } else {
-          d[t] = b.feat_ns[o[t].arg];
+          d[t] = plain ? (int64_t)b.feat_d32[o[t].arg] : feat_dur(b, o[t].arg);
         }
       }
     }

@@ -42,7 +42,8 @@ struct DevBatch {
   RCX *rcx;                   // entry + wire time of each rank-collective entry (resolve)
   ExecOp *exec;
   // scratch / outputs
-  int64_t *feat_ns;
+  uint32_t *feat_d32;          // per feature: duration (ns) when < DUR32_WIDE, else DUR32_*
+  int64_t *feat_ns;            // per feature: the duration when feat_d32 is DUR32_WIDE
   int64_t *wire;
   int64_t *fire;
   int64_t *delay;
@@ -71,7 +72,27 @@ struct DevBatch {
   uint64_t n_ops, n_rcolls;
 };
 
+// Roofline constants of one (device, dtype, op kind) class, for the straight-
+// line fast path of the estimator (kernels.cu estimate_fast):
+// compute = ceil(flops * K / D) with K = 1e9 * eff_den, D = peak * eff_num
+// (= the reference's ceil(ceil(flops * 1e9 * den / peak) / num)), exact while
+// flops <= maxf; memory = ceil(bytes * 1e9 / H).  D == 0 / H == 0: no fast path.
+// M* = floor(2^64 / y), ~0 for y == 1 (kernels.cu ceil_div_magic).
+struct EstClass {
+  uint64_t K, D, MD, maxf, H, MH;
+};
+
+// feature durations are stored in 4 B (the common case: below 4.29 s) with
+// two escapes: WIDE = read the 8 B value from feat_ns, FAIL = EstimationError
+static constexpr uint32_t DUR32_WIDE = 0xfffffffeu, DUR32_FAIL = 0xffffffffu;
+// err_flag bits: 1 = a feature estimate failed, 2 = a wire estimate failed,
+// ERR_WIDE_DUR = some feature duration needs its 8-byte escape (not an error)
+static constexpr int32_t ERR_WIDE_DUR = 4;
+
 struct DevTables {
+  const EstClass *cls;         // [device][MAYA_MAX_DTYPES][n_op_kinds]
+  const DevTables *gtab;       // this table's copy in device memory (the general
+                               // estimator reads it there: no per-thread param copy)
   maya_device_params devs[8];
   int64_t eff_num[64];
   int64_t eff_den[64];

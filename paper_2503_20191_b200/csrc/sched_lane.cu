@@ -62,6 +62,58 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+// Global-memory accesses other threads (or other CTAs of a grid job) race on:
+// relaxed at GPU scope (a generic volatile access would be system scope).
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const void *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int64_t ld_relaxed_s64(const void *p) {
+  int64_t v;
+  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Collective rendezvous slot (sim.py:326-343) on a shared-memory ring or a
+// global slot, with explicit address spaces: post = max(maxarr, ready) then
+// count += 1 (release), returning the new count; count / maxarr reads acquire.
+__device__ __forceinline__ uint32_t rdv_post(bool shared, CollSlot *cs, uint64_t ready) {
+  uint32_t old;
+  uint64_t mx;
+  if (shared) {
+    const uint32_t a = smem_u32(cs);
+    asm volatile("atom.shared.max.u64 %0, [%1], %2;" : "=l"(mx) : "r"(a), "l"(ready) : "memory");
+    asm volatile("fence.acq_rel.cta;" ::: "memory");
+    asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(a + 8u) : "memory");
+  } else {
+    asm volatile("atom.global.max.u64 %0, [%1], %2;" : "=l"(mx) : "l"(&cs->maxarr), "l"(ready) : "memory");
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&cs->count) : "memory");
+  }
+  (void)mx;
+  return old + 1;
+}
+__device__ __forceinline__ uint32_t rdv_count(bool shared, const CollSlot *cs) {
+  if (shared) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&cs->count)) : "memory");
+    return v;
+  }
+  return ld_relaxed_u32(&cs->count);
+}
+__device__ __forceinline__ int64_t rdv_max(bool shared, const CollSlot *cs) {
+  int64_t v;
+  if (shared) {
+    asm volatile("fence.acq_rel.cta;" ::: "memory");
+    asm volatile("ld.volatile.shared.s64 %0, [%1];" : "=l"(v) : "r"(smem_u32(&cs->maxarr)) : "memory");
+  } else {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    v = ld_relaxed_s64(&cs->maxarr);
+  }
+  return v;
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t *bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -190,7 +242,7 @@ __device__ __forceinline__ void fire_store(const LaneSh &sh, uint32_t idx, int64
     asm volatile("st.volatile.shared.s64 [%0], %1;" ::"r"(smem_u32(sh.fire + idx)), "l"(v)
                  : "memory");
   } else {
-    asm volatile("st.volatile.global.s64 [%0], %1;" ::"l"(sh.fire + idx), "l"(v) : "memory");
+    asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(sh.fire + idx), "l"(v) : "memory");
     asm volatile("st.volatile.shared.v2.s64 [%0], {%1, %2};" ::"r"(
                      smem_u32(sh.fcache + (idx & sh.fmask))),
                  "l"(v), "l"((int64_t)idx)
@@ -208,7 +260,7 @@ __device__ __forceinline__ int64_t fire_load(const LaneSh &sh, uint32_t idx, boo
                : "r"(smem_u32(sh.fcache + (idx & sh.fmask)))
                : "memory");
   if (t == (int64_t)idx) return v;
-  return full ? ld_vol_global_s64(sh.fire + idx) : -1;
+  return full ? ld_relaxed_s64(sh.fire + idx) : -1;
 }
 
 __device__ __forceinline__ RCX ld_rcx(const RCX *p, bool smem) {
@@ -248,7 +300,7 @@ __device__ __forceinline__ int lane_step(const DevBatch &b, const LaneSh &sh, co
     if (fire_load(sh, s.wtgt, full) < 0) return ADV_IDLE;
     s.flags &= ~ST_WFIRE;
   } else if (s.flags & ST_WCOUNT) {
-    const uint32_t cnt = __isShared(s.waddr) ? (uint32_t)ld_vol_shared_u32(s.waddr) : vld(s.waddr);
+    const uint32_t cnt = __isShared(s.waddr) ? (uint32_t)ld_vol_shared_u32(s.waddr) : ld_relaxed_u32(s.waddr);
     if (cnt < s.wtgt) return ADV_IDLE;
     s.flags &= ~ST_WCOUNT;
   }
@@ -344,7 +396,8 @@ __device__ __forceinline__ int lane_step(const DevBatch &b, const LaneSh &sh, co
     } else {
       CollSlot *cs;
       uint32_t target;
-      if (sh.ring && (!sh.comm_part || sh.comm_part[g] == sh.part)) {   // on-chip rendezvous
+      const bool on_chip = sh.ring && (!sh.comm_part || sh.comm_part[g] == sh.part);
+      if (on_chip) {   // on-chip rendezvous
         cs = sh.ring + 2 * g + (idx & 1u);
         target = ((idx >> 1) + 1u) * nr;
       } else {
@@ -352,25 +405,22 @@ __device__ __forceinline__ int lane_step(const DevBatch &b, const LaneSh &sh, co
         target = nr;
       }
       if (!(s.flags & ST_POSTED)) {
-        atomicMax(&cs->maxarr, (unsigned long long)ready);
-        __threadfence_block();
-        const uint32_t old = atomicAdd(&cs->count, 1u);
+        const uint32_t cnt = rdv_post(on_chip, cs, (uint64_t)ready);
         s.flags |= ST_POSTED;
-        if (old + 1 > target) { err = MAYA_ST_INTERNAL; return ADV_IDLE; }
-        if (old + 1 < target) {                     // posted; completes in a later step
+        if (cnt > target) { err = MAYA_ST_INTERNAL; return ADV_IDLE; }
+        if (cnt < target) {                         // posted; completes in a later step
           s.flags |= ST_WCOUNT;
           s.wtgt = target;
           s.waddr = &cs->count;
           return ADV_PROG;
         }
-      } else if (vld(&cs->count) < target) {
+      } else if (rdv_count(on_chip, cs) < target) {
         s.flags |= ST_WCOUNT;
         s.wtgt = target;
         s.waddr = &cs->count;
         return ADV_IDLE;
       }
-      __threadfence_block();
-      const int64_t m = (int64_t)vld(&cs->maxarr);
+      const int64_t m = rdv_max(on_chip, cs);
       if (w8 > INT64_MAX - m) { err = MAYA_ST_OVERFLOW; return ADV_IDLE; }
       done = m + w8;
       s.flags &= ~ST_POSTED;
@@ -994,7 +1044,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1)
         if (err) atomicMax(&s_err, err);
         __syncwarp();
       }
-      if (vld(&gs->err) != 0) {
+      if ((int)ld_relaxed_u32(&gs->err) != 0) {
         if (!idle && lane == 0) atomicSub(&gs->active, 1);
         break;
       }
@@ -1013,7 +1063,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1)
         idle = true;
       }
       __syncwarp();
-      if (vld(&gs->active) <= 0) break;         // every warp of the job is idle
+      if ((int)ld_relaxed_u32(&gs->active) <= 0) break;   // every warp of the job is idle
       if (spin > 16) __nanosleep(128);
     }
     fifos_end_round(sh, tid, f);

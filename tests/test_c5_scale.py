@@ -39,3 +39,29 @@ def test_c5_schedulers_agree_and_match_oracle(shape):
     o = oracle.simulate_many(jobs, threads=8)
     for f in ("status", "total_ns", "peak_mem_bytes", "oom"):
         assert np.array_equal(base[f], o[f]), (shape, f)
+
+
+def test_wide_durations_match_oracle():
+    """Feature durations of 2^32 ns and more take the 8-byte escape of the
+    estimator's 4-byte duration words (kernels.cu feat_dur, DUR32_WIDE): jobs
+    whose kernels run for seconds, batched with ordinary ones, folded and not,
+    equal the CPU restatement."""
+    import dataclasses
+    from paper_2503_20191_b200.rawtrace import EV_KERNEL
+    from paper_2503_20191_b200.synth import c5_job
+    from oracle import oracle
+    jobs = []
+    for c in range(4):
+        j = c5_job(8, 1000, cfg=c)
+        if c < 2:   # flops x 2^23: kernel times from ~0 to ~10 s, both sides of 2^32 ns
+            f = j.ev_f.copy()
+            k = j.ev_kind == EV_KERNEL
+            f[k, 2] <<= 23
+            j = dataclasses.replace(j, ev_f=f)
+        jobs.append(j)
+    o = oracle.simulate_many(jobs, threads=4)
+    assert int(o["total_ns"][0]) > 2 ** 33
+    for kw in (dict(), dict(fold=False), dict(sched="warp")):
+        r = _results(jobs, **kw)
+        for fld in ("status", "total_ns", "peak_mem_bytes", "oom"):
+            assert np.array_equal(np.asarray(r[fld]), np.asarray(o[fld])), (kw, fld)

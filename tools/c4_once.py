@@ -15,3 +15,5 @@ eng.upload()
 for _ in range(runs):
     eng.run(); eng.results()
 print(len(cfgs), eng.last_timings_ms())
+import collections
+print("kernels", collections.Counter(eng.kernels()))
