@@ -384,7 +384,7 @@ LanePlan plan_lane(const JobPack &P, uint32_t budget, bool force) {
       const LaneLayout L =
           lane_layout(W, R, nc, fl, (uint32_t)slots, P.hdr.n_fire, P.hdr.n_rcolls, fc);
       if (L.bytes > cap) continue;
-      pl.flags = fl | (getenv("MAYA_LANE_CHASE") ? LANE_CHASE : 0u);
+      pl.flags = fl;
       pl.n_slots = (uint32_t)slots;
       pl.smem = L.bytes;
       pl.lgd_max = t.lgd;

@@ -208,7 +208,6 @@ struct LaneSh {
   uint32_t part;
   int record;
   bool fire_sm, rcx_sm;       // fire / rcx tables in shared memory
-  bool chase;                 // LANE_CHASE: run each FIFO until it blocks, every step
 };
 
 // ---- typed accesses --------------------------------------------------------
@@ -532,7 +531,6 @@ __device__ void lane_setup(const DevBatch &b, uint32_t j, uint8_t *base, uint32_
   sh.fcache = (FireEnt *)(base + L.fcache);
   sh.fmask = LJ.fc_log2 ? (1u << LJ.fc_log2) - 1u : 0u;
   sh.rcx_sm = (LJ.flags & LANE_RCX_SMEM) != 0;
-  sh.chase = (LJ.flags & LANE_CHASE) != 0;
   sh.rcx = sh.rcx_sm ? (const RCX *)(base + L.rcx) : b.rcx + J.rcolls;
   sh.delay = b.delay + J.delay;
   sh.perm = b.lane_perm + LJ.perm;
@@ -650,11 +648,6 @@ __device__ __forceinline__ void fifos_step(const DevBatch &b, const LaneSh &sh, 
       int a = ADV_IDLE;
       if (f.valid) {
         a = lane_step(b, sh, f.c, f.s, tmax, err, full && m == 0, sh.rcx_sm ? nullptr : &f.pf);
-        if (sh.chase)
-          for (int q = 0; q < 64 && a == ADV_PROG && !err; q++) {
-            const int a2 = lane_step(b, sh, f.c, f.s, tmax, err, false, sh.rcx_sm ? nullptr : &f.pf);
-            if (a2 != ADV_PROG) break;
-          }
       }
       prog |= a == ADV_PROG;
       data |= a == ADV_DATA;
@@ -669,9 +662,6 @@ __device__ __forceinline__ void fifos_step(const DevBatch &b, const LaneSh &sh, 
     if (s.i >= s.lim) continue;
     const LCtx c = sh.ctx[w];
     int a = lane_step(b, sh, c, s, tmax, err, full, nullptr);
-    if (sh.chase)
-      for (int q = 0; q < 64 && a == ADV_PROG && !err; q++)
-        if (lane_step(b, sh, c, s, tmax, err, false, nullptr) != ADV_PROG) break;
     if (a != ADV_IDLE || err || (s.flags & (ST_WFIRE | ST_WCOUNT))) sh.st[w] = s;
     prog |= a == ADV_PROG;
     data |= a == ADV_DATA;

@@ -120,7 +120,6 @@ enum LaneFlags : uint32_t {
   LANE_RCX_SMEM = 4,    // per-rank collective table in shared memory
   LANE_CTX_SMEM = 8,    // FIFO contexts in shared memory (lanes own several FIFOs)
   LANE_ST_GLOBAL = 16,  // FIFO states in global memory (jobs with thousands of FIFOs)
-  LANE_CHASE = 32,      // a lane retires every ready op of its FIFO per step (latency-bound jobs)
 };
 struct LaneJob {
   uint64_t mbase;       // chain jobs: batch index of the job's first macro op (DevBatch.macros)
