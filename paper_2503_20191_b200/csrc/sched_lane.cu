@@ -290,6 +290,9 @@ struct RcxPf {                // next collective-table entry of a FIFO, prefetch
   uint32_t key;               // job-local table index of rx (0xFFFFFFFF: none)
 };
 
+// FAST: folded runs and no timeline (the kernel prelude and the timeline
+// stores are compiled out); else both are decided at run time.
+template <bool FAST = false>
 __device__ __forceinline__ int lane_step(const DevBatch &b, const LaneSh &sh, const LCtx &c,
                                          LSt &s, int64_t &tmax, int &err, bool full,
                                          RcxPf *pf) {
@@ -310,7 +313,7 @@ __device__ __forceinline__ int lane_step(const DevBatch &b, const LaneSh &sh, co
   }
   longlong2 v;
   const bool ring = c.lgd != 0xffu;
-  if (ring && (s.i & SMASK) != 0 && !sh.record && !b.clen) {   // folded runs: no prelude
+  if (!FAST && ring && (s.i & SMASK) != 0 && !sh.record && !b.clen) {   // folded runs: no prelude
     // kernel prelude: up to 3 kernel ops of the staged chunk, operands < 2^61
     // (no sum can leave int64), before the one general op below
     constexpr int64_t LIM = (int64_t)1 << 61;
@@ -431,7 +434,7 @@ __device__ __forceinline__ int lane_step(const DevBatch &b, const LaneSh &sh, co
       pf->key = key + 1;
     }
   }
-  if (sh.record) {
+  if (!FAST && sh.record) {
     b.tl_start[c.tl + s.i] = ready;
     b.tl_end[c.tl + s.i] = done;
   }
@@ -635,6 +638,7 @@ __device__ __forceinline__ void fifos_end_round(const LaneSh &sh, uint32_t tid, 
   if (f.one && f.valid) sh.st[sh.w0 + tid] = f.s;
 }
 
+template <bool FAST = false>
 __device__ __forceinline__ void fifos_step(const DevBatch &b, const LaneSh &sh, uint32_t tid,
                                            uint32_t nt, LaneFifos &f, int64_t &tmax, int &err,
                                            bool &prog, bool &data, bool full) {
@@ -647,7 +651,7 @@ __device__ __forceinline__ void fifos_step(const DevBatch &b, const LaneSh &sh, 
     for (int m = 0; m < LANE_SUBSTEPS; m++) {
       int a = ADV_IDLE;
       if (f.valid) {
-        a = lane_step(b, sh, f.c, f.s, tmax, err, full && m == 0, sh.rcx_sm ? nullptr : &f.pf);
+        a = lane_step<FAST>(b, sh, f.c, f.s, tmax, err, full && m == 0, sh.rcx_sm ? nullptr : &f.pf);
       }
       prog |= a == ADV_PROG;
       data |= a == ADV_DATA;
@@ -661,7 +665,7 @@ __device__ __forceinline__ void fifos_step(const DevBatch &b, const LaneSh &sh, 
     LSt s = sh.st[w];
     if (s.i >= s.lim) continue;
     const LCtx c = sh.ctx[w];
-    int a = lane_step(b, sh, c, s, tmax, err, full, nullptr);
+    int a = lane_step<FAST>(b, sh, c, s, tmax, err, full, nullptr);
     if (a != ADV_IDLE || err || (s.flags & (ST_WFIRE | ST_WCOUNT))) sh.st[w] = s;
     prog |= a == ADV_PROG;
     data |= a == ADV_DATA;
@@ -761,6 +765,7 @@ __device__ __forceinline__ void fifos_init(const LaneSh &sh, uint32_t tid, LaneF
 #ifndef LANE_WARP_MINB
 #define LANE_WARP_MINB 2
 #endif
+template <bool FAST>
 __global__ void __launch_bounds__(256, LANE_WARP_MINB) sched_lane_warp_kernel(DevBatch b, const int32_t *order,
                                                               uint32_t n_jobs, uint32_t region,
                                                               int record) {
@@ -800,7 +805,7 @@ __global__ void __launch_bounds__(256, LANE_WARP_MINB) sched_lane_warp_kernel(De
 #ifdef MAYA_PROFILE
       const long long t0 = clock64();
 #endif
-      fifos_step(b, sh, lane, 32, f, tmax, err, prog, data, full);
+      fifos_step<FAST>(b, sh, lane, 32, f, tmax, err, prog, data, full);
       __syncwarp();
       const bool ap = __any_sync(FULL, prog), ad = __any_sync(FULL, data);
 #ifdef MAYA_PROFILE
@@ -1140,13 +1145,19 @@ void launch_schedule_lane_warp(const DevBatch &b, const int32_t *order, uint32_t
   if (!n) return;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(sched_lane_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sched_lane_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)LANE_SMEM_CAP);
+    cudaFuncSetAttribute(sched_lane_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)LANE_SMEM_CAP);
     attr = true;
   }
   const uint32_t grid = (n + warps_per_cta - 1) / warps_per_cta;
-  sched_lane_warp_kernel<<<grid, warps_per_cta * 32, warps_per_cta * region, s>>>(b, order, n,
-                                                                                  region, record);
+  if (b.clen && !record)   // folded runs, no timeline
+    sched_lane_warp_kernel<true><<<grid, warps_per_cta * 32, warps_per_cta * region, s>>>(
+        b, order, n, region, 0);
+  else
+    sched_lane_warp_kernel<false><<<grid, warps_per_cta * 32, warps_per_cta * region, s>>>(
+        b, order, n, region, record);
 }
 
 void launch_schedule_lane(const DevBatch &b, const int32_t *order, uint32_t n, uint32_t threads,
