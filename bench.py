@@ -55,7 +55,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=5.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 lattice sub-line")
-    ap.add_argument("--c5", default="8x10000x4096",
+    # 4,736 configs = 2 full waves of the lane scheduler (148 SMs x 2 CTAs x 8
+    # one-warp jobs): a batch that is a whole number of waves leaves no tail
+    ap.add_argument("--c5", default="8x10000x4736",
                     help="C5 synthetic sweep point RANKSxOPSxCONFIGS for the HBM-roofline line "
                          "('' to skip)")
     return ap.parse_args()
@@ -353,7 +355,9 @@ def c5_sweep(spec: str, steps: int, dev_index: int) -> dict:
     del flush
     traffic = c5_ncu_traffic(R, n, B)
     return {"workload": f"C5 synthetic: {R} ranks x {n} events/rank, {B} configs per batch "
-                        f"({distinct} distinct seeds tiled; every config has its own arena copy)",
+                        f"({distinct} distinct seeds tiled; every config has its own arena copy; "
+                        f"the default batch is 2 full waves of the lane scheduler: "
+                        f"148 SMs x 16 resident one-warp jobs x 2)",
             "configs_per_s": round(B / (step_ms / 1000), 1),
             "rank_ops_per_s": round(st["rank_ops"] / (step_ms / 1000), 1),
             "class_ops_per_s": round(st["class_ops"] / (step_ms / 1000), 1),
