@@ -95,3 +95,64 @@ def test_collective_estimator_matches_reference():
            if STATUS_NAMES[int(r["status"])] != "ok" or int(r["total_ns"]) != c["expected"]]
     eng.close()
     assert not bad, bad[:5]
+
+
+def _roofline_exact(flops, nbytes, peak, eff, hbm, overhead):
+    """estimate.py:120-134 in exact integers: max(ceil(flops*1e9/(peak*eff)),
+    ceil(bytes*1e9/hbm)) + overhead, eff as Fraction(str(eff))."""
+    from fractions import Fraction
+    fr = Fraction(str(eff))
+    cdiv = lambda a, b: -(-a // b)
+    comp = cdiv(flops * 10 ** 9 * fr.denominator, peak * fr.numerator) if flops > 0 else 0
+    mem = cdiv(nbytes * 10 ** 9, hbm) if nbytes > 0 else 0
+    return max(comp, mem) + overhead
+
+
+def test_kernel_estimator_fast_path_boundaries():
+    """The estimator's straight-line path (kernels.cu estimate_fast: one
+    invariant division per term through EstClass) hands every case it cannot
+    do exactly to the general u128 routine: flops at and past floor(2^64 / K),
+    bytes at and past 2^64 / 1e9, K = 1e9 * den or D = peak * num past 2^64,
+    divisors of 1 (the ~0 magic), zero terms.  Each result equals the
+    reference formula in exact integer arithmetic."""
+    from paper_2503_20191_b200.engine import Engine
+    U64 = 2 ** 64 - 1
+    out = []
+    for peak, hbm, eff in [(10 ** 15, 8 * 10 ** 12, 0.7), (1, 1, 1.0), (3, 7, 0.5),
+                           (2_250_000_000_000_000, 7_700_000_000_000, 0.123456789),
+                           (10 ** 15, 10 ** 12, 0.1234567891234), (999_999_999_989, 3, 0.75)]:
+        from fractions import Fraction
+        fr = Fraction(str(eff))
+        K = 10 ** 9 * fr.denominator
+        maxf = U64 // K
+        flops_cases = {0, 1, 12345, maxf - 1, maxf, maxf + 1, 2 * maxf + 3, 10 ** 12}
+        bytes_cases = {0, 1, 18446744073, 18446744074, 10 ** 11}
+        for fl in sorted(flops_cases):
+            for by in sorted(bytes_cases):
+                if fl < 0 or fl >= 2 ** 63 or by >= 2 ** 63:
+                    continue
+                exp = _roofline_exact(fl, by, peak, eff, hbm, 500)
+                if exp >= 2 ** 62 - 1:   # the schedulers' documented range (DESIGN.md: a
+                    continue             # duration >= 2^62 ns reports OVERFLOW)
+                out.append({"device": {"name": "d", "peak_flops": {"bf16": peak}, "hbm": hbm,
+                                       "intra": [0, 10 ** 9], "inter": [0, 10 ** 9]},
+                            "op": "gemm", "dtype": "bf16", "flops": fl, "bytes": by,
+                            "overhead": 500, "efficiency": {"gemm": eff}, "expected": exp})
+    assert len(out) > 100
+    groups = defaultdict(list)
+    for c in out:
+        groups[(json.dumps(c["device"], sort_keys=True), json.dumps(c["efficiency"]))].append(c)
+    eng = Engine(0)
+    bad = []
+    try:
+        for (_, eff), cs in groups.items():
+            res = eng.simulate([kernel_job(c) for c in cs], efficiency=json.loads(eff),
+                               overhead_ns=500)
+            for c, r in zip(cs, res):
+                st = STATUS_NAMES[int(r["status"])]
+                if st != "ok" or int(r["total_ns"]) != c["expected"]:
+                    bad.append((c["flops"], c["bytes"], c["device"]["peak_flops"], st,
+                                int(r["total_ns"]), c["expected"]))
+    finally:
+        eng.close()
+    assert not bad, bad[:5]
