@@ -184,7 +184,8 @@ __device__ __forceinline__ int64_t estimate_fast(const DevTables &t, longlong2 f
   if (meta & FMETA_FIXED) return fv.x;
   const int32_t op = fmeta_op(meta), dt = fmeta_dtype(meta), dv = fmeta_device(meta);
   if (op < t.n_op_kinds && dt < MAYA_MAX_DTYPES && dv < t.n_devs) {
-    const EstClass *c = t.cls + ((size_t)(dv * MAYA_MAX_DTYPES + dt) * t.n_op_kinds + op);
+    // < 8 x 16 x 4096 entries: 32-bit index arithmetic
+    const EstClass *c = t.cls + (uint32_t)((dv * MAYA_MAX_DTYPES + dt) * t.n_op_kinds + op);
     const ulonglong2 kd = __ldg(reinterpret_cast<const ulonglong2 *>(c));
     const ulonglong2 mm = __ldg(reinterpret_cast<const ulonglong2 *>(c) + 1);
     const ulonglong2 hh = __ldg(reinterpret_cast<const ulonglong2 *>(c) + 2);
