@@ -497,7 +497,9 @@ struct BTpl {
   int id = -2;                                   // -2: not captured, -1: not replayable
   int tries = 0;                                 // captures attempted (the first occurrence
                                                  // of a phase often opens communicators)
-  std::vector<std::pair<int, std::pair<int8_t, int64_t>>> calls;   // (lc, (kind, bytes)), by lc
+  // the calls a replay appends: runs (lc, [begin, end) of call_data), by lc
+  std::vector<std::pair<int, std::pair<uint32_t, uint32_t>>> call_runs;
+  std::vector<std::pair<int8_t, int64_t>> call_data;     // (kind, bytes)
   std::vector<std::pair<int64_t, int64_t>> vers; // (event id, records)
   int64_t allocs = 0;
 };
@@ -734,12 +736,11 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
     if (replay && bt.id >= 0 && sink->phase_replay(bt.id, B.next_alloc)) {
       act(st.chunk, st.mb) = st.phase == FWD ? B.next_alloc : -1;   // its one allocation
       B.next_alloc += bt.allocs;
-      for (size_t q = 0; q < bt.calls.size();) {   // runs of one communicator
-        const int lc = bt.calls[q].first;
-        size_t e = q;
-        while (e < bt.calls.size() && bt.calls[e].first == lc) B.calls[lc].push_back(bt.calls[e++].second);
-        B.call_idx[lc] += (int64_t)(e - q);
-        q = e;
+      for (const auto &run : bt.call_runs) {   // one range append per communicator
+        auto &dst = B.calls[run.first];
+        dst.insert(dst.end(), bt.call_data.begin() + run.second.first,
+                   bt.call_data.begin() + run.second.second);
+        B.call_idx[run.first] += (int64_t)(run.second.second - run.second.first);
       }
       for (const auto &e : bt.vers) {
         B.next_version[e.first] += e.second;
@@ -760,16 +761,20 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
     B.flush();
     if (capture) {
       bt.tries++;
-      bt.calls.clear();
+      bt.call_runs.clear();
+      bt.call_data.clear();
       bt.vers.clear();
       bt.id = sink->phase_end();
       bt.allocs = B.next_alloc - aid0;
       if (st.phase == FWD && bt.allocs != 1) bt.id = -1;   // replay assumes one activation alloc
       // call lists in issue order across communicators are not needed: each
       // communicator's list is appended in its own order
-      for (size_t lc = 0; lc < B.calls.size(); lc++)
-        for (size_t q = calls0[lc]; q < B.calls[lc].size(); q++)
-          bt.calls.push_back({(int)lc, B.calls[lc][q]});
+      for (size_t lc = 0; lc < B.calls.size(); lc++) {
+        if (B.calls[lc].size() <= calls0[lc]) continue;
+        const uint32_t b0 = (uint32_t)bt.call_data.size();
+        bt.call_data.insert(bt.call_data.end(), B.calls[lc].begin() + calls0[lc], B.calls[lc].end());
+        bt.call_runs.push_back({(int)lc, {b0, (uint32_t)bt.call_data.size()}});
+      }
       for (size_t e = 0; e < B.next_version.size(); e++) {
         const int64_t before = e < vers0.size() ? vers0[e] : 0;
         if (B.next_version[e] != before) bt.vers.push_back({(int64_t)e, B.next_version[e] - before});
