@@ -175,14 +175,17 @@ enum { ADV_IDLE = 0, ADV_PROG = 1, ADV_DATA = 2 };
 #ifndef LANE_SUBSTEPS
 #define LANE_SUBSTEPS 1
 #endif
-// warp jobs on folded runs and CTA jobs: lockstep sub-steps per vote.  A job's steps are
-// dependency-bound (~9 of 32 lanes retire an op per step on C5), so several
-// sub-steps between the warp votes let hand-offs inside the warp resolve
-// without paying the votes and the round bookkeeping each time (C5 8 x 10 k:
-// 2.26 -> 2.20 ms; CTA jobs, 64 x 10 k: 2.23 -> 1.98 ms).  Grid jobs keep one
-// (512 x 2 k: 0.29 -> 0.31 ms with 4 or more)
+// Lockstep sub-steps per warp vote.  A job's steps are dependency-bound (~9
+// of 32 lanes retire an op per step on C5), so several sub-steps between the
+// votes let hand-offs inside the warp resolve without paying the votes and
+// the round bookkeeping each time.  Warp jobs on folded runs and CTA jobs: 8
+// (C5 8 x 10 k: 2.26 -> 2.20 ms; CTA jobs, 64 x 10 k: 2.23 -> 1.98 ms); grid
+// jobs: 3 (512 x 10 k: 1.35 -> 1.23 ms, 2,048 x 1 k: 0.17 -> 0.155 ms).
 #ifndef LANE_WARP_SUBSTEPS
 #define LANE_WARP_SUBSTEPS 8
+#endif
+#ifndef LANE_GRID_SUBSTEPS
+#define LANE_GRID_SUBSTEPS 3
 #endif
 
 #ifdef MAYA_PROFILE
@@ -1044,7 +1047,8 @@ __global__ void __launch_bounds__(GRID_THREADS, 1)
     bool idle = false;
     for (uint32_t spin = 0;; spin++) {
       bool prog = false, data = false;
-      fifos_step(b, sh, tid, nt, f, tmax, err, prog, data, spin == 0 && !idle);
+      fifos_step<false, LANE_GRID_SUBSTEPS>(b, sh, tid, nt, f, tmax, err, prog, data,
+                                            spin == 0 && !idle);
       if (__any_sync(FULL, err != 0)) {
         if (err && lane == 0) atomicMax(&gs->err, err);
         if (err) atomicMax(&s_err, err);
