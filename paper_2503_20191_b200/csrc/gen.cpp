@@ -507,6 +507,25 @@ typedef std::array<int64_t, 20> TplKey;
 typedef std::map<TplKey, BTpl> JobTpls;        // per job, shared by its reps
 
 // workload.py:571-780 for one representative rank; appends events.
+// A few dozen keyed entries per trace (communicator roles, p2p streams,
+// event ids): a flat vector searched linearly, no node allocation per entry.
+template <class K, class V>
+struct FlatMap {
+  std::vector<std::pair<K, V>> v;
+  const V *get(const K &k) const {
+    for (const auto &e : v)
+      if (e.first == k) return &e.second;
+    return nullptr;
+  }
+  std::pair<V *, bool> emplace(const K &k, const V &val) {
+    for (auto &e : v)
+      if (e.first == k) return {&e.second, false};
+    v.emplace_back(k, val);
+    return {&v.back().second, true};
+  }
+  V &operator[](const K &k) { return *emplace(k, V{}).first; }
+};
+
 void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int schedule,
                     int64_t rank, int64_t overhead, int32_t dtype, GenJob &G, RepCalls &rc,
                     EventSink *sink, JobTpls *jtpl) {
@@ -536,7 +555,7 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   worker_comms(C, v, rank, roles);
   // local comm index of each role (first CommInit of a comm id); keyed by the
   // role's integer fields, which comm_name spells out one to one
-  std::map<std::tuple<int, int64_t, int64_t, int64_t>, int> local;
+  FlatMap<std::tuple<int, int64_t, int64_t, int64_t>, int> local;
   for (const CommRole &r : roles) {
     int lc = (int)B.comm_nranks.size();
     if (!local.emplace(std::make_tuple(r.type, r.a, r.b, r.c), lc).second)
@@ -547,14 +566,14 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
     B.ev(MAYA_EV_COMMINIT, 0, lc, r.nranks, r.my_rank);
   }
   auto lc_of = [&](int type, int64_t a, int64_t b2, int64_t c2) {
-    auto it = local.find(std::make_tuple(type, a, b2, c2));
-    if (it == local.end()) throw GenFail{"communicator missing from worker_comms"};
-    return it->second;
+    const int *q = local.get(std::make_tuple(type, a, b2, c2));
+    if (!q) throw GenFail{"communicator missing from worker_comms"};
+    return *q;
   };
 
   std::vector<Chunk> chunks = device_chunks(M, (int)p, (int)v, (int)stage);
-  std::map<std::pair<int64_t, int>, int32_t> p2p_stream;  // (boundary, role) -> stream
-  std::map<std::pair<int, int64_t>, int64_t> eid;         // (key kind, boundary) -> id
+  FlatMap<std::pair<int64_t, int>, int32_t> p2p_stream;  // (boundary, role) -> stream
+  FlatMap<std::pair<int, int64_t>, int64_t> eid;         // (key kind, boundary) -> id
   enum { R_FIN = 0, R_BOUT, R_FOUT, R_BIN };
   enum { E_FIN = 0, E_BOUT, E_FOUT, E_BIN, E_GRADS, E_DP_DONE, E_OPT_DONE, E_AG_DONE };
   int32_t next_stream = FIRST_P2P_STREAM;
@@ -725,7 +744,17 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
     }
   std::vector<size_t> calls0;
   std::vector<int64_t> vers0;
-  for (const Step &st : pipeline_order(schedule, p, m, v, stage)) {
+  // the order is a pure function of (schedule, p, m, v, stage): memoised per
+  // worker thread (configs of a batch share their pipeline shapes); a failing
+  // shape throws before it is stored
+  thread_local std::map<std::array<int64_t, 5>, std::vector<Step>> po_memo;
+  const std::array<int64_t, 5> po_key{schedule, p, m, v, stage};
+  auto po_it = po_memo.find(po_key);
+  if (po_it == po_memo.end()) {
+    if (po_memo.size() > 4096) po_memo.clear();
+    po_it = po_memo.emplace(po_key, pipeline_order(schedule, p, m, v, stage)).first;
+  }
+  for (const Step &st : po_it->second) {
     if (!tpl_on) {
       if (st.phase == FWD) emit_forward(st.mb, st.chunk);
       else emit_backward(st.mb, st.chunk);
