@@ -51,7 +51,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--threads", type=int, default=0, help="host threads (0 = all)")
-    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="0 = 3 x --steps (at least 30): a host-bound step of ~3.5 ms needs "
+                         "~0.1 s of timed steps to average out host scheduling jitter")
     ap.add_argument("--cpu-seconds", type=float, default=5.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 lattice sub-line")
@@ -645,8 +647,8 @@ def bench_ours(args):
     # the host clock over the K steps, device synchronised on both sides.
     from paper_2503_20191_b200.api import GenPipeline
     pipe = GenPipeline(local, chunks=1)
-    e2e_steps = args.e2e_steps or args.steps
-    for _ in pipe.evaluate_stream(model, [configs] * 3, cluster, k=TOPK, key_orders=[kr] * 3,
+    e2e_steps = args.e2e_steps or max(30, 3 * args.steps)
+    for _ in pipe.evaluate_stream(model, [configs] * 6, cluster, k=TOPK, key_orders=[kr] * 6,
                                   dispatch_overhead_ns=5000, threads=threads):
         pass
     if world > 1:
@@ -701,7 +703,7 @@ def bench_ours(args):
                         "the reference's work unit); class_ops_per_s: the ops the engine "
                         "executed (rank classes of collapsed jobs, SURVEY 7.8)",
             "e2e": {"value": round(n_total / (e2e_ms_max / 1000), 2), "unit": "configs/s",
-                    "ms_per_step": round(e2e_ms_max, 3),
+                    "ms_per_step": round(e2e_ms_max, 3), "steps": e2e_steps,
                     "h2d_bytes_per_step": int(stats["arena_bytes"]),
                     "d2h_bytes_per_step": int(N_CONFIGS * 64 + TOPK * 16),
                     "path": "api.GenPipeline.evaluate_stream: per step, config list -> fused "
