@@ -679,7 +679,9 @@ struct RepPacker {
     // prefetches) its entries sequentially
     {
       const uint32_t nc = (uint32_t)(P->coll_lc.size() - coll0);
-      std::vector<uint32_t> lc(nc), ix(nc);
+      thread_local std::vector<uint32_t> lc, ix;   // scratch, capacity kept per worker
+      lc.resize(nc);
+      ix.resize(nc);
       uint32_t next = 0;
       for (size_t si = 0; si < RB.size(); si++)
         for (Op &o : RB.sops[si])
