@@ -612,12 +612,34 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   std::vector<int64_t> act_ids(chunks.size() * (size_t)m, -1);
   auto act = [&](int c, int64_t mb) -> int64_t & { return act_ids[(size_t)c * (size_t)m + (size_t)mb]; };
 
-  const std::vector<KSpec> lks = layer_fwd(M, b, t, sp);
-  const std::vector<KSpec> hks = head_fwd(M, b, t, sp);
-  const KSpec eks = embed_fwd(M, b, t, sp);
-  const std::vector<KSpec> mlp_bwd = bwd_of(lks, 7, 12);
-  const std::vector<KSpec> attn_bwd = bwd_of(lks, 0, 7);
-  const std::vector<KSpec> head_bwd = bwd_of(hks, 0, 3);
+  // the kernel lists are a pure function of (model shape, micro-batch size,
+  // tp, sp): memoised per worker thread (128-bit shape arithmetic per rep
+  // otherwise); a shape that overflows throws before it is stored
+  struct KSets {
+    std::vector<KSpec> lks, hks, mlp_bwd, attn_bwd, head_bwd;
+    KSpec eks;
+  };
+  thread_local std::map<std::array<int64_t, 8>, KSets> ks_memo;
+  const std::array<int64_t, 8> ks_key{(int64_t)M.s, (int64_t)M.h, (int64_t)M.v, (int64_t)M.esz,
+                                      (int64_t)M.L, (int64_t)b, (int64_t)t, sp ? 1 : 0};
+  auto ks_it = ks_memo.find(ks_key);
+  if (ks_it == ks_memo.end()) {
+    KSets k;
+    k.lks = layer_fwd(M, b, t, sp);
+    k.hks = head_fwd(M, b, t, sp);
+    k.eks = embed_fwd(M, b, t, sp);
+    k.mlp_bwd = bwd_of(k.lks, 7, 12);
+    k.attn_bwd = bwd_of(k.lks, 0, 7);
+    k.head_bwd = bwd_of(k.hks, 0, 3);
+    if (ks_memo.size() > 4096) ks_memo.clear();
+    ks_it = ks_memo.emplace(ks_key, std::move(k)).first;
+  }
+  const std::vector<KSpec> &lks = ks_it->second.lks;
+  const std::vector<KSpec> &hks = ks_it->second.hks;
+  const KSpec eks = ks_it->second.eks;
+  const std::vector<KSpec> &mlp_bwd = ks_it->second.mlp_bwd;
+  const std::vector<KSpec> &attn_bwd = ks_it->second.attn_bwd;
+  const std::vector<KSpec> &head_bwd = ks_it->second.head_bwd;
 
   auto tp_pair_fwd = [&]() {
     if (t > 1) B.collective(STREAM_COMPUTE, tp_lc, sp ? K_REDUCESCATTER : K_ALLREDUCE, tp_coll_bytes);
