@@ -539,6 +539,7 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
   const i128 u = sp ? t : 1;
 
   Builder B{G.ev_kind, G.ev_stream, G.ev_f, sink, overhead, dtype, {}, {}, {}, {}, {}, 0};
+  std::vector<std::vector<std::pair<int8_t, int64_t>>> spare = std::move(rc.calls);   // capacity
   B.blocks = sink && sink->takes_blocks();
   {  // reserve for this trace: ~ (2 x kernels per layer-microbatch) + specials
     const size_t est = (size_t)(cfg.micro_mult) * (size_t)cfg.pp * (size_t)(M.L / cfg.pp + 2) *
@@ -562,7 +563,12 @@ void generate_trace(const Shape &M, const maya_config &cfg, const Coords &C, int
       throw GenFail{"duplicate communicator"};
     B.comm_nranks.push_back(r.nranks);
     B.call_idx.push_back(0);
-    B.calls.emplace_back();
+    if (B.calls.size() < spare.size()) {
+      B.calls.push_back(std::move(spare[B.calls.size()]));
+      B.calls.back().clear();
+    } else {
+      B.calls.emplace_back();
+    }
     B.ev(MAYA_EV_COMMINIT, 0, lc, r.nranks, r.my_rank);
   }
   auto lc_of = [&](int type, int64_t a, int64_t b2, int64_t c2) {
@@ -1037,6 +1043,10 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
     G.capacity = cl.device_memory_bytes;
     // representatives: one per stage (unique_workers, :281-298)
     std::vector<RepCalls> rcalls(cfg.pp);
+    // the previous config's call lists (this worker's GenJob) lend their
+    // capacity to this one's (generate_trace reuses them, cleared)
+    for (size_t k = 0; k < rcalls.size() && k < G.rep_calls.size(); k++)
+      rcalls[k].calls = std::move(G.rep_calls[k]);
     JobTpls jtpl;   // phase templates of the job
     G.ev_off.push_back(0);
     for (int k = 0; k < cfg.pp; k++) {

@@ -68,7 +68,9 @@ struct GenJob {
     rep_ranks.clear(); rank_rep.clear(); ev_off.clear(); ev_kind.clear(); ev_stream.clear();
     ev_f.clear(); comm_names.clear(); comm_nranks.clear(); comm_topo.clear(); call_off.clear();
     call_kind.clear(); call_bytes.clear(); rank_comm_off.clear(); rank_comm.clear();
-    lazy_calls = false; rep_calls.clear(); comm_first_stage.clear(); comm_first_lc.clear();
+    // rep_calls keeps its lists (read only while lazy_calls): the next config's
+    // generator reuses their capacity (gen.cpp generate_job)
+    lazy_calls = false; comm_first_stage.clear(); comm_first_lc.clear();
     n_calls_total = 0;
     comm_blob.clear();
   }
