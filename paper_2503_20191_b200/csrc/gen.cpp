@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -504,7 +505,37 @@ struct BTpl {
   int64_t allocs = 0;
 };
 typedef std::array<int64_t, 20> TplKey;
-typedef std::map<TplKey, BTpl> JobTpls;        // per job, shared by its reps
+// The phase templates of one job, shared by its reps: a worker-thread object
+// reset per job, whose entries (and their vectors' capacity) are reused; a
+// deque keeps the BTpl addresses the generator holds stable as it grows.
+struct JobTpls {
+  struct Ent {
+    uint64_t hash = 0;
+    TplKey key{};
+    BTpl tpl;
+  };
+  std::deque<Ent> store;
+  size_t used = 0;
+  void reset() { used = 0; }
+  BTpl &operator[](const TplKey &k) {
+    uint64_t h = 1469598103934665603ull;
+    for (int64_t x : k) h = (h ^ (uint64_t)x) * 1099511628211ull;
+    for (size_t i = 0; i < used; i++)
+      if (store[i].hash == h && store[i].key == k) return store[i].tpl;
+    if (used == store.size()) store.emplace_back();
+    Ent &e = store[used++];
+    e.hash = h;
+    e.key = k;
+    BTpl &b = e.tpl;
+    b.id = -2;
+    b.tries = 0;
+    b.call_runs.clear();
+    b.call_data.clear();
+    b.vers.clear();
+    b.allocs = 0;
+    return b;
+  }
+};
 
 // workload.py:571-780 for one representative rank; appends events.
 // A few dozen keyed entries per trace (communicator roles, p2p streams,
@@ -1047,7 +1078,8 @@ int generate_job(const maya_model &model, const maya_config &cfg, const maya_clu
     // capacity to this one's (generate_trace reuses them, cleared)
     for (size_t k = 0; k < rcalls.size() && k < G.rep_calls.size(); k++)
       rcalls[k].calls = std::move(G.rep_calls[k]);
-    JobTpls jtpl;   // phase templates of the job
+    thread_local JobTpls jtpl;   // phase templates of the job
+    jtpl.reset();
     G.ev_off.push_back(0);
     for (int k = 0; k < cfg.pp; k++) {
       int64_t rep = rank_of(C, 0, 0, k);
