@@ -106,6 +106,38 @@ class Timeline:
                         self.end[m])
 
 
+_GEN_BATCHES: dict = {}
+
+
+def _generated_batch(device, efficiency, overhead_ns) -> Batch:
+    """The estimator tables and device record of a generated batch (read-only
+    once built: the native calls copy them), shared by every batch with the
+    same device class, efficiency table and kernel overhead."""
+    from .rawtrace import DeviceParams
+    # keyed by the device object's identity (the entry keeps it alive, so the
+    # id cannot be reused while cached) and its rates (a frozen dataclass whose
+    # peak_flops mapping could still be edited), and the efficiency table
+    try:
+        key = (id(device), tuple(sorted(getattr(device, "peak_flops", {}).items())),
+               getattr(device, "hbm_bytes_per_s", None),
+               None if efficiency is None else tuple(sorted(efficiency.items())), int(overhead_ns))
+        hash(key)
+    except TypeError:
+        key = None
+    hit = _GEN_BATCHES.get(key) if key is not None else None
+    if hit is not None and hit[0] is device:
+        return hit[1]
+    b = Batch([], efficiency, overhead_ns)
+    b.devices.append(DeviceParams.from_reference(device))
+    b.c_devices = (DeviceParamsC * 1)()
+    b._fill_device(b.c_devices[0], b.devices[0])
+    if key is not None:
+        if len(_GEN_BATCHES) > 64:
+            _GEN_BATCHES.clear()
+        _GEN_BATCHES[key] = (device, b)
+    return b
+
+
 class Engine:
     """One engine per CUDA device (C ABI: maya_open ... maya_close)."""
 
@@ -279,13 +311,9 @@ class Engine:
                         key_ranks=None, threads: int = 8) -> np.ndarray:
         """Generate + pack configs natively into the batch (no RawJob round trip).
         Returns per-config generation status (0 ok, <0 invalid config)."""
-        from .rawtrace import DeviceParams
         from .workload import _gen_lib, cluster_c, configs_array, model_c, schedule_code
         L = _gen_lib()
-        b = Batch([], efficiency, overhead_ns)
-        b.devices.append(DeviceParams.from_reference(cluster.device))
-        b.c_devices = (DeviceParamsC * 1)()
-        b._fill_device(b.c_devices[0], b.devices[0])
+        b = _generated_batch(cluster.device, efficiency, overhead_ns)
         self.batch = b
         n = len(configs)
         _check(L.maya_batch_reset(self._h))
